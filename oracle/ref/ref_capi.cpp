@@ -1,0 +1,436 @@
+// TEST INFRASTRUCTURE (oracle only; never linked into the product).
+//
+// extern "C" entry points over the REAL reference implementation compiled
+// from /root/reference/proj/core/src (see oracle/ref/Makefile). Tests and the
+// bench's CPU arm call these through ctypes to (a) pin the restated oracle
+// (oracle/bo_oracle.cpp) and (b) produce golden fixtures under tests/golden/.
+//
+// Every entry point calls the reference function it is named after:
+//   ref_f32_to_f16 / ref_f16_to_f32      half.cpp:23-77
+//   ref_unscale_gradients                half.cpp:105-115
+//   ref_lamb_step                        lamb.cpp:140-201
+//   ref_ring_allreduce                   collective.hpp:53-99 / collective.cpp:163-212
+//   ref_bucket_layout                    trainer.cpp:73-134
+//   ref_train                            trainer.cpp:217-373 (DistributedTrainer::train_step)
+//                                        + the dynamic loss-scaler extension
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <thread>
+#include <vector>
+
+#include "bertopt/collective.hpp"
+#include "bertopt/graph.hpp"
+#include "bertopt/half.hpp"
+#include "bertopt/lamb.hpp"
+#include "bertopt/trainer.hpp"
+#include "bertopt/transport.hpp"
+#include "ref_shim.hpp"
+
+extern "C" {
+#include "../synth_grad.h"
+}
+
+using namespace bertopt;
+
+namespace {
+
+// Status codes mirror include/bertopt_b200.h (bo_status).
+enum {
+  kOk = 0, kShapeMismatch = 1, kNonFinite = 2, kOverflow = 3, kLength = 4,
+  kInvalidConfig = 5, kLayoutMismatch = 6, kPeerDisc = 7, kWatchdog = 8,
+  kProtocol = 9, kOther = 99
+};
+
+int map_exception(std::exception_ptr e, char* err, int errlen) {
+  int code = kOther;
+  std::string msg = "unknown";
+  try {
+    std::rethrow_exception(e);
+  } catch (const ShapeMismatch& x) { code = kShapeMismatch; msg = x.what();
+  } catch (const NonFiniteGradient& x) { code = kNonFinite; msg = x.what();
+  } catch (const OverflowDetected& x) { code = kOverflow; msg = x.what();
+  } catch (const LengthMismatch& x) { code = kLength; msg = x.what();
+  } catch (const InvalidConfig& x) { code = kInvalidConfig; msg = x.what();
+  } catch (const BucketLayoutMismatch& x) { code = kLayoutMismatch; msg = x.what();
+  } catch (const PeerDisconnected& x) { code = kPeerDisc; msg = x.what();
+  } catch (const WatchdogTimeout& x) { code = kWatchdog; msg = x.what();
+  } catch (const ProtocolError& x) { code = kProtocol; msg = x.what();
+  } catch (const std::exception& x) { code = kOther; msg = x.what(); }
+  if (err && errlen > 0) {
+    std::snprintf(err, static_cast<size_t>(errlen), "%s", msg.c_str());
+  }
+  return code;
+}
+
+// Root-cause preference, as trainer.cpp:473-487.
+std::exception_ptr preferred(const std::vector<std::exception_ptr>& errs) {
+  std::exception_ptr first;
+  for (const auto& e : errs) {
+    if (!e) continue;
+    if (!first) first = e;
+    try {
+      std::rethrow_exception(e);
+    } catch (const PeerDisconnected&) {
+    } catch (const WatchdogTimeout&) {
+    } catch (...) {
+      return e;
+    }
+  }
+  return first;
+}
+
+}  // namespace
+
+extern "C" {
+
+struct bo_spec_c {
+  int n_tensors;
+  const char* const* names;
+  const int* ndims;
+  const int64_t* dims;      // flattened shapes
+  const int* init;          // 0 randn, 1 ones, 2 zeros
+  const int* first_use;     // permutation: tensor ids in forward first-use order
+};
+
+struct bo_scaler_c {
+  float init_scale, growth_factor, backoff_factor, min_scale, max_scale;
+  int growth_interval;
+  int dynamic;
+};
+
+}  // extern "C"
+
+namespace {
+
+refshim::ModelSpec to_spec(const bo_spec_c* s) {
+  refshim::ModelSpec out;
+  size_t k = 0;
+  for (int t = 0; t < s->n_tensors; ++t) {
+    out.names.emplace_back(s->names[t]);
+    std::vector<int64_t> shp;
+    for (int d = 0; d < s->ndims[t]; ++d) shp.push_back(s->dims[k++]);
+    out.shapes.push_back(shp);
+    out.init.push_back(s->init[t]);
+  }
+  return out;
+}
+
+LambConfig to_lamb(const float* c) {
+  LambConfig l;
+  l.lr = c[0]; l.beta1 = c[1]; l.beta2 = c[2];
+  l.eps = c[3]; l.weight_decay = c[4]; l.trust_clip = c[5];
+  return l;
+}
+
+}  // namespace
+
+extern "C" {
+
+void ref_f32_to_f16(const float* x, uint16_t* out, size_t n) {
+  for (size_t i = 0; i < n; ++i) out[i] = f32_to_f16(x[i]).bits;
+}
+
+void ref_f16_to_f32(const uint16_t* h, float* out, size_t n) {
+  for (size_t i = 0; i < n; ++i) out[i] = f16_to_f32(Binary16{h[i]});
+}
+
+void ref_narrow_block(const float* x, uint16_t* out, size_t n) { narrow_f16_block(x, out, n); }
+void ref_widen_block(const uint16_t* h, float* out, size_t n) { widen_f16_block(h, out, n); }
+
+uint64_t ref_fnv1a(const void* data, size_t len, uint64_t seed) { return fnv1a(data, len, seed); }
+size_t ref_ring_chunk_elems(size_t n, int world) { return ring_chunk_elems(n, world); }
+uint64_t ref_ring_allreduce_bytes(size_t n, int world, size_t e) {
+  return ring_allreduce_bytes(n, world, e);
+}
+
+int ref_unscale_gradients(float* g, size_t n, float scale, int enabled, char* err, int errlen) {
+  try {
+    LossScaler s(scale, enabled != 0);
+    unscale_gradients(std::span<float>(g, n), s);
+    return kOk;
+  } catch (...) {
+    return map_exception(std::current_exception(), err, errlen);
+  }
+}
+
+// Real lamb_step over n_tensors tensors stored flat (model order).
+// m/v are taken as the incoming LambState (zeros on a fresh state).
+int ref_lamb_step(int n_tensors, const int64_t* numels, float* w, const float* g,
+                  float* m, float* v, int64_t* step, const float* lamb6,
+                  char* err, int errlen) {
+  try {
+    std::vector<Tensor> params, grads;
+    LambState st;
+    size_t off = 0;
+    for (int t = 0; t < n_tensors; ++t) {
+      const size_t n = static_cast<size_t>(numels[t]);
+      params.push_back(Tensor::from({numels[t]}, std::vector<float>(w + off, w + off + n)));
+      grads.push_back(Tensor::from({numels[t]}, std::vector<float>(g + off, g + off + n)));
+      st.m.push_back(Tensor::from({numels[t]}, std::vector<float>(m + off, m + off + n)));
+      st.v.push_back(Tensor::from({numels[t]}, std::vector<float>(v + off, v + off + n)));
+      off += n;
+    }
+    st.step = *step;
+    int rc = kOk;
+    try {
+      lamb_step(params, grads, st, to_lamb(lamb6));
+    } catch (...) {
+      rc = map_exception(std::current_exception(), err, errlen);
+    }
+    // Copy back whatever the reference left behind (including the partial
+    // update that precedes a NonFiniteGradient throw).
+    off = 0;
+    for (int t = 0; t < n_tensors; ++t) {
+      const size_t n = static_cast<size_t>(numels[t]);
+      std::memcpy(w + off, params[static_cast<size_t>(t)].data.data(), n * 4);
+      std::memcpy(m + off, st.m[static_cast<size_t>(t)].data.data(), n * 4);
+      std::memcpy(v + off, st.v[static_cast<size_t>(t)].data.data(), n * 4);
+      off += n;
+    }
+    *step = st.step;
+    return rc;
+  } catch (...) {
+    return map_exception(std::current_exception(), err, errlen);
+  }
+}
+
+// Real ring all-reduce over `world` InProcHub threads. data is [world][n].
+// kind: 0 float, 1 float with f16 wire, 2 int64 (data reinterpreted).
+int ref_ring_allreduce(int world, size_t n, void* data, int kind, uint64_t* payload_sent,
+                       char* err, int errlen) {
+  auto hub = std::make_shared<InProcHub>(world);
+  std::vector<std::exception_ptr> errs(static_cast<size_t>(world));
+  std::vector<std::thread> th;
+  for (int r = 0; r < world; ++r) {
+    th.emplace_back([&, r] {
+      try {
+        InProcTransport tr(hub, r);
+        tr.set_watchdog(60.0);
+        WorkerGroup g{r, world, 0, r, &tr};
+        if (kind == 2) {
+          int64_t* d = static_cast<int64_t*>(data) + static_cast<size_t>(r) * n;
+          ring_allreduce<int64_t>(g, d, n, 7);
+        } else {
+          float* d = static_cast<float*>(data) + static_cast<size_t>(r) * n;
+          if (kind == 1) ring_allreduce_f16_wire(g, d, n, 7);
+          else ring_allreduce<float>(g, d, n, 7);
+        }
+        if (payload_sent) payload_sent[r] = tr.payload_bytes_sent();
+      } catch (...) {
+        errs[static_cast<size_t>(r)] = std::current_exception();
+      }
+    });
+  }
+  for (auto& t : th) t.join();
+  if (auto e = preferred(errs)) return map_exception(e, err, errlen);
+  return kOk;
+}
+
+// Real BucketLayout::build + hash. Outputs: bucket_of[T], offset_of[T],
+// ready_order[T], bucket_elems[<=T]; returns bucket count (or -code).
+int ref_bucket_layout(const bo_spec_c* spec, const int* firsts, uint64_t bucket_bytes,
+                      int* bucket_of, int64_t* offset_of, int* ready_order,
+                      int64_t* bucket_elems, uint64_t* hash_out, char* err, int errlen) {
+  try {
+    refshim::ModelSpec ms = to_spec(spec);
+    Model m;
+    for (size_t t = 0; t < ms.names.size(); ++t) {
+      m.index[ms.names[t]] = static_cast<int>(t);
+      m.names.push_back(ms.names[t]);
+      m.params.push_back(Tensor::zeros(ms.shapes[t]));
+    }
+    std::vector<int> f(firsts, firsts + spec->n_tensors);
+    BucketLayout L = BucketLayout::build(m, f, bucket_bytes);
+    for (int t = 0; t < spec->n_tensors; ++t) {
+      bucket_of[t] = L.bucket_of[static_cast<size_t>(t)];
+      offset_of[t] = static_cast<int64_t>(L.offset_of[static_cast<size_t>(t)]);
+      ready_order[t] = L.ready_order[static_cast<size_t>(t)];
+    }
+    for (size_t b = 0; b < L.buckets.size(); ++b) {
+      bucket_elems[b] = static_cast<int64_t>(L.buckets[b].elems);
+    }
+    if (hash_out) *hash_out = L.hash(m);
+    return static_cast<int>(L.buckets.size());
+  } catch (...) {
+    return -map_exception(std::current_exception(), err, errlen);
+  }
+}
+
+// Initial parameters exactly as the restated build_model draws them.
+int ref_build_params(const bo_spec_c* spec, uint64_t seed, float* out) {
+  Model m = refshim::build_model_from_spec(to_spec(spec), seed);
+  size_t off = 0;
+  for (const Tensor& t : m.params) {
+    std::memcpy(out + off, t.data.data(), t.data.size() * 4);
+    off += t.data.size();
+  }
+  return kOk;
+}
+
+// Full data-parallel run of the REAL DistributedTrainer::train_step with the
+// builder-defined dynamic loss-scaler extension:
+//   * micro k of rank r at step t gets fp16 gradients h = f32_to_f16(g * S_t)
+//     from the synthetic spec (synth_grad.h), overridden by injections;
+//   * the synthetic forward makes the trainer's live gradient exactly
+//     widen(h) (the loss is multiplied by S_t through tape.scalar_mul);
+//   * found_inf := train_step threw NonFiniteGradient (lamb.cpp:179-182: the
+//     reduced gradient lamb_step consumes held a non-finite). The step is then
+//     skipped: params / m / v / step are restored to their pre-step values;
+//   * scaler: found_inf -> S = max(S*backoff, min), good = 0;
+//     else good++, good == interval -> S = min(S*growth, max), good = 0.
+//     With dynamic == 0 the scale never changes (skips still apply).
+// inj is [n_inj][5] = (step, rank, micro, flat_index, f16 bits).
+int ref_train(const bo_spec_c* spec, uint64_t init_seed, int world, int K,
+              uint64_t bucket_bytes, int f16_exchange, int overlap, const float* lamb6,
+              const bo_scaler_c* sc, uint64_t grad_seed, uint32_t spike_ppm, int spike_exp,
+              const int64_t* inj, int n_inj, int steps, float* params_out, float* m_out,
+              float* v_out, int64_t* lamb_step_out, float* scale_used, int* found_inf,
+              float* final_scale, int* final_good, char* err, int errlen) {
+  try {
+    const refshim::ModelSpec ms = to_spec(spec);
+    const int T = spec->n_tensors;
+    std::vector<int> first_use(spec->first_use, spec->first_use + T);
+    std::vector<int64_t> numel(static_cast<size_t>(T));
+    std::vector<int64_t> flat_off(static_cast<size_t>(T));
+    int64_t P = 0;
+    for (int t = 0; t < T; ++t) {
+      int64_t n = 1;
+      for (int64_t e : ms.shapes[static_cast<size_t>(t)]) n *= e;
+      numel[static_cast<size_t>(t)] = n;
+      flat_off[static_cast<size_t>(t)] = P;
+      P += n;
+    }
+    auto hub = world > 1 ? std::make_shared<InProcHub>(world) : nullptr;
+    std::vector<std::exception_ptr> errs(static_cast<size_t>(world));
+    std::vector<uint64_t> hashes(static_cast<size_t>(world));
+    std::vector<float> scales(static_cast<size_t>(world));
+    std::vector<std::thread> th;
+    for (int r = 0; r < world; ++r) {
+      th.emplace_back([&, r] {
+        try {
+          std::unique_ptr<InProcTransport> tr;
+          WorkerGroup g;
+          g.rank = r;
+          g.world = world;
+          g.gpu = r;
+          if (world > 1) {
+            tr = std::make_unique<InProcTransport>(hub, r);
+            tr->set_watchdog(600.0);
+            g.transport = tr.get();
+          }
+          Model m = refshim::build_model_from_spec(ms, init_seed);
+          TrainerConfig tc;
+          tc.lamb = to_lamb(lamb6);
+          tc.accumulation = K;
+          tc.bucket_bytes = static_cast<size_t>(bucket_bytes);
+          tc.overlap = overlap != 0;
+          tc.f16_exchange = f16_exchange != 0;
+          LambState saved;
+          float S = sc->init_scale;
+          int good = 0;
+          std::vector<refshim::SynthMicro> micros(static_cast<size_t>(K));
+          for (int step = 0; step < steps; ++step) {
+            std::vector<Batch> batches(static_cast<size_t>(K));
+            for (int k = 0; k < K; ++k) {
+              refshim::SynthMicro& sm = micros[static_cast<size_t>(k)];
+              sm.first_use_order = first_use;
+              sm.G.assign(static_cast<size_t>(T), {});
+              const uint64_t base = bo_synth_base(grad_seed, static_cast<uint64_t>(r),
+                                                  static_cast<uint64_t>(step),
+                                                  static_cast<uint64_t>(k));
+              for (int t = 0; t < T; ++t) {
+                std::vector<float>& G = sm.G[static_cast<size_t>(t)];
+                G.resize(static_cast<size_t>(numel[static_cast<size_t>(t)]));
+                for (int64_t i = 0; i < numel[static_cast<size_t>(t)]; ++i) {
+                  const int64_t fi = flat_off[static_cast<size_t>(t)] + i;
+                  const float gt = bo_synth_true_grad(base, static_cast<uint64_t>(fi),
+                                                      spike_ppm, spike_exp);
+                  uint16_t h = f32_to_f16(gt * S).bits;
+                  for (int q = 0; q < n_inj; ++q) {
+                    const int64_t* e = inj + 5 * q;
+                    if (e[0] == step && e[1] == r && e[2] == k && e[3] == fi) {
+                      h = static_cast<uint16_t>(e[4]);
+                    }
+                  }
+                  G[static_cast<size_t>(i)] = f16_to_f32(Binary16{h}) / S;
+                }
+              }
+              const int64_t handle = (static_cast<int64_t>(r) << 40) |
+                                     (static_cast<int64_t>(step) << 8) | k;
+              refshim::register_micro(handle, &sm);
+              batches[static_cast<size_t>(k)].ids = {handle};
+            }
+            const std::vector<Tensor> saved_params = m.params;
+            tc.loss_scale = S;
+            if (r == 0) scale_used[step] = S;
+            bool found = false;
+            {
+              DistributedTrainer trainer(g, m, tc);
+              trainer.state() = saved;
+              try {
+                (void)trainer.train_step(batches);
+                saved = trainer.state();
+              } catch (const NonFiniteGradient&) {
+                found = true;
+                for (size_t p = 0; p < m.params.size(); ++p) {
+                  m.params[p].data = saved_params[p].data;
+                }
+              }
+            }
+            for (int k = 0; k < K; ++k) {
+              refshim::unregister_micro((static_cast<int64_t>(r) << 40) |
+                                        (static_cast<int64_t>(step) << 8) | k);
+            }
+            if (r == 0) found_inf[step] = found ? 1 : 0;
+            if (sc->dynamic) {
+              if (found) {
+                S = std::max(S * sc->backoff_factor, sc->min_scale);
+                good = 0;
+              } else if (++good == sc->growth_interval) {
+                S = std::min(S * sc->growth_factor, sc->max_scale);
+                good = 0;
+              }
+            }
+          }
+          hashes[static_cast<size_t>(r)] = model_param_hash(m);
+          scales[static_cast<size_t>(r)] = S;
+          if (r == 0) {
+            size_t off = 0;
+            for (size_t p = 0; p < m.params.size(); ++p) {
+              const size_t n = m.params[p].data.size();
+              std::memcpy(params_out + off, m.params[p].data.data(), n * 4);
+              if (!saved.m.empty()) {
+                std::memcpy(m_out + off, saved.m[p].data.data(), n * 4);
+                std::memcpy(v_out + off, saved.v[p].data.data(), n * 4);
+              } else {
+                std::memset(m_out + off, 0, n * 4);
+                std::memset(v_out + off, 0, n * 4);
+              }
+              off += n;
+            }
+            *lamb_step_out = saved.step;
+            *final_scale = S;
+            *final_good = good;
+          }
+        } catch (...) {
+          errs[static_cast<size_t>(r)] = std::current_exception();
+        }
+      });
+    }
+    for (auto& t : th) t.join();
+    if (auto e = preferred(errs)) return map_exception(e, err, errlen);
+    for (int r = 1; r < world; ++r) {
+      if (hashes[static_cast<size_t>(r)] != hashes[0] || scales[static_cast<size_t>(r)] != scales[0]) {
+        throw Error("replica divergence across ranks");
+      }
+    }
+    return kOk;
+  } catch (...) {
+    return map_exception(std::current_exception(), err, errlen);
+  }
+}
+
+}  // extern "C"
