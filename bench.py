@@ -1,0 +1,426 @@
+#!/usr/bin/env python
+"""BERT-large gradient-to-update step on B200: accumulate -> unscale/overflow
+-> reduce-scatter -> sharded LAMB -> loss-scaler -> all-gather.
+
+One JSON line on rank 0:
+  value       = world * P / step_time  (gradient-params/s; every rank consumes
+                a full P-parameter gradient of K micro-batches per step)
+  ms_per_step = device time of one optimizer step (CUDA events, max over ranks)
+  e2e         = the same metric through the public API with the K micro-batch
+                fp16 gradients copied from pinned host memory every step and
+                the step status read back
+  roofline    = dominant kernel's algorithmic bytes / its average duration
+  step_roofline = SURVEY §8(d) stage-sum roofline of the whole step
+  cpu_baseline  = the reference's own CPU hot path (oracle/_ref) on this host
+
+Launch: python bench.py [--gpus N --steps K --warmup W]; N > 1 under
+torch.distributed.run (one process per GPU). --impl reference times the
+reference CPU implementation instead (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "BERT-large optimizer step params/sec"
+UNIT = "params/s"
+
+# Algorithmic HBM bytes per element of each stage.
+BYTES_ACCUMULATE_FIRST = 2 + 4          # read fp16, write fp32 acc
+BYTES_ACCUMULATE = 2 + 4 + 4            # read fp16 + acc, write acc
+BYTES_FINALIZE = 2 + 4 + 4              # read fp16 + acc, write fusion buffer (fp32)
+BYTES_FINALIZE_K1 = 2 + 4
+BYTES_LAMB_NORMS = 4 * 4                # read g, w, m, v
+BYTES_LAMB_UPDATE = 4 * 4 + 3 * 4       # read g, w, m, v; write w, m, v
+BYTES_LAMB_ALGO = 28                    # single-pass LAMB (the algorithmic minimum)
+
+STAGES = ["accumulate", "finalize", "reduce", "lamb_norms", "trust", "lamb_update", "allgather"]
+
+MODELS = {"bert-large": "BERT_LARGE", "bert-large-128": "BERT_LARGE_PHASE1", "bert-base": "BERT_BASE"}
+
+REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+           0x8: "hw_slowdown", 0x20: "sync_boost", 0x40: "sw_thermal_slowdown",
+           0x80: "hw_thermal_slowdown", 0x100: "hw_power_brake_slowdown",
+           0x200: "display_clock_setting"}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--model", default="bert-large", choices=sorted(MODELS))
+    ap.add_argument("--accumulation", type=int, default=4)
+    ap.add_argument("--bucket-mb", type=float, default=4.0)
+    ap.add_argument("--wire", default="f16", choices=["f16", "f32"])
+    ap.add_argument("--algo", default="auto", choices=["auto", "ring", "nccl"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-steps", type=int, default=3)
+    return ap.parse_args()
+
+
+def env_rank():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:  # noqa: BLE001
+        return 6650.0, "fallback"
+
+
+NVLINK_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md)
+
+
+def model_spec(name):
+    from paper_2008_00177_b200 import model_spec as ms
+
+    return ms.bert_spec(getattr(ms, MODELS[name]))
+
+
+def cpu_sample(spec):
+    """Bounded sample of the workload for the CPU reference: layer0 plus the heads."""
+    idx = [i for i, n in enumerate(spec.names)
+           if n.startswith("layer0.") or n.startswith(("mlm.transform", "mlm.ln", "pooler.", "nsp."))]
+    numels = [spec.numels()[i] for i in idx]
+    firsts = [spec.first_consumer_ids()[i] for i in idx]
+    return numels, firsts, f"{len(idx)} BERT tensors (layer0 + MLM/pooler/NSP heads), {sum(numels)} params"
+
+
+def run_cpu_reference(spec, world, K, bucket_bytes, f16, warmup, steps, groups=None):
+    """Time the reference's own stages (oracle/_ref, else report the port)."""
+    from oracle import oracle as orc
+
+    numels, firsts, sample = cpu_sample(spec)
+    ncpu = os.cpu_count() or 1
+    if groups is None:
+        groups = max(1, min(ncpu // max(world, 1), 16))
+    if orc.reference_available():
+        ref = orc.Reference()
+        secs, stages = ref.stage_bench(numels, firsts, world, K, bucket_bytes, f16, groups, warmup,
+                                       steps)
+        kind = "reference"
+    else:
+        raise RuntimeError("oracle/_ref missing: build it with __graft_entry__.build()")
+    t = statistics.median(secs)
+    P = sum(numels)
+    value = groups * world * P / t
+    return {"value": value, "unit": UNIT, "cores": groups * world, "kind": kind,
+            "sample": f"{sample}; {groups} concurrent replica group(s) x {world} rank thread(s), "
+                      f"K={K}, median of {steps} steps ({t * 1e3:.1f} ms/step)",
+            "stage_seconds_rank0": dict(zip(["accumulate", "flatten", "reduce", "lamb"],
+                                            [s / max(steps, 1) for s in stages]))}
+
+
+class ClockSampler:
+    """NVML sampling of SM clocks and throttle reasons during the timed region."""
+
+    def __init__(self, gpus):
+        self.samples, self.reasons, self.max_mhz = [], 0, None
+        self._stop = threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.handles = [pynvml.nvmlDeviceGetHandleByIndex(i) for i in gpus]
+            self.max_mhz = max(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+                               for h in self.handles)
+            self.ok = True
+        except Exception:  # noqa: BLE001
+            self.ok = False
+
+    def _poll(self):
+        nv = self.nv
+        while True:
+            for h in self.handles:
+                try:
+                    self.samples.append(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+                    self.reasons |= int(nv.nvmlDeviceGetCurrentClocksEventReasons(h))
+                except Exception:  # noqa: BLE001
+                    pass
+            if self._stop.wait(0.01):
+                break
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._poll, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        names = [n for b, n in REASONS.items() if self.reasons & b and b != 0x1]
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": names, "samples": len(self.samples)}
+
+
+def traffic_from_profiles(kernel):
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(kernel)
+    except Exception:  # noqa: BLE001
+        return None
+
+
+def main_b200(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2008_00177_b200.pipeline import (REDUCE_AUTO, REDUCE_NCCL, REDUCE_RING, GradPipeline,
+                                                LambConfig, ScalerConfig, TrainerConfig, synth_grads)
+
+    rank, world, local = env_rank()
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    K = args.accumulation
+    spec = model_spec(args.model)
+    P = spec.param_count()
+    f16 = args.wire == "f16" and world > 1
+    algo = {"auto": REDUCE_AUTO, "ring": REDUCE_RING, "nccl": REDUCE_NCCL}[args.algo]
+    bucket_bytes = int(args.bucket_mb * (1 << 20))
+    cfg = TrainerConfig(LambConfig(lr=1e-4), K, bucket_bytes, f16, algo,
+                        ScalerConfig(init_scale=65536.0, growth_interval=1 << 30))
+    pipe = GradPipeline(spec, cfg, device=local, rank=rank, world=world)
+    if world > 1:
+        pipe.comm_init_torch()
+    # random-init weights of the BERT-large architecture (synthetic)
+    gen = torch.Generator(device=f"cuda:{local}").manual_seed(1234 + rank * 0)
+    w0 = torch.randn(P, device=f"cuda:{local}", generator=gen) * 0.02
+    pipe.load_params(w0)
+    del w0
+
+    # K micro-batches of fp16 gradients, resident in HBM (per-tensor 256 B slots)
+    numels = spec.numels()
+    slots, off = [], 0
+    for n in numels:
+        slots.append(off)
+        off += (n + 127) // 128 * 128
+    total = off
+    model_off = np.concatenate([[0], np.cumsum(numels)[:-1]])
+    S0 = pipe.status().loss_scale
+    bufs = []
+    for k in range(K):
+        b = torch.empty(total, dtype=torch.int16, device=f"cuda:{local}")
+        for t, n in enumerate(numels):
+            synth_grads(b[slots[t]:slots[t] + n], int(model_off[t]), 1, rank, 0, k, S0)
+        bufs.append(b)
+    ptr_arrays = [GradPipeline.make_ptr_array([b.data_ptr() + 2 * s for s in slots]) for b in bufs]
+    torch.cuda.synchronize()
+
+    stream = torch.cuda.ExternalStream(pipe.stream_handle())
+
+    def step():
+        for k in range(K):
+            pipe.accumulate_ptr_array(k, ptr_arrays[k])
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    launches0 = pipe.lib.bo_launch_count(pipe.ctx)
+    gpus = list(range(world)) if rank == 0 else []
+    sampler = ClockSampler(gpus) if rank == 0 else None
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    if sampler:
+        sampler.__enter__()
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    barrier()
+    if sampler:
+        sampler.__exit__()
+    ms = e0.elapsed_time(e1) / args.steps
+    launches = pipe.lib.bo_launch_count(pipe.ctx) - launches0
+    if world > 1:
+        t = torch.tensor([ms], device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    st = pipe.status()
+    assert st.found_inf is False and st.skipped_steps == 0, "synthetic bench overflowed"
+
+    # stage profile: an identical pass with CUDA events around every stage
+    pipe.lib.bo_profile_enable(pipe.ctx, 1)
+    stage_ms = (C.c_double * 7)()
+    stage_n = (C.c_int64 * 7)()
+    pipe.lib.bo_profile_read(pipe.ctx, stage_ms, stage_n, 1)
+    barrier()
+    for _ in range(args.steps):
+        step()
+    barrier()
+    pipe.lib.bo_profile_read(pipe.ctx, stage_ms, stage_n, 1)
+    pipe.lib.bo_profile_enable(pipe.ctx, 0)
+    S_shard = pipe.shard_elems()
+    hbm, peak_kind = peaks()
+    per_elem = {"accumulate": None, "finalize": BYTES_FINALIZE if K > 1 else BYTES_FINALIZE_K1,
+                "lamb_norms": BYTES_LAMB_NORMS, "lamb_update": BYTES_LAMB_UPDATE}
+    stages = {}
+    for i, name in enumerate(STAGES):
+        if stage_n[i] == 0:
+            continue
+        avg = stage_ms[i] / stage_n[i]
+        entry = {"ms": round(avg, 5), "launches_per_step": round(stage_n[i] / args.steps, 2)}
+        if name == "accumulate":
+            nbytes = (BYTES_ACCUMULATE_FIRST + BYTES_ACCUMULATE * (K - 2)) * P / (K - 1)
+        elif name in ("finalize",):
+            nbytes = per_elem[name] * P
+        elif name in ("lamb_norms", "lamb_update"):
+            nbytes = per_elem[name] * S_shard
+        else:
+            nbytes = None
+        if nbytes:
+            gbs = nbytes / (avg * 1e-3) / 1e9
+            entry.update({"bytes": int(nbytes), "GB/s": round(gbs, 1), "frac": round(gbs / hbm, 4)})
+        stages[name] = entry
+    dom = max((n for n in stages if "bytes" in stages[n]),
+              key=lambda n: stages[n]["ms"] * stages[n]["launches_per_step"])
+    kernel_names = {"accumulate": "k_accumulate", "finalize": "k_finalize",
+                    "lamb_norms": "k_lamb_norms", "lamb_update": "k_lamb_update"}
+    roofline = {"kernel": kernel_names[dom], "bound": "hbm", "achieved": stages[dom]["GB/s"],
+                "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s", "frac": stages[dom]["frac"],
+                "traffic": traffic_from_profiles(kernel_names[dom]),
+                "algorithmic_bytes_per_launch": stages[dom]["bytes"]}
+
+    # whole-step roofline: sum over stages of max(HBM, NVLink) time
+    E = 2 if f16 else 4
+    hbm_a = (BYTES_ACCUMULATE_FIRST + BYTES_ACCUMULATE * (K - 2) + BYTES_FINALIZE) * P if K > 1 \
+        else BYTES_FINALIZE_K1 * P
+    hbm_c = BYTES_LAMB_ALGO * P / world
+    nvl_b = (world - 1) / world * E * P
+    nvl_d = (world - 1) / world * 4 * P
+    t_roof = hbm_a / (hbm * 1e9) + hbm_c / (hbm * 1e9) + nvl_b / (NVLINK_GBS * 1e9) + \
+        nvl_d / (NVLINK_GBS * 1e9)
+    step_roofline = {"t_roof_ms": round(t_roof * 1e3, 4), "frac": round(t_roof * 1e3 / ms, 4),
+                     "hbm_bytes": int(hbm_a + hbm_c), "nvlink_bytes": int(nvl_b + nvl_d),
+                     "hbm_gbs": hbm, "nvlink_gbs": NVLINK_GBS,
+                     "formula": "sum_stages max(HBM/BW_hbm, NVL/BW_nvl); A=acc+finalize, "
+                                "C=28 B/param LAMB on the shard, B=RS, D=AG"}
+
+    # end to end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        host = [torch.empty(total, dtype=torch.int16, pin_memory=True) for _ in range(K)]
+        for k in range(K):
+            host[k].copy_(bufs[k])
+        stage_dev = bufs  # reuse the device slots as the H2D destination
+        n_e2e = max(1, min(args.e2e_steps, args.steps))
+
+        def e2e_step():
+            with torch.cuda.stream(stream):
+                for k in range(K):
+                    stage_dev[k].copy_(host[k], non_blocking=True)
+                    pipe.accumulate_ptr_array(k, ptr_arrays[k])
+            return pipe.status()  # D2H of the step result (syncs the stream)
+
+        e2e_step()
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(n_e2e):
+            e2e_step()
+        barrier()
+        e2e_s = (time.perf_counter() - t0) / n_e2e
+        if world > 1:
+            t = torch.tensor([e2e_s], device=f"cuda:{local}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t.item())
+        e2e = {"value": world * P / e2e_s, "unit": UNIT, "ms_per_step": round(e2e_s * 1e3, 3),
+               "h2d_bytes_per_step": int(K * total * 2),
+               "d2h_bytes_per_step": int(C.sizeof(C.c_int64) * 5), "steps": n_e2e}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = run_cpu_reference(spec, 1, K, bucket_bytes, False, 1, args.cpu_steps)
+        except Exception as e:  # noqa: BLE001
+            cpu = {"value": None, "error": str(e)}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": world * P / (ms * 1e-3), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (counter-based fp16 gradients, random-init fp32 weights)",
+            "config": {"workload": f"{args.model} optimizer step, K={K} micro-batch fp16 gradient "
+                                   f"accumulation, dynamic loss scaling, "
+                                   f"{'sharded LAMB + ' + args.wire + '-wire reduce-scatter/all-gather' if world > 1 else 'LAMB'}",
+                       "params": P, "tensors": spec.n_tensors, "accumulation": K,
+                       "bucket_bytes": bucket_bytes, "buckets": pipe.num_buckets,
+                       "wire": args.wire if world > 1 else None,
+                       "reduce_algo": args.algo if world > 1 else None,
+                       "parallelism": f"dp{world} (reduce-scatter + sharded LAMB + all-gather)",
+                       "l2": "inputs (K x 2 B x P) larger than L2, no flush"},
+            "roofline": roofline, "step_roofline": step_roofline, "stages": stages,
+            "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": int(launches),
+            "clocks": sampler.summary() if sampler else None,
+        }
+        print(json.dumps(line), flush=True)
+    pipe.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main_reference(args):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return
+    spec = model_spec(args.model)
+    K = args.accumulation
+    bucket_bytes = int(args.bucket_mb * (1 << 20))
+    f16 = args.wire == "f16" and world > 1
+    steps = max(1, min(args.steps, 10))
+    cpu = run_cpu_reference(spec, world, K, bucket_bytes, f16, max(1, min(args.warmup, 2)), steps)
+    line = {"metric": METRIC, "value": cpu["value"], "unit": UNIT, "n_gpus": world,
+            "steps": steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": f"{args.model} optimizer step (reference CPU path, sample)",
+                       "accumulation": K, "bucket_bytes": bucket_bytes,
+                       "wire": args.wire if world > 1 else None,
+                       "parallelism": f"{world} rank threads (InProcHub ring)"},
+            "cpu_baseline": cpu,
+            "e2e": {"value": cpu["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    a = parse()
+    if a.impl == "reference":
+        main_reference(a)
+    else:
+        main_b200(a)

@@ -1,0 +1,217 @@
+/*
+ * bertopt_b200 — C ABI of the B200-native gradient-to-update pipeline.
+ *
+ * Drop-in boundary for the reference's hot path. The
+ * reference C++ operator API in proj/core stays unchanged; a maintainer binds
+ * these entry points behind it. Plain pointers and sizes
+ * only: no torch or CUDA types appear in the signatures (streams are void*).
+ *
+ * Reference interfaces each entry point replaces (paths relative to
+ * /root/reference/proj/core):
+ *   bo_create / bo_layout_*      BucketLayout::build + hash    trainer.cpp:73-134
+ *                                TrainerConfig                 trainer.hpp:75-85
+ *   bo_comm_*                    WorkerGroup + Transport       collective.hpp:30-40,
+ *                                                              transport.hpp:38-53
+ *   bo_accumulate (micro<K-1)    accum_[p][i] += g[i]          trainer.cpp:240-244
+ *   bo_accumulate (micro=K-1)    flatten_param + reduce_bucket trainer.cpp:186-215
+ *                                + unpack + lamb_step          trainer.cpp:356-366
+ *                                (the sync micro of train_step trainer.cpp:217-373)
+ *   bo_lamb_step                 lamb_step                     lamb.hpp:182-183, lamb.cpp:140-201
+ *   bo_ring_allreduce_f32        ring_allreduce<float>         collective.hpp:104-107
+ *   bo_ring_allreduce_f16_wire   ring_allreduce_f16_wire       collective.hpp:113-114
+ *   bo_unscale_gradients         unscale_gradients             half.hpp:131, half.cpp:105-115
+ *   bo_narrow_f16 / bo_widen_f16 narrow/widen_f16_block        graph.hpp:160-163
+ *   bo_scale_loss                scale_loss                    half.hpp:127
+ *
+ * Error convention: every call returns a bo_status whose values map 1:1 onto
+ * the bertopt::Error subclasses (errors.hpp:35-48), plus CUDA/NCCL failures.
+ * The C++ adapter (include/bertopt_b200_adapter.hpp) re-throws them as the
+ * typed reference exceptions. One deliberate difference on the pipeline path:
+ * a non-finite reduced gradient is not an error there — it sets the step's
+ * found_inf flag, the LAMB step is skipped on device (no host sync) and the
+ * dynamic loss scaler backs off (the scaler extension).
+ */
+#ifndef BERTOPT_B200_H_
+#define BERTOPT_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BO_ABI_VERSION 1
+
+typedef enum {
+  BO_OK = 0,
+  BO_ERR_SHAPE_MISMATCH = 1,         /* bertopt::ShapeMismatch */
+  BO_ERR_NON_FINITE_GRADIENT = 2,    /* bertopt::NonFiniteGradient */
+  BO_ERR_OVERFLOW_DETECTED = 3,      /* bertopt::OverflowDetected */
+  BO_ERR_LENGTH_MISMATCH = 4,        /* bertopt::LengthMismatch */
+  BO_ERR_INVALID_CONFIG = 5,         /* bertopt::InvalidConfig */
+  BO_ERR_BUCKET_LAYOUT_MISMATCH = 6, /* bertopt::BucketLayoutMismatch */
+  BO_ERR_PEER_DISCONNECTED = 7,      /* bertopt::PeerDisconnected */
+  BO_ERR_WATCHDOG_TIMEOUT = 8,       /* bertopt::WatchdogTimeout */
+  BO_ERR_PROTOCOL = 9,               /* bertopt::ProtocolError */
+  BO_ERR_CUDA = 20,
+  BO_ERR_NCCL = 21,
+  BO_ERR_NO_DEVICE = 22
+} bo_status;
+
+/* bertopt::LambConfig (lamb.hpp:165-172); defaults via bo_default_config. */
+typedef struct {
+  float lr, beta1, beta2, eps, weight_decay, trust_clip;
+} bo_lamb_config;
+
+/* Dynamic loss scaler (builder-defined extension; the reference scaler is
+ * static, half.hpp:106-124). Scales stay powers of two. dynamic = 0 keeps
+ * init_scale for the whole run (the reference behaviour). */
+typedef struct {
+  float init_scale, growth_factor, backoff_factor, min_scale, max_scale;
+  int32_t growth_interval;
+  int32_t dynamic;
+} bo_scaler_config;
+
+typedef enum {
+  BO_REDUCE_AUTO = 0,  /* RING when f16_exchange, NCCL otherwise */
+  BO_REDUCE_RING = 1,  /* reference ring order, bit-exact (fp32 or f16 wire) */
+  BO_REDUCE_NCCL = 2   /* ncclReduceScatter (fp32 wire only; reassociated sum) */
+} bo_reduce_algo;
+
+/* bertopt::TrainerConfig (trainer.hpp:75-85) restricted to the hot path. */
+typedef struct {
+  bo_lamb_config lamb;
+  int32_t accumulation;   /* K micro-batches per optimizer step */
+  uint64_t bucket_bytes;  /* fusion-buffer threshold (4 MiB default) */
+  int32_t f16_exchange;   /* binary16 wire for the gradient reduction */
+  int32_t reduce_algo;    /* bo_reduce_algo */
+  bo_scaler_config scaler;
+} bo_trainer_config;
+
+/* Device-resident step status (read back by bo_get_status; host sync). */
+typedef struct {
+  float loss_scale;       /* scale the NEXT step will use */
+  int32_t good_steps;     /* consecutive finite steps since last change */
+  int64_t lamb_step;      /* LambState::step (lamb.hpp:174-178) */
+  int64_t steps;          /* optimizer steps attempted (incl. skipped) */
+  int64_t skipped_steps;  /* steps skipped on overflow */
+  int32_t found_inf;      /* last step's global overflow flag */
+  int32_t reserved;
+} bo_step_status;
+
+typedef struct bo_ctx bo_ctx;
+
+int32_t bo_abi_version(void);
+const char* bo_status_name(int32_t status);
+/* Last error message of the calling thread (any entry point). */
+const char* bo_last_error(void);
+void bo_default_config(bo_trainer_config* cfg);
+
+/* ---- context / layout -------------------------------------------------- */
+/* One context per rank (one process or thread per GPU). numels and
+ * first_consumers are in model parameter order; first_consumers[p] is the op
+ * id of p's first consumer in the forward (gradients become final in
+ * descending order, trainer.cpp:85-90). names/ndims/dims are optional (may be
+ * NULL) and only feed the layout hash. */
+bo_status bo_create(const bo_trainer_config* cfg, int32_t n_tensors, const int64_t* numels,
+                    const int32_t* first_consumers, const char* const* names,
+                    const int32_t* ndims, const int64_t* dims, int32_t device, int32_t rank,
+                    int32_t world, bo_ctx** out);
+void bo_destroy(bo_ctx* ctx);
+
+int32_t bo_layout_num_buckets(const bo_ctx* ctx);
+/* BucketLayout fields: bucket_of[T], offset_of[T], ready_order[T], bucket_elems[B]. */
+bo_status bo_layout_query(const bo_ctx* ctx, int32_t* bucket_of, int64_t* offset_of,
+                          int32_t* ready_order, int64_t* bucket_elems);
+/* BucketLayout::hash salted with f16_exchange and K (trainer.cpp:161-168). */
+uint64_t bo_layout_hash(const bo_ctx* ctx);
+/* Elements of this rank's shard (sum of ceil(n_b / world) over buckets). */
+int64_t bo_shard_elems(const bo_ctx* ctx);
+/* Device bytes held by the context. */
+uint64_t bo_device_bytes(const bo_ctx* ctx);
+
+/* ---- communication (world > 1) ----------------------------------------- */
+/* 128-byte NCCL unique id; rank 0 creates it, the host harness broadcasts it. */
+bo_status bo_comm_unique_id(uint8_t* out128);
+/* Collective over all ranks: NCCL communicator + layout-hash agreement
+ * (BO_ERR_BUCKET_LAYOUT_MISMATCH on disagreement, trainer.cpp:169-183). */
+bo_status bo_comm_init(bo_ctx* ctx, const uint8_t* id128);
+
+/* ---- streams ----------------------------------------------------------- */
+/* Run all work of ctx on the caller's cudaStream_t (NULL: ctx's own stream). */
+bo_status bo_set_stream(bo_ctx* ctx, void* cuda_stream);
+void* bo_get_stream(const bo_ctx* ctx);
+bo_status bo_synchronize(bo_ctx* ctx);
+
+/* ---- state ------------------------------------------------------------- */
+/* Parameters in model order, flat (all tensors concatenated). */
+bo_status bo_load_params(bo_ctx* ctx, const float* src, int32_t src_on_host);
+bo_status bo_read_params(bo_ctx* ctx, float* dst, int32_t dst_on_host);
+/* LAMB moments of the elements this rank owns, scattered into model-order
+ * flat arrays (elements owned by other ranks are left untouched). */
+bo_status bo_read_moments(bo_ctx* ctx, float* m, float* v, int32_t dst_on_host);
+bo_status bo_get_status(bo_ctx* ctx, bo_step_status* out);
+/* Per-tensor device pointer into the full-replica parameter buffer. */
+bo_status bo_param_ptr(bo_ctx* ctx, int32_t tensor, float** out);
+
+/* ---- hot path ------------------------------------------------------------ */
+/* Feed micro-batch `micro` (0..K-1) of the current optimizer step. grads[p]
+ * is a device pointer to tensor p's binary16 gradient (loss-scaled by the
+ * current scale). Micros 0..K-2 accumulate in fp32. micro == K-1 is the sync
+ * micro: finalize (accumulate + unscale + overflow check + pack into the
+ * fusion buffer) -> reduce-scatter -> sharded LAMB (per-tensor norms, trust
+ * ratio; skipped on overflow) -> loss-scaler update -> all-gather of the
+ * updated parameters. Asynchronous on the context stream. */
+bo_status bo_accumulate(bo_ctx* ctx, int32_t micro, const uint16_t* const* grads);
+
+/* ---- measurement ---------------------------------------------------------- */
+/* Stage timing with CUDA events recorded on the context stream around every
+ * stage of bo_accumulate (off by default). Stages: */
+#define BO_STAGE_ACCUMULATE 0   /* micros 0..K-2 */
+#define BO_STAGE_FINALIZE 1     /* unscale + pack (sync micro) */
+#define BO_STAGE_REDUCE 2       /* reduce-scatter (ring hops or NCCL) */
+#define BO_STAGE_LAMB_NORMS 3   /* LAMB phase 1 */
+#define BO_STAGE_TRUST 4        /* norm reduction, partials all-gather, trust/scaler */
+#define BO_STAGE_LAMB_UPDATE 5  /* LAMB phase 2 */
+#define BO_STAGE_ALLGATHER 6    /* parameter all-gather */
+#define BO_NUM_STAGES 7
+bo_status bo_profile_enable(bo_ctx* ctx, int32_t enable);
+/* Total milliseconds and event count per stage since the last reset; syncs. */
+bo_status bo_profile_read(bo_ctx* ctx, double* stage_ms, int64_t* stage_count, int32_t reset);
+/* Kernels this library has launched on ctx (NCCL kernels not included). */
+int64_t bo_launch_count(const bo_ctx* ctx);
+
+/* ---- operator-level drop-ins -------------------------------------------- */
+/* lamb_step (lamb.cpp:140-201) over device tensors; exact reference numerics
+ * and error behaviour (step incremented first; on a non-finite gradient the
+ * tensors before it are updated and BO_ERR_NON_FINITE_GRADIENT returned). */
+bo_status bo_lamb_step(int32_t n_tensors, const int64_t* numels, float* const* params,
+                       const float* const* grads, float* const* m, float* const* v,
+                       int64_t* step, const bo_lamb_config* cfg, void* stream);
+/* In-place elementwise sum over all ranks of ctx's communicator, reference
+ * fold order, identical bits on every rank. data is a device pointer. */
+bo_status bo_ring_allreduce_f32(bo_ctx* ctx, float* data, size_t n);
+bo_status bo_ring_allreduce_f16_wire(bo_ctx* ctx, float* data, size_t n);
+/* unscale_gradients: BO_ERR_OVERFLOW_DETECTED (and no change) if any entry is
+ * non-finite, else divide by scale when enabled. BO_ERR_INVALID_CONFIG when
+ * scale is not a positive power of two. Device pointer; synchronizes. */
+bo_status bo_unscale_gradients(float* grads, size_t n, float scale, int32_t enabled,
+                               void* stream);
+bo_status bo_narrow_f16(const float* src, uint16_t* dst, size_t n, void* stream);
+bo_status bo_widen_f16(const uint16_t* src, float* dst, size_t n, void* stream);
+float bo_scale_loss(float loss, float scale, int32_t enabled);
+
+/* ---- synthetic workload (bench / test harness utility) ------------------- */
+/* fp16 gradient bits of the synthetic spec
+ * for elements [flat_begin, flat_begin + n) of model-order flat index space,
+ * written to dst (device). */
+bo_status bo_synth_grads(uint16_t* dst, int64_t flat_begin, int64_t n, uint64_t seed,
+                         int32_t rank, int32_t step, int32_t micro, float scale,
+                         uint32_t spike_ppm, int32_t spike_exp, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BERTOPT_B200_H_ */

@@ -268,7 +268,23 @@ class Reference:
                                 C.c_int, _f32p, C.POINTER(_Scaler), C.c_uint64, C.c_uint32, C.c_int,
                                 _i64p, C.c_int, C.c_int, _f32p, _f32p, _f32p, _i64p, _f32p, _i32p,
                                 _f32p, _i32p, C.c_char_p, C.c_int]
+        L.ref_stage_bench.argtypes = [C.c_int, _i64p, _i32p, C.c_int, C.c_int, C.c_uint64, C.c_int,
+                                      C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double),
+                                      C.POINTER(C.c_double), C.c_char_p, C.c_int]
         self._keep = []
+
+    def stage_bench(self, numels, firsts, world, K, bucket_bytes, f16, groups, warmup, steps):
+        """Wall seconds per timed step (max over all threads) and rank-0 stage seconds."""
+        nm = np.asarray(numels, np.int64)
+        fs = np.asarray(firsts, np.int32)
+        secs = (C.c_double * steps)()
+        stages = (C.c_double * 4)()
+        err = C.create_string_buffer(1024)
+        rc = self.lib.ref_stage_bench(len(nm), _ptr(nm, _i64p), _ptr(fs, _i32p), world, K,
+                                      bucket_bytes, int(f16), groups, warmup, steps, secs, stages,
+                                      err, 1024)
+        self._check(rc, err)
+        return list(secs), list(stages)
 
     def _spec(self, spec):
         names = (C.c_char_p * spec.n_tensors)(*[n.encode() for n in spec.names])

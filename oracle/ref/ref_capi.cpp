@@ -14,6 +14,7 @@
 //   ref_train                            trainer.cpp:217-373 (DistributedTrainer::train_step)
 //                                        + the dynamic loss-scaler extension
 #include <algorithm>
+#include <barrier>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -256,6 +257,141 @@ int ref_bucket_layout(const bo_spec_c* spec, const int* firsts, uint64_t bucket_
     return static_cast<int>(L.buckets.size());
   } catch (...) {
     return -map_exception(std::current_exception(), err, errlen);
+  }
+}
+
+// CPU baseline: times the reference's own hot-path stages on a sample of the
+// workload. Per rank (one thread, as the reference runs it):
+//   K-1 accumulate passes          trainer.cpp:240-244 (fp32 tape gradients)
+//   flatten into the fusion buckets trainer.cpp:186-203
+//   ring_allreduce[_f16_wire] per bucket + x 1/world (real, InProcHub)
+//                                  trainer.cpp:205-215, collective.hpp:53-99
+//   unpack + the real lamb_step    trainer.cpp:356-366, lamb.cpp:140-201
+// `groups` independent replicas (groups * world threads) run concurrently so
+// that all host cores are used. seconds[s] is the wall time of timed step s
+// between all-thread barriers; stage_seconds[4] sums rank 0 of group 0's
+// accumulate / flatten / reduce / lamb time over the timed steps.
+int ref_stage_bench(int T, const int64_t* numels, const int* firsts, int world, int K,
+                    uint64_t bucket_bytes, int f16, int groups, int warmup, int steps,
+                    double* seconds, double* stage_seconds, char* err, int errlen) {
+  try {
+    if (world < 1 || K < 1 || groups < 1) throw InvalidConfig("bad bench config");
+    const int nthreads = groups * world;
+    std::vector<std::shared_ptr<InProcHub>> hubs;
+    for (int g = 0; g < groups; ++g) hubs.push_back(std::make_shared<InProcHub>(world));
+    std::barrier<> bar(nthreads);
+    std::vector<std::exception_ptr> errs(static_cast<size_t>(nthreads));
+    std::vector<std::thread> th;
+    using clk = std::chrono::steady_clock;
+    for (int id = 0; id < nthreads; ++id) {
+      th.emplace_back([&, id] {
+        const int grp = id / world, r = id % world;
+        try {
+          std::unique_ptr<InProcTransport> tr;
+          WorkerGroup wg;
+          wg.rank = r;
+          wg.world = world;
+          if (world > 1) {
+            tr = std::make_unique<InProcTransport>(hubs[static_cast<size_t>(grp)], r);
+            tr->set_watchdog(3600.0);
+            wg.transport = tr.get();
+          }
+          Model m;
+          std::vector<std::vector<Tensor>> micro(static_cast<size_t>(K));
+          for (int t = 0; t < T; ++t) {
+            m.names.push_back("t" + std::to_string(t));
+            m.params.push_back(Tensor::randn({numels[t]}, 1000 + static_cast<uint64_t>(t), 0.02f));
+            for (int k = 0; k < K; ++k) {
+              std::vector<float> g(static_cast<size_t>(numels[t]));
+              const uint64_t base = bo_synth_base(1, static_cast<uint64_t>(r), 0, static_cast<uint64_t>(k));
+              for (int64_t i = 0; i < numels[t]; ++i) {
+                g[static_cast<size_t>(i)] = bo_synth_true_grad(base, static_cast<uint64_t>(i), 0, 1);
+              }
+              micro[static_cast<size_t>(k)].push_back(Tensor::from({numels[t]}, std::move(g)));
+            }
+          }
+          std::vector<int> fs(firsts, firsts + T);
+          const BucketLayout L = BucketLayout::build(m, fs, static_cast<size_t>(bucket_bytes));
+          LambState st;
+          LambConfig lc;
+          std::vector<std::vector<float>> accum(static_cast<size_t>(T));
+          std::vector<std::vector<float>> flat(L.buckets.size());
+          const float inv = 1.0f / (static_cast<float>(K) * 1.0f);
+          double acc_s = 0, flat_s = 0, red_s = 0, lamb_s = 0;
+          for (int it = 0; it < warmup + steps; ++it) {
+            bar.arrive_and_wait();
+            const auto t0 = clk::now();
+            for (int k = 0; k + 1 < K; ++k) {  // trainer.cpp:240-244
+              for (int t = 0; t < T; ++t) {
+                const Tensor& g = micro[static_cast<size_t>(k)][static_cast<size_t>(t)];
+                std::vector<float>& a = accum[static_cast<size_t>(t)];
+                if (a.empty()) a.assign(g.data.size(), 0.0f);
+                for (size_t i = 0; i < g.data.size(); ++i) a[i] += g.data[i];
+              }
+            }
+            const auto t1 = clk::now();
+            for (size_t b = 0; b < L.buckets.size(); ++b) flat[b].assign(L.buckets[b].elems, 0.0f);
+            for (int p : L.ready_order) {  // flatten_param, trainer.cpp:186-203
+              const size_t sp = static_cast<size_t>(p);
+              float* dst = flat[static_cast<size_t>(L.bucket_of[sp])].data() + L.offset_of[sp];
+              const float* live = micro[static_cast<size_t>(K - 1)][sp].data.data();
+              const float* summed = accum[sp].empty() ? nullptr : accum[sp].data();
+              for (int64_t i = 0; i < numels[p]; ++i) {
+                float v = live[i];
+                if (summed) v += summed[i];
+                dst[i] = v * inv;
+              }
+            }
+            const auto t2 = clk::now();
+            if (world > 1) {  // reduce_bucket, trainer.cpp:205-215
+              for (size_t b = 0; b < flat.size(); ++b) {
+                const uint32_t tag = static_cast<uint32_t>((it * flat.size() + b) & 0x7fffffffu);
+                if (f16) ring_allreduce_f16_wire(wg, flat[b].data(), flat[b].size(), tag);
+                else ring_allreduce<float>(wg, flat[b].data(), flat[b].size(), tag);
+                const float invn = 1.0f / static_cast<float>(world);
+                for (float& v : flat[b]) v *= invn;
+              }
+            }
+            const auto t3 = clk::now();
+            std::vector<Tensor> gvec(static_cast<size_t>(T));
+            for (int t = 0; t < T; ++t) {  // unpack, trainer.cpp:356-365
+              Tensor g = Tensor::zeros({numels[t]});
+              const std::vector<float>& fb = flat[static_cast<size_t>(L.bucket_of[static_cast<size_t>(t)])];
+              std::copy_n(fb.data() + L.offset_of[static_cast<size_t>(t)], numels[t], g.data.data());
+              gvec[static_cast<size_t>(t)] = std::move(g);
+            }
+            lamb_step(m.params, gvec, st, lc);
+            for (auto& a : accum) a.clear();
+            const auto t4 = clk::now();
+            bar.arrive_and_wait();
+            const auto t5 = clk::now();
+            if (it >= warmup) {
+              if (id == 0) {
+                seconds[it - warmup] = std::chrono::duration<double>(t5 - t0).count();
+                acc_s += std::chrono::duration<double>(t1 - t0).count();
+                flat_s += std::chrono::duration<double>(t2 - t1).count();
+                red_s += std::chrono::duration<double>(t3 - t2).count();
+                lamb_s += std::chrono::duration<double>(t4 - t3).count();
+              }
+            }
+          }
+          if (id == 0) {
+            stage_seconds[0] = acc_s;
+            stage_seconds[1] = flat_s;
+            stage_seconds[2] = red_s;
+            stage_seconds[3] = lamb_s;
+          }
+        } catch (...) {
+          errs[static_cast<size_t>(id)] = std::current_exception();
+          bar.arrive_and_drop();
+        }
+      });
+    }
+    for (auto& t : th) t.join();
+    if (auto e = preferred(errs)) return map_exception(e, err, errlen);
+    return kOk;
+  } catch (...) {
+    return map_exception(std::current_exception(), err, errlen);
   }
 }
 

@@ -1,0 +1,556 @@
+// C ABI of the pipeline context: creation, layout, communication, state, and
+// the hot-path entry point bo_accumulate (see include/bertopt_b200.h).
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+
+#include "bo_internal.hpp"
+
+namespace bo {
+
+namespace {
+thread_local std::string g_last_error;
+}
+
+void fail(bo_status code, const std::string& msg) { throw Failure{code, msg}; }
+void set_thread_error(const std::string& msg) { g_last_error = msg; }
+
+void* dev_alloc(bo_ctx* c, size_t bytes) {
+  void* p = nullptr;
+  if (bytes == 0) bytes = 256;
+  BO_CUDA(cudaMalloc(&p, bytes));
+  BO_CUDA(cudaMemsetAsync(p, 0, bytes, c->stream));
+  c->allocations.push_back(p);
+  c->device_bytes += bytes;
+  return p;
+}
+
+template <typename T>
+static T* upload(bo_ctx* c, const std::vector<T>& v) {
+  T* d = static_cast<T*>(dev_alloc(c, v.size() * sizeof(T)));
+  if (!v.empty()) {
+    BO_CUDA(cudaMemcpyAsync(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, c->stream));
+  }
+  return d;
+}
+
+// Work tables: accumulate/finalize tiles over tensors, LAMB tiles over this
+// rank's shard (split at tensor boundaries), ring tiles over the shard.
+void upload_tables(bo_ctx* c) {
+  const Layout& L = c->L;
+  std::vector<TensorDev> td(static_cast<size_t>(L.T));
+  std::vector<AccTile> acc_tiles;
+  for (int t = 0; t < L.T; ++t) {
+    td[static_cast<size_t>(t)] = TensorDev{L.acc_off[static_cast<size_t>(t)], L.flat_off[static_cast<size_t>(t)]};
+    for (int64_t e = 0; e < L.numel[static_cast<size_t>(t)]; e += kTileElems) {
+      const int64_t len = std::min<int64_t>(kTileElems, L.numel[static_cast<size_t>(t)] - e);
+      acc_tiles.push_back(AccTile{t, static_cast<int32_t>(len), e});
+    }
+  }
+  std::vector<LambTile> lamb_tiles;
+  std::vector<int> tile_begin(static_cast<size_t>(L.T) + 1, 0);
+  std::vector<std::vector<LambTile>> per_tensor(static_cast<size_t>(L.T));
+  std::vector<HopTile> hop_tiles;
+  const int q = c->rank;  // owned chunk
+  for (int b = 0; b < L.B; ++b) {
+    const int64_t cb = L.chunk[static_cast<size_t>(b)];
+    const int64_t lo = q * cb;
+    const int64_t hi = std::min<int64_t>((q + 1) * cb, L.elems[static_cast<size_t>(b)]);
+    for (int p : L.buckets[static_cast<size_t>(b)]) {
+      const int64_t t0 = L.offset_of[static_cast<size_t>(p)];
+      const int64_t t1 = t0 + L.numel[static_cast<size_t>(p)];
+      const int64_t a = std::max(lo, t0), z = std::min(hi, t1);
+      for (int64_t e = a; e < z; e += kTileElems) {
+        const int64_t len = std::min<int64_t>(kTileElems, z - e);
+        per_tensor[static_cast<size_t>(p)].push_back(
+            LambTile{L.shoff[static_cast<size_t>(b)] + (e - lo), L.base[static_cast<size_t>(b)] + e,
+                     static_cast<int32_t>(len), p});
+      }
+    }
+    for (int64_t e = 0; e < cb; e += kTileElems) {
+      const int64_t len = std::min<int64_t>(kTileElems, cb - e);
+      hop_tiles.push_back(HopTile{L.shoff[static_cast<size_t>(b)] + e, static_cast<int32_t>(len), b});
+    }
+  }
+  // Tiles grouped per tensor so each tensor's partials are contiguous; within
+  // a tensor, shard order.
+  for (int t = 0; t < L.T; ++t) {
+    tile_begin[static_cast<size_t>(t)] = static_cast<int>(lamb_tiles.size());
+    for (const LambTile& lt : per_tensor[static_cast<size_t>(t)]) lamb_tiles.push_back(lt);
+  }
+  tile_begin[static_cast<size_t>(L.T)] = static_cast<int>(lamb_tiles.size());
+  std::vector<int64_t> geo;
+  geo.insert(geo.end(), L.base.begin(), L.base.end());
+  geo.insert(geo.end(), L.chunk.begin(), L.chunk.end());
+  geo.insert(geo.end(), L.shoff.begin(), L.shoff.end());
+
+  c->d_tensors = upload(c, td);
+  c->d_acc_tiles = upload(c, acc_tiles);
+  c->n_acc_tiles = static_cast<int>(acc_tiles.size());
+  c->d_lamb_tiles = upload(c, lamb_tiles);
+  c->n_lamb_tiles = static_cast<int>(lamb_tiles.size());
+  c->d_tensor_tile_begin = upload(c, tile_begin);
+  c->d_hop_tiles = upload(c, hop_tiles);
+  c->n_hop_tiles = static_cast<int>(hop_tiles.size());
+  c->d_bucket_geo = upload(c, geo);
+}
+
+// Bias corrections bc_t = 1 - pow(double(beta), double(t)) evaluated on the
+// host with the same libm the reference uses (lamb.cpp:158-161), with their
+// reciprocals; the device indexes the table by its own step counter.
+void grow_bc_table(bo_ctx* c, int64_t need) {
+  if (need <= c->bc_cap) return;
+  int64_t cap = std::max<int64_t>(4096, c->bc_cap * 2);
+  while (cap < need) cap *= 2;
+  std::vector<double> tab(static_cast<size_t>(cap) * 4);
+  for (int64_t i = 0; i < cap; ++i) {
+    const double t = static_cast<double>(i + 1);
+    const double bc1 = 1.0 - std::pow(static_cast<double>(c->cfg.lamb.beta1), t);
+    const double bc2 = 1.0 - std::pow(static_cast<double>(c->cfg.lamb.beta2), t);
+    tab[static_cast<size_t>(4 * i)] = bc1;
+    tab[static_cast<size_t>(4 * i + 1)] = bc2;
+    tab[static_cast<size_t>(4 * i + 2)] = 1.0 / bc1;
+    tab[static_cast<size_t>(4 * i + 3)] = 1.0 / bc2;
+  }
+  double* d = nullptr;
+  BO_CUDA(cudaMalloc(&d, tab.size() * sizeof(double)));
+  BO_CUDA(cudaMemcpyAsync(d, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  // The old table may still be read by queued kernels: keep it alive.
+  if (c->bc_table) c->allocations.push_back(c->bc_table);
+  BO_CUDA(cudaStreamSynchronize(c->stream));  // tab is pageable host memory
+  c->bc_table = d;
+  c->bc_cap = cap;
+}
+
+static cudaEvent_t take_event(bo_ctx* c) {
+  if (!c->event_pool.empty()) {
+    cudaEvent_t e = c->event_pool.back();
+    c->event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  BO_CUDA(cudaEventCreate(&e));
+  return e;
+}
+
+StageTimer::StageTimer(bo_ctx* ctx, int s) : c(ctx), stage(s) {
+  if (!c->profiling) return;
+  b = take_event(c);
+  BO_CUDA(cudaEventRecord(b, c->stream));
+}
+
+StageTimer::~StageTimer() {
+  if (!c->profiling || !b) return;
+  cudaEvent_t e = take_event(c);
+  if (cudaEventRecord(e, c->stream) == cudaSuccess) c->marks.push_back({stage, b, e});
+}
+
+static void drain_marks(bo_ctx* c) {
+  BO_CUDA(cudaStreamSynchronize(c->stream));
+  for (const auto& mk : c->marks) {
+    float ms = 0.0f;
+    BO_CUDA(cudaEventElapsedTime(&ms, mk.a, mk.b));
+    c->stage_ms[mk.stage] += ms;
+    c->stage_count[mk.stage] += 1;
+    c->event_pool.push_back(mk.a);
+    c->event_pool.push_back(mk.b);
+  }
+  c->marks.clear();
+}
+
+static bool is_pow2(float s) {
+  if (!(s > 0.0f) || !std::isfinite(s)) return false;
+  int e = 0;
+  return std::frexp(s, &e) == 0.5f;
+}
+
+static uint64_t fnv1a(const void* data, size_t len, uint64_t h) {
+  const auto* p = static_cast<const uint8_t*>(data);
+  for (size_t i = 0; i < len; ++i) h = (h ^ p[i]) * 1099511628211ull;
+  return h;
+}
+
+// BucketLayout::hash (trainer.cpp:118-134) salted like ensure_layout
+// (trainer.cpp:165-168). Without names, the tensor index stands in.
+static uint64_t layout_hash(const Layout& L, const char* const* names, const int32_t* ndims,
+                            const int64_t* dims, bool f16, int K) {
+  std::vector<size_t> doff(static_cast<size_t>(L.T) + 1, 0);
+  if (ndims) {
+    for (int t = 0; t < L.T; ++t) doff[static_cast<size_t>(t) + 1] = doff[static_cast<size_t>(t)] + static_cast<size_t>(ndims[t]);
+  }
+  uint64_t h = fnv1a("bucket-layout", 13, 14695981039346656037ull);
+  const uint64_t nb = static_cast<uint64_t>(L.B);
+  h = fnv1a(&nb, 8, h);
+  for (int b = 0; b < L.B; ++b) {
+    for (int p : L.buckets[static_cast<size_t>(b)]) {
+      if (names) {
+        h = fnv1a(names[p], std::strlen(names[p]), h);
+      } else {
+        const int64_t id = p;
+        h = fnv1a(&id, 8, h);
+      }
+      if (ndims && dims) {
+        for (size_t d = doff[static_cast<size_t>(p)]; d < doff[static_cast<size_t>(p) + 1]; ++d) h = fnv1a(&dims[d], 8, h);
+      } else {
+        h = fnv1a(&L.numel[static_cast<size_t>(p)], 8, h);
+      }
+    }
+    const uint64_t el = static_cast<uint64_t>(L.elems[static_cast<size_t>(b)]);
+    h = fnv1a(&el, 8, h);
+  }
+  const bool f16b = f16;
+  h = fnv1a(&f16b, sizeof(bool), h);
+  const uint64_t salt = static_cast<uint64_t>(K);
+  return fnv1a(&salt, 8, h);
+}
+
+static void validate(const bo_trainer_config& c) {
+  if (c.accumulation < 1) fail(BO_ERR_INVALID_CONFIG, "accumulation must be >= 1");
+  if (c.bucket_bytes == 0) fail(BO_ERR_INVALID_CONFIG, "bucket_bytes must be > 0");
+  const bo_scaler_config& s = c.scaler;
+  if (!is_pow2(s.init_scale)) fail(BO_ERR_INVALID_CONFIG, "loss scale must be a positive power of two");
+  if (s.dynamic) {
+    if (!is_pow2(s.min_scale) || !is_pow2(s.max_scale) || s.min_scale > s.max_scale ||
+        !is_pow2(s.growth_factor) || !is_pow2(s.backoff_factor) || s.growth_interval < 1) {
+      fail(BO_ERR_INVALID_CONFIG, "dynamic scaler needs power-of-two bounds/factors and interval >= 1");
+    }
+  }
+  if (c.reduce_algo < 0 || c.reduce_algo > BO_REDUCE_NCCL) fail(BO_ERR_INVALID_CONFIG, "bad reduce_algo");
+  if (c.reduce_algo == BO_REDUCE_NCCL && c.f16_exchange) {
+    fail(BO_ERR_INVALID_CONFIG, "the binary16 wire needs the ring reduction (NCCL half sums differ)");
+  }
+}
+
+}  // namespace bo
+
+using namespace bo;
+
+#define BO_GUARD_BEGIN try {
+#define BO_GUARD_END                          \
+  }                                           \
+  catch (const Failure& f) {                  \
+    set_thread_error(f.msg);                  \
+    return f.code;                            \
+  }                                           \
+  catch (const std::exception& e) {           \
+    set_thread_error(e.what());               \
+    return BO_ERR_CUDA;                       \
+  }                                           \
+  return BO_OK;
+
+extern "C" {
+
+int32_t bo_abi_version(void) { return BO_ABI_VERSION; }
+
+const char* bo_status_name(int32_t s) {
+  switch (s) {
+    case BO_OK: return "OK";
+    case BO_ERR_SHAPE_MISMATCH: return "ShapeMismatch";
+    case BO_ERR_NON_FINITE_GRADIENT: return "NonFiniteGradient";
+    case BO_ERR_OVERFLOW_DETECTED: return "OverflowDetected";
+    case BO_ERR_LENGTH_MISMATCH: return "LengthMismatch";
+    case BO_ERR_INVALID_CONFIG: return "InvalidConfig";
+    case BO_ERR_BUCKET_LAYOUT_MISMATCH: return "BucketLayoutMismatch";
+    case BO_ERR_PEER_DISCONNECTED: return "PeerDisconnected";
+    case BO_ERR_WATCHDOG_TIMEOUT: return "WatchdogTimeout";
+    case BO_ERR_PROTOCOL: return "ProtocolError";
+    case BO_ERR_CUDA: return "CudaError";
+    case BO_ERR_NCCL: return "NcclError";
+    case BO_ERR_NO_DEVICE: return "NoDevice";
+    default: return "Unknown";
+  }
+}
+
+const char* bo_last_error(void) { return g_last_error.c_str(); }
+
+void bo_default_config(bo_trainer_config* cfg) {
+  std::memset(cfg, 0, sizeof(*cfg));
+  cfg->lamb = bo_lamb_config{1e-3f, 0.9f, 0.999f, 1e-6f, 0.01f, 10.0f};  // lamb.hpp:165-172
+  cfg->accumulation = 1;
+  cfg->bucket_bytes = 4ull << 20;  // trainer.hpp:78
+  cfg->f16_exchange = 0;
+  cfg->reduce_algo = BO_REDUCE_AUTO;
+  cfg->scaler = bo_scaler_config{65536.0f, 2.0f, 0.5f, 1.0f, 16777216.0f, 2000, 1};
+}
+
+bo_status bo_create(const bo_trainer_config* cfg, int32_t n_tensors, const int64_t* numels,
+                    const int32_t* first_consumers, const char* const* names, const int32_t* ndims,
+                    const int64_t* dims, int32_t device, int32_t rank, int32_t world, bo_ctx** out) {
+  bo_ctx* c = nullptr;
+  BO_GUARD_BEGIN
+  *out = nullptr;
+  if (!cfg || !numels || !first_consumers) fail(BO_ERR_INVALID_CONFIG, "null argument");
+  validate(*cfg);
+  if (n_tensors > kMaxTensors) fail(BO_ERR_INVALID_CONFIG, "more than 1024 tensors");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    fail(BO_ERR_NO_DEVICE, "no CUDA device visible");
+  }
+  c = new bo_ctx();
+  c->cfg = *cfg;
+  c->device = device;
+  c->rank = rank;
+  c->world = world;
+  c->algo = cfg->reduce_algo == BO_REDUCE_AUTO ? (cfg->f16_exchange ? BO_REDUCE_RING : BO_REDUCE_NCCL)
+                                               : cfg->reduce_algo;
+  BO_CUDA(cudaSetDevice(device));
+  BO_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  c->own_stream = true;
+  c->L = Layout::build(n_tensors, numels, first_consumers, cfg->bucket_bytes, world, rank);
+  c->L.hash = layout_hash(c->L, names, ndims, dims, cfg->f16_exchange != 0, cfg->accumulation);
+  const Layout& L = c->L;
+  c->lamb = LambConsts{cfg->lamb.beta1, cfg->lamb.beta2, 1.0f - cfg->lamb.beta1, 1.0f - cfg->lamb.beta2,
+                       cfg->lamb.eps, cfg->lamb.weight_decay, cfg->lamb.lr, cfg->lamb.trust_clip};
+  c->scaler = ScalerConsts{cfg->scaler.growth_factor, cfg->scaler.backoff_factor, cfg->scaler.min_scale,
+                           cfg->scaler.max_scale, cfg->scaler.growth_interval, cfg->scaler.dynamic};
+  upload_tables(c);
+  c->acc = static_cast<float*>(dev_alloc(c, static_cast<size_t>(L.acc_total) * 4));
+  c->x = static_cast<float*>(dev_alloc(c, static_cast<size_t>(L.flat_total) * 4));
+  c->gshard = world == 1 ? c->x : static_cast<float*>(dev_alloc(c, static_cast<size_t>(L.shard_total) * 4));
+  c->w = static_cast<float*>(dev_alloc(c, static_cast<size_t>(L.flat_total) * 4));
+  c->m = static_cast<float*>(dev_alloc(c, static_cast<size_t>(L.shard_total) * 4));
+  c->v = static_cast<float*>(dev_alloc(c, static_cast<size_t>(L.shard_total) * 4));
+  if (world > 1 && c->algo == BO_REDUCE_RING) {
+    const size_t e = cfg->f16_exchange ? 2 : 4;
+    c->wire[0] = dev_alloc(c, static_cast<size_t>(L.shard_total) * e);
+    c->wire[1] = dev_alloc(c, static_cast<size_t>(L.shard_total) * e);
+  }
+  c->tile_part = static_cast<double*>(dev_alloc(c, static_cast<size_t>(std::max(c->n_lamb_tiles, 1)) * 16));
+  c->rank_part = static_cast<double*>(dev_alloc(c, static_cast<size_t>(2 * L.T + 1) * 8));
+  c->all_part = world == 1 ? c->rank_part
+                           : static_cast<double*>(dev_alloc(c, static_cast<size_t>(world) * (2 * L.T + 1) * 8));
+  c->trust = static_cast<float*>(dev_alloc(c, static_cast<size_t>(L.T) * 4));
+  c->state = static_cast<DevState*>(dev_alloc(c, sizeof(DevState)));
+  DevState st{};
+  st.scale = cfg->scaler.init_scale;
+  BO_CUDA(cudaMemcpyAsync(c->state, &st, sizeof(st), cudaMemcpyHostToDevice, c->stream));
+  grow_bc_table(c, 16);
+  BO_CUDA(cudaStreamSynchronize(c->stream));
+  *out = c;
+  c = nullptr;
+  }
+  catch (const Failure& f) {
+    set_thread_error(f.msg);
+    if (c) bo_destroy(c);
+    return f.code;
+  }
+  return BO_OK;
+}
+
+void bo_destroy(bo_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  for (const auto& mk : c->marks) {
+    cudaEventDestroy(mk.a);
+    cudaEventDestroy(mk.b);
+  }
+  for (cudaEvent_t e : c->event_pool) cudaEventDestroy(e);
+  if (c->comm) ncclCommDestroy(c->comm);
+  for (void* p : c->allocations) cudaFree(p);
+  if (c->bc_table) cudaFree(c->bc_table);
+  if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+int32_t bo_layout_num_buckets(const bo_ctx* c) { return c ? c->L.B : 0; }
+
+bo_status bo_layout_query(const bo_ctx* c, int32_t* bucket_of, int64_t* offset_of, int32_t* ready_order,
+                          int64_t* bucket_elems) {
+  BO_GUARD_BEGIN
+  if (!c) fail(BO_ERR_INVALID_CONFIG, "null ctx");
+  for (int t = 0; t < c->L.T; ++t) {
+    if (bucket_of) bucket_of[t] = c->L.bucket_of[static_cast<size_t>(t)];
+    if (offset_of) offset_of[t] = c->L.offset_of[static_cast<size_t>(t)];
+    if (ready_order) ready_order[t] = c->L.ready[static_cast<size_t>(t)];
+  }
+  if (bucket_elems) {
+    for (int b = 0; b < c->L.B; ++b) bucket_elems[b] = c->L.elems[static_cast<size_t>(b)];
+  }
+  BO_GUARD_END
+}
+
+uint64_t bo_layout_hash(const bo_ctx* c) { return c ? c->L.hash : 0; }
+int64_t bo_shard_elems(const bo_ctx* c) {
+  if (!c) return 0;
+  int64_t s = 0;
+  for (int b = 0; b < c->L.B; ++b) s += c->L.chunk[static_cast<size_t>(b)];
+  return s;
+}
+uint64_t bo_device_bytes(const bo_ctx* c) { return c ? c->device_bytes : 0; }
+
+bo_status bo_comm_unique_id(uint8_t* out128) {
+  BO_GUARD_BEGIN
+  static_assert(sizeof(ncclUniqueId) == 128, "nccl id size");
+  ncclUniqueId id;
+  BO_NCCL(ncclGetUniqueId(&id));
+  std::memcpy(out128, &id, 128);
+  BO_GUARD_END
+}
+
+bo_status bo_comm_init(bo_ctx* c, const uint8_t* id128) {
+  BO_GUARD_BEGIN
+  if (!c) fail(BO_ERR_INVALID_CONFIG, "null ctx");
+  if (c->world == 1) return BO_OK;
+  BO_CUDA(cudaSetDevice(c->device));
+  ncclUniqueId id;
+  std::memcpy(&id, id128, 128);
+  BO_NCCL(ncclCommInitRank(&c->comm, c->world, id, c->rank));
+  // Layout agreement (trainer.cpp:169-183): all-gather the salted hash.
+  uint64_t* d = static_cast<uint64_t*>(dev_alloc(c, static_cast<size_t>(c->world + 1) * 8));
+  BO_CUDA(cudaMemcpyAsync(d, &c->L.hash, 8, cudaMemcpyHostToDevice, c->stream));
+  BO_NCCL(ncclAllGather(d, d + 1, 1, ncclUint64, c->comm, c->stream));
+  std::vector<uint64_t> all(static_cast<size_t>(c->world));
+  BO_CUDA(cudaMemcpyAsync(all.data(), d + 1, all.size() * 8, cudaMemcpyDeviceToHost, c->stream));
+  BO_CUDA(cudaStreamSynchronize(c->stream));
+  for (uint64_t h : all) {
+    if (h != c->L.hash) {
+      fail(BO_ERR_BUCKET_LAYOUT_MISMATCH,
+           "rank " + std::to_string(c->rank) + " bucket layout disagrees with peers");
+    }
+  }
+  BO_GUARD_END
+}
+
+bo_status bo_set_stream(bo_ctx* c, void* s) {
+  BO_GUARD_BEGIN
+  if (!c) fail(BO_ERR_INVALID_CONFIG, "null ctx");
+  BO_CUDA(cudaStreamSynchronize(c->stream));
+  if (c->own_stream) BO_CUDA(cudaStreamDestroy(c->stream));
+  if (s) {
+    c->stream = static_cast<cudaStream_t>(s);
+    c->own_stream = false;
+  } else {
+    BO_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    c->own_stream = true;
+  }
+  BO_GUARD_END
+}
+
+void* bo_get_stream(const bo_ctx* c) { return c ? c->stream : nullptr; }
+
+bo_status bo_synchronize(bo_ctx* c) {
+  BO_GUARD_BEGIN
+  BO_CUDA(cudaStreamSynchronize(c->stream));
+  BO_GUARD_END
+}
+
+bo_status bo_load_params(bo_ctx* c, const float* src, int32_t on_host) {
+  BO_GUARD_BEGIN
+  const Layout& L = c->L;
+  const cudaMemcpyKind k = on_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+  for (int t = 0; t < L.T; ++t) {
+    BO_CUDA(cudaMemcpyAsync(c->w + L.flat_off[static_cast<size_t>(t)], src + L.model_off[static_cast<size_t>(t)],
+                            static_cast<size_t>(L.numel[static_cast<size_t>(t)]) * 4, k, c->stream));
+  }
+  BO_CUDA(cudaStreamSynchronize(c->stream));
+  BO_GUARD_END
+}
+
+bo_status bo_read_params(bo_ctx* c, float* dst, int32_t on_host) {
+  BO_GUARD_BEGIN
+  const Layout& L = c->L;
+  const cudaMemcpyKind k = on_host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+  for (int t = 0; t < L.T; ++t) {
+    BO_CUDA(cudaMemcpyAsync(dst + L.model_off[static_cast<size_t>(t)], c->w + L.flat_off[static_cast<size_t>(t)],
+                            static_cast<size_t>(L.numel[static_cast<size_t>(t)]) * 4, k, c->stream));
+  }
+  BO_CUDA(cudaStreamSynchronize(c->stream));
+  BO_GUARD_END
+}
+
+bo_status bo_read_moments(bo_ctx* c, float* m, float* v, int32_t on_host) {
+  BO_GUARD_BEGIN
+  const Layout& L = c->L;
+  const cudaMemcpyKind k = on_host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+  const int q = c->rank;
+  for (int b = 0; b < L.B; ++b) {
+    const int64_t cb = L.chunk[static_cast<size_t>(b)];
+    const int64_t lo = q * cb, hi = std::min<int64_t>((q + 1) * cb, L.elems[static_cast<size_t>(b)]);
+    for (int p : L.buckets[static_cast<size_t>(b)]) {
+      const int64_t t0 = L.offset_of[static_cast<size_t>(p)], t1 = t0 + L.numel[static_cast<size_t>(p)];
+      const int64_t a = std::max(lo, t0), z = std::min(hi, t1);
+      if (a >= z) continue;
+      const int64_t s = L.shoff[static_cast<size_t>(b)] + (a - lo);
+      const int64_t dsti = L.model_off[static_cast<size_t>(p)] + (a - t0);
+      BO_CUDA(cudaMemcpyAsync(m + dsti, c->m + s, static_cast<size_t>(z - a) * 4, k, c->stream));
+      BO_CUDA(cudaMemcpyAsync(v + dsti, c->v + s, static_cast<size_t>(z - a) * 4, k, c->stream));
+    }
+  }
+  BO_CUDA(cudaStreamSynchronize(c->stream));
+  BO_GUARD_END
+}
+
+bo_status bo_get_status(bo_ctx* c, bo_step_status* out) {
+  BO_GUARD_BEGIN
+  DevState st;
+  BO_CUDA(cudaMemcpyAsync(&st, c->state, sizeof(st), cudaMemcpyDeviceToHost, c->stream));
+  BO_CUDA(cudaStreamSynchronize(c->stream));
+  out->loss_scale = st.scale;
+  out->good_steps = st.good;
+  out->lamb_step = st.lamb_step;
+  out->steps = st.steps;
+  out->skipped_steps = st.skipped;
+  out->found_inf = st.found_inf;
+  out->reserved = 0;
+  BO_GUARD_END
+}
+
+bo_status bo_param_ptr(bo_ctx* c, int32_t t, float** out) {
+  BO_GUARD_BEGIN
+  if (t < 0 || t >= c->L.T) fail(BO_ERR_SHAPE_MISMATCH, "tensor index out of range");
+  *out = c->w + c->L.flat_off[static_cast<size_t>(t)];
+  BO_GUARD_END
+}
+
+bo_status bo_profile_enable(bo_ctx* c, int32_t enable) {
+  BO_GUARD_BEGIN
+  if (!c) fail(BO_ERR_INVALID_CONFIG, "null ctx");
+  c->profiling = enable != 0;
+  BO_GUARD_END
+}
+
+bo_status bo_profile_read(bo_ctx* c, double* stage_ms, int64_t* stage_count, int32_t reset) {
+  BO_GUARD_BEGIN
+  if (!c) fail(BO_ERR_INVALID_CONFIG, "null ctx");
+  drain_marks(c);
+  for (int s = 0; s < BO_NUM_STAGES; ++s) {
+    if (stage_ms) stage_ms[s] = c->stage_ms[s];
+    if (stage_count) stage_count[s] = c->stage_count[s];
+    if (reset) {
+      c->stage_ms[s] = 0.0;
+      c->stage_count[s] = 0;
+    }
+  }
+  BO_GUARD_END
+}
+
+int64_t bo_launch_count(const bo_ctx* c) { return c ? c->launches : 0; }
+
+bo_status bo_accumulate(bo_ctx* c, int32_t micro, const uint16_t* const* grads) {
+  BO_GUARD_BEGIN
+  if (!c || !grads) fail(BO_ERR_INVALID_CONFIG, "null argument");
+  const int K = c->cfg.accumulation;
+  if (micro < 0 || micro >= K) fail(BO_ERR_INVALID_CONFIG, "micro index outside [0, K)");
+  if (c->world > 1 && !c->comm) fail(BO_ERR_INVALID_CONFIG, "bo_comm_init has not run");
+  PtrTable tab;
+  bool aligned = true;
+  for (int t = 0; t < c->L.T; ++t) {
+    tab.p[t] = grads[t];
+    if (!grads[t]) fail(BO_ERR_SHAPE_MISMATCH, "null gradient for tensor " + std::to_string(t));
+    aligned &= (reinterpret_cast<uintptr_t>(grads[t]) & 15u) == 0;
+  }
+  if (micro + 1 < K) {
+    launch_accumulate(c, micro, tab, aligned);
+    return BO_OK;
+  }
+  grow_bc_table(c, c->calls + 2);
+  launch_finalize(c, tab);
+  run_reduce(c);
+  run_lamb(c);
+  run_allgather(c);
+  c->calls += 1;
+  BO_GUARD_END
+}
+
+}  // extern "C"

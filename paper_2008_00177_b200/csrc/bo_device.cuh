@@ -1,0 +1,58 @@
+// Device helpers shared by the pipeline and the operator-level kernels.
+// All float arithmetic is explicitly round-to-nearest (no FMA contraction):
+// the reference is compiled without FMA (proj/CMakeLists.txt:13-14).
+#ifndef BO_DEVICE_CUH_
+#define BO_DEVICE_CUH_
+
+#include <cuda_fp16.h>
+
+#include "bo_internal.hpp"
+
+namespace bo {
+
+__device__ __forceinline__ float widen(uint16_t h) { return __half2float(__ushort_as_half(h)); }
+__device__ __forceinline__ uint16_t narrow(float x) { return __half_as_ushort(__float2half_rn(x)); }
+
+__device__ __forceinline__ bool finite(float x) { return fabsf(x) <= 3.402823466e38f; }
+
+// float(double(x) / d) with the reference's double rounding (lamb.cpp:185-186),
+// computed as a multiply by the host-rounded reciprocal. The product is within
+// ~3 double ulps of RN_d(x/d); only when it lies that close to a binary32
+// rounding midpoint (or in the binary32 subnormal range) can the two round to
+// different floats, and then the exact IEEE division is used instead.
+__device__ __forceinline__ float div_to_float(float x, double d, double inv_d) {
+  double q = __dmul_rn(static_cast<double>(x), inv_d);
+  const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(q));
+  const int low = static_cast<int>(b & 0x1FFFFFFFull) - 0x10000000;
+  const unsigned e = static_cast<unsigned>((b >> 52) & 0x7FF);
+  if (e < 898u || (low >= -16 && low <= 16)) q = __ddiv_rn(static_cast<double>(x), d);
+  return __double2float_rn(q);
+}
+
+struct Moments {
+  float m, v, u;
+};
+
+// One element of lamb_step's fused loop (lamb.cpp:183-187), operation order kept.
+__device__ __forceinline__ Moments lamb_elem(float g, float w, float m, float v, const LambConsts& c,
+                                             const double* bc) {
+  Moments o;
+  o.m = __fadd_rn(__fmul_rn(c.beta1, m), __fmul_rn(c.omb1, g));
+  o.v = __fadd_rn(__fmul_rn(c.beta2, v), __fmul_rn(__fmul_rn(c.omb2, g), g));
+  const float mh = div_to_float(o.m, bc[0], bc[2]);
+  const float vh = div_to_float(o.v, bc[1], bc[3]);
+  const float den = __fadd_rn(__fsqrt_rn(vh), c.eps);
+  o.u = __fadd_rn(__fdiv_rn(mh, den), __fmul_rn(c.wd, w));
+  return o;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+
+}  // namespace bo
+
+#endif  // BO_DEVICE_CUH_

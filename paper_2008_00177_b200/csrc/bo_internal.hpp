@@ -1,0 +1,195 @@
+// Internal declarations of the B200 gradient-to-update pipeline.
+#ifndef BO_INTERNAL_HPP_
+#define BO_INTERNAL_HPP_
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "bertopt_b200.h"
+
+namespace bo {
+
+constexpr int kMaxTensors = 1024;     // per-micro pointer table travels as a kernel parameter
+constexpr int kTileElems = 4096;      // elements per CTA work tile
+constexpr int kAlignElems = 64;       // 256-byte alignment of every buffer region
+constexpr int kThreads = 256;
+
+// Thrown inside the library, turned into a bo_status at the C boundary.
+struct Failure {
+  bo_status code;
+  std::string msg;
+};
+
+[[noreturn]] void fail(bo_status code, const std::string& msg);
+void set_thread_error(const std::string& msg);
+
+#define BO_CUDA(expr)                                                          \
+  do {                                                                         \
+    cudaError_t e_ = (expr);                                                   \
+    if (e_ != cudaSuccess)                                                     \
+      ::bo::fail(BO_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+#define BO_NCCL(expr)                                                          \
+  do {                                                                         \
+    ncclResult_t r_ = (expr);                                                  \
+    if (r_ != ncclSuccess)                                                     \
+      ::bo::fail(BO_ERR_NCCL, std::string(#expr) + ": " + ncclGetErrorString(r_)); \
+  } while (0)
+
+inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+// ---------------------------------------------------------------- layout
+// Fusion-buffer layout (restates BucketLayout::build, trainer.cpp:73-116)
+// plus the HBM placement of every device buffer:
+//   flat  : bucket b at base[b], N*chunk[b] elements (reference zero padding,
+//           collective.hpp:58-60); tensor p at base[bucket_of[p]] + offset_of[p]
+//   shard : rank r owns chunk r of every bucket, concatenated at shoff[b]
+//   acc   : per-tensor fp32 accumulators at acc_off[p] (model order)
+struct Layout {
+  int T = 0, B = 0, N = 1, rank = 0;
+  std::vector<int64_t> numel;
+  std::vector<int> bucket_of, ready;
+  std::vector<int64_t> offset_of;
+  std::vector<std::vector<int>> buckets;
+  std::vector<int64_t> elems, chunk, base, shoff;
+  std::vector<int64_t> flat_off, acc_off, model_off;
+  int64_t flat_total = 0, shard_total = 0, acc_total = 0, P = 0;
+  uint64_t hash = 0;
+
+  static Layout build(int T, const int64_t* numel, const int32_t* firsts, uint64_t bucket_bytes,
+                      int world, int rank);
+};
+
+// Work tiles (device tables, built once per context).
+struct AccTile {        // a slice of one tensor, model order
+  int32_t t;
+  int32_t len;
+  int64_t e0;           // element offset inside the tensor
+};
+struct LambTile {       // a slice of one tensor inside this rank's shard
+  int64_t s0;           // shard index of the first element
+  int64_t w0;           // flat index of the first element
+  int32_t len;
+  int32_t t;
+};
+struct HopTile {        // a slice of one bucket's chunk in shard space
+  int64_t s0;
+  int32_t len;
+  int32_t b;
+};
+
+// Per-tensor constants used by the accumulate / finalize kernels.
+struct TensorDev {
+  int64_t acc_off;
+  int64_t flat_off;
+};
+
+// Device-resident optimizer / scaler state (one per rank, replicated values).
+struct DevState {
+  float scale;
+  int32_t good;
+  int64_t lamb_step;
+  int64_t steps;
+  int64_t skipped;
+  int32_t found_inf;
+  int32_t do_update;
+  int32_t local_flag;   // set by LAMB phase 1 on this rank
+  int32_t pad;
+  double bc1, bc2, ibc1, ibc2;   // bias corrections of the current LAMB step
+};
+
+struct LambConsts {
+  float beta1, beta2, omb1, omb2, eps, wd, lr, clip;
+};
+
+struct ScalerConsts {
+  float growth, backoff, min_scale, max_scale;
+  int32_t interval, dynamic;
+};
+
+struct PtrTable {
+  const uint16_t* p[kMaxTensors];
+};
+
+}  // namespace bo
+
+struct bo_ctx {
+  bo_trainer_config cfg{};
+  int device = 0, rank = 0, world = 1, algo = BO_REDUCE_NCCL;
+  bo::Layout L;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  ncclComm_t comm = nullptr;
+
+  // device tables
+  bo::TensorDev* d_tensors = nullptr;
+  bo::AccTile* d_acc_tiles = nullptr;
+  int n_acc_tiles = 0;
+  bo::LambTile* d_lamb_tiles = nullptr;
+  int n_lamb_tiles = 0;
+  int* d_tensor_tile_begin = nullptr;   // [T+1] lamb-tile ranges per tensor
+  bo::HopTile* d_hop_tiles = nullptr;
+  int n_hop_tiles = 0;
+  int64_t* d_bucket_geo = nullptr;      // [3][B]: base, chunk, shoff
+
+  // device buffers
+  float* acc = nullptr;
+  float* x = nullptr;        // finalized local gradients, flat layout
+  float* gshard = nullptr;   // reduced gradient shard (aliases x when world == 1)
+  float* w = nullptr;        // full parameter replica, flat layout
+  float* m = nullptr;
+  float* v = nullptr;
+  void* wire[3] = {nullptr, nullptr, nullptr};  // ring staging (shard-sized)
+  double* tile_part = nullptr;    // [n_lamb_tiles][2]
+  double* rank_part = nullptr;    // [2T+1]
+  double* all_part = nullptr;     // [world][2T+1]
+  float* trust = nullptr;         // [T]
+  bo::DevState* state = nullptr;
+  double* bc_table = nullptr;     // [bc_cap][4] (bc1, bc2, 1/bc1, 1/bc2) for steps 1..cap
+  int64_t bc_cap = 0;
+  int64_t calls = 0;              // sync micros issued (upper bound of lamb_step)
+  uint64_t device_bytes = 0;
+
+  bo::LambConsts lamb{};
+  bo::ScalerConsts scaler{};
+  std::vector<void*> allocations;
+  // measurement
+  bool profiling = false;
+  int64_t launches = 0;
+  struct Mark { int stage; cudaEvent_t a, b; };
+  std::vector<Mark> marks;
+  std::vector<cudaEvent_t> event_pool;
+  double stage_ms[BO_NUM_STAGES] = {};
+  int64_t stage_count[BO_NUM_STAGES] = {};
+  std::vector<bool> ptr_aligned_cache;
+};
+
+namespace bo {
+void* dev_alloc(bo_ctx* c, size_t bytes);
+void upload_tables(bo_ctx* c);
+void grow_bc_table(bo_ctx* c, int64_t need);
+
+// kernels / pipeline stages (bo_pipeline.cu)
+void launch_accumulate(bo_ctx* c, int micro, const PtrTable& tab, bool vec_ok);
+void launch_finalize(bo_ctx* c, const PtrTable& tab);
+void run_reduce(bo_ctx* c);
+void run_lamb(bo_ctx* c);
+void run_allgather(bo_ctx* c);
+void launch_init_state(bo_ctx* c);
+
+// Stage bracket: records events when profiling is on.
+struct StageTimer {
+  bo_ctx* c;
+  int stage;
+  cudaEvent_t b = nullptr;
+  StageTimer(bo_ctx* ctx, int s);
+  ~StageTimer();
+};
+}  // namespace bo
+
+#endif  // BO_INTERNAL_HPP_

@@ -1,0 +1,419 @@
+// Operator-level drop-ins for the reference's hot-path functions, each with
+// the reference's argument meaning and error behaviour, plus the synthetic
+// gradient generator used by the bench and the tests.
+//
+//   bo_lamb_step               lamb_step              lamb.cpp:140-201
+//   bo_ring_allreduce_f32      ring_allreduce<float>  collective.hpp:53-99
+//   bo_ring_allreduce_f16_wire ring_allreduce_f16_wire collective.cpp:163-212
+//   bo_unscale_gradients       unscale_gradients      half.cpp:105-115
+//   bo_narrow_f16/bo_widen_f16 narrow/widen_f16_block graph.cpp:176-199
+#include <cmath>
+#include <cstring>
+
+#include "bo_device.cuh"
+#include "bo_internal.hpp"
+
+namespace bo {
+namespace {
+
+struct OpTensor {
+  float* w;
+  const float* g;
+  float* m;
+  float* v;
+  int64_t n;
+};
+
+struct OpTile {
+  int32_t t;
+  int32_t len;
+  int64_t e0;
+};
+
+// Smallest (tensor, element) key holding a non-finite gradient.
+__global__ void k_first_nonfinite(const OpTile* tiles, const OpTensor* ts,
+                                  unsigned long long* key) {
+  const OpTile tile = tiles[blockIdx.x];
+  const float* g = ts[tile.t].g + tile.e0;
+  for (int e = threadIdx.x; e < tile.len; e += blockDim.x) {
+    if (!finite(g[e])) {
+      const unsigned long long k = (static_cast<unsigned long long>(tile.t) << 40) |
+                                   static_cast<unsigned long long>(tile.e0 + e);
+      atomicMin(key, k);
+    }
+  }
+}
+
+__global__ void k_op_norms(const OpTile* tiles, const OpTensor* ts, int limit_t, LambConsts c,
+                           const double* bc, double* part) {
+  const OpTile tile = tiles[blockIdx.x];
+  double wn = 0.0, un = 0.0;
+  if (tile.t < limit_t) {
+    const OpTensor T = ts[tile.t];
+    for (int e = threadIdx.x; e < tile.len; e += blockDim.x) {
+      const int64_t i = tile.e0 + e;
+      const float wi = T.w[i];
+      const Moments o = lamb_elem(T.g[i], wi, T.m[i], T.v[i], c, bc);
+      wn = __dadd_rn(wn, __dmul_rn(static_cast<double>(wi), static_cast<double>(wi)));
+      un = __dadd_rn(un, __dmul_rn(static_cast<double>(o.u), static_cast<double>(o.u)));
+    }
+  }
+  __shared__ double red[2][kThreads];
+  red[0][threadIdx.x] = wn;
+  red[1][threadIdx.x] = un;
+  __syncthreads();
+  for (int s = kThreads / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) {
+      red[0][threadIdx.x] += red[0][threadIdx.x + s];
+      red[1][threadIdx.x] += red[1][threadIdx.x + s];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = red[0][0];
+    part[2 * blockIdx.x + 1] = red[1][0];
+  }
+}
+
+__global__ void k_op_trust(const int* tile_begin, const double* part, int T, float clip,
+                           float* trust) {
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < T; t += gridDim.x * blockDim.x) {
+    double W = 0.0, U = 0.0;
+    for (int i = tile_begin[t]; i < tile_begin[t + 1]; ++i) {
+      W = __dadd_rn(W, part[2 * i]);
+      U = __dadd_rn(U, part[2 * i + 1]);
+    }
+    float r = 1.0f;
+    if (W > 0.0 && U > 0.0) {
+      r = __double2float_rn(__ddiv_rn(__dsqrt_rn(W), __dsqrt_rn(U)));
+      r = fminf(fmaxf(r, 0.0f), clip);
+    }
+    trust[t] = r;
+  }
+}
+
+// Full update for tensors < limit_t; for tensor limit_t, only the moments of
+// the elements before the offending one (the reference's partial loop).
+__global__ void k_op_update(const OpTile* tiles, const OpTensor* ts, int limit_t, int64_t limit_e,
+                            LambConsts c, const double* bc, const float* trust) {
+  const OpTile tile = tiles[blockIdx.x];
+  if (tile.t > limit_t) return;
+  const OpTensor T = ts[tile.t];
+  const float step_scale = __fmul_rn(c.lr, tile.t < limit_t ? trust[tile.t] : 0.0f);
+  for (int e = threadIdx.x; e < tile.len; e += blockDim.x) {
+    const int64_t i = tile.e0 + e;
+    if (tile.t == limit_t && i >= limit_e) continue;
+    const float wi = T.w[i];
+    const Moments o = lamb_elem(T.g[i], wi, T.m[i], T.v[i], c, bc);
+    T.m[i] = o.m;
+    T.v[i] = o.v;
+    if (tile.t < limit_t) T.w[i] = __fsub_rn(wi, __fmul_rn(step_scale, o.u));
+  }
+}
+
+__global__ void k_any_nonfinite(const float* g, size_t n, int* flag) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    if (!finite(g[i])) *flag = 1;
+  }
+}
+
+__global__ void k_scale(float* g, size_t n, float inv) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    g[i] = __fmul_rn(g[i], inv);
+  }
+}
+
+__global__ void k_narrow(const float* s, uint16_t* d, size_t n) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    d[i] = narrow(s[i]);
+  }
+}
+
+__global__ void k_widen(const uint16_t* s, float* d, size_t n) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    d[i] = widen(s[i]);
+  }
+}
+
+// mine = widen(in) + mine (f16) or in + mine (fp32): collective.cpp:184-187
+template <typename W>
+__global__ void k_ring_add(const W* in, float* mine, size_t n) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    float w;
+    if constexpr (sizeof(W) == 2) w = widen(in[i]); else w = in[i];
+    mine[i] = __fadd_rn(w, mine[i]);
+  }
+}
+
+__global__ void k_round_f16(float* d, size_t n) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    d[i] = widen(narrow(d[i]));
+  }
+}
+
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+// Synthetic spec: g = ±(1 + mant/1024) 2^E, E in [-24, -15] (or the
+// spike exponent), h = binary16_RNE(g * S). Independent of oracle/synth_grad.h;
+// tests check the two agree bit for bit.
+__global__ void k_synth(uint16_t* dst, int64_t begin, int64_t n, uint64_t base, float scale,
+                        uint32_t spike_ppm, int spike_exp) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t z = mix64(base + static_cast<uint64_t>(begin + i));
+    const uint32_t sign = static_cast<uint32_t>(z & 1u);
+    int e = -24 + static_cast<int>((z >> 1) % 10u);
+    const uint32_t mant = static_cast<uint32_t>((z >> 8) & 0x3FFu);
+    if (spike_ppm && ((z >> 32) % 1000000u) < spike_ppm) e = spike_exp;
+    const uint32_t bits = (sign << 31) | (static_cast<uint32_t>(e + 127) << 23) | (mant << 13);
+    dst[i] = narrow(__fmul_rn(__uint_as_float(bits), scale));
+  }
+}
+
+int grid_for(size_t n) {
+  const size_t b = (n + kThreads - 1) / kThreads;
+  return static_cast<int>(std::min<size_t>(std::max<size_t>(b, 1), 148 * 16));
+}
+
+void check(const char* what) {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) fail(BO_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+struct DevBuf {
+  void* p = nullptr;
+  explicit DevBuf(size_t bytes) { BO_CUDA(cudaMalloc(&p, std::max<size_t>(bytes, 16))); }
+  ~DevBuf() { if (p) cudaFree(p); }
+  template <typename T> T* as() { return static_cast<T*>(p); }
+};
+
+bool is_pow2(float s) {
+  if (!(s > 0.0f) || !std::isfinite(s)) return false;
+  int e = 0;
+  return std::frexp(s, &e) == 0.5f;
+}
+
+template <typename W>
+void ring_allreduce_impl(bo_ctx* c, float* data, size_t n, bool f16) {
+  const int N = c->world, r = c->rank;
+  if (N == 1 || n == 0) return;
+  if (!c->comm) fail(BO_ERR_INVALID_CONFIG, "bo_comm_init has not run");
+  cudaStream_t s = c->stream;
+  const size_t ch = (n + static_cast<size_t>(N) - 1) / static_cast<size_t>(N);  // collective.cpp:50-52
+  DevBuf buf(ch * static_cast<size_t>(N) * 4), wire(ch * sizeof(W)), in(ch * sizeof(W));
+  float* B = buf.as<float>();
+  BO_CUDA(cudaMemsetAsync(B, 0, ch * static_cast<size_t>(N) * 4, s));
+  BO_CUDA(cudaMemcpyAsync(B, data, n * 4, cudaMemcpyDeviceToDevice, s));
+  const ncclDataType_t dt = f16 ? ncclFloat16 : ncclFloat32;
+  const int right = (r + 1) % N, left = (r - 1 + N) % N;
+  auto send_recv = [&](const float* chunk) {
+    const void* out = chunk;
+    if (f16) {
+      k_narrow<<<grid_for(ch), kThreads, 0, s>>>(chunk, wire.as<uint16_t>(), ch);
+      check("k_narrow");
+      out = wire.p;
+    }
+    BO_NCCL(ncclGroupStart());
+    BO_NCCL(ncclSend(out, ch, dt, right, c->comm, s));
+    BO_NCCL(ncclRecv(in.p, ch, dt, left, c->comm, s));
+    BO_NCCL(ncclGroupEnd());
+  };
+  for (int st = 0; st < N - 1; ++st) {  // reduce-scatter (collective.hpp:65-80)
+    const size_t send_idx = static_cast<size_t>((r - st + 2 * N) % N);
+    const size_t recv_idx = static_cast<size_t>((r - st - 1 + 2 * N) % N);
+    send_recv(B + send_idx * ch);
+    k_ring_add<W><<<grid_for(ch), kThreads, 0, s>>>(in.as<W>(), B + recv_idx * ch, ch);
+    check("k_ring_add");
+  }
+  for (int st = 0; st < N - 1; ++st) {  // all-gather (collective.hpp:83-96)
+    const size_t send_idx = static_cast<size_t>((r + 1 - st + 2 * N) % N);
+    const size_t recv_idx = static_cast<size_t>((r - st + 2 * N) % N);
+    send_recv(B + send_idx * ch);
+    if (f16) {
+      k_widen<<<grid_for(ch), kThreads, 0, s>>>(in.as<uint16_t>(), B + recv_idx * ch, ch);
+      check("k_widen");
+    } else {
+      BO_CUDA(cudaMemcpyAsync(B + recv_idx * ch, in.p, ch * 4, cudaMemcpyDeviceToDevice, s));
+    }
+  }
+  if (f16) {  // owner re-round (collective.cpp:205-209)
+    k_round_f16<<<grid_for(ch), kThreads, 0, s>>>(B + static_cast<size_t>((r + 1) % N) * ch, ch);
+    check("k_round_f16");
+  }
+  BO_CUDA(cudaMemcpyAsync(data, B, n * 4, cudaMemcpyDeviceToDevice, s));
+  BO_CUDA(cudaStreamSynchronize(s));
+}
+
+}  // namespace
+}  // namespace bo
+
+using namespace bo;
+
+#define BO_OP_BEGIN try {
+#define BO_OP_END                \
+  }                              \
+  catch (const Failure& f) {     \
+    set_thread_error(f.msg);     \
+    return f.code;               \
+  }                              \
+  return BO_OK;
+
+extern "C" {
+
+bo_status bo_lamb_step(int32_t T, const int64_t* numels, float* const* params,
+                       const float* const* grads, float* const* m, float* const* v, int64_t* step,
+                       const bo_lamb_config* cfg, void* stream) {
+  BO_OP_BEGIN
+  if (T < 0 || !numels || !params || !grads || !m || !v || !step || !cfg) {
+    fail(BO_ERR_SHAPE_MISMATCH, "lamb_step: null argument");
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  *step += 1;  // lamb.cpp:157, before any check
+  const double t = static_cast<double>(*step);
+  double bc[4];
+  bc[0] = 1.0 - std::pow(static_cast<double>(cfg->beta1), t);
+  bc[1] = 1.0 - std::pow(static_cast<double>(cfg->beta2), t);
+  bc[2] = 1.0 / bc[0];
+  bc[3] = 1.0 / bc[1];
+  if (T == 0) return BO_OK;
+  std::vector<OpTensor> ts(static_cast<size_t>(T));
+  std::vector<OpTile> tiles;
+  std::vector<int> tile_begin(static_cast<size_t>(T) + 1);
+  for (int i = 0; i < T; ++i) {
+    ts[static_cast<size_t>(i)] = OpTensor{params[i], grads[i], m[i], v[i], numels[i]};
+    tile_begin[static_cast<size_t>(i)] = static_cast<int>(tiles.size());
+    for (int64_t e = 0; e < numels[i]; e += kTileElems) {
+      tiles.push_back(OpTile{i, static_cast<int32_t>(std::min<int64_t>(kTileElems, numels[i] - e)), e});
+    }
+  }
+  tile_begin[static_cast<size_t>(T)] = static_cast<int>(tiles.size());
+  const size_t nt = tiles.size();
+  DevBuf d_ts(ts.size() * sizeof(OpTensor)), d_tiles(nt * sizeof(OpTile)), d_tb(tile_begin.size() * 4),
+      d_bc(32), d_key(8), d_part(std::max<size_t>(nt, 1) * 16), d_trust(static_cast<size_t>(T) * 4);
+  BO_CUDA(cudaMemcpyAsync(d_ts.p, ts.data(), ts.size() * sizeof(OpTensor), cudaMemcpyHostToDevice, s));
+  if (nt) BO_CUDA(cudaMemcpyAsync(d_tiles.p, tiles.data(), nt * sizeof(OpTile), cudaMemcpyHostToDevice, s));
+  BO_CUDA(cudaMemcpyAsync(d_tb.p, tile_begin.data(), tile_begin.size() * 4, cudaMemcpyHostToDevice, s));
+  BO_CUDA(cudaMemcpyAsync(d_bc.p, bc, 32, cudaMemcpyHostToDevice, s));
+  BO_CUDA(cudaMemsetAsync(d_key.p, 0xFF, 8, s));
+  unsigned long long key = ~0ull;
+  if (nt) {
+    k_first_nonfinite<<<static_cast<int>(nt), kThreads, 0, s>>>(d_tiles.as<OpTile>(), d_ts.as<OpTensor>(),
+                                                               d_key.as<unsigned long long>());
+    check("k_first_nonfinite");
+    BO_CUDA(cudaMemcpyAsync(&key, d_key.p, 8, cudaMemcpyDeviceToHost, s));
+    BO_CUDA(cudaStreamSynchronize(s));
+  }
+  int limit_t = T;
+  int64_t limit_e = 0;
+  if (key != ~0ull) {
+    limit_t = static_cast<int>(key >> 40);
+    limit_e = static_cast<int64_t>(key & ((1ull << 40) - 1));
+  }
+  const LambConsts lc{cfg->beta1, cfg->beta2, 1.0f - cfg->beta1, 1.0f - cfg->beta2, cfg->eps,
+                      cfg->weight_decay, cfg->lr, cfg->trust_clip};
+  if (nt) {
+    k_op_norms<<<static_cast<int>(nt), kThreads, 0, s>>>(d_tiles.as<OpTile>(), d_ts.as<OpTensor>(), limit_t, lc,
+                                                        d_bc.as<double>(), d_part.as<double>());
+    check("k_op_norms");
+    k_op_trust<<<(T + 255) / 256, 256, 0, s>>>(d_tb.as<int>(), d_part.as<double>(), T, cfg->trust_clip,
+                                              d_trust.as<float>());
+    check("k_op_trust");
+    k_op_update<<<static_cast<int>(nt), kThreads, 0, s>>>(d_tiles.as<OpTile>(), d_ts.as<OpTensor>(), limit_t,
+                                                         limit_e, lc, d_bc.as<double>(), d_trust.as<float>());
+    check("k_op_update");
+  }
+  BO_CUDA(cudaStreamSynchronize(s));
+  if (limit_t < T) {
+    fail(BO_ERR_NON_FINITE_GRADIENT, "non-finite gradient in tensor " + std::to_string(limit_t));
+  }
+  BO_OP_END
+}
+
+bo_status bo_ring_allreduce_f32(bo_ctx* c, float* data, size_t n) {
+  BO_OP_BEGIN
+  ring_allreduce_impl<float>(c, data, n, false);
+  BO_OP_END
+}
+
+bo_status bo_ring_allreduce_f16_wire(bo_ctx* c, float* data, size_t n) {
+  BO_OP_BEGIN
+  ring_allreduce_impl<uint16_t>(c, data, n, true);
+  BO_OP_END
+}
+
+bo_status bo_unscale_gradients(float* g, size_t n, float scale, int32_t enabled, void* stream) {
+  BO_OP_BEGIN
+  if (!is_pow2(scale)) {
+    fail(BO_ERR_INVALID_CONFIG, "loss scale must be a positive power of two");  // half.cpp:93-98
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (n == 0) return BO_OK;
+  DevBuf flag(4);
+  BO_CUDA(cudaMemsetAsync(flag.p, 0, 4, s));
+  k_any_nonfinite<<<grid_for(n), kThreads, 0, s>>>(g, n, flag.as<int>());
+  check("k_any_nonfinite");
+  int h = 0;
+  BO_CUDA(cudaMemcpyAsync(&h, flag.p, 4, cudaMemcpyDeviceToHost, s));
+  BO_CUDA(cudaStreamSynchronize(s));
+  if (h) fail(BO_ERR_OVERFLOW_DETECTED, "non-finite gradient before unscale");
+  if (!enabled) return BO_OK;
+  k_scale<<<grid_for(n), kThreads, 0, s>>>(g, n, 1.0f / scale);
+  check("k_scale");
+  BO_CUDA(cudaStreamSynchronize(s));
+  BO_OP_END
+}
+
+bo_status bo_narrow_f16(const float* src, uint16_t* dst, size_t n, void* stream) {
+  BO_OP_BEGIN
+  if (n) {
+    k_narrow<<<grid_for(n), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(src, dst, n);
+    check("k_narrow");
+  }
+  BO_OP_END
+}
+
+bo_status bo_widen_f16(const uint16_t* src, float* dst, size_t n, void* stream) {
+  BO_OP_BEGIN
+  if (n) {
+    k_widen<<<grid_for(n), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(src, dst, n);
+    check("k_widen");
+  }
+  BO_OP_END
+}
+
+float bo_scale_loss(float loss, float scale, int32_t enabled) { return enabled ? loss * scale : loss; }
+
+bo_status bo_synth_grads(uint16_t* dst, int64_t begin, int64_t n, uint64_t seed, int32_t rank,
+                         int32_t step, int32_t micro, float scale, uint32_t spike_ppm,
+                         int32_t spike_exp, void* stream) {
+  BO_OP_BEGIN
+  auto mix = [](uint64_t x) {
+    uint64_t z = x + 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+  };
+  uint64_t h = mix(seed);
+  h = mix(h ^ static_cast<uint64_t>(rank));
+  h = mix(h ^ static_cast<uint64_t>(step));
+  h = mix(h ^ static_cast<uint64_t>(micro));
+  if (n > 0) {
+    k_synth<<<grid_for(static_cast<size_t>(n)), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+        dst, begin, n, h, scale, spike_ppm, spike_exp);
+    check("k_synth");
+  }
+  BO_OP_END
+}
+
+}  // extern "C"

@@ -1,0 +1,446 @@
+// B200 gradient-to-update pipeline: device kernels and stage orchestration.
+//
+// Stage map onto the reference (proj/core/src, read-only):
+//   k_accumulate   accum_[p][i] += g[i]                  trainer.cpp:240-244
+//   k_finalize     flatten_param: (live + accum) * inv   trainer.cpp:186-203
+//   ring hops      ring_allreduce RS phase, fold order   collective.hpp:65-80
+//                  and the binary16 wire semantics       collective.cpp:170-190, 205-209
+//   k_lamb_norms   lamb_step moments + fp64 norms        lamb.cpp:176-190
+//   k_trust        trust ratio (lamb.cpp:192-196) + found_inf + loss-scaler
+//   k_lamb_update  w -= (lr * r) * u                      lamb.cpp:197-198
+//
+// Bit-level contract: every float operation uses an
+// explicit round-to-nearest intrinsic and the file is compiled with
+// --fmad=false, so nothing contracts into an FMA the reference does not have.
+#include <cuda_fp16.h>
+
+#include "bo_device.cuh"
+#include "bo_internal.hpp"
+
+namespace bo {
+namespace {
+
+// ------------------------------------------------------------ accumulate
+// acc = (micro == 0 ? 0 + g : acc + g) over one tensor slice; 16-byte loads of
+// 8 binary16 values, 2 x 16-byte fp32 accesses (trainer.cpp:240-244: the
+// accumulator starts at 0.0f, so -0 becomes +0 exactly as in the reference).
+template <bool kVec>
+__global__ void __launch_bounds__(kThreads) k_accumulate(const AccTile* __restrict__ tiles,
+                                                         const TensorDev* __restrict__ td,
+                                                         const __grid_constant__ PtrTable tab,
+                                                         float* __restrict__ acc, int first) {
+  const AccTile tile = tiles[blockIdx.x];
+  const uint16_t* __restrict__ src = tab.p[tile.t] + tile.e0;
+  float* __restrict__ dst = acc + td[tile.t].acc_off + tile.e0;
+  const int len = tile.len;
+  int done = 0;
+  if (kVec) {
+    const int nvec = len >> 3;
+#pragma unroll 2
+    for (int i = threadIdx.x; i < nvec; i += kThreads) {
+      const uint4 hv = __ldcs(reinterpret_cast<const uint4*>(src) + i);
+      float4* d4 = reinterpret_cast<float4*>(dst) + 2 * i;
+      float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0;
+      if (!first) {
+        a0 = d4[0];
+        a1 = d4[1];
+      }
+      const uint32_t hw[4] = {hv.x, hv.y, hv.z, hv.w};
+      float g[8];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        g[2 * j] = widen(static_cast<uint16_t>(hw[j] & 0xFFFFu));
+        g[2 * j + 1] = widen(static_cast<uint16_t>(hw[j] >> 16));
+      }
+      a0.x = __fadd_rn(a0.x, g[0]); a0.y = __fadd_rn(a0.y, g[1]);
+      a0.z = __fadd_rn(a0.z, g[2]); a0.w = __fadd_rn(a0.w, g[3]);
+      a1.x = __fadd_rn(a1.x, g[4]); a1.y = __fadd_rn(a1.y, g[5]);
+      a1.z = __fadd_rn(a1.z, g[6]); a1.w = __fadd_rn(a1.w, g[7]);
+      d4[0] = a0;
+      d4[1] = a1;
+    }
+    done = nvec << 3;
+  }
+  for (int i = done + threadIdx.x; i < len; i += kThreads) {
+    const float a = first ? 0.0f : dst[i];
+    dst[i] = __fadd_rn(a, widen(src[i]));
+  }
+}
+
+// -------------------------------------------------------------- finalize
+// The sync micro's flatten_param (trainer.cpp:186-203): v = live (+ summed),
+// dst = v * inv with inv = 1/(K*S) in float, S the current (device) scale.
+// Writes the fusion-buffer position of every element (the packer).
+__global__ void __launch_bounds__(kThreads) k_finalize(const AccTile* __restrict__ tiles,
+                                                       const TensorDev* __restrict__ td,
+                                                       const __grid_constant__ PtrTable tab,
+                                                       const float* __restrict__ acc,
+                                                       float* __restrict__ x,
+                                                       const DevState* __restrict__ st, int K) {
+  const AccTile tile = tiles[blockIdx.x];
+  const float inv = __fdiv_rn(1.0f, __fmul_rn(static_cast<float>(K), st->scale));
+  const uint16_t* __restrict__ src = tab.p[tile.t] + tile.e0;
+  const float* __restrict__ a = acc + td[tile.t].acc_off + tile.e0;
+  float* __restrict__ dst = x + td[tile.t].flat_off + tile.e0;
+  constexpr int kPer = kTileElems / kThreads;
+  float gv[kPer];
+#pragma unroll
+  for (int j = 0; j < kPer; ++j) {
+    const int e = threadIdx.x + j * kThreads;
+    gv[j] = 0.0f;
+    if (e < tile.len) {
+      const float g = widen(__ldcs(src + e));
+      gv[j] = K > 1 ? __fadd_rn(g, __ldcs(a + e)) : g;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < kPer; ++j) {
+    const int e = threadIdx.x + j * kThreads;
+    if (e < tile.len) dst[e] = __fmul_rn(gv[j], inv);
+  }
+}
+
+// --------------------------------------------------------------- ring hops
+struct BucketGeo {
+  const int64_t* base;
+  const int64_t* chunk;
+  const int64_t* shoff;
+};
+
+template <typename W>
+__device__ __forceinline__ W to_wire(float p);
+template <>
+__device__ __forceinline__ float to_wire<float>(float p) { return p; }
+template <>
+__device__ __forceinline__ uint16_t to_wire<uint16_t>(float p) { return narrow(p); }
+__device__ __forceinline__ float from_wire(float w) { return w; }
+__device__ __forceinline__ float from_wire(uint16_t w) { return widen(w); }
+
+// combine == 0: out = wire(x[chunk q])                     (first send)
+// combine == 1: out = wire(from_wire(in) + x[chunk q])     (every later hop;
+//   the last one is the owner's re-rounded result, collective.cpp:205-209)
+template <typename W>
+__global__ void __launch_bounds__(kThreads) k_hop(const HopTile* __restrict__ tiles, BucketGeo geo,
+                                                  const float* __restrict__ x,
+                                                  const W* __restrict__ in, W* __restrict__ out,
+                                                  int q, int combine) {
+  const HopTile tile = tiles[blockIdx.x];
+  const int64_t src0 = geo.base[tile.b] + q * geo.chunk[tile.b] + (tile.s0 - geo.shoff[tile.b]);
+  constexpr int kPer = kTileElems / kThreads;
+#pragma unroll
+  for (int j = 0; j < kPer; ++j) {
+    const int e = threadIdx.x + j * kThreads;
+    if (e < tile.len) {
+      float p = __ldcs(x + src0 + e);
+      if (combine) p = __fadd_rn(from_wire(__ldcs(in + tile.s0 + e)), p);
+      out[tile.s0 + e] = to_wire<W>(p);
+    }
+  }
+}
+
+template <typename W>
+__global__ void __launch_bounds__(kThreads) k_unwire(const HopTile* __restrict__ tiles,
+                                                     const W* __restrict__ in,
+                                                     float* __restrict__ g) {
+  const HopTile tile = tiles[blockIdx.x];
+  for (int e = threadIdx.x; e < tile.len; e += kThreads) g[tile.s0 + e] = from_wire(in[tile.s0 + e]);
+}
+
+// ------------------------------------------------------------------- LAMB
+// Phase 1: per-tile fp64 partials of ||w||^2 and ||u||^2 and the non-finite
+// flag of the reduced gradient (lamb.cpp:176-190; the flag is the
+// NonFiniteGradient condition, lamb.cpp:179). Nothing is written to w/m/v.
+__global__ void __launch_bounds__(kThreads) k_lamb_norms(const LambTile* __restrict__ tiles,
+                                                         const float* __restrict__ g,
+                                                         const float* __restrict__ w,
+                                                         const float* __restrict__ m,
+                                                         const float* __restrict__ v,
+                                                         DevState* __restrict__ st, LambConsts c,
+                                                         const double* __restrict__ bc_table,
+                                                         float invn, int scale_g,
+                                                         double* __restrict__ tile_part) {
+  const LambTile tile = tiles[blockIdx.x];
+  __shared__ double bc[4];
+  __shared__ double red[2][kThreads / 32];
+  __shared__ int bad_any;
+  if (threadIdx.x < 4) bc[threadIdx.x] = bc_table[4 * st->lamb_step + threadIdx.x];
+  if (threadIdx.x == 0) bad_any = 0;
+  __syncthreads();
+  constexpr int kPer = kTileElems / kThreads;
+  double wn = 0.0, un = 0.0;
+  bool bad = false;
+#pragma unroll 4
+  for (int j = 0; j < kPer; ++j) {
+    const int e = threadIdx.x + j * kThreads;
+    if (e < tile.len) {
+      float gi = __ldcs(g + tile.s0 + e);
+      if (scale_g) gi = __fmul_rn(gi, invn);
+      const float wi = w[tile.w0 + e];
+      bad |= !finite(gi);
+      const Moments o = lamb_elem(gi, wi, __ldcs(m + tile.s0 + e), __ldcs(v + tile.s0 + e), c, bc);
+      wn = __dadd_rn(wn, __dmul_rn(static_cast<double>(wi), static_cast<double>(wi)));
+      un = __dadd_rn(un, __dmul_rn(static_cast<double>(o.u), static_cast<double>(o.u)));
+    }
+  }
+  wn = warp_sum(wn);
+  un = warp_sum(un);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) {
+    red[0][wid] = wn;
+    red[1][wid] = un;
+  }
+  if (bad) bad_any = 1;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0, b = 0.0;
+    for (int i = 0; i < kThreads / 32; ++i) {
+      a += red[0][i];
+      b += red[1][i];
+    }
+    tile_part[2 * blockIdx.x] = a;
+    tile_part[2 * blockIdx.x + 1] = b;
+    if (bad_any) atomicOr(&st->local_flag, 1);
+  }
+}
+
+// Per-tensor sums of the tile partials in a fixed order (deterministic), plus
+// this rank's flag, into rank_part[2T+1].
+__global__ void __launch_bounds__(kThreads) k_norm_reduce(const int* __restrict__ tile_begin,
+                                                          const double* __restrict__ tile_part,
+                                                          const DevState* __restrict__ st, int T,
+                                                          double* __restrict__ rank_part) {
+  const int t = blockIdx.x;
+  const int b0 = tile_begin[t], b1 = tile_begin[t + 1];
+  double a = 0.0, b = 0.0;
+  for (int i = b0 + threadIdx.x; i < b1; i += kThreads) {
+    a += tile_part[2 * i];
+    b += tile_part[2 * i + 1];
+  }
+  __shared__ double red[2][kThreads];
+  red[0][threadIdx.x] = a;
+  red[1][threadIdx.x] = b;
+  __syncthreads();
+  for (int s = kThreads / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) {
+      red[0][threadIdx.x] += red[0][threadIdx.x + s];
+      red[1][threadIdx.x] += red[1][threadIdx.x + s];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    rank_part[2 * t] = red[0][0];
+    rank_part[2 * t + 1] = red[1][0];
+    if (t == 0) rank_part[2 * T] = st->local_flag ? 1.0 : 0.0;
+  }
+}
+
+// Global decision: found_inf = any rank flagged; trust ratios from the
+// rank-ordered sums (identical on every rank); LAMB step counter; dynamic
+// loss-scaler state machine.
+__global__ void __launch_bounds__(1024) k_trust(const double* __restrict__ all_part, int N, int T,
+                                                DevState* __restrict__ st, LambConsts c,
+                                                ScalerConsts sc, float* __restrict__ trust) {
+  __shared__ int found;
+  if (threadIdx.x == 0) {
+    int f = 0;
+    for (int r = 0; r < N; ++r) f |= all_part[static_cast<size_t>(r) * (2 * T + 1) + 2 * T] != 0.0;
+    found = f;
+  }
+  __syncthreads();
+  if (!found) {
+    for (int t = threadIdx.x; t < T; t += blockDim.x) {
+      double W = 0.0, U = 0.0;
+      for (int r = 0; r < N; ++r) {
+        W = __dadd_rn(W, all_part[static_cast<size_t>(r) * (2 * T + 1) + 2 * t]);
+        U = __dadd_rn(U, all_part[static_cast<size_t>(r) * (2 * T + 1) + 2 * t + 1]);
+      }
+      float r = 1.0f;
+      if (W > 0.0 && U > 0.0) {
+        r = __double2float_rn(__ddiv_rn(__dsqrt_rn(W), __dsqrt_rn(U)));
+        r = fminf(fmaxf(r, 0.0f), c.clip);
+      }
+      trust[t] = r;
+    }
+  }
+  if (threadIdx.x == 0) {
+    st->found_inf = found;
+    st->do_update = !found;
+    st->steps += 1;
+    st->local_flag = 0;
+    if (found) {
+      st->skipped += 1;
+    } else {
+      st->lamb_step += 1;
+    }
+    if (sc.dynamic) {
+      if (found) {
+        st->scale = fmaxf(__fmul_rn(st->scale, sc.backoff), sc.min_scale);
+        st->good = 0;
+      } else if (++st->good == sc.interval) {
+        st->scale = fminf(__fmul_rn(st->scale, sc.growth), sc.max_scale);
+        st->good = 0;
+      }
+    }
+  }
+}
+
+// Phase 2: recompute the element (bit-identical to phase 1) and apply
+// w -= (lr * r) * u, storing w, m, v (lamb.cpp:197-198). Skipped steps exit.
+__global__ void __launch_bounds__(kThreads) k_lamb_update(const LambTile* __restrict__ tiles,
+                                                          const float* __restrict__ g,
+                                                          float* __restrict__ w,
+                                                          float* __restrict__ m,
+                                                          float* __restrict__ v,
+                                                          const DevState* __restrict__ st,
+                                                          LambConsts c,
+                                                          const double* __restrict__ bc_table,
+                                                          float invn, int scale_g,
+                                                          const float* __restrict__ trust) {
+  if (!st->do_update) return;
+  const LambTile tile = tiles[blockIdx.x];
+  __shared__ double bc[4];
+  if (threadIdx.x < 4) bc[threadIdx.x] = bc_table[4 * (st->lamb_step - 1) + threadIdx.x];
+  __syncthreads();
+  const float step_scale = __fmul_rn(c.lr, trust[tile.t]);
+  constexpr int kPer = kTileElems / kThreads;
+#pragma unroll 4
+  for (int j = 0; j < kPer; ++j) {
+    const int e = threadIdx.x + j * kThreads;
+    if (e < tile.len) {
+      float gi = __ldcs(g + tile.s0 + e);
+      if (scale_g) gi = __fmul_rn(gi, invn);
+      const float wi = w[tile.w0 + e];
+      const Moments o = lamb_elem(gi, wi, m[tile.s0 + e], v[tile.s0 + e], c, bc);
+      w[tile.w0 + e] = __fsub_rn(wi, __fmul_rn(step_scale, o.u));
+      m[tile.s0 + e] = o.m;
+      v[tile.s0 + e] = o.v;
+    }
+  }
+}
+
+void check_launch(bo_ctx* c, const char* what) {
+  c->launches += 1;
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) fail(BO_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+BucketGeo geo_of(bo_ctx* c) {
+  const int64_t* p = c->d_bucket_geo;
+  return BucketGeo{p, p + c->L.B, p + 2 * c->L.B};
+}
+
+}  // namespace
+
+void launch_accumulate(bo_ctx* c, int micro, const PtrTable& tab, bool vec_ok) {
+  StageTimer timer(c, BO_STAGE_ACCUMULATE);
+  if (vec_ok) {
+    k_accumulate<true><<<c->n_acc_tiles, kThreads, 0, c->stream>>>(c->d_acc_tiles, c->d_tensors,
+                                                                    tab, c->acc, micro == 0);
+  } else {
+    k_accumulate<false><<<c->n_acc_tiles, kThreads, 0, c->stream>>>(c->d_acc_tiles, c->d_tensors,
+                                                                     tab, c->acc, micro == 0);
+  }
+  check_launch(c, "k_accumulate");
+}
+
+void launch_finalize(bo_ctx* c, const PtrTable& tab) {
+  StageTimer timer(c, BO_STAGE_FINALIZE);
+  k_finalize<<<c->n_acc_tiles, kThreads, 0, c->stream>>>(c->d_acc_tiles, c->d_tensors, tab, c->acc,
+                                                          c->x, c->state, c->cfg.accumulation);
+  check_launch(c, "k_finalize");
+}
+
+template <typename W>
+static void ring_reduce_scatter(bo_ctx* c, ncclDataType_t dt) {
+  const int N = c->world, r = c->rank;
+  const int right = (r + 1) % N, left = (r - 1 + N) % N;
+  const size_t S = static_cast<size_t>(c->L.shard_total);
+  W* a = static_cast<W*>(c->wire[0]);
+  W* b = static_cast<W*>(c->wire[1]);
+  const BucketGeo geo = geo_of(c);
+  // hop 0 payload: this rank's own chunk r, narrowed (collective.cpp:178)
+  k_hop<W><<<c->n_hop_tiles, kThreads, 0, c->stream>>>(c->d_hop_tiles, geo, c->x, nullptr, a, r, 0);
+  check_launch(c, "k_hop(pack)");
+  for (int s = 0; s < N - 1; ++s) {
+    BO_NCCL(ncclGroupStart());
+    BO_NCCL(ncclSend(a, S, dt, right, c->comm, c->stream));
+    BO_NCCL(ncclRecv(b, S, dt, left, c->comm, c->stream));
+    BO_NCCL(ncclGroupEnd());
+    const int q = (r - s - 1 + 2 * N) % N;  // chunk received at hop s (collective.hpp:70-71)
+    k_hop<W><<<c->n_hop_tiles, kThreads, 0, c->stream>>>(c->d_hop_tiles, geo, c->x, b, a, q, 1);
+    check_launch(c, "k_hop");
+  }
+  // After N-1 hops rank r holds the finished chunk (r+1) % N. One more hop
+  // hands it to rank r+1, so that rank r owns chunk r (the ncclAllGather
+  // placement); the payload is already wire-exact, so this moves no bits.
+  BO_NCCL(ncclGroupStart());
+  BO_NCCL(ncclSend(a, S, dt, right, c->comm, c->stream));
+  BO_NCCL(ncclRecv(b, S, dt, left, c->comm, c->stream));
+  BO_NCCL(ncclGroupEnd());
+  k_unwire<W><<<c->n_hop_tiles, kThreads, 0, c->stream>>>(c->d_hop_tiles, b, c->gshard);
+  check_launch(c, "k_unwire");
+}
+
+void run_reduce(bo_ctx* c) {
+  if (c->world == 1) return;
+  StageTimer timer(c, BO_STAGE_REDUCE);
+  if (c->algo == BO_REDUCE_NCCL) {
+    BO_NCCL(ncclGroupStart());
+    for (int b = 0; b < c->L.B; ++b) {
+      BO_NCCL(ncclReduceScatter(c->x + c->L.base[b], c->gshard + c->L.shoff[b],
+                                static_cast<size_t>(c->L.chunk[b]), ncclFloat, ncclSum, c->comm,
+                                c->stream));
+    }
+    BO_NCCL(ncclGroupEnd());
+  } else if (c->cfg.f16_exchange) {
+    ring_reduce_scatter<uint16_t>(c, ncclFloat16);
+  } else {
+    ring_reduce_scatter<float>(c, ncclFloat32);
+  }
+}
+
+void run_lamb(bo_ctx* c) {
+  const int T = c->L.T;
+  const float invn = 1.0f / static_cast<float>(c->world);  // trainer.cpp:212
+  const int scale_g = c->world > 1;
+  {
+  StageTimer timer(c, BO_STAGE_LAMB_NORMS);
+  k_lamb_norms<<<c->n_lamb_tiles, kThreads, 0, c->stream>>>(c->d_lamb_tiles, c->gshard, c->w, c->m,
+                                                             c->v, c->state, c->lamb, c->bc_table,
+                                                             invn, scale_g, c->tile_part);
+  check_launch(c, "k_lamb_norms");
+  }
+  {
+  StageTimer timer(c, BO_STAGE_TRUST);
+  k_norm_reduce<<<T, kThreads, 0, c->stream>>>(c->d_tensor_tile_begin, c->tile_part, c->state, T,
+                                                c->rank_part);
+  check_launch(c, "k_norm_reduce");
+  if (c->world > 1) {
+    BO_NCCL(ncclAllGather(c->rank_part, c->all_part, static_cast<size_t>(2 * T + 1), ncclFloat64,
+                          c->comm, c->stream));
+  }
+  k_trust<<<1, 1024, 0, c->stream>>>(c->all_part, c->world, T, c->state, c->lamb, c->scaler,
+                                     c->trust);
+  check_launch(c, "k_trust");
+  }
+  StageTimer timer(c, BO_STAGE_LAMB_UPDATE);
+  k_lamb_update<<<c->n_lamb_tiles, kThreads, 0, c->stream>>>(c->d_lamb_tiles, c->gshard, c->w, c->m,
+                                                              c->v, c->state, c->lamb, c->bc_table,
+                                                              invn, scale_g, c->trust);
+  check_launch(c, "k_lamb_update");
+}
+
+void run_allgather(bo_ctx* c) {
+  if (c->world == 1) return;
+  StageTimer timer(c, BO_STAGE_ALLGATHER);
+  BO_NCCL(ncclGroupStart());
+  for (int b = 0; b < c->L.B; ++b) {
+    const size_t cb = static_cast<size_t>(c->L.chunk[b]);
+    float* base = c->w + c->L.base[b];
+    BO_NCCL(ncclAllGather(base + static_cast<size_t>(c->rank) * cb, base, cb, ncclFloat, c->comm,
+                          c->stream));
+  }
+  BO_NCCL(ncclGroupEnd());
+}
+
+}  // namespace bo

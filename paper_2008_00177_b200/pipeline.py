@@ -1,0 +1,329 @@
+"""Host-side mirror of the reference hot-path interface over the C ABI.
+
+Names and argument meaning follow the reference (proj/core/include/bertopt):
+
+* ``LambConfig``     — lamb.hpp:165-172
+* ``TrainerConfig``  — trainer.hpp:75-85 (hot-path fields) + the dynamic
+  loss-scaler extension ``ScalerConfig``
+* ``GradPipeline``   — one rank's DistributedTrainer gradient-to-update path
+  (trainer.cpp:217-373): ``accumulate(k, grads)`` for each micro-batch; the
+  last micro runs finalize → reduce-scatter → LAMB → scaler → all-gather.
+* ``lamb_step``, ``ring_allreduce``, ``ring_allreduce_f16_wire``,
+  ``unscale_gradients``, ``scale_loss`` — operator-level drop-ins with the
+  reference signatures' meaning and error behaviour (errors.py).
+
+Tensors are torch CUDA tensors (torch is the device-memory plumbing only);
+all compute runs in libbertopt_b200.so.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .errors import InvalidConfig, ShapeMismatch
+from .model_spec import ModelSpec
+
+REDUCE_AUTO, REDUCE_RING, REDUCE_NCCL = 0, 1, 2
+
+
+@dataclass
+class LambConfig:
+    lr: float = 1e-3
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-6
+    weight_decay: float = 0.01
+    trust_clip: float = 10.0
+
+    def c(self) -> _lib.LambConfigC:
+        return _lib.LambConfigC(self.lr, self.beta1, self.beta2, self.eps, self.weight_decay,
+                                self.trust_clip)
+
+
+@dataclass
+class ScalerConfig:
+    """Dynamic loss scaler (powers of two). dynamic=0: the reference's static S."""
+
+    init_scale: float = 65536.0
+    growth_factor: float = 2.0
+    backoff_factor: float = 0.5
+    min_scale: float = 1.0
+    max_scale: float = 16777216.0
+    growth_interval: int = 2000
+    dynamic: int = 1
+
+    def c(self) -> _lib.ScalerConfigC:
+        return _lib.ScalerConfigC(self.init_scale, self.growth_factor, self.backoff_factor,
+                                  self.min_scale, self.max_scale, self.growth_interval, self.dynamic)
+
+
+@dataclass
+class TrainerConfig:
+    lamb: LambConfig = field(default_factory=LambConfig)
+    accumulation: int = 1
+    bucket_bytes: int = 4 << 20
+    f16_exchange: bool = False
+    reduce_algo: int = REDUCE_AUTO
+    scaler: ScalerConfig = field(default_factory=ScalerConfig)
+
+    def c(self) -> _lib.TrainerConfigC:
+        return _lib.TrainerConfigC(self.lamb.c(), self.accumulation, self.bucket_bytes,
+                                   int(self.f16_exchange), self.reduce_algo, self.scaler.c())
+
+
+@dataclass
+class StepStatus:
+    loss_scale: float
+    good_steps: int
+    lamb_step: int
+    steps: int
+    skipped_steps: int
+    found_inf: bool
+
+
+def _ptr_array(ptrs) -> C.Array:
+    return (C.c_void_p * len(ptrs))(*ptrs)
+
+
+class GradPipeline:
+    """One rank of the device-resident gradient-to-update pipeline."""
+
+    def __init__(self, spec: ModelSpec, cfg: TrainerConfig, device: int = 0, rank: int = 0,
+                 world: int = 1):
+        self.lib = _lib.load()
+        self.spec = spec
+        self.cfg = cfg
+        self.rank, self.world, self.device = rank, world, device
+        T = spec.n_tensors
+        self._numels = np.asarray(spec.numels(), np.int64)
+        firsts = np.asarray(spec.first_consumer_ids(), np.int32)
+        names = (C.c_char_p * T)(*[n.encode() for n in spec.names])
+        ndims = np.asarray([len(s) for s in spec.shapes], np.int32)
+        dims = np.asarray([d for s in spec.shapes for d in s], np.int64)
+        ctx = C.c_void_p()
+        cc = cfg.c()
+        _lib.check(self.lib.bo_create(
+            C.byref(cc), T, self._numels.ctypes.data_as(C.POINTER(C.c_int64)),
+            firsts.ctypes.data_as(C.POINTER(C.c_int32)), names,
+            ndims.ctypes.data_as(C.POINTER(C.c_int32)), dims.ctypes.data_as(C.POINTER(C.c_int64)),
+            device, rank, world, C.byref(ctx)))
+        self.ctx = ctx
+        self.P = int(self._numels.sum())
+
+    def close(self) -> None:
+        if self.ctx:
+            self.lib.bo_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- layout
+    @property
+    def num_buckets(self) -> int:
+        return self.lib.bo_layout_num_buckets(self.ctx)
+
+    def layout(self):
+        T, B = self.spec.n_tensors, self.num_buckets
+        bo = np.empty(T, np.int32)
+        off = np.empty(T, np.int64)
+        ro = np.empty(T, np.int32)
+        be = np.empty(B, np.int64)
+        _lib.check(self.lib.bo_layout_query(self.ctx, bo.ctypes.data_as(C.POINTER(C.c_int32)),
+                                            off.ctypes.data_as(C.POINTER(C.c_int64)),
+                                            ro.ctypes.data_as(C.POINTER(C.c_int32)),
+                                            be.ctypes.data_as(C.POINTER(C.c_int64))))
+        return bo, off, ro, be
+
+    def layout_hash(self) -> int:
+        return self.lib.bo_layout_hash(self.ctx)
+
+    def shard_elems(self) -> int:
+        return self.lib.bo_shard_elems(self.ctx)
+
+    def device_bytes(self) -> int:
+        return self.lib.bo_device_bytes(self.ctx)
+
+    # -- comm
+    @staticmethod
+    def unique_id() -> bytes:
+        lib = _lib.load()
+        buf = C.create_string_buffer(128)
+        _lib.check(lib.bo_comm_unique_id(buf))
+        return buf.raw
+
+    def comm_init(self, uid: bytes) -> None:
+        if len(uid) != 128:
+            raise InvalidConfig("InvalidConfig: NCCL unique id must be 128 bytes")
+        _lib.check(self.lib.bo_comm_init(self.ctx, uid))
+
+    def comm_init_torch(self) -> None:
+        """Exchange the NCCL id over an initialised torch.distributed group."""
+        import torch
+        import torch.distributed as dist
+
+        buf = torch.zeros(128, dtype=torch.uint8)
+        if self.rank == 0:
+            buf[:] = torch.frombuffer(bytearray(self.unique_id()), dtype=torch.uint8)
+        if dist.get_backend() == "nccl":
+            buf = buf.cuda(self.device)
+        dist.broadcast(buf, 0)
+        self.comm_init(bytes(buf.cpu().numpy().tobytes()))
+
+    # -- streams
+    def set_stream(self, stream) -> None:
+        handle = None if stream is None else C.c_void_p(int(stream.cuda_stream))
+        _lib.check(self.lib.bo_set_stream(self.ctx, handle))
+
+    def stream_handle(self) -> int:
+        return int(self.lib.bo_get_stream(self.ctx) or 0)
+
+    def synchronize(self) -> None:
+        _lib.check(self.lib.bo_synchronize(self.ctx))
+
+    # -- state
+    def load_params(self, params) -> None:
+        """params: flat float32 model-order array (numpy) or CUDA tensor."""
+        if isinstance(params, np.ndarray):
+            a = np.ascontiguousarray(params, np.float32)
+            if a.size != self.P:
+                raise ShapeMismatch("ShapeMismatch: parameter count")
+            _lib.check(self.lib.bo_load_params(self.ctx, a.ctypes.data, 1))
+        else:
+            if params.numel() != self.P or not params.is_contiguous():
+                raise ShapeMismatch("ShapeMismatch: parameter count")
+            _lib.check(self.lib.bo_load_params(self.ctx, params.data_ptr(), 0))
+
+    def read_params(self) -> np.ndarray:
+        out = np.empty(self.P, np.float32)
+        _lib.check(self.lib.bo_read_params(self.ctx, out.ctypes.data, 1))
+        return out
+
+    def read_moments(self, m: np.ndarray | None = None, v: np.ndarray | None = None):
+        m = np.zeros(self.P, np.float32) if m is None else m
+        v = np.zeros(self.P, np.float32) if v is None else v
+        _lib.check(self.lib.bo_read_moments(self.ctx, m.ctypes.data, v.ctypes.data, 1))
+        return m, v
+
+    def status(self) -> StepStatus:
+        st = _lib.StepStatusC()
+        _lib.check(self.lib.bo_get_status(self.ctx, C.byref(st)))
+        return StepStatus(st.loss_scale, st.good_steps, st.lamb_step, st.steps, st.skipped_steps,
+                          bool(st.found_inf))
+
+    def param_ptr(self, t: int) -> int:
+        p = C.c_void_p()
+        _lib.check(self.lib.bo_param_ptr(self.ctx, t, C.byref(p)))
+        return p.value
+
+    # -- hot path
+    def accumulate(self, micro: int, grads) -> None:
+        """grads: per-tensor device pointers (ints) or fp16/int16 CUDA tensors."""
+        if len(grads) != self.spec.n_tensors:
+            raise ShapeMismatch(f"ShapeMismatch: {len(grads)} gradients for "
+                                f"{self.spec.n_tensors} parameters")
+        ptrs = [g if isinstance(g, int) else g.data_ptr() for g in grads]
+        _lib.check(self.lib.bo_accumulate(self.ctx, micro, _ptr_array(ptrs)))
+
+    def accumulate_ptr_array(self, micro: int, arr) -> None:
+        """Fast path: a prebuilt ctypes pointer array (see make_ptr_array)."""
+        _lib.check(self.lib.bo_accumulate(self.ctx, micro, arr))
+
+    @staticmethod
+    def make_ptr_array(ptrs) -> C.Array:
+        return _ptr_array(ptrs)
+
+    def train_step(self, micro_grads) -> None:
+        """All K micro-batches of one optimizer step (the train_step analog)."""
+        K = self.cfg.accumulation
+        if len(micro_grads) != K:
+            raise InvalidConfig("InvalidConfig: train_step expects exactly K micro batches")
+        for k, g in enumerate(micro_grads):
+            self.accumulate(k, g)
+
+
+# ---------------------------------------------------------------- operators
+def _stream(stream) -> C.c_void_p:
+    if stream is None:
+        import torch
+
+        stream = torch.cuda.current_stream()
+    return C.c_void_p(int(stream.cuda_stream))
+
+
+def lamb_step(params, grads, state: dict, cfg: LambConfig, stream=None) -> None:
+    """``lamb_step(params, grads, state, cfg)`` (lamb.hpp:182-183) on CUDA fp32 tensors.
+
+    ``state`` mirrors LambState: {'m': [...], 'v': [...], 'step': int}; m/v are
+    created lazily as zeros (lamb.cpp:147-152). Raises ShapeMismatch /
+    NonFiniteGradient like the reference (after the same partial update).
+    """
+    import torch
+
+    lib = _lib.load()
+    if len(grads) != len(params):
+        raise ShapeMismatch(f"ShapeMismatch: lamb_step: {len(grads)} gradients for "
+                            f"{len(params)} parameters")
+    if not state.get("m"):
+        state["m"] = [torch.zeros_like(p) for p in params]
+        state["v"] = [torch.zeros_like(p) for p in params]
+        state.setdefault("step", 0)
+    if len(state["m"]) != len(params) or len(state["v"]) != len(params):
+        raise ShapeMismatch("ShapeMismatch: lamb_step: optimizer state layout mismatch")
+    for i, (p, g) in enumerate(zip(params, grads)):
+        if g.shape != p.shape:
+            raise ShapeMismatch(f"ShapeMismatch: lamb_step: gradient shape mismatch at tensor {i}")
+    n = len(params)
+    numels = (C.c_int64 * n)(*[p.numel() for p in params])
+    step = C.c_int64(state["step"])
+    st = lib.bo_lamb_step(n, numels, _ptr_array([p.data_ptr() for p in params]),
+                          _ptr_array([g.data_ptr() for g in grads]),
+                          _ptr_array([t.data_ptr() for t in state["m"]]),
+                          _ptr_array([t.data_ptr() for t in state["v"]]), C.byref(step),
+                          C.byref(cfg.c()), _stream(stream))
+    state["step"] = step.value
+    _lib.check(st)
+
+
+def unscale_gradients(grads, scale: float, enabled: bool = True, stream=None) -> None:
+    """In place on a contiguous CUDA fp32 tensor (half.cpp:105-115)."""
+    lib = _lib.load()
+    _lib.check(lib.bo_unscale_gradients(grads.data_ptr(), grads.numel(), scale, int(enabled),
+                                        _stream(stream)))
+
+
+def scale_loss(loss: float, scale: float, enabled: bool = True) -> float:
+    return _lib.load().bo_scale_loss(loss, scale, int(enabled))
+
+
+def narrow_f16(src, dst, stream=None) -> None:
+    _lib.check(_lib.load().bo_narrow_f16(src.data_ptr(), dst.data_ptr(), src.numel(),
+                                         _stream(stream)))
+
+
+def widen_f16(src, dst, stream=None) -> None:
+    _lib.check(_lib.load().bo_widen_f16(src.data_ptr(), dst.data_ptr(), src.numel(),
+                                        _stream(stream)))
+
+
+def ring_allreduce(pipe: GradPipeline, data) -> None:
+    """ring_allreduce<float> over pipe's communicator, in place (collective.hpp:104-107)."""
+    _lib.check(pipe.lib.bo_ring_allreduce_f32(pipe.ctx, data.data_ptr(), data.numel()))
+
+
+def ring_allreduce_f16_wire(pipe: GradPipeline, data) -> None:
+    """ring_allreduce_f16_wire (collective.hpp:113-114), in place."""
+    _lib.check(pipe.lib.bo_ring_allreduce_f16_wire(pipe.ctx, data.data_ptr(), data.numel()))
+
+
+def synth_grads(dst, flat_begin: int, seed: int, rank: int, step: int, micro: int, scale: float,
+                spike_ppm: int = 0, spike_exp: int = 1, stream=None) -> None:
+    """Fill an int16/fp16 CUDA tensor with the synthetic spec's binary16 bits."""
+    _lib.check(_lib.load().bo_synth_grads(dst.data_ptr(), flat_begin, dst.numel(), seed, rank, step,
+                                          micro, scale, spike_ppm, spike_exp, _stream(stream)))
