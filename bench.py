@@ -45,7 +45,8 @@ BYTES_LAMB_ALGO = 28                    # single-pass LAMB (the algorithmic mini
 
 STAGES = ["accumulate", "finalize", "reduce", "lamb_norms", "trust", "lamb_update", "allgather"]
 
-MODELS = {"bert-large": "BERT_LARGE", "bert-large-128": "BERT_LARGE_PHASE1", "bert-base": "BERT_BASE"}
+MODELS = {"bert-large": "BERT_LARGE", "bert-large-128": "BERT_LARGE_PHASE1", "bert-base": "BERT_BASE",
+          "bert-tiny": "BERT_TINY"}
 
 REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
            0x8: "hw_slowdown", 0x20: "sync_boost", 0x40: "sw_thermal_slowdown",
@@ -237,7 +238,9 @@ def main_b200(args):
     ptr_arrays = [GradPipeline.make_ptr_array([b.data_ptr() + 2 * s for s in slots]) for b in bufs]
     torch.cuda.synchronize()
 
-    stream = torch.cuda.ExternalStream(pipe.stream_handle())
+    # the pipeline runs on a torch-owned stream (torch's allocators record on it)
+    stream = torch.cuda.Stream()
+    pipe.set_stream(stream)
 
     def step():
         for k in range(K):

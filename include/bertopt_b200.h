@@ -108,6 +108,21 @@ const char* bo_status_name(int32_t status);
 const char* bo_last_error(void);
 void bo_default_config(bo_trainer_config* cfg);
 
+/* ---- layout (host only, no device needed) -------------------------------- */
+/* BucketLayout::build (trainer.cpp:73-116): fills bucket_of[T], offset_of[T],
+ * ready_order[T], bucket_elems[T] (first *n_buckets entries valid) and the
+ * salted layout hash (names/ndims/dims optional, as in bo_create). */
+bo_status bo_bucket_layout(int32_t n_tensors, const int64_t* numels, const int32_t* first_consumers,
+                           uint64_t bucket_bytes, const char* const* names, const int32_t* ndims,
+                           const int64_t* dims, int32_t f16_exchange, int32_t accumulation,
+                           int32_t* bucket_of, int64_t* offset_of, int32_t* ready_order,
+                           int64_t* bucket_elems, int32_t* n_buckets, uint64_t* hash);
+/* Elements rank `rank` of `world` owns: for every bucket b the range
+ * [lo[b], hi[b]) of bucket-local element indices (chunk `rank` of the ring's
+ * ceil(n_b/world) chunking, clipped to n_b). */
+bo_status bo_shard_ranges(int32_t n_buckets, const int64_t* bucket_elems, int32_t world,
+                          int32_t rank, int64_t* lo, int64_t* hi);
+
 /* ---- context / layout -------------------------------------------------- */
 /* One context per rank (one process or thread per GPU). numels and
  * first_consumers are in model parameter order; first_consumers[p] is the op

@@ -48,7 +48,12 @@ SIGNATURES = {
     "bo_status_name": (C.c_char_p, [_i32]),
     "bo_last_error": (C.c_char_p, []),
     "bo_default_config": (None, [C.POINTER(TrainerConfigC)]),
-    "bo_create": (_i32, [C.POINTER(TrainerConfigC), _i32, C.POINTER(_i64), C.POINTER(_i32),
+    "bo_bucket_layout": (_i32, [_i32, C.POINTER(_i64), C.POINTER(_i32), _u64, C.POINTER(C.c_char_p),
+                                C.POINTER(_i32), C.POINTER(_i64), _i32, _i32, C.POINTER(_i32),
+                                C.POINTER(_i64), C.POINTER(_i32), C.POINTER(_i64), C.POINTER(_i32),
+                                C.POINTER(_u64)]),
+    "bo_shard_ranges": (_i32, [_i32, C.POINTER(_i64), _i32, _i32, C.POINTER(_i64), C.POINTER(_i64)]),
+    "bo_create": (_i32,[C.POINTER(TrainerConfigC), _i32, C.POINTER(_i64), C.POINTER(_i32),
                          C.POINTER(C.c_char_p), C.POINTER(_i32), C.POINTER(_i64), _i32, _i32, _i32,
                          C.POINTER(_vp)]),
     "bo_destroy": (None, [_vp]),

@@ -1,7 +1,9 @@
 // C ABI of the pipeline context: creation, layout, communication, state, and
 // the hot-path entry point bo_accumulate (see include/bertopt_b200.h).
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "bo_internal.hpp"
@@ -63,8 +65,7 @@ void upload_tables(bo_ctx* c) {
       for (int64_t e = a; e < z; e += kTileElems) {
         const int64_t len = std::min<int64_t>(kTileElems, z - e);
         per_tensor[static_cast<size_t>(p)].push_back(
-            LambTile{L.shoff[static_cast<size_t>(b)] + (e - lo), L.base[static_cast<size_t>(b)] + e,
-                     static_cast<int32_t>(len), p});
+            LambTile{L.shard_pos(b, p, e), L.flat_pos(b, p, e), static_cast<int32_t>(len), p});
       }
     }
     for (int64_t e = 0; e < cb; e += kTileElems) {
@@ -84,6 +85,53 @@ void upload_tables(bo_ctx* c) {
   geo.insert(geo.end(), L.chunk.begin(), L.chunk.end());
   geo.insert(geo.end(), L.shoff.begin(), L.shoff.end());
 
+  if (c->world == 1) {
+    // Fused single-rank LAMB: tiles in model order, groups of consecutive whole
+    // tensors of ~4M elements (w + u = 32 MB in L2 per group in flight).
+    constexpr int64_t kGroupElems = 4 << 20;
+    std::vector<FusedTile> ft;
+    std::vector<FusedGroup> fg;
+    std::vector<int> ttiles(static_cast<size_t>(L.T) + 1), tids(static_cast<size_t>(L.T));
+    int64_t cur = 0;
+    for (int t = 0; t < L.T; ++t) {
+      const int64_t n = L.numel[static_cast<size_t>(t)];
+      if (fg.empty() || (cur > 0 && cur + n > kGroupElems)) {
+        fg.push_back(FusedGroup{static_cast<int32_t>(ft.size()), 0, t, 0});
+        cur = 0;
+      }
+      tids[static_cast<size_t>(t)] = t;
+      ttiles[static_cast<size_t>(t)] = static_cast<int>(ft.size());
+      for (int64_t e = 0; e < n; e += kTileElems) {
+        ft.push_back(FusedTile{L.acc_off[static_cast<size_t>(t)] + e, e,
+                               static_cast<int32_t>(std::min<int64_t>(kTileElems, n - e)), t,
+                               static_cast<int32_t>(fg.size()) - 1, 0});
+      }
+      cur += n;
+      fg.back().tile_end = static_cast<int32_t>(ft.size());
+      fg.back().t_end = t + 1;
+    }
+    ttiles[static_cast<size_t>(L.T)] = static_cast<int>(ft.size());
+    std::vector<uint32_t> work;
+    auto phase = [&](int g, uint32_t ph) {
+      for (int i = fg[static_cast<size_t>(g)].tile_begin; i < fg[static_cast<size_t>(g)].tile_end; ++i) {
+        work.push_back((static_cast<uint32_t>(i) << 1) | ph);
+      }
+    };
+    for (int g = 0; g < static_cast<int>(fg.size()); ++g) {
+      phase(g, 0);
+      if (g > 0) phase(g - 1, 1);
+    }
+    phase(static_cast<int>(fg.size()) - 1, 1);
+    c->d_fused_tiles = upload(c, ft);
+    c->n_fused_tiles = static_cast<int>(ft.size());
+    c->d_fused_groups = upload(c, fg);
+    c->n_fused_groups = static_cast<int>(fg.size());
+    c->d_fused_tensor_tiles = upload(c, ttiles);
+    c->d_fused_tensor_ids = upload(c, tids);
+    c->d_fused_work = upload(c, work);
+    c->n_fused_work = static_cast<int>(work.size());
+    c->d_fused_sync = static_cast<unsigned long long*>(dev_alloc(c, (2 * fg.size() + 1) * 8));
+  }
   c->d_tensors = upload(c, td);
   c->d_acc_tiles = upload(c, acc_tiles);
   c->n_acc_tiles = static_cast<int>(acc_tiles.size());
@@ -273,6 +321,39 @@ void bo_default_config(bo_trainer_config* cfg) {
   cfg->scaler = bo_scaler_config{65536.0f, 2.0f, 0.5f, 1.0f, 16777216.0f, 2000, 1};
 }
 
+bo_status bo_bucket_layout(int32_t n_tensors, const int64_t* numels, const int32_t* firsts,
+                           uint64_t bucket_bytes, const char* const* names, const int32_t* ndims,
+                           const int64_t* dims, int32_t f16_exchange, int32_t accumulation,
+                           int32_t* bucket_of, int64_t* offset_of, int32_t* ready_order,
+                           int64_t* bucket_elems, int32_t* n_buckets, uint64_t* hash) {
+  BO_GUARD_BEGIN
+  if (!numels || !firsts) fail(BO_ERR_INVALID_CONFIG, "null argument");
+  const Layout L = Layout::build(n_tensors, numels, firsts, bucket_bytes, 1, 0);
+  for (int t = 0; t < L.T; ++t) {
+    if (bucket_of) bucket_of[t] = L.bucket_of[static_cast<size_t>(t)];
+    if (offset_of) offset_of[t] = L.offset_of[static_cast<size_t>(t)];
+    if (ready_order) ready_order[t] = L.ready[static_cast<size_t>(t)];
+  }
+  if (bucket_elems) {
+    for (int b = 0; b < L.B; ++b) bucket_elems[b] = L.elems[static_cast<size_t>(b)];
+  }
+  if (n_buckets) *n_buckets = L.B;
+  if (hash) *hash = layout_hash(L, names, ndims, dims, f16_exchange != 0, accumulation);
+  BO_GUARD_END
+}
+
+bo_status bo_shard_ranges(int32_t n_buckets, const int64_t* bucket_elems, int32_t world, int32_t rank,
+                          int64_t* lo, int64_t* hi) {
+  BO_GUARD_BEGIN
+  if (world < 1 || rank < 0 || rank >= world) fail(BO_ERR_INVALID_CONFIG, "bad rank/world");
+  for (int b = 0; b < n_buckets; ++b) {
+    const int64_t c = (bucket_elems[b] + world - 1) / world;  // collective.cpp:50-52
+    lo[b] = std::min<int64_t>(rank * c, bucket_elems[b]);
+    hi[b] = std::min<int64_t>((rank + 1) * c, bucket_elems[b]);
+  }
+  BO_GUARD_END
+}
+
 bo_status bo_create(const bo_trainer_config* cfg, int32_t n_tensors, const int64_t* numels,
                     const int32_t* first_consumers, const char* const* names, const int32_t* ndims,
                     const int64_t* dims, int32_t device, int32_t rank, int32_t world, bo_ctx** out) {
@@ -291,6 +372,7 @@ bo_status bo_create(const bo_trainer_config* cfg, int32_t n_tensors, const int64
   c->device = device;
   c->rank = rank;
   c->world = world;
+  if (const char* e = std::getenv("BO_UNFUSED")) c->force_unfused = std::strcmp(e, "0") != 0;
   c->algo = cfg->reduce_algo == BO_REDUCE_AUTO ? (cfg->f16_exchange ? BO_REDUCE_RING : BO_REDUCE_NCCL)
                                                : cfg->reduce_algo;
   BO_CUDA(cudaSetDevice(device));
@@ -315,7 +397,15 @@ bo_status bo_create(const bo_trainer_config* cfg, int32_t n_tensors, const int64
     c->wire[0] = dev_alloc(c, static_cast<size_t>(L.shard_total) * e);
     c->wire[1] = dev_alloc(c, static_cast<size_t>(L.shard_total) * e);
   }
-  c->tile_part = static_cast<double*>(dev_alloc(c, static_cast<size_t>(std::max(c->n_lamb_tiles, 1)) * 16));
+  c->tile_part = static_cast<double*>(
+      dev_alloc(c, static_cast<size_t>(std::max({c->n_lamb_tiles, c->n_fused_tiles, 1})) * 16));
+  if (world == 1) {
+    c->u = static_cast<float*>(dev_alloc(c, static_cast<size_t>(L.acc_total) * 4));
+    int nsm = 0;
+    BO_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
+    c->fused_blocks = fused_occupancy(kThreads) * nsm;
+    if (c->fused_blocks < 1) fail(BO_ERR_CUDA, "fused LAMB kernel cannot be resident");
+  }
   c->rank_part = static_cast<double*>(dev_alloc(c, static_cast<size_t>(2 * L.T + 1) * 8));
   c->all_part = world == 1 ? c->rank_part
                            : static_cast<double*>(dev_alloc(c, static_cast<size_t>(world) * (2 * L.T + 1) * 8));
@@ -471,7 +561,7 @@ bo_status bo_read_moments(bo_ctx* c, float* m, float* v, int32_t on_host) {
       const int64_t t0 = L.offset_of[static_cast<size_t>(p)], t1 = t0 + L.numel[static_cast<size_t>(p)];
       const int64_t a = std::max(lo, t0), z = std::min(hi, t1);
       if (a >= z) continue;
-      const int64_t s = L.shoff[static_cast<size_t>(b)] + (a - lo);
+      const int64_t s = L.shard_pos(b, p, a);
       const int64_t dsti = L.model_off[static_cast<size_t>(p)] + (a - t0);
       BO_CUDA(cudaMemcpyAsync(m + dsti, c->m + s, static_cast<size_t>(z - a) * 4, k, c->stream));
       BO_CUDA(cudaMemcpyAsync(v + dsti, c->v + s, static_cast<size_t>(z - a) * 4, k, c->stream));
@@ -545,10 +635,14 @@ bo_status bo_accumulate(bo_ctx* c, int32_t micro, const uint16_t* const* grads) 
     return BO_OK;
   }
   grow_bc_table(c, c->calls + 2);
-  launch_finalize(c, tab);
-  run_reduce(c);
-  run_lamb(c);
-  run_allgather(c);
+  if (c->world == 1 && aligned && !c->force_unfused) {
+    run_fused_single_rank(c, tab);
+  } else {
+    launch_finalize(c, tab);
+    run_reduce(c);
+    run_lamb(c);
+    run_allgather(c);
+  }
   c->calls += 1;
   BO_GUARD_END
 }

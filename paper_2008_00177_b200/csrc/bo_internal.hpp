@@ -63,6 +63,17 @@ struct Layout {
 
   static Layout build(int T, const int64_t* numel, const int32_t* firsts, uint64_t bucket_bytes,
                       int world, int rank);
+
+  // Positions of bucket-local element a of tensor p (bucket b) in the flat
+  // (parameter / fusion) buffer and in this rank's shard (m, v, reduced g).
+  int64_t flat_pos(int b, int p, int64_t a) const {
+    return N == 1 ? flat_off[static_cast<size_t>(p)] + (a - offset_of[static_cast<size_t>(p)])
+                  : base[static_cast<size_t>(b)] + a;
+  }
+  int64_t shard_pos(int b, int p, int64_t a) const {
+    return N == 1 ? flat_pos(b, p, a)
+                  : shoff[static_cast<size_t>(b)] + (a - rank * chunk[static_cast<size_t>(b)]);
+  }
 };
 
 // Work tiles (device tables, built once per context).
@@ -81,6 +92,24 @@ struct HopTile {        // a slice of one bucket's chunk in shard space
   int64_t s0;
   int32_t len;
   int32_t b;
+};
+
+// Single-rank fused LAMB (k_lamb_fused): a slice of one tensor; every
+// per-tensor array uses the aligned tensor layout, so one index a0 serves
+// acc, w, m, v and the u scratch; e0 indexes the caller's gradient tensor.
+struct FusedTile {
+  int64_t a0;
+  int64_t e0;
+  int32_t len;
+  int32_t t;
+  int32_t g;            // group
+  int32_t pad;
+};
+// Consecutive whole tensors whose norms are completed together; phase 2 of a
+// group runs while phase 1 of the next streams, so w and u are re-read from L2.
+struct FusedGroup {
+  int32_t tile_begin, tile_end;   // fused-tile range (phase-1 partial slots)
+  int32_t t_begin, t_end;         // tensors [t_begin, t_end) in fused order
 };
 
 // Per-tensor constants used by the accumulate / finalize kernels.
@@ -137,6 +166,21 @@ struct bo_ctx {
   int n_hop_tiles = 0;
   int64_t* d_bucket_geo = nullptr;      // [3][B]: base, chunk, shoff
 
+  // single-rank fused LAMB (world == 1)
+  bo::FusedTile* d_fused_tiles = nullptr;
+  int n_fused_tiles = 0;
+  bo::FusedGroup* d_fused_groups = nullptr;
+  int n_fused_groups = 0;
+  int* d_fused_tensor_tiles = nullptr;  // [T+1] fused-tile ranges per tensor (fused order)
+  int* d_fused_tensor_ids = nullptr;    // [T] tensor id at fused position
+  uint32_t* d_fused_work = nullptr;     // (tile << 1) | phase, execution order
+  int n_fused_work = 0;
+  unsigned long long* d_fused_sync = nullptr;  // [2 * groups + 1]: done, ready, work counter
+  float* u = nullptr;                   // LAMB update scratch (L2-resident between phases)
+  int fused_blocks = 0;
+  bool force_unfused = false;           // BO_UNFUSED=1: use the multi-kernel path on one rank
+  unsigned long long fused_epoch = 0;
+
   // device buffers
   float* acc = nullptr;
   float* x = nullptr;        // finalized local gradients, flat layout
@@ -180,7 +224,8 @@ void launch_finalize(bo_ctx* c, const PtrTable& tab);
 void run_reduce(bo_ctx* c);
 void run_lamb(bo_ctx* c);
 void run_allgather(bo_ctx* c);
-void launch_init_state(bo_ctx* c);
+void run_fused_single_rank(bo_ctx* c, const PtrTable& tab);
+int fused_occupancy(int threads);
 
 // Stage bracket: records events when profiling is on.
 struct StageTimer {

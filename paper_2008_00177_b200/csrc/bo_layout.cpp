@@ -78,6 +78,15 @@ Layout Layout::build(int T, const int64_t* numel, const int32_t* firsts, uint64_
   }
   L.acc_total = acc;
   L.P = model;
+  if (world == 1) {
+    // One rank: no collective touches the fusion buffer, so every per-tensor
+    // array (params, moments, gradients) uses the 256-byte aligned tensor
+    // layout and the LAMB kernels run fully vectorised. The bucket layout
+    // itself (bucket_of / offset_of / hash) is unchanged.
+    L.flat_off = L.acc_off;
+    L.flat_total = L.acc_total;
+    L.shard_total = L.acc_total;
+  }
   return L;
 }
 

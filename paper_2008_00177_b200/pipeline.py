@@ -88,6 +88,54 @@ def _ptr_array(ptrs) -> C.Array:
     return (C.c_void_p * len(ptrs))(*ptrs)
 
 
+@dataclass
+class BucketLayout:
+    """``BucketLayout`` (trainer.hpp:59-73) as built by the library (host only)."""
+
+    bucket_of: np.ndarray
+    offset_of: np.ndarray
+    ready_order: np.ndarray
+    bucket_elems: np.ndarray
+    hash: int
+
+    @staticmethod
+    def build(spec: ModelSpec, bucket_bytes: int, f16_exchange: bool = False,
+              accumulation: int = 1) -> "BucketLayout":
+        lib = _lib.load()
+        T = spec.n_tensors
+        numels = np.asarray(spec.numels(), np.int64)
+        firsts = np.asarray(spec.first_consumer_ids(), np.int32)
+        names = (C.c_char_p * T)(*[n.encode() for n in spec.names])
+        ndims = np.asarray([len(s) for s in spec.shapes], np.int32)
+        dims = np.asarray([d for s in spec.shapes for d in s] or [0], np.int64)
+        bo = np.empty(T, np.int32)
+        off = np.empty(T, np.int64)
+        ro = np.empty(T, np.int32)
+        be = np.empty(T, np.int64)
+        nb = C.c_int32()
+        h = C.c_uint64()
+        i64p, i32p = C.POINTER(C.c_int64), C.POINTER(C.c_int32)
+        _lib.check(lib.bo_bucket_layout(T, numels.ctypes.data_as(i64p), firsts.ctypes.data_as(i32p),
+                                        bucket_bytes, names, ndims.ctypes.data_as(i32p),
+                                        dims.ctypes.data_as(i64p), int(f16_exchange), accumulation,
+                                        bo.ctypes.data_as(i32p), off.ctypes.data_as(i64p),
+                                        ro.ctypes.data_as(i32p), be.ctypes.data_as(i64p),
+                                        C.byref(nb), C.byref(h)))
+        return BucketLayout(bo, off, ro, be[:nb.value].copy(), h.value)
+
+    def shard_ranges(self, world: int, rank: int):
+        """Bucket-local [lo, hi) this rank owns in every bucket."""
+        lib = _lib.load()
+        B = len(self.bucket_elems)
+        lo = np.empty(B, np.int64)
+        hi = np.empty(B, np.int64)
+        be = np.ascontiguousarray(self.bucket_elems, np.int64)
+        i64p = C.POINTER(C.c_int64)
+        _lib.check(lib.bo_shard_ranges(B, be.ctypes.data_as(i64p), world, rank,
+                                       lo.ctypes.data_as(i64p), hi.ctypes.data_as(i64p)))
+        return lo, hi
+
+
 class GradPipeline:
     """One rank of the device-resident gradient-to-update pipeline."""
 
@@ -164,17 +212,11 @@ class GradPipeline:
         _lib.check(self.lib.bo_comm_init(self.ctx, uid))
 
     def comm_init_torch(self) -> None:
-        """Exchange the NCCL id over an initialised torch.distributed group."""
-        import torch
-        import torch.distributed as dist
+        """Exchange the NCCL id over an initialised torch.distributed group,
+        after checking that every rank built the same bucket layout."""
+        agree_layout(self.layout_hash(), self.device)
+        self.comm_init(broadcast_unique_id(self.device))
 
-        buf = torch.zeros(128, dtype=torch.uint8)
-        if self.rank == 0:
-            buf[:] = torch.frombuffer(bytearray(self.unique_id()), dtype=torch.uint8)
-        if dist.get_backend() == "nccl":
-            buf = buf.cuda(self.device)
-        dist.broadcast(buf, 0)
-        self.comm_init(bytes(buf.cpu().numpy().tobytes()))
 
     # -- streams
     def set_stream(self, stream) -> None:
@@ -327,3 +369,40 @@ def synth_grads(dst, flat_begin: int, seed: int, rank: int, step: int, micro: in
     """Fill an int16/fp16 CUDA tensor with the synthetic spec's binary16 bits."""
     _lib.check(_lib.load().bo_synth_grads(dst.data_ptr(), flat_begin, dst.numel(), seed, rank, step,
                                           micro, scale, spike_ppm, spike_exp, _stream(stream)))
+
+
+def _dist_device(device: int):
+    import torch
+    import torch.distributed as dist
+
+    return torch.device(f"cuda:{device}") if dist.get_backend() == "nccl" else torch.device("cpu")
+
+
+def broadcast_unique_id(device: int = 0) -> bytes:
+    """Rank 0 creates the 128-byte NCCL id; torch.distributed broadcasts it."""
+    import torch
+    import torch.distributed as dist
+
+    buf = torch.zeros(128, dtype=torch.uint8)
+    if dist.get_rank() == 0:
+        buf[:] = torch.frombuffer(bytearray(GradPipeline.unique_id()), dtype=torch.uint8)
+    buf = buf.to(_dist_device(device))
+    dist.broadcast(buf, 0)
+    return bytes(buf.cpu().numpy().tobytes())
+
+
+def agree_layout(layout_hash: int, device: int = 0) -> None:
+    """All ranks must hold the same salted layout hash (trainer.cpp:169-183);
+    raises BucketLayoutMismatch otherwise."""
+    import torch
+    import torch.distributed as dist
+
+    from .errors import BucketLayoutMismatch
+
+    mine = torch.tensor([layout_hash - (1 << 64) if layout_hash >= 1 << 63 else layout_hash],
+                        dtype=torch.int64, device=_dist_device(device))
+    allh = [torch.zeros_like(mine) for _ in range(dist.get_world_size())]
+    dist.all_gather(allh, mine)
+    if any(int(h.item()) != int(mine.item()) for h in allh):
+        raise BucketLayoutMismatch(f"BucketLayoutMismatch: rank {dist.get_rank()} bucket layout "
+                                   "disagrees with peers")
