@@ -42,8 +42,11 @@ BYTES_FINALIZE_K1 = 2 + 4
 BYTES_LAMB_NORMS = 4 * 4                # read g, w, m, v
 BYTES_LAMB_UPDATE = 4 * 4 + 3 * 4       # read g, w, m, v; write w, m, v
 BYTES_LAMB_ALGO = 28                    # single-pass LAMB (the algorithmic minimum)
+BYTES_LAMB_FUSED = 2 + 4 + 3 * 4 + 3 * 4  # one rank: read h, acc, w, m, v; write w, m, v
 
-STAGES = ["accumulate", "finalize", "reduce", "lamb_norms", "trust", "lamb_update", "allgather"]
+# index = BO_STAGE_* in include/bertopt_b200.h
+STAGES = ["accumulate", "finalize", "reduce", "lamb_norms", "trust", "lamb_update", "allgather",
+          "flag", "lamb_fused"]
 
 MODELS = {"bert-large": "BERT_LARGE", "bert-large-128": "BERT_LARGE_PHASE1", "bert-base": "BERT_BASE",
           "bert-tiny": "BERT_TINY"}
@@ -279,8 +282,8 @@ def main_b200(args):
 
     # stage profile: an identical pass with CUDA events around every stage
     pipe.lib.bo_profile_enable(pipe.ctx, 1)
-    stage_ms = (C.c_double * 7)()
-    stage_n = (C.c_int64 * 7)()
+    stage_ms = (C.c_double * len(STAGES))()
+    stage_n = (C.c_int64 * len(STAGES))()
     pipe.lib.bo_profile_read(pipe.ctx, stage_ms, stage_n, 1)
     barrier()
     for _ in range(args.steps):
@@ -290,30 +293,38 @@ def main_b200(args):
     pipe.lib.bo_profile_enable(pipe.ctx, 0)
     S_shard = pipe.shard_elems()
     hbm, peak_kind = peaks()
-    per_elem = {"accumulate": None, "finalize": BYTES_FINALIZE if K > 1 else BYTES_FINALIZE_K1,
-                "lamb_norms": BYTES_LAMB_NORMS, "lamb_update": BYTES_LAMB_UPDATE}
+    E = 2 if f16 else 4
+    # algorithmic bytes per launch of each stage (HBM) / per rank (NVLink)
+    hbm_bytes = {
+        "accumulate": (BYTES_ACCUMULATE_FIRST + BYTES_ACCUMULATE * (K - 2)) * P / max(K - 1, 1),
+        "finalize": (BYTES_FINALIZE if K > 1 else BYTES_FINALIZE_K1) * P,
+        "lamb_norms": BYTES_LAMB_NORMS * S_shard,
+        "lamb_update": BYTES_LAMB_UPDATE * S_shard,
+        "flag": 2 * P,
+        "lamb_fused": (BYTES_LAMB_FUSED if K > 1 else BYTES_LAMB_FUSED - 4) * P,
+    }
+    nvl_bytes = {"reduce": (world - 1) / world * E * P, "allgather": (world - 1) / world * 4 * P}
     stages = {}
     for i, name in enumerate(STAGES):
         if stage_n[i] == 0:
             continue
         avg = stage_ms[i] / stage_n[i]
         entry = {"ms": round(avg, 5), "launches_per_step": round(stage_n[i] / args.steps, 2)}
-        if name == "accumulate":
-            nbytes = (BYTES_ACCUMULATE_FIRST + BYTES_ACCUMULATE * (K - 2)) * P / (K - 1)
-        elif name in ("finalize",):
-            nbytes = per_elem[name] * P
-        elif name in ("lamb_norms", "lamb_update"):
-            nbytes = per_elem[name] * S_shard
-        else:
-            nbytes = None
-        if nbytes:
+        if name in hbm_bytes:
+            nbytes = hbm_bytes[name]
             gbs = nbytes / (avg * 1e-3) / 1e9
             entry.update({"bytes": int(nbytes), "GB/s": round(gbs, 1), "frac": round(gbs / hbm, 4)})
+        elif name in nvl_bytes and world > 1:
+            nbytes = nvl_bytes[name]
+            gbs = nbytes / (avg * 1e-3) / 1e9
+            entry.update({"nvlink_bytes": int(nbytes), "nvlink_GB/s": round(gbs, 1),
+                          "nvlink_frac": round(gbs / NVLINK_GBS, 4)})
         stages[name] = entry
     dom = max((n for n in stages if "bytes" in stages[n]),
               key=lambda n: stages[n]["ms"] * stages[n]["launches_per_step"])
-    kernel_names = {"accumulate": "k_accumulate", "finalize": "k_finalize",
-                    "lamb_norms": "k_lamb_norms", "lamb_update": "k_lamb_update"}
+    kernel_names = {"accumulate": "k_accumulate", "finalize": "k_finalize", "flag": "k_flag",
+                    "lamb_norms": "k_lamb_norms", "lamb_update": "k_lamb_update",
+                    "lamb_fused": "k_lamb_fused"}
     roofline = {"kernel": kernel_names[dom], "bound": "hbm", "achieved": stages[dom]["GB/s"],
                 "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s", "frac": stages[dom]["frac"],
                 "traffic": traffic_from_profiles(kernel_names[dom]),

@@ -190,7 +190,9 @@ bo_status bo_accumulate(bo_ctx* ctx, int32_t micro, const uint16_t* const* grads
 #define BO_STAGE_TRUST 4        /* norm reduction, partials all-gather, trust/scaler */
 #define BO_STAGE_LAMB_UPDATE 5  /* LAMB phase 2 */
 #define BO_STAGE_ALLGATHER 6    /* parameter all-gather */
-#define BO_NUM_STAGES 7
+#define BO_STAGE_FLAG 7         /* one rank: overflow pre-check of the sync micro */
+#define BO_STAGE_LAMB_FUSED 8   /* one rank: fused pipelined LAMB (k_lamb_fused + epilogue) */
+#define BO_NUM_STAGES 9
 bo_status bo_profile_enable(bo_ctx* ctx, int32_t enable);
 /* Total milliseconds and event count per stage since the last reset; syncs. */
 bo_status bo_profile_read(bo_ctx* ctx, double* stage_ms, int64_t* stage_count, int32_t reset);
@@ -216,6 +218,12 @@ bo_status bo_unscale_gradients(float* grads, size_t n, float scale, int32_t enab
 bo_status bo_narrow_f16(const float* src, uint16_t* dst, size_t n, void* stream);
 bo_status bo_widen_f16(const uint16_t* src, float* dst, size_t n, void* stream);
 float bo_scale_loss(float loss, float scale, int32_t enabled);
+
+/* ---- device memory for hosts without the CUDA toolkit (cgo / JNI / C++) -- */
+bo_status bo_malloc(void** ptr, size_t bytes, int32_t device);
+bo_status bo_free(void* ptr);
+/* kind: 0 host->device, 1 device->host, 2 device->device; synchronous. */
+bo_status bo_memcpy(void* dst, const void* src, size_t bytes, int32_t kind);
 
 /* ---- synthetic workload (bench / test harness utility) ------------------- */
 /* fp16 gradient bits of the synthetic spec

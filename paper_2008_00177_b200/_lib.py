@@ -84,7 +84,10 @@ SIGNATURES = {
     "bo_narrow_f16": (_i32, [_vp, _vp, _sz, _vp]),
     "bo_widen_f16": (_i32, [_vp, _vp, _sz, _vp]),
     "bo_scale_loss": (C.c_float, [C.c_float, C.c_float, _i32]),
-    "bo_synth_grads": (_i32, [_vp, _i64, _i64, _u64, _i32, _i32, _i32, C.c_float, C.c_uint32, _i32, _vp]),
+    "bo_malloc": (_i32, [C.POINTER(_vp), _sz, _i32]),
+    "bo_free": (_i32, [_vp]),
+    "bo_memcpy": (_i32, [_vp, _vp, _sz, _i32]),
+    "bo_synth_grads":(_i32, [_vp, _i64, _i64, _u64, _i32, _i32, _i32, C.c_float, C.c_uint32, _i32, _vp]),
 }
 
 _lib = None

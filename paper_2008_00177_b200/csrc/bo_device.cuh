@@ -53,6 +53,21 @@ __device__ __forceinline__ T warp_sum(T x) {
   return x;
 }
 
+// Any binary16 in the packed pair x has an all-ones exponent (inf or NaN).
+__device__ __forceinline__ bool pair_nonfinite(uint32_t x) {
+  const uint32_t e = x & 0x7C007C00u;
+  return (e & 0xFFFFu) == 0x7C00u || (e >> 16) == 0x7C00u;
+}
+
+// The step's overflow flag accumulates across micro-batches: a non-finite
+// binary16 input makes the accumulated gradient non-finite (an fp32 sum of at
+// most K values <= 65504 cannot overflow on its own), so OR-ing the inputs'
+// flags equals checking the finalized gradient lamb_step would see
+// (lamb.cpp:179) on a single rank.
+__device__ __forceinline__ void raise_flag(bool bad, DevState* st) {
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&st->local_flag, 1);
+}
+
 }  // namespace bo
 
 #endif  // BO_DEVICE_CUH_

@@ -394,6 +394,29 @@ bo_status bo_widen_f16(const uint16_t* src, float* dst, size_t n, void* stream) 
 
 float bo_scale_loss(float loss, float scale, int32_t enabled) { return enabled ? loss * scale : loss; }
 
+bo_status bo_malloc(void** ptr, size_t bytes, int32_t device) {
+  BO_OP_BEGIN
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) fail(BO_ERR_NO_DEVICE, "no CUDA device visible");
+  BO_CUDA(cudaSetDevice(device));
+  BO_CUDA(cudaMalloc(ptr, std::max<size_t>(bytes, 1)));
+  BO_OP_END
+}
+
+bo_status bo_free(void* ptr) {
+  BO_OP_BEGIN
+  if (ptr) BO_CUDA(cudaFree(ptr));
+  BO_OP_END
+}
+
+bo_status bo_memcpy(void* dst, const void* src, size_t bytes, int32_t kind) {
+  BO_OP_BEGIN
+  const cudaMemcpyKind k = kind == 0 ? cudaMemcpyHostToDevice
+                           : kind == 1 ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+  if (bytes) BO_CUDA(cudaMemcpy(dst, src, bytes, k));
+  BO_OP_END
+}
+
 bo_status bo_synth_grads(uint16_t* dst, int64_t begin, int64_t n, uint64_t seed, int32_t rank,
                          int32_t step, int32_t micro, float scale, uint32_t spike_ppm,
                          int32_t spike_exp, void* stream) {

@@ -24,21 +24,6 @@ namespace {
 // acc = (micro == 0 ? 0 + g : acc + g) over one tensor slice; 16-byte loads of
 // 8 binary16 values, 2 x 16-byte fp32 accesses (trainer.cpp:240-244: the
 // accumulator starts at 0.0f, so -0 becomes +0 exactly as in the reference).
-// Any binary16 in the packed pair x has an all-ones exponent (inf or NaN).
-__device__ __forceinline__ bool pair_nonfinite(uint32_t x) {
-  const uint32_t e = x & 0x7C007C00u;
-  return (e & 0xFFFFu) == 0x7C00u || (e >> 16) == 0x7C00u;
-}
-
-// The step's overflow flag accumulates across micro-batches: a non-finite
-// binary16 input makes the accumulated gradient non-finite (an fp32 sum of at
-// most K values <= 65504 cannot overflow on its own), so OR-ing the inputs'
-// flags equals checking the finalized gradient lamb_step would see
-// (lamb.cpp:179) on a single rank.
-__device__ __forceinline__ void raise_flag(bool bad, DevState* st) {
-  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&st->local_flag, 1);
-}
-
 template <bool kVec>
 __global__ void __launch_bounds__(kThreads) k_accumulate(const AccTile* __restrict__ tiles,
                                                          const TensorDev* __restrict__ td,
@@ -87,277 +72,6 @@ __global__ void __launch_bounds__(kThreads) k_accumulate(const AccTile* __restri
     dst[i] = __fadd_rn(a, g);
   }
   raise_flag(bad, st);
-}
-
-// Overflow check of the sync micro's inputs ahead of the fused LAMB kernel,
-// which writes the moments in its first phase and so must know the step's
-// found_inf before it starts (2 bytes per parameter).
-__global__ void __launch_bounds__(kThreads) k_flag(const AccTile* __restrict__ tiles,
-                                                   const __grid_constant__ PtrTable tab,
-                                                   DevState* __restrict__ st) {
-  const AccTile tile = tiles[blockIdx.x];
-  const uint16_t* __restrict__ src = tab.p[tile.t] + tile.e0;
-  bool bad = false;
-  const int nvec = tile.len >> 3;
-#pragma unroll 2
-  for (int i = threadIdx.x; i < nvec; i += kThreads) {
-    const uint4 hv = __ldcs(reinterpret_cast<const uint4*>(src) + i);
-    bad |= pair_nonfinite(hv.x) | pair_nonfinite(hv.y) | pair_nonfinite(hv.z) | pair_nonfinite(hv.w);
-  }
-  for (int i = (nvec << 3) + threadIdx.x; i < tile.len; i += kThreads) bad |= !finite(widen(src[i]));
-  raise_flag(bad, st);
-}
-
-// ------------------------------------------------ single-rank fused LAMB
-// Cache-policy helpers: data read once streams with evict_first; w and the
-// update u, re-read by phase 2 of the same group, are kept with evict_last.
-__device__ __forceinline__ uint64_t policy_evict_first() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ uint64_t policy_evict_last() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ float4 ld4(const float* p, uint64_t pol) {
-  float4 r;
-  asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
-               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p), "l"(pol));
-  return r;
-}
-// L2-only load (the data was written by other CTAs during this launch).
-__device__ __forceinline__ float4 ld4_cg(const float* p, uint64_t pol) {
-  float4 r;
-  asm volatile("ld.global.cg.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
-               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p), "l"(pol) : "memory");
-  return r;
-}
-__device__ __forceinline__ uint2 ld2u(const uint16_t* p, uint64_t pol) {
-  uint2 r;
-  asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;"
-               : "=r"(r.x), "=r"(r.y) : "l"(p), "l"(pol));
-  return r;
-}
-__device__ __forceinline__ void st4(float* p, float4 v, uint64_t pol) {
-  asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1,%2,%3,%4}, %5;"
-               :: "l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol) : "memory");
-}
-
-__device__ __forceinline__ float elem(const float4& v, int i) {
-  return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
-}
-__device__ __forceinline__ void set_elem(float4& v, int i, float x) {
-  if (i == 0) v.x = x; else if (i == 1) v.y = x; else if (i == 2) v.z = x; else v.w = x;
-}
-
-__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-
-// One persistent, cooperative launch does the whole single-rank LAMB step
-// (lamb.cpp:140-201) reading the gradient straight from the sync micro's
-// binary16 input and the fp32 accumulator (flatten_param fused in):
-//   phase 1 (tile): g = (h + acc) * inv; m', v', u; store m', v' and u;
-//                   fp64 partials of ||w||^2, ||u||^2 for the tile
-//   group done   : the CTA finishing a group's last phase-1 tile reduces the
-//                  partials (fixed order) into the trust ratios and publishes
-//   phase 2 (tile): w -= (lr * r) * u, after the group is published
-// Work items are claimed in order P1(g0) P1(g1) P2(g0) P1(g2) P2(g1) ..., so
-// a phase-2 tile's data (w, u) is still in L2 from phase 1. found_inf is known
-// before launch (k_accumulate / k_flag); on overflow every CTA exits at once.
-__global__ void __launch_bounds__(kThreads) k_lamb_fused(
-    const FusedTile* __restrict__ tiles, const FusedGroup* __restrict__ groups,
-    const int* __restrict__ tensor_tiles, const int* __restrict__ tensor_ids,
-    const uint32_t* __restrict__ work, int n_work, const __grid_constant__ PtrTable tab,
-    const float* __restrict__ acc, float* __restrict__ w, float* __restrict__ m,
-    float* __restrict__ v, float* __restrict__ u, const DevState* __restrict__ st, LambConsts c,
-    const double* __restrict__ bc_table, int K, double* __restrict__ tile_part,
-    float* __restrict__ trust, unsigned long long* __restrict__ sync, int n_groups,
-    unsigned long long epoch) {
-  if (st->local_flag) return;  // overflow: the step is skipped
-  // sync = [done counters (reset per launch)] [work counter (reset)] [ready epochs]
-  unsigned long long* done = sync;
-  unsigned long long* counter = sync + n_groups;
-  unsigned long long* ready = sync + n_groups + 1;
-  __shared__ double bc[4];
-  __shared__ int s_item, s_last;
-  __shared__ double red[2][kThreads / 32];
-  if (threadIdx.x < 4) bc[threadIdx.x] = bc_table[4 * st->lamb_step + threadIdx.x];
-  const float inv = __fdiv_rn(1.0f, __fmul_rn(static_cast<float>(K), st->scale));
-  const uint64_t pf = policy_evict_first(), pl = policy_evict_last();
-  constexpr int kIters = kTileElems / (4 * kThreads);
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (;;) {
-    __syncthreads();
-    if (threadIdx.x == 0) s_item = static_cast<int>(atomicAdd(counter, 1ull));
-    __syncthreads();
-    const int item = s_item;
-    if (item >= n_work) break;
-    const uint32_t wk = work[item];
-    const FusedTile tile = tiles[wk >> 1];
-    const int nv = tile.len >> 2;  // float4 groups; the < 4 tail is scalar
-    if ((wk & 1u) == 0) {
-      // ---------------- phase 1
-      const uint16_t* hsrc = tab.p[tile.t] + tile.e0;
-      double wn = 0.0, un = 0.0;
-#pragma unroll
-      for (int j = 0; j < kIters; ++j) {
-        const int q = threadIdx.x + j * kThreads;
-        if (q < nv) {
-          const int64_t a = tile.a0 + 4 * q;
-          const uint2 hh = ld2u(hsrc + 4 * q, pf);
-          const float4 ac = K > 1 ? ld4(acc + a, pf) : make_float4(0.f, 0.f, 0.f, 0.f);
-          const float4 wv = ld4(w + a, pl);
-          const float4 mv = ld4(m + a, pf);
-          const float4 vv = ld4(v + a, pf);
-          const float hg[4] = {widen(static_cast<uint16_t>(hh.x & 0xFFFFu)),
-                               widen(static_cast<uint16_t>(hh.x >> 16)),
-                               widen(static_cast<uint16_t>(hh.y & 0xFFFFu)),
-                               widen(static_cast<uint16_t>(hh.y >> 16))};
-          float4 mo, vo, uo;
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const float g = __fmul_rn(K > 1 ? __fadd_rn(hg[i], elem(ac, i)) : hg[i], inv);
-            const float wi = elem(wv, i);
-            const Moments o = lamb_elem(g, wi, elem(mv, i), elem(vv, i), c, bc);
-            set_elem(mo, i, o.m);
-            set_elem(vo, i, o.v);
-            set_elem(uo, i, o.u);
-            wn = __dadd_rn(wn, __dmul_rn(static_cast<double>(wi), static_cast<double>(wi)));
-            un = __dadd_rn(un, __dmul_rn(static_cast<double>(o.u), static_cast<double>(o.u)));
-          }
-          st4(m + a, mo, pf);
-          st4(v + a, vo, pf);
-          st4(u + a, uo, pl);
-        }
-      }
-      for (int e = 4 * nv + threadIdx.x; e < tile.len; e += kThreads) {
-        const int64_t a = tile.a0 + e;
-        const float h = widen(hsrc[e]);
-        const float g = __fmul_rn(K > 1 ? __fadd_rn(h, acc[a]) : h, inv);
-        const float wi = w[a];
-        const Moments o = lamb_elem(g, wi, m[a], v[a], c, bc);
-        m[a] = o.m;
-        v[a] = o.v;
-        u[a] = o.u;
-        wn = __dadd_rn(wn, __dmul_rn(static_cast<double>(wi), static_cast<double>(wi)));
-        un = __dadd_rn(un, __dmul_rn(static_cast<double>(o.u), static_cast<double>(o.u)));
-      }
-      wn = warp_sum(wn);
-      un = warp_sum(un);
-      if (lane == 0) {
-        red[0][wid] = wn;
-        red[1][wid] = un;
-      }
-      __threadfence();  // u of this tile visible GPU-wide before the group completes
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        double a = 0.0, b = 0.0;
-        for (int i = 0; i < kThreads / 32; ++i) {
-          a += red[0][i];
-          b += red[1][i];
-        }
-        tile_part[2 * (wk >> 1)] = a;
-        tile_part[2 * (wk >> 1) + 1] = b;
-        __threadfence();
-        const FusedGroup gr = groups[tile.g];
-        const unsigned long long n = static_cast<unsigned long long>(gr.tile_end - gr.tile_begin);
-        s_last = atomicAdd(&done[tile.g], 1ull) + 1 == n;
-      }
-      __syncthreads();
-      if (s_last) {
-        // this CTA completed the group: trust ratios (lamb.cpp:192-196)
-        __threadfence();
-        const FusedGroup gr = groups[tile.g];
-        for (int f = gr.t_begin; f < gr.t_end; ++f) {
-          double a = 0.0, b = 0.0;
-          for (int i = tensor_tiles[f] + threadIdx.x; i < tensor_tiles[f + 1]; i += kThreads) {
-            a += __ldcg(tile_part + 2 * i);
-            b += __ldcg(tile_part + 2 * i + 1);
-          }
-          a = warp_sum(a);
-          b = warp_sum(b);
-          __syncthreads();
-          if (lane == 0) {
-            red[0][wid] = a;
-            red[1][wid] = b;
-          }
-          __syncthreads();
-          if (threadIdx.x == 0) {
-            double W = 0.0, U = 0.0;
-            for (int i = 0; i < kThreads / 32; ++i) {
-              W += red[0][i];
-              U += red[1][i];
-            }
-            float r = 1.0f;
-            if (W > 0.0 && U > 0.0) {
-              r = __double2float_rn(__ddiv_rn(__dsqrt_rn(W), __dsqrt_rn(U)));
-              r = fminf(fmaxf(r, 0.0f), c.clip);
-            }
-            trust[tensor_ids[f]] = r;
-          }
-        }
-        if (threadIdx.x == 0) {
-          __threadfence();
-          atomicExch(&ready[tile.g], epoch);
-        }
-      }
-    } else {
-      // ---------------- phase 2
-      if (threadIdx.x == 0) {
-        while (ld_acquire(&ready[tile.g]) < epoch) __nanosleep(128);
-      }
-      __syncthreads();
-      const float step_scale = __fmul_rn(c.lr, __ldcg(trust + tile.t));
-#pragma unroll
-      for (int j = 0; j < kIters; ++j) {
-        const int q = threadIdx.x + j * kThreads;
-        if (q < nv) {
-          const int64_t a = tile.a0 + 4 * q;
-          const float4 wv = ld4_cg(w + a, pf);
-          const float4 uv = ld4_cg(u + a, pf);
-          float4 o;
-          o.x = __fsub_rn(wv.x, __fmul_rn(step_scale, uv.x));
-          o.y = __fsub_rn(wv.y, __fmul_rn(step_scale, uv.y));
-          o.z = __fsub_rn(wv.z, __fmul_rn(step_scale, uv.z));
-          o.w = __fsub_rn(wv.w, __fmul_rn(step_scale, uv.w));
-          st4(w + a, o, pf);
-        }
-      }
-      for (int e = 4 * nv + threadIdx.x; e < tile.len; e += kThreads) {
-        const int64_t a = tile.a0 + e;
-        w[a] = __fsub_rn(__ldcg(w + a), __fmul_rn(step_scale, __ldcg(u + a)));
-      }
-    }
-  }
-}
-
-// Step bookkeeping after the fused kernel: counters and the loss-scaler state
-// machine (same transitions as k_trust).
-__global__ void k_fused_epilogue(DevState* st, ScalerConsts sc) {
-  const int found = st->local_flag != 0;
-  st->found_inf = found;
-  st->do_update = !found;
-  st->steps += 1;
-  st->local_flag = 0;
-  if (found) {
-    st->skipped += 1;
-  } else {
-    st->lamb_step += 1;
-  }
-  if (sc.dynamic) {
-    if (found) {
-      st->scale = fmaxf(__fmul_rn(st->scale, sc.backoff), sc.min_scale);
-      st->good = 0;
-    } else if (++st->good == sc.interval) {
-      st->scale = fminf(__fmul_rn(st->scale, sc.growth), sc.max_scale);
-      st->good = 0;
-    }
-  }
 }
 
 // -------------------------------------------------------------- finalize
@@ -634,39 +348,6 @@ void launch_accumulate(bo_ctx* c, int micro, const PtrTable& tab, bool vec_ok) {
                                                                      tab, c->acc, micro == 0, c->state);
   }
   check_launch(c, "k_accumulate");
-}
-
-int fused_occupancy(int threads) {
-  int nb = 0;
-  BO_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_lamb_fused, threads, 0));
-  return nb;
-}
-
-// Single-rank sync micro with 16-byte aligned inputs: overflow pre-check, the
-// fused persistent LAMB kernel, then the scaler/step epilogue.
-void run_fused_single_rank(bo_ctx* c, const PtrTable& tab) {
-  {
-    StageTimer timer(c, BO_STAGE_FINALIZE);
-    k_flag<<<c->n_acc_tiles, kThreads, 0, c->stream>>>(c->d_acc_tiles, tab, c->state);
-    check_launch(c, "k_flag");
-  }
-  StageTimer timer(c, BO_STAGE_LAMB_UPDATE);
-  BO_CUDA(cudaMemsetAsync(c->d_fused_sync, 0, static_cast<size_t>(c->n_fused_groups + 1) * 8,
-                          c->stream));
-  c->fused_epoch += 1;
-  const int K = c->cfg.accumulation;
-  const float* acc = c->acc;
-  unsigned long long epoch = c->fused_epoch;
-  int n_work = c->n_fused_work, n_groups = c->n_fused_groups;
-  void* args[] = {&c->d_fused_tiles, &c->d_fused_groups, &c->d_fused_tensor_tiles,
-                  &c->d_fused_tensor_ids, &c->d_fused_work, &n_work, const_cast<PtrTable*>(&tab),
-                  &acc, &c->w, &c->m, &c->v, &c->u, &c->state, &c->lamb, &c->bc_table,
-                  const_cast<int*>(&K), &c->tile_part, &c->trust, &c->d_fused_sync, &n_groups, &epoch};
-  BO_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_lamb_fused), c->fused_blocks,
-                                      kThreads, args, 0, c->stream));
-  check_launch(c, "k_lamb_fused");
-  k_fused_epilogue<<<1, 1, 0, c->stream>>>(c->state, c->scaler);
-  check_launch(c, "k_fused_epilogue");
 }
 
 void launch_finalize(bo_ctx* c, const PtrTable& tab) {

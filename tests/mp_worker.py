@@ -1,0 +1,118 @@
+"""Multi-GPU parity worker (one process per GPU, launched by torchrun).
+
+Every rank drives its GradPipeline with its own synthetic gradients; rank 0
+gathers parameters (replicated) and moments (sharded) and compares them with
+the CPU oracle's emulation of the same world (oracle.train). Prints one JSON
+result line on rank 0 and exits non-zero on a parity failure.
+
+    torchrun --nproc-per-node 2 --master-addr 127.0.0.1 tests/mp_worker.py \
+        --case ring16 --steps 4
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+CASES = {
+    # name: (f16_exchange, reduce_algo, K, bucket_bytes, scaler kwargs, spike_ppm, spike_exp, exact)
+    "ring16": (True, 1, 2, 8192, dict(init_scale=2.0 ** 13, growth_interval=3), 20, 3, True),
+    "ring32": (False, 1, 3, 4096, dict(init_scale=1024.0), 0, 1, True),
+    "nccl32": (False, 2, 2, 1 << 20, dict(init_scale=1024.0), 0, 1, False),
+    "ring16_1bucket": (True, 1, 1, 1 << 30, dict(init_scale=4096.0), 0, 1, True),
+    "ring16_tinybuckets": (True, 1, 2, 1, dict(init_scale=4096.0), 0, 1, True),
+}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--case", default="ring16")
+    ap.add_argument("--steps", type=int, default=4)
+    ap.add_argument("--model", default="tiny")
+    args = ap.parse_args()
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+
+    from oracle.oracle import LambConfig as OL, Oracle, ScalerConfig as OS
+    from paper_2008_00177_b200.model_spec import BERT_TINY, ModelConfig, bert_spec, flat_spec
+    from paper_2008_00177_b200.pipeline import GradPipeline, LambConfig, ScalerConfig, TrainerConfig
+    from tests.harness import max_rel_or_abs, run_pipeline
+
+    f16, algo, K, bb, sc, ppm, sexp, exact = CASES[args.case]
+    if args.model == "tiny":
+        spec = bert_spec(BERT_TINY)
+    elif args.model == "ragged":
+        spec = flat_spec([1, 7, 4099, 13, 2, 30000, 3], first_use=[3, 0, 6, 1, 5, 2, 4])
+    else:
+        spec = bert_spec(ModelConfig(layers=2, hidden=128, heads=4, vocab=3000, max_seq=64))
+    orc = Oracle()
+    p0 = orc.build_params(spec, 21)
+    P = spec.param_count()
+    inj = [(1, world - 1, K - 1, P // 3, 0x7C00)] if ppm else []
+    cfg = TrainerConfig(LambConfig(lr=5e-3), K, bb, f16, algo, ScalerConfig(**sc))
+    pipe = GradPipeline(spec, cfg, device=local, rank=rank, world=world)
+    pipe.load_params(p0)
+    pipe.comm_init_torch()
+    pipe, su, fi = run_pipeline(spec, cfg, None, args.steps, grad_seed=9, spike_ppm=ppm,
+                                spike_exp=sexp, injections=inj, rank=rank, world=world, pipe=pipe,
+                                device=local)
+    w = pipe.read_params()
+    m = np.zeros(P, np.float32)
+    v = np.zeros(P, np.float32)
+    pipe.read_moments(m, v)
+    owned = np.zeros(P, np.float32)
+    # moments are sharded: sum the per-rank scatters (each element owned once)
+    tm, tv = torch.from_numpy(m).cuda(), torch.from_numpy(v).cuda()
+    dist.all_reduce(tm)
+    dist.all_reduce(tv)
+    tw = torch.from_numpy(w).cuda()
+    allw = [torch.zeros_like(tw) for _ in range(world)]
+    dist.all_gather(allw, tw)
+    st = pipe.status()
+    result = {"rank": rank}
+    if rank == 0:
+        ref = orc.train(spec, p0, world, K, bb, f16, OL(lr=5e-3), OS(**sc), args.steps, grad_seed=9,
+                        spike_ppm=ppm, spike_exp=sexp, injections=inj)
+        mm, vv = tm.cpu().numpy(), tv.cpu().numpy()
+        replicas_equal = all(torch.equal(allw[0], x) for x in allw)
+        result.update({
+            "case": args.case, "world": world, "params": P, "steps": args.steps,
+            "found_inf": fi.tolist(), "ref_found_inf": ref.found_inf.tolist(),
+            "scales_equal": bool(np.array_equal(su, ref.scale_used)),
+            "final_scale": st.loss_scale, "ref_final_scale": ref.final_scale,
+            "lamb_step": st.lamb_step, "ref_lamb_step": ref.lamb_step,
+            "replicas_identical": bool(replicas_equal),
+            "w_rel": max_rel_or_abs(w, ref.params), "m_rel": max_rel_or_abs(mm, ref.m, 1e-12),
+            "v_rel": max_rel_or_abs(vv, ref.v, 1e-20),
+            "w_bit_exact_frac": float(np.mean(w.view(np.uint32) == ref.params.view(np.uint32))),
+            "m_bit_exact": bool(np.array_equal(mm.view(np.uint32), ref.m.view(np.uint32))),
+            "v_bit_exact": bool(np.array_equal(vv.view(np.uint32), ref.v.view(np.uint32))),
+        })
+        ok = (result["found_inf"] == result["ref_found_inf"] and result["scales_equal"]
+              and st.loss_scale == ref.final_scale and st.lamb_step == ref.lamb_step
+              and replicas_equal and result["w_rel"] <= 1e-5 and result["m_rel"] <= 1e-5
+              and result["v_rel"] <= 1e-5)
+        if exact:
+            ok = ok and result["m_bit_exact"] and result["v_bit_exact"]
+        result["ok"] = bool(ok)
+        print(json.dumps(result), flush=True)
+    del owned
+    pipe.close()
+    dist.barrier()
+    dist.destroy_process_group()
+    if rank == 0 and not result["ok"]:
+        sys.exit(1)
+
+
+if __name__ == "__main__":
+    main()

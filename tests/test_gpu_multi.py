@@ -1,0 +1,64 @@
+"""Multi-GPU parity (reduce-scatter -> sharded LAMB -> all-gather) against the
+oracle's emulation of the same world. Needs >= 2 GPUs; each case runs
+tests/mp_worker.py under torchrun, one process per GPU."""
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _ngpu():
+    torch = pytest.importorskip("torch")
+    return torch.cuda.device_count() if torch.cuda.is_available() else 0
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def run_case(case, nproc, model="tiny", steps=4):
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+           "--master-addr", "127.0.0.1", f"--master-port={_port()}",
+           os.path.join(ROOT, "tests", "mp_worker.py"), "--case", case, "--steps", str(steps),
+           "--model", model]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert lines, r.stdout[-3000:] + r.stderr[-3000:]
+    res = json.loads(lines[-1])
+    assert r.returncode == 0 and res["ok"], json.dumps(res)
+    return res
+
+
+@pytest.mark.parametrize("case", ["ring16", "ring32", "nccl32", "ring16_1bucket",
+                                  "ring16_tinybuckets"])
+def test_two_gpus(case):
+    if _ngpu() < 2:
+        pytest.skip("needs 2 GPUs")
+    res = run_case(case, 2)
+    if case.startswith("ring"):
+        assert res["m_bit_exact"] and res["v_bit_exact"]
+
+
+@pytest.mark.parametrize("model", ["ragged", "small"])
+def test_two_gpus_shapes(model):
+    if _ngpu() < 2:
+        pytest.skip("needs 2 GPUs")
+    run_case("ring16", 2, model=model)
+
+
+@pytest.mark.parametrize("n", [4, 8])
+def test_more_gpus(n):
+    if _ngpu() < n:
+        pytest.skip(f"needs {n} GPUs")
+    run_case("ring16", n)
+    run_case("nccl32", n)
