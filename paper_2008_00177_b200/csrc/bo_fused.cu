@@ -131,7 +131,9 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_lamb_fused(
     const float* __restrict__ acc, float* __restrict__ w, float* __restrict__ m,
     float* __restrict__ v, float* __restrict__ u, const DevState* __restrict__ st, LambConsts c,
     const double* __restrict__ bc_table, int K, double* __restrict__ tile_part,
-    float* __restrict__ trust, unsigned long long* __restrict__ sync, int n_groups) {
+    float* __restrict__ trust, unsigned long long* __restrict__ sync, int n_groups,
+    const int* __restrict__ sb_tiles, const int* __restrict__ tensor_sbs,
+    double* __restrict__ sb_part, int n_sb) {
   if (st->local_flag) return;  // overflow: the step is skipped (epilogue backs off)
   extern __shared__ __align__(1024) unsigned char smem[];
   unsigned char* tail = smem + kStages * kStageBytes;
@@ -140,10 +142,11 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_lamb_fused(
   StageHdr* hdr = reinterpret_cast<StageHdr*>(tail + 64);                  // [kStages]
   double* part = reinterpret_cast<double*>(tail + 256);                      // [kStages][16][2]
   int* cnt = reinterpret_cast<int*>(tail + 256 + kStages * kConsumerWarps * 16);  // [kStages]
-  // sync = [done counters (reset per launch)] [work counter (reset)] [ready epochs]
+  // sync = [group done | work counter | superblock done] (reset per launch) [ready epochs]
   unsigned long long* done = sync;
   unsigned long long* counter = sync + n_groups;
-  unsigned long long* ready = sync + n_groups + 1;
+  unsigned long long* sb_done = sync + n_groups + 1;
+  unsigned long long* ready = sync + n_groups + 1 + n_sb;
   const unsigned long long epoch = static_cast<unsigned long long>(st->steps) + 1;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -299,9 +302,31 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_lamb_fused(
           // the partials become visible GPU-wide, to generic and async proxies
           asm volatile("fence.proxy.async.global;" ::: "memory");
           __threadfence();
-          const FusedGroup gr = groups[t.g];
-          group_last = atomicAdd(&done[t.g], 1ull) + 1 ==
-                       static_cast<unsigned long long>(gr.tile_end - gr.tile_begin);
+          group_last = atomicAdd(&sb_done[t.sb], 1ull) + 1 ==
+                       static_cast<unsigned long long>(sb_tiles[t.sb + 1] - sb_tiles[t.sb]);
+        }
+        // superblock complete: its <= 32 tile partials, one per lane
+        if (__shfl_sync(0xffffffffu, group_last, 0)) {
+          __threadfence();
+          const int i = sb_tiles[t.sb] + lane;
+          double A = 0.0, B = 0.0;
+          if (i < sb_tiles[t.sb + 1]) {
+            A = __ldcg(tile_part + 2 * i);
+            B = __ldcg(tile_part + 2 * i + 1);
+          }
+          A = warp_sum(A);
+          B = warp_sum(B);
+          group_last = 0;
+          if (lane == 0) {
+            sb_part[2 * t.sb] = A;
+            sb_part[2 * t.sb + 1] = B;
+            __threadfence();
+            const FusedGroup gr = groups[t.g];
+            group_last = atomicAdd(&done[t.g], 1ull) + 1 ==
+                         static_cast<unsigned long long>(gr.sb_end - gr.sb_begin);
+          }
+        } else {
+          group_last = 0;
         }
         group_last = __shfl_sync(0xffffffffu, group_last, 0);
         if (group_last) {
@@ -310,9 +335,9 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_lamb_fused(
           const FusedGroup gr = groups[t.g];
           for (int f = gr.t_begin; f < gr.t_end; ++f) {
             double W = 0.0, U = 0.0;
-            for (int i = tensor_tiles[f] + lane; i < tensor_tiles[f + 1]; i += 32) {
-              W += __ldcg(tile_part + 2 * i);
-              U += __ldcg(tile_part + 2 * i + 1);
+            for (int i = tensor_sbs[f] + lane; i < tensor_sbs[f + 1]; i += 32) {
+              W += __ldcg(sb_part + 2 * i);
+              U += __ldcg(sb_part + 2 * i + 1);
             }
             W = warp_sum(W);
             U = warp_sum(U);
@@ -412,15 +437,16 @@ void run_fused_single_rank(bo_ctx* c, const PtrTable& tab) {
     check(c, "k_flag");
   }
   StageTimer timer(c, BO_STAGE_LAMB_FUSED);
-  BO_CUDA(cudaMemsetAsync(c->d_fused_sync, 0, static_cast<size_t>(c->n_fused_groups + 1) * 8,
-                          c->stream));
+  BO_CUDA(cudaMemsetAsync(c->d_fused_sync, 0,
+                          static_cast<size_t>(c->n_fused_groups + 1 + c->n_fused_sb) * 8, c->stream));
   const int K = c->cfg.accumulation;
   const float* acc = c->acc;
-  int n_work = c->n_fused_work, n_groups = c->n_fused_groups;
+  int n_work = c->n_fused_work, n_groups = c->n_fused_groups, n_sb = c->n_fused_sb;
   void* args[] = {&c->d_fused_tiles, &c->d_fused_groups, &c->d_fused_tensor_tiles,
                   &c->d_fused_tensor_ids, &c->d_fused_work, &n_work, const_cast<PtrTable*>(&tab),
                   &acc, &c->w, &c->m, &c->v, &c->u, &c->state, &c->lamb, &c->bc_table,
-                  const_cast<int*>(&K), &c->tile_part, &c->trust, &c->d_fused_sync, &n_groups};
+                  const_cast<int*>(&K), &c->tile_part, &c->trust, &c->d_fused_sync, &n_groups,
+                  &c->d_fused_sb_tiles, &c->d_fused_tensor_sbs, &c->sb_part, &n_sb};
   BO_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_lamb_fused), c->fused_blocks,
                                       kFusedThreads, args, kSmemBytes, c->stream));
   check(c, "k_lamb_fused");

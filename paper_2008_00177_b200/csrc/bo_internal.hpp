@@ -103,14 +103,18 @@ struct FusedTile {
   int32_t len;
   int32_t t;
   int32_t g;            // group
-  int32_t pad;
+  int32_t sb;           // superblock (<= 32 consecutive tiles of one tensor)
 };
 // Consecutive whole tensors whose norms are completed together; phase 2 of a
-// group runs while phase 1 of the next streams, so w and u are re-read from L2.
+// group runs while phase 1 of later groups streams, so w and u come from L2.
+// Norm partials reduce tile -> superblock -> tensor, each level finished by
+// whichever warp completes it (fixed summation order, so deterministic).
 struct FusedGroup {
   int32_t tile_begin, tile_end;   // fused-tile range (phase-1 partial slots)
   int32_t t_begin, t_end;         // tensors [t_begin, t_end) in fused order
+  int32_t sb_begin, sb_end;       // superblock range
 };
+constexpr int kSbTiles = 32;
 
 // Per-tensor constants used by the accumulate / finalize kernels.
 struct TensorDev {
@@ -175,7 +179,12 @@ struct bo_ctx {
   int* d_fused_tensor_ids = nullptr;    // [T] tensor id at fused position
   uint32_t* d_fused_work = nullptr;     // (tile << 1) | phase, execution order
   int n_fused_work = 0;
-  unsigned long long* d_fused_sync = nullptr;  // [2 * groups + 1]: done, ready, work counter
+  int* d_fused_sb_tiles = nullptr;      // [NSB+1] fused-tile range per superblock
+  int* d_fused_tensor_sbs = nullptr;    // [T+1] superblock range per tensor (fused order)
+  double* sb_part = nullptr;            // [NSB][2]
+  int n_fused_sb = 0;
+  // [groups] done | [1] work counter | [NSB] superblock done | [groups] ready epoch
+  unsigned long long* d_fused_sync = nullptr;
   float* u = nullptr;                   // LAMB update scratch (L2-resident between phases)
   int fused_blocks = 0;
   bool force_unfused = false;           // BO_UNFUSED=1: use the multi-kernel path on one rank
