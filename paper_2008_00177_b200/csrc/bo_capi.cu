@@ -86,75 +86,23 @@ void upload_tables(bo_ctx* c) {
   geo.insert(geo.end(), L.shoff.begin(), L.shoff.end());
 
   if (c->world == 1) {
-    // Fused single-rank LAMB: tiles in model order, groups of consecutive whole
-    // tensors of ~1M elements. Phase 2 of a group is scheduled once ~2M more
-    // elements of phase 1 have been issued after it: slack for the group's
-    // last tiles and its trust reduction, while the window's w + u
-    // (8 B/element) stays well inside L2.
-    constexpr int64_t kGroupElems = 1 << 20;
-    constexpr int64_t kLagElems = 2 << 20;
+    // Single-rank LAMB (bo_fused.cu): tiles of <= kTileElems elements of one
+    // tensor, model order, in the aligned tensor layout; per-tensor tile
+    // ranges for the fixed-order norm reduction.
     std::vector<FusedTile> ft;
-    std::vector<FusedGroup> fg;
-    std::vector<int> ttiles(static_cast<size_t>(L.T) + 1), tids(static_cast<size_t>(L.T));
-    std::vector<int> sb_tiles, tsbs(static_cast<size_t>(L.T) + 1);
-    int64_t cur = 0;
+    std::vector<int> ttiles(static_cast<size_t>(L.T) + 1);
     for (int t = 0; t < L.T; ++t) {
       const int64_t n = L.numel[static_cast<size_t>(t)];
-      if (fg.empty() || (cur > 0 && cur + n > kGroupElems)) {
-        fg.push_back(FusedGroup{static_cast<int32_t>(ft.size()), 0, t, 0,
-                                static_cast<int32_t>(sb_tiles.size()), 0});
-        cur = 0;
-      }
-      tids[static_cast<size_t>(t)] = t;
       ttiles[static_cast<size_t>(t)] = static_cast<int>(ft.size());
-      tsbs[static_cast<size_t>(t)] = static_cast<int>(sb_tiles.size());
-      int k = 0;
-      for (int64_t e = 0; e < n; e += kTileElems, ++k) {
-        if (k % kSbTiles == 0) sb_tiles.push_back(static_cast<int>(ft.size()));
+      for (int64_t e = 0; e < n; e += kTileElems) {
         ft.push_back(FusedTile{L.acc_off[static_cast<size_t>(t)] + e, e,
-                               static_cast<int32_t>(std::min<int64_t>(kTileElems, n - e)), t,
-                               static_cast<int32_t>(fg.size()) - 1,
-                               static_cast<int32_t>(sb_tiles.size()) - 1});
+                               static_cast<int32_t>(std::min<int64_t>(kTileElems, n - e)), t});
       }
-      cur += n;
-      fg.back().tile_end = static_cast<int32_t>(ft.size());
-      fg.back().t_end = t + 1;
-      fg.back().sb_end = static_cast<int32_t>(sb_tiles.size());
     }
     ttiles[static_cast<size_t>(L.T)] = static_cast<int>(ft.size());
-    tsbs[static_cast<size_t>(L.T)] = static_cast<int>(sb_tiles.size());
-    const int nsb = static_cast<int>(sb_tiles.size());
-    sb_tiles.push_back(static_cast<int>(ft.size()));
-    std::vector<uint32_t> work;
-    auto phase = [&](int g, uint32_t ph) {
-      for (int i = fg[static_cast<size_t>(g)].tile_begin; i < fg[static_cast<size_t>(g)].tile_end; ++i) {
-        work.push_back((static_cast<uint32_t>(i) << 1) | ph);
-      }
-    };
-    // Phase 1 of every tile, then phase 2 in reverse tile order: a phase-2
-    // tile then waits for nothing but the (long finished) norms of its group,
-    // and the last phase-1 tiles' w and u are still in L2 when phase 2
-    // starts. (Interleaving P2(g) shortly after P1(g) keeps all of w and u in
-    // L2 but makes every group a grid-wide rendezvous; measured slower.)
-    (void)kLagElems;
-    for (int g = 0; g < static_cast<int>(fg.size()); ++g) phase(g, 0);
-    for (int i = static_cast<int>(ft.size()) - 1; i >= 0; --i) {
-      work.push_back((static_cast<uint32_t>(i) << 1) | 1u);
-    }
     c->d_fused_tiles = upload(c, ft);
     c->n_fused_tiles = static_cast<int>(ft.size());
-    c->d_fused_groups = upload(c, fg);
-    c->n_fused_groups = static_cast<int>(fg.size());
     c->d_fused_tensor_tiles = upload(c, ttiles);
-    c->d_fused_tensor_ids = upload(c, tids);
-    c->d_fused_work = upload(c, work);
-    c->n_fused_work = static_cast<int>(work.size());
-    c->d_fused_sb_tiles = upload(c, sb_tiles);
-    c->d_fused_tensor_sbs = upload(c, tsbs);
-    c->n_fused_sb = nsb;
-    c->sb_part = static_cast<double*>(dev_alloc(c, static_cast<size_t>(nsb) * 16));
-    c->d_fused_sync = static_cast<unsigned long long*>(
-        dev_alloc(c, (2 * fg.size() + 1 + static_cast<size_t>(nsb)) * 8));
   }
   c->d_tensors = upload(c, td);
   c->d_acc_tiles = upload(c, acc_tiles);
@@ -423,13 +371,7 @@ bo_status bo_create(const bo_trainer_config* cfg, int32_t n_tensors, const int64
   }
   c->tile_part = static_cast<double*>(
       dev_alloc(c, static_cast<size_t>(std::max({c->n_lamb_tiles, c->n_fused_tiles, 1})) * 16));
-  if (world == 1) {
-    c->u = static_cast<float*>(dev_alloc(c, static_cast<size_t>(L.acc_total) * 4));
-    int nsm = 0;
-    BO_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
-    c->fused_blocks = fused_occupancy(kThreads) * nsm;
-    if (c->fused_blocks < 1) fail(BO_ERR_CUDA, "fused LAMB kernel cannot be resident");
-  }
+  if (world == 1) c->u = static_cast<float*>(dev_alloc(c, static_cast<size_t>(L.acc_total) * 4));
   c->rank_part = static_cast<double*>(dev_alloc(c, static_cast<size_t>(2 * L.T + 1) * 8));
   c->all_part = world == 1 ? c->rank_part
                            : static_cast<double*>(dev_alloc(c, static_cast<size_t>(world) * (2 * L.T + 1) * 8));

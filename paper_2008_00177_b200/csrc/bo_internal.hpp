@@ -94,27 +94,15 @@ struct HopTile {        // a slice of one bucket's chunk in shard space
   int32_t b;
 };
 
-// Single-rank fused LAMB (k_lamb_fused): a slice of one tensor; every
-// per-tensor array uses the aligned tensor layout, so one index a0 serves
-// acc, w, m, v and the u scratch; e0 indexes the caller's gradient tensor.
+// Single-rank LAMB (bo_fused.cu): a slice of one tensor; every per-tensor
+// array uses the aligned tensor layout, so one index a0 serves acc, w, m, v
+// and the update scratch u; e0 indexes the caller's gradient tensor.
 struct FusedTile {
   int64_t a0;
   int64_t e0;
   int32_t len;
   int32_t t;
-  int32_t g;            // group
-  int32_t sb;           // superblock (<= 32 consecutive tiles of one tensor)
 };
-// Consecutive whole tensors whose norms are completed together; phase 2 of a
-// group runs while phase 1 of later groups streams, so w and u come from L2.
-// Norm partials reduce tile -> superblock -> tensor, each level finished by
-// whichever warp completes it (fixed summation order, so deterministic).
-struct FusedGroup {
-  int32_t tile_begin, tile_end;   // fused-tile range (phase-1 partial slots)
-  int32_t t_begin, t_end;         // tensors [t_begin, t_end) in fused order
-  int32_t sb_begin, sb_end;       // superblock range
-};
-constexpr int kSbTiles = 32;
 
 // Per-tensor constants used by the accumulate / finalize kernels.
 struct TensorDev {
@@ -173,20 +161,8 @@ struct bo_ctx {
   // single-rank fused LAMB (world == 1)
   bo::FusedTile* d_fused_tiles = nullptr;
   int n_fused_tiles = 0;
-  bo::FusedGroup* d_fused_groups = nullptr;
-  int n_fused_groups = 0;
-  int* d_fused_tensor_tiles = nullptr;  // [T+1] fused-tile ranges per tensor (fused order)
-  int* d_fused_tensor_ids = nullptr;    // [T] tensor id at fused position
-  uint32_t* d_fused_work = nullptr;     // (tile << 1) | phase, execution order
-  int n_fused_work = 0;
-  int* d_fused_sb_tiles = nullptr;      // [NSB+1] fused-tile range per superblock
-  int* d_fused_tensor_sbs = nullptr;    // [T+1] superblock range per tensor (fused order)
-  double* sb_part = nullptr;            // [NSB][2]
-  int n_fused_sb = 0;
-  // [groups] done | [1] work counter | [NSB] superblock done | [groups] ready epoch
-  unsigned long long* d_fused_sync = nullptr;
-  float* u = nullptr;                   // LAMB update scratch (L2-resident between phases)
-  int fused_blocks = 0;
+  int* d_fused_tensor_tiles = nullptr;  // [T+1] fused-tile ranges per tensor
+  float* u = nullptr;                   // LAMB update scratch
   bool force_unfused = false;           // BO_UNFUSED=1: use the multi-kernel path on one rank
   unsigned long long fused_epoch = 0;
 
@@ -234,7 +210,6 @@ void run_reduce(bo_ctx* c);
 void run_lamb(bo_ctx* c);
 void run_allgather(bo_ctx* c);
 void run_fused_single_rank(bo_ctx* c, const PtrTable& tab);
-int fused_occupancy(int threads);
 
 // Stage bracket: records events when profiling is on.
 struct StageTimer {
