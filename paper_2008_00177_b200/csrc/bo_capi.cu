@@ -104,6 +104,31 @@ void upload_tables(bo_ctx* c) {
     c->n_fused_tiles = static_cast<int>(ft.size());
     c->d_fused_tensor_tiles = upload(c, ttiles);
   }
+  if (c->world > 1) {
+    // Ring hops with the finalize fused in: for every chunk index q, the
+    // valid (non-padding) elements of chunk q of every bucket, split at tensor
+    // boundaries, in shard order.
+    std::vector<HopXTile> hx;
+    c->hopx_begin.assign(static_cast<size_t>(c->world) + 1, 0);
+    for (int qq = 0; qq < c->world; ++qq) {
+      c->hopx_begin[static_cast<size_t>(qq)] = static_cast<int>(hx.size());
+      for (int b = 0; b < L.B; ++b) {
+        const int64_t cb = L.chunk[static_cast<size_t>(b)];
+        const int64_t lo = qq * cb;
+        const int64_t hi = std::min<int64_t>((qq + 1) * cb, L.elems[static_cast<size_t>(b)]);
+        for (int p : L.buckets[static_cast<size_t>(b)]) {
+          const int64_t t0 = L.offset_of[static_cast<size_t>(p)];
+          const int64_t a = std::max(lo, t0), z = std::min(hi, t0 + L.numel[static_cast<size_t>(p)]);
+          for (int64_t e = a; e < z; e += kTileElems) {
+            hx.push_back(HopXTile{L.shoff[static_cast<size_t>(b)] + (e - lo), e - t0,
+                                  static_cast<int32_t>(std::min<int64_t>(kTileElems, z - e)), p});
+          }
+        }
+      }
+    }
+    c->hopx_begin[static_cast<size_t>(c->world)] = static_cast<int>(hx.size());
+    c->d_hopx_tiles = upload(c, hx);
+  }
   c->d_tensors = upload(c, td);
   c->d_acc_tiles = upload(c, acc_tiles);
   c->n_acc_tiles = static_cast<int>(acc_tiles.size());
@@ -359,8 +384,13 @@ bo_status bo_create(const bo_trainer_config* cfg, int32_t n_tensors, const int64
                            cfg->scaler.max_scale, cfg->scaler.growth_interval, cfg->scaler.dynamic};
   upload_tables(c);
   c->acc = static_cast<float*>(dev_alloc(c, static_cast<size_t>(L.acc_total) * 4));
-  c->x = static_cast<float*>(dev_alloc(c, static_cast<size_t>(L.flat_total) * 4));
-  c->gshard = world == 1 ? c->x : static_cast<float*>(dev_alloc(c, static_cast<size_t>(L.shard_total) * 4));
+  // the fusion buffer x and the fp32 reduced shard exist only where a kernel
+  // materialises them: one rank's multi-kernel fallback and the NCCL wire (the
+  // ring computes x inside its hops and LAMB reads the final wire buffer)
+  if (world == 1 || c->algo == BO_REDUCE_NCCL) {
+    c->x = static_cast<float*>(dev_alloc(c, static_cast<size_t>(L.flat_total) * 4));
+    c->gshard = world == 1 ? c->x : static_cast<float*>(dev_alloc(c, static_cast<size_t>(L.shard_total) * 4));
+  }
   c->w = static_cast<float*>(dev_alloc(c, static_cast<size_t>(L.flat_total) * 4));
   c->m = static_cast<float*>(dev_alloc(c, static_cast<size_t>(L.shard_total) * 4));
   c->v = static_cast<float*>(dev_alloc(c, static_cast<size_t>(L.shard_total) * 4));
@@ -604,8 +634,9 @@ bo_status bo_accumulate(bo_ctx* c, int32_t micro, const uint16_t* const* grads) 
   if (c->world == 1 && aligned && !c->force_unfused) {
     run_fused_single_rank(c, tab);
   } else {
-    launch_finalize(c, tab);
-    run_reduce(c);
+    // the ring fuses flatten_param into its hops; NCCL needs the fusion buffer
+    if (c->world == 1 || c->algo == BO_REDUCE_NCCL) launch_finalize(c, tab);
+    run_reduce(c, tab);
     run_lamb(c);
     run_allgather(c);
   }

@@ -29,6 +29,53 @@ __device__ __forceinline__ float div_to_float(float x, double d, double inv_d) {
   return __double2float_rn(q);
 }
 
+// Fast path of div_to_float: the product and whether the exact division is
+// needed (result within 16 double-ulps of a binary32 midpoint, or binary32
+// subnormal range).
+__device__ __forceinline__ float div_to_float_fast(float x, double inv_d, bool& need_exact) {
+  const double q = __dmul_rn(static_cast<double>(x), inv_d);
+  const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(q));
+  const unsigned low = static_cast<unsigned>(b & 0x1FFFFFFFull) - 0x0FFFFFF0u;  // in [0, 32] near a midpoint
+  const unsigned e = static_cast<unsigned>((b >> 52) & 0x7FF);
+  need_exact |= (e < 898u) | (low <= 32u);
+  return __double2float_rn(q);
+}
+
+// Four LAMB elements (lamb.cpp:183-187, operation order kept) with one rarely
+// taken branch for the exact double divisions instead of one per value.
+struct Lamb4 {
+  float m[4], v[4], u[4];
+};
+
+template <typename C>
+__device__ __forceinline__ Lamb4 lamb_elem4(const float (&g)[4], const float (&w)[4],
+                                            const float (&m)[4], const float (&v)[4], const C& c,
+                                            double bc1, double bc2, double ibc1, double ibc2) {
+  Lamb4 o;
+  float mh[4], vh[4];
+  bool need = false;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    o.m[i] = __fadd_rn(__fmul_rn(c.beta1, m[i]), __fmul_rn(c.omb1, g[i]));
+    o.v[i] = __fadd_rn(__fmul_rn(c.beta2, v[i]), __fmul_rn(__fmul_rn(c.omb2, g[i]), g[i]));
+    mh[i] = div_to_float_fast(o.m[i], ibc1, need);
+    vh[i] = div_to_float_fast(o.v[i], ibc2, need);
+  }
+  if (__builtin_expect(need, 0)) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      mh[i] = __double2float_rn(__ddiv_rn(static_cast<double>(o.m[i]), bc1));
+      vh[i] = __double2float_rn(__ddiv_rn(static_cast<double>(o.v[i]), bc2));
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float den = __fadd_rn(__fsqrt_rn(vh[i]), c.eps);
+    o.u[i] = __fadd_rn(__fdiv_rn(mh[i], den), __fmul_rn(c.wd, w[i]));
+  }
+  return o;
+}
+
 struct Moments {
   float m, v, u;
 };

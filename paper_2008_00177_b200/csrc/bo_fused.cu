@@ -59,8 +59,7 @@ __device__ __forceinline__ uint2 ld2u(const uint16_t* p, uint64_t pol) {
 }
 __device__ __forceinline__ void st4(float* p, float4 v, uint64_t pol) {
   asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "f"(v.x),
-               "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol)
-               : "memory");
+               "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol));
 }
 __device__ __forceinline__ float at(const float4& v, int i) {
   return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
@@ -93,9 +92,9 @@ __global__ void __launch_bounds__(kP1Threads, 2) k_lamb_p1(
     float* __restrict__ v, float* __restrict__ u, const DevState* __restrict__ st, LambConsts c,
     const double* __restrict__ bc_table, int K, double* __restrict__ tile_part) {
   if (st->local_flag) return;  // overflow: the step is skipped
-  __shared__ double bc[4];
   __shared__ double red[2][kP1Threads / 32];
-  if (threadIdx.x < 4) bc[threadIdx.x] = bc_table[4 * st->lamb_step + threadIdx.x];
+  const double* bcp = bc_table + 4 * st->lamb_step;
+  const double bc1 = bcp[0], bc2 = bcp[1], ibc1 = bcp[2], ibc2 = bcp[3];
   const FusedTile t = tiles[blockIdx.x];
   const float inv = __fdiv_rn(1.0f, __fmul_rn(static_cast<float>(K), st->scale));
   const uint64_t pf = policy_evict_first(), pl = policy_evict_last();
@@ -114,29 +113,43 @@ __global__ void __launch_bounds__(kP1Threads, 2) k_lamb_p1(
       vv[j] = ld4(v + a, pf);
     }
   }
-  __syncthreads();  // bc
   double wn = 0.0, un = 0.0;
 #pragma unroll
   for (int j = 0; j < 2; ++j) {
     const int e0 = 4 * (threadIdx.x + j * kP1Threads);
     if (e0 >= t.len) continue;
+    const int n = min(4, t.len - e0);  // < 4 only in a tensor's last float4
     const float hg[4] = {widen(static_cast<uint16_t>(hv[j].x & 0xFFFFu)),
                          widen(static_cast<uint16_t>(hv[j].x >> 16)),
                          widen(static_cast<uint16_t>(hv[j].y & 0xFFFFu)),
                          widen(static_cast<uint16_t>(hv[j].y >> 16))};
-    float4 mo = mv[j], vo = vv[j], uo = make_float4(0.f, 0.f, 0.f, 0.f);
-    const int n = min(4, t.len - e0);
+    const float wa[4] = {wv[j].x, wv[j].y, wv[j].z, wv[j].w};
+    const float ma[4] = {mv[j].x, mv[j].y, mv[j].z, mv[j].w};
+    const float va[4] = {vv[j].x, vv[j].y, vv[j].z, vv[j].w};
+    const float aa[4] = {av[j].x, av[j].y, av[j].z, av[j].w};
+    float ga[4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      if (i < n) {
-        const float g = __fmul_rn(K > 1 ? __fadd_rn(hg[i], at(av[j], i)) : hg[i], inv);
-        const float wi = at(wv[j], i);
-        const Moments o = lamb_elem(g, wi, at(mv[j], i), at(vv[j], i), c, bc);
-        put(mo, i, o.m);
-        put(vo, i, o.v);
-        put(uo, i, o.u);
-        wn = __dadd_rn(wn, __dmul_rn(static_cast<double>(wi), static_cast<double>(wi)));
-        un = __dadd_rn(un, __dmul_rn(static_cast<double>(o.u), static_cast<double>(o.u)));
+    for (int i = 0; i < 4; ++i) ga[i] = __fmul_rn(K > 1 ? __fadd_rn(hg[i], aa[i]) : hg[i], inv);
+    const Lamb4 o = lamb_elem4(ga, wa, ma, va, c, bc1, bc2, ibc1, ibc2);
+    float4 mo = make_float4(o.m[0], o.m[1], o.m[2], o.m[3]);
+    float4 vo = make_float4(o.v[0], o.v[1], o.v[2], o.v[3]);
+    float4 uo = make_float4(o.u[0], o.u[1], o.u[2], o.u[3]);
+    if (n == 4) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        wn = __dadd_rn(wn, __dmul_rn(static_cast<double>(wa[i]), static_cast<double>(wa[i])));
+        un = __dadd_rn(un, __dmul_rn(static_cast<double>(o.u[i]), static_cast<double>(o.u[i])));
+      }
+    } else {
+      // padding lanes past len keep their old m/v bits and contribute nothing
+      for (int i = n; i < 4; ++i) {
+        put(mo, i, ma[i]);
+        put(vo, i, va[i]);
+        put(uo, i, 0.0f);
+      }
+      for (int i = 0; i < n; ++i) {
+        wn = __dadd_rn(wn, __dmul_rn(static_cast<double>(wa[i]), static_cast<double>(wa[i])));
+        un = __dadd_rn(un, __dmul_rn(static_cast<double>(o.u[i]), static_cast<double>(o.u[i])));
       }
     }
     const int64_t a = t.a0 + e0;

@@ -93,6 +93,16 @@ struct HopTile {        // a slice of one bucket's chunk in shard space
   int32_t len;
   int32_t b;
 };
+// Ring hop with the finalize fused in: a slice of one tensor inside chunk q of
+// one bucket. x = (h + acc) * inv is computed on the fly from the caller's
+// binary16 gradient and the accumulator instead of a materialised fusion
+// buffer (each element of x is needed by exactly one hop).
+struct HopXTile {
+  int64_t s0;           // shard (wire staging) index of the first element
+  int64_t e0;           // element offset inside tensor t
+  int32_t len;
+  int32_t t;
+};
 
 // Single-rank LAMB (bo_fused.cu): a slice of one tensor; every per-tensor
 // array uses the aligned tensor layout, so one index a0 serves acc, w, m, v
@@ -157,6 +167,8 @@ struct bo_ctx {
   bo::HopTile* d_hop_tiles = nullptr;
   int n_hop_tiles = 0;
   int64_t* d_bucket_geo = nullptr;      // [3][B]: base, chunk, shoff
+  bo::HopXTile* d_hopx_tiles = nullptr; // ring hops with fused finalize, grouped by chunk
+  std::vector<int> hopx_begin;          // [N+1] tile range of chunk q
 
   // single-rank fused LAMB (world == 1)
   bo::FusedTile* d_fused_tiles = nullptr;
@@ -206,7 +218,7 @@ void grow_bc_table(bo_ctx* c, int64_t need);
 // kernels / pipeline stages (bo_pipeline.cu)
 void launch_accumulate(bo_ctx* c, int micro, const PtrTable& tab, bool vec_ok);
 void launch_finalize(bo_ctx* c, const PtrTable& tab);
-void run_reduce(bo_ctx* c);
+void run_reduce(bo_ctx* c, const PtrTable& tab);
 void run_lamb(bo_ctx* c);
 void run_allgather(bo_ctx* c);
 void run_fused_single_rank(bo_ctx* c, const PtrTable& tab);

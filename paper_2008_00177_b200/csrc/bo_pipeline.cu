@@ -153,12 +153,50 @@ __global__ void __launch_bounds__(kThreads) k_unwire(const HopTile* __restrict__
   for (int e = threadIdx.x; e < tile.len; e += kThreads) g[tile.s0 + e] = from_wire(in[tile.s0 + e]);
 }
 
+// Ring hop with flatten_param fused in (trainer.cpp:186-203 + collective.hpp:65-80
+// / collective.cpp:170-190): x = (h + acc) * inv for the elements of chunk q,
+// out = wire(x) (combine == 0, the first send) or wire(from_wire(in) + x).
+template <typename W>
+__global__ void __launch_bounds__(kThreads) k_hopx(const HopXTile* __restrict__ tiles,
+                                                   const TensorDev* __restrict__ td,
+                                                   const __grid_constant__ PtrTable tab,
+                                                   const float* __restrict__ acc,
+                                                   const DevState* __restrict__ st, int K,
+                                                   const W* __restrict__ in, W* __restrict__ out,
+                                                   int combine) {
+  const HopXTile tile = tiles[blockIdx.x];
+  const float inv = __fdiv_rn(1.0f, __fmul_rn(static_cast<float>(K), st->scale));
+  const uint16_t* __restrict__ h = tab.p[tile.t] + tile.e0;
+  const float* __restrict__ a = acc + td[tile.t].acc_off + tile.e0;
+  constexpr int kPer = kTileElems / kThreads;
+  float xv[kPer];
+#pragma unroll
+  for (int j = 0; j < kPer; ++j) {
+    const int e = threadIdx.x + j * kThreads;
+    xv[j] = 0.0f;
+    if (e < tile.len) {
+      const float g = widen(__ldcs(h + e));
+      xv[j] = __fmul_rn(K > 1 ? __fadd_rn(g, __ldcs(a + e)) : g, inv);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < kPer; ++j) {
+    const int e = threadIdx.x + j * kThreads;
+    if (e < tile.len) {
+      float p = xv[j];
+      if (combine) p = __fadd_rn(from_wire(__ldcs(in + tile.s0 + e)), p);
+      out[tile.s0 + e] = to_wire<W>(p);
+    }
+  }
+}
+
 // ------------------------------------------------------------------- LAMB
 // Phase 1: per-tile fp64 partials of ||w||^2 and ||u||^2 and the non-finite
 // flag of the reduced gradient (lamb.cpp:176-190; the flag is the
 // NonFiniteGradient condition, lamb.cpp:179). Nothing is written to w/m/v.
+template <typename G>
 __global__ void __launch_bounds__(kThreads) k_lamb_norms(const LambTile* __restrict__ tiles,
-                                                         const float* __restrict__ g,
+                                                         const G* __restrict__ g,
                                                          const float* __restrict__ w,
                                                          const float* __restrict__ m,
                                                          const float* __restrict__ v,
@@ -180,7 +218,7 @@ __global__ void __launch_bounds__(kThreads) k_lamb_norms(const LambTile* __restr
   for (int j = 0; j < kPer; ++j) {
     const int e = threadIdx.x + j * kThreads;
     if (e < tile.len) {
-      float gi = __ldcs(g + tile.s0 + e);
+      float gi = from_wire(__ldcs(g + tile.s0 + e));
       if (scale_g) gi = __fmul_rn(gi, invn);
       const float wi = w[tile.w0 + e];
       bad |= !finite(gi);
@@ -293,8 +331,9 @@ __global__ void __launch_bounds__(1024) k_trust(const double* __restrict__ all_p
 
 // Phase 2: recompute the element (bit-identical to phase 1) and apply
 // w -= (lr * r) * u, storing w, m, v (lamb.cpp:197-198). Skipped steps exit.
+template <typename G>
 __global__ void __launch_bounds__(kThreads) k_lamb_update(const LambTile* __restrict__ tiles,
-                                                          const float* __restrict__ g,
+                                                          const G* __restrict__ g,
                                                           float* __restrict__ w,
                                                           float* __restrict__ m,
                                                           float* __restrict__ v,
@@ -314,7 +353,7 @@ __global__ void __launch_bounds__(kThreads) k_lamb_update(const LambTile* __rest
   for (int j = 0; j < kPer; ++j) {
     const int e = threadIdx.x + j * kThreads;
     if (e < tile.len) {
-      float gi = __ldcs(g + tile.s0 + e);
+      float gi = from_wire(__ldcs(g + tile.s0 + e));
       if (scale_g) gi = __fmul_rn(gi, invn);
       const float wi = w[tile.w0 + e];
       const Moments o = lamb_elem(gi, wi, m[tile.s0 + e], v[tile.s0 + e], c, bc);
@@ -357,38 +396,46 @@ void launch_finalize(bo_ctx* c, const PtrTable& tab) {
   check_launch(c, "k_finalize");
 }
 
+// The reference ring's reduce-scatter phase (collective.hpp:65-80, binary16
+// wire collective.cpp:170-190) with flatten_param fused into every hop: the
+// local addend x of chunk q is computed from the sync micro's binary16 input
+// and the accumulator as the hop needs it. One grouped ncclSend/ncclRecv of
+// one contiguous message (all buckets' current chunks) per hop.
 template <typename W>
-static void ring_reduce_scatter(bo_ctx* c, ncclDataType_t dt) {
+static void ring_reduce_scatter(bo_ctx* c, const PtrTable& tab, ncclDataType_t dt) {
   const int N = c->world, r = c->rank;
   const int right = (r + 1) % N, left = (r - 1 + N) % N;
   const size_t S = static_cast<size_t>(c->L.shard_total);
   W* a = static_cast<W*>(c->wire[0]);
   W* b = static_cast<W*>(c->wire[1]);
-  const BucketGeo geo = geo_of(c);
-  // hop 0 payload: this rank's own chunk r, narrowed (collective.cpp:178)
-  k_hop<W><<<c->n_hop_tiles, kThreads, 0, c->stream>>>(c->d_hop_tiles, geo, c->x, nullptr, a, r, 0);
-  check_launch(c, "k_hop(pack)");
+  const int K = c->cfg.accumulation;
+  auto hop = [&](int q, const W* in, W* out, int combine) {
+    const int t0 = c->hopx_begin[static_cast<size_t>(q)], t1 = c->hopx_begin[static_cast<size_t>(q) + 1];
+    if (t1 > t0) {
+      k_hopx<W><<<t1 - t0, kThreads, 0, c->stream>>>(c->d_hopx_tiles + t0, c->d_tensors, tab, c->acc,
+                                                      c->state, K, in, out, combine);
+      check_launch(c, "k_hopx");
+    }
+  };
+  hop(r, nullptr, a, 0);  // hop 0 payload: this rank's own chunk r (collective.cpp:178)
   for (int s = 0; s < N - 1; ++s) {
     BO_NCCL(ncclGroupStart());
     BO_NCCL(ncclSend(a, S, dt, right, c->comm, c->stream));
     BO_NCCL(ncclRecv(b, S, dt, left, c->comm, c->stream));
     BO_NCCL(ncclGroupEnd());
-    const int q = (r - s - 1 + 2 * N) % N;  // chunk received at hop s (collective.hpp:70-71)
-    k_hop<W><<<c->n_hop_tiles, kThreads, 0, c->stream>>>(c->d_hop_tiles, geo, c->x, b, a, q, 1);
-    check_launch(c, "k_hop");
+    hop((r - s - 1 + 2 * N) % N, b, a, 1);  // chunk received at hop s (collective.hpp:70-71)
   }
-  // After N-1 hops rank r holds the finished chunk (r+1) % N. One more hop
-  // hands it to rank r+1, so that rank r owns chunk r (the ncclAllGather
-  // placement); the payload is already wire-exact, so this moves no bits.
+  // After N-1 hops rank r holds the finished chunk (r+1) % N (already
+  // wire-rounded: the owner re-round of collective.cpp:205-209). One more
+  // hop hands it to rank r+1, so rank r owns chunk r (the ncclAllGather
+  // placement). LAMB reads the wire buffer b directly.
   BO_NCCL(ncclGroupStart());
   BO_NCCL(ncclSend(a, S, dt, right, c->comm, c->stream));
   BO_NCCL(ncclRecv(b, S, dt, left, c->comm, c->stream));
   BO_NCCL(ncclGroupEnd());
-  k_unwire<W><<<c->n_hop_tiles, kThreads, 0, c->stream>>>(c->d_hop_tiles, b, c->gshard);
-  check_launch(c, "k_unwire");
 }
 
-void run_reduce(bo_ctx* c) {
+void run_reduce(bo_ctx* c, const PtrTable& tab) {
   if (c->world == 1) return;
   StageTimer timer(c, BO_STAGE_REDUCE);
   if (c->algo == BO_REDUCE_NCCL) {
@@ -400,21 +447,22 @@ void run_reduce(bo_ctx* c) {
     }
     BO_NCCL(ncclGroupEnd());
   } else if (c->cfg.f16_exchange) {
-    ring_reduce_scatter<uint16_t>(c, ncclFloat16);
+    ring_reduce_scatter<uint16_t>(c, tab, ncclFloat16);
   } else {
-    ring_reduce_scatter<float>(c, ncclFloat32);
+    ring_reduce_scatter<float>(c, tab, ncclFloat32);
   }
 }
 
-void run_lamb(bo_ctx* c) {
+template <typename G>
+static void lamb_shard(bo_ctx* c, const G* g) {
   const int T = c->L.T;
   const float invn = 1.0f / static_cast<float>(c->world);  // trainer.cpp:212
   const int scale_g = c->world > 1;
   {
   StageTimer timer(c, BO_STAGE_LAMB_NORMS);
-  k_lamb_norms<<<c->n_lamb_tiles, kThreads, 0, c->stream>>>(c->d_lamb_tiles, c->gshard, c->w, c->m,
-                                                             c->v, c->state, c->lamb, c->bc_table,
-                                                             invn, scale_g, c->tile_part);
+  k_lamb_norms<G><<<c->n_lamb_tiles, kThreads, 0, c->stream>>>(c->d_lamb_tiles, g, c->w, c->m, c->v,
+                                                                c->state, c->lamb, c->bc_table, invn,
+                                                                scale_g, c->tile_part);
   check_launch(c, "k_lamb_norms");
   }
   {
@@ -431,10 +479,23 @@ void run_lamb(bo_ctx* c) {
   check_launch(c, "k_trust");
   }
   StageTimer timer(c, BO_STAGE_LAMB_UPDATE);
-  k_lamb_update<<<c->n_lamb_tiles, kThreads, 0, c->stream>>>(c->d_lamb_tiles, c->gshard, c->w, c->m,
-                                                              c->v, c->state, c->lamb, c->bc_table,
-                                                              invn, scale_g, c->trust);
+  k_lamb_update<G><<<c->n_lamb_tiles, kThreads, 0, c->stream>>>(c->d_lamb_tiles, g, c->w, c->m, c->v,
+                                                                 c->state, c->lamb, c->bc_table, invn,
+                                                                 scale_g, c->trust);
   check_launch(c, "k_lamb_update");
+}
+
+void run_lamb(bo_ctx* c) {
+  if (c->world > 1 && c->algo == BO_REDUCE_RING) {
+    // the reduced shard is the ring's final wire buffer (wire-exact values)
+    if (c->cfg.f16_exchange) {
+      lamb_shard<uint16_t>(c, static_cast<const uint16_t*>(c->wire[1]));
+    } else {
+      lamb_shard<float>(c, static_cast<const float*>(c->wire[1]));
+    }
+  } else {
+    lamb_shard<float>(c, c->gshard);
+  }
 }
 
 void run_allgather(bo_ctx* c) {
