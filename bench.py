@@ -193,6 +193,10 @@ def traffic_from_profiles(kernel):
 
 
 def main_b200(args):
+    # Libraries print to stdout (NCCL's version banner); the contract is ONE
+    # JSON line there, so everything else goes to stderr.
+    json_fd = os.dup(1)
+    os.dup2(2, 1)
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -402,7 +406,8 @@ def main_b200(args):
             "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": int(launches),
             "clocks": sampler.summary() if sampler else None,
         }
-        print(json.dumps(line), flush=True)
+        sys.stdout.flush()
+        os.write(json_fd, (json.dumps(line) + "\n").encode())
     pipe.close()
     if world > 1:
         dist.destroy_process_group()

@@ -52,8 +52,7 @@ void upload_tables(bo_ctx* c) {
   std::vector<LambTile> lamb_tiles;
   std::vector<int> tile_begin(static_cast<size_t>(L.T) + 1, 0);
   std::vector<std::vector<LambTile>> per_tensor(static_cast<size_t>(L.T));
-  std::vector<HopTile> hop_tiles;
-  const int q = c->rank;  // owned chunk
+  const int q = L.own;  // owned chunk
   for (int b = 0; b < L.B; ++b) {
     const int64_t cb = L.chunk[static_cast<size_t>(b)];
     const int64_t lo = q * cb;
@@ -68,10 +67,6 @@ void upload_tables(bo_ctx* c) {
             LambTile{L.shard_pos(b, p, e), L.flat_pos(b, p, e), static_cast<int32_t>(len), p});
       }
     }
-    for (int64_t e = 0; e < cb; e += kTileElems) {
-      const int64_t len = std::min<int64_t>(kTileElems, cb - e);
-      hop_tiles.push_back(HopTile{L.shoff[static_cast<size_t>(b)] + e, static_cast<int32_t>(len), b});
-    }
   }
   // Tiles grouped per tensor so each tensor's partials are contiguous; within
   // a tensor, shard order.
@@ -80,10 +75,6 @@ void upload_tables(bo_ctx* c) {
     for (const LambTile& lt : per_tensor[static_cast<size_t>(t)]) lamb_tiles.push_back(lt);
   }
   tile_begin[static_cast<size_t>(L.T)] = static_cast<int>(lamb_tiles.size());
-  std::vector<int64_t> geo;
-  geo.insert(geo.end(), L.base.begin(), L.base.end());
-  geo.insert(geo.end(), L.chunk.begin(), L.chunk.end());
-  geo.insert(geo.end(), L.shoff.begin(), L.shoff.end());
 
   if (c->world == 1) {
     // Single-rank LAMB (bo_fused.cu): tiles of <= kTileElems elements of one
@@ -135,9 +126,6 @@ void upload_tables(bo_ctx* c) {
   c->d_lamb_tiles = upload(c, lamb_tiles);
   c->n_lamb_tiles = static_cast<int>(lamb_tiles.size());
   c->d_tensor_tile_begin = upload(c, tile_begin);
-  c->d_hop_tiles = upload(c, hop_tiles);
-  c->n_hop_tiles = static_cast<int>(hop_tiles.size());
-  c->d_bucket_geo = upload(c, geo);
 }
 
 // Bias corrections bc_t = 1 - pow(double(beta), double(t)) evaluated on the
@@ -360,6 +348,9 @@ bo_status bo_create(const bo_trainer_config* cfg, int32_t n_tensors, const int64
   if (!cfg || !numels || !first_consumers) fail(BO_ERR_INVALID_CONFIG, "null argument");
   validate(*cfg);
   if (n_tensors > kMaxTensors) fail(BO_ERR_INVALID_CONFIG, "more than 1024 tensors");
+  if (world < 1 || world > 8) {
+    fail(BO_ERR_INVALID_CONFIG, "world must be 1..8 (the GPUs of one NVSwitch node)");
+  }
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
     fail(BO_ERR_NO_DEVICE, "no CUDA device visible");
@@ -377,6 +368,7 @@ bo_status bo_create(const bo_trainer_config* cfg, int32_t n_tensors, const int64
   c->own_stream = true;
   c->L = Layout::build(n_tensors, numels, first_consumers, cfg->bucket_bytes, world, rank);
   c->L.hash = layout_hash(c->L, names, ndims, dims, cfg->f16_exchange != 0, cfg->accumulation);
+  if (world > 1 && c->algo == BO_REDUCE_RING) c->L.own = (rank + 1) % world;
   const Layout& L = c->L;
   c->lamb = LambConsts{cfg->lamb.beta1, cfg->lamb.beta2, 1.0f - cfg->lamb.beta1, 1.0f - cfg->lamb.beta2,
                        cfg->lamb.eps, cfg->lamb.weight_decay, cfg->lamb.lr, cfg->lamb.trust_clip};
@@ -394,6 +386,15 @@ bo_status bo_create(const bo_trainer_config* cfg, int32_t n_tensors, const int64
   c->w = static_cast<float*>(dev_alloc(c, static_cast<size_t>(L.flat_total) * 4));
   c->m = static_cast<float*>(dev_alloc(c, static_cast<size_t>(L.shard_total) * 4));
   c->v = static_cast<float*>(dev_alloc(c, static_cast<size_t>(L.shard_total) * 4));
+  // double-buffered moments: LAMB phase 1 writes the new m, v before the
+  // step's overflow flag is final (DevState::parity picks the current set)
+  c->m_alt = static_cast<float*>(dev_alloc(c, static_cast<size_t>(L.shard_total) * 4));
+  c->v_alt = static_cast<float*>(dev_alloc(c, static_cast<size_t>(L.shard_total) * 4));
+  if (world > 1) {
+    c->wsh = static_cast<float*>(dev_alloc(c, static_cast<size_t>(L.shard_total) * 4));
+    c->u = static_cast<float*>(dev_alloc(c, static_cast<size_t>(L.shard_total) * 4));
+    c->d_barrier = static_cast<int*>(dev_alloc(c, 4));
+  }
   if (world > 1 && c->algo == BO_REDUCE_RING) {
     const size_t e = cfg->f16_exchange ? 2 : 4;
     c->wire[0] = dev_alloc(c, static_cast<size_t>(L.shard_total) * e);
@@ -432,6 +433,7 @@ void bo_destroy(bo_ctx* c) {
     cudaEventDestroy(mk.b);
   }
   for (cudaEvent_t e : c->event_pool) cudaEventDestroy(e);
+  for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
   if (c->comm) ncclCommDestroy(c->comm);
   for (void* p : c->allocations) cudaFree(p);
   if (c->bc_table) cudaFree(c->bc_table);
@@ -495,6 +497,33 @@ bo_status bo_comm_init(bo_ctx* c, const uint8_t* id128) {
            "rank " + std::to_string(c->rank) + " bucket layout disagrees with peers");
     }
   }
+  // Map every rank's flat parameter replica into this process (CUDA IPC over
+  // NVLink/NVSwitch): LAMB phase 2 stores each updated shard element straight
+  // into all replicas, which replaces the parameter all-gather.
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "ipc handle size");
+  cudaIpcMemHandle_t mine;
+  BO_CUDA(cudaIpcGetMemHandle(&mine, c->w));
+  uint8_t* dh = static_cast<uint8_t*>(dev_alloc(c, static_cast<size_t>(c->world + 1) * 64));
+  BO_CUDA(cudaMemcpyAsync(dh, &mine, 64, cudaMemcpyHostToDevice, c->stream));
+  BO_NCCL(ncclAllGather(dh, dh + 64, 64, ncclUint8, c->comm, c->stream));
+  std::vector<cudaIpcMemHandle_t> handles(static_cast<size_t>(c->world));
+  BO_CUDA(cudaMemcpyAsync(handles.data(), dh + 64, handles.size() * 64, cudaMemcpyDeviceToHost, c->stream));
+  BO_CUDA(cudaStreamSynchronize(c->stream));
+  std::vector<float*> peers(static_cast<size_t>(c->world));
+  for (int j = 0; j < c->world; ++j) {
+    if (j == c->rank) {
+      peers[static_cast<size_t>(j)] = c->w;
+      continue;
+    }
+    void* p = nullptr;
+    BO_CUDA(cudaIpcOpenMemHandle(&p, handles[static_cast<size_t>(j)], cudaIpcMemLazyEnablePeerAccess));
+    c->ipc_opened.push_back(p);
+    peers[static_cast<size_t>(j)] = static_cast<float*>(p);
+  }
+  c->d_peer_w = static_cast<float**>(dev_alloc(c, peers.size() * sizeof(float*)));
+  BO_CUDA(cudaMemcpyAsync(c->d_peer_w, peers.data(), peers.size() * sizeof(float*),
+                          cudaMemcpyHostToDevice, c->stream));
+  BO_CUDA(cudaStreamSynchronize(c->stream));
   BO_GUARD_END
 }
 
@@ -529,6 +558,7 @@ bo_status bo_load_params(bo_ctx* c, const float* src, int32_t on_host) {
     BO_CUDA(cudaMemcpyAsync(c->w + L.flat_off[static_cast<size_t>(t)], src + L.model_off[static_cast<size_t>(t)],
                             static_cast<size_t>(L.numel[static_cast<size_t>(t)]) * 4, k, c->stream));
   }
+  gather_shard(c);  // world > 1: the fp32 master shard of the owned chunks
   BO_CUDA(cudaStreamSynchronize(c->stream));
   BO_GUARD_END
 }
@@ -549,7 +579,12 @@ bo_status bo_read_moments(bo_ctx* c, float* m, float* v, int32_t on_host) {
   BO_GUARD_BEGIN
   const Layout& L = c->L;
   const cudaMemcpyKind k = on_host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
-  const int q = c->rank;
+  DevState st;
+  BO_CUDA(cudaMemcpyAsync(&st, c->state, sizeof(st), cudaMemcpyDeviceToHost, c->stream));
+  BO_CUDA(cudaStreamSynchronize(c->stream));
+  const float* mc = st.parity ? c->m_alt : c->m;
+  const float* vc = st.parity ? c->v_alt : c->v;
+  const int q = L.own;
   for (int b = 0; b < L.B; ++b) {
     const int64_t cb = L.chunk[static_cast<size_t>(b)];
     const int64_t lo = q * cb, hi = std::min<int64_t>((q + 1) * cb, L.elems[static_cast<size_t>(b)]);
@@ -559,8 +594,8 @@ bo_status bo_read_moments(bo_ctx* c, float* m, float* v, int32_t on_host) {
       if (a >= z) continue;
       const int64_t s = L.shard_pos(b, p, a);
       const int64_t dsti = L.model_off[static_cast<size_t>(p)] + (a - t0);
-      BO_CUDA(cudaMemcpyAsync(m + dsti, c->m + s, static_cast<size_t>(z - a) * 4, k, c->stream));
-      BO_CUDA(cudaMemcpyAsync(v + dsti, c->v + s, static_cast<size_t>(z - a) * 4, k, c->stream));
+      BO_CUDA(cudaMemcpyAsync(m + dsti, mc + s, static_cast<size_t>(z - a) * 4, k, c->stream));
+      BO_CUDA(cudaMemcpyAsync(v + dsti, vc + s, static_cast<size_t>(z - a) * 4, k, c->stream));
     }
   }
   BO_CUDA(cudaStreamSynchronize(c->stream));
@@ -637,8 +672,7 @@ bo_status bo_accumulate(bo_ctx* c, int32_t micro, const uint16_t* const* grads) 
     // the ring fuses flatten_param into its hops; NCCL needs the fusion buffer
     if (c->world == 1 || c->algo == BO_REDUCE_NCCL) launch_finalize(c, tab);
     run_reduce(c, tab);
-    run_lamb(c);
-    run_allgather(c);
+    run_lamb(c);  // world > 1: includes the fused parameter all-gather (IPC push)
   }
   c->calls += 1;
   BO_GUARD_END

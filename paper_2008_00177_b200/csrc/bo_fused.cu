@@ -1,18 +1,19 @@
 // Single-rank sync micro: the whole LAMB step (lamb.cpp:140-201) with the
 // flatten_param unscale (trainer.cpp:186-203) fused in.
 //
-//   k_flag        overflow pre-check of the sync micro's binary16 inputs
-//                 (found_inf must be known before the moments are written;
-//                 micros 0..K-2 were checked by k_accumulate)             2 B/elem
 //   k_lamb_p1     g = (h + acc) * inv; m', v', u (one pass, vectorised);
-//                 stores m', v' and the update u; per-tile fp64 partials
+//                 stores m', v' into the OTHER moment buffer set (double
+//                 buffering: the step's overflow flag — micros 0..K-2 from
+//                 k_accumulate, micro K-1 checked here — is only final at the
+//                 end of this pass) and the update u; per-tile fp64 partials
 //                 of ||w||^2 and ||u||^2                                   30 B/elem
 //   k_lamb_trust  per-tensor fixed-order sums of the tile partials ->
 //                 trust ratios (lamb.cpp:192-196)
 //   k_lamb_p2     w -= (lr * r) * u, tiles in reverse order so the update
 //                 and weights phase 1 wrote last are still in L2; the dead
 //                 u lines are then dropped from L2 (discard.global.L2)      12 B/elem
-//   k_fused_epilogue  step counters and the loss-scaler state machine
+//   k_fused_epilogue  step counters, the moment-buffer flip and the
+//                 loss-scaler state machine
 //
 // Every per-tensor array (acc, w, m, v, u) uses the aligned tensor layout, so
 // a tile index a0 serves all of them and every access is a 16-byte vector.
@@ -68,30 +69,21 @@ __device__ __forceinline__ void put(float4& v, int i, float x) {
   if (i == 0) v.x = x; else if (i == 1) v.y = x; else if (i == 2) v.z = x; else v.w = x;
 }
 
-__global__ void __launch_bounds__(kThreads) k_flag(const AccTile* __restrict__ tiles,
-                                                   const __grid_constant__ PtrTable tab,
-                                                   DevState* __restrict__ st) {
-  const AccTile tile = tiles[blockIdx.x];
-  const uint16_t* __restrict__ src = tab.p[tile.t] + tile.e0;
-  bool bad = false;
-  const int nvec = tile.len >> 3;
-#pragma unroll 2
-  for (int i = threadIdx.x; i < nvec; i += kThreads) {
-    const uint4 hv = __ldcs(reinterpret_cast<const uint4*>(src) + i);
-    bad |= pair_nonfinite(hv.x) | pair_nonfinite(hv.y) | pair_nonfinite(hv.z) | pair_nonfinite(hv.w);
-  }
-  for (int i = (nvec << 3) + threadIdx.x; i < tile.len; i += kThreads) bad |= !finite(widen(src[i]));
-  raise_flag(bad, st);
-}
-
 // Phase 1, one tile per CTA (the fused tiles are 16-byte aligned slices of one
 // tensor). Elements past len inside the last float4 keep their old m/v bits.
 __global__ void __launch_bounds__(kP1Threads, 2) k_lamb_p1(
     const FusedTile* __restrict__ tiles, const __grid_constant__ PtrTable tab,
-    const float* __restrict__ acc, const float* __restrict__ w, float* __restrict__ m,
-    float* __restrict__ v, float* __restrict__ u, const DevState* __restrict__ st, LambConsts c,
+    const float* __restrict__ acc, const float* __restrict__ w, float* m0, float* v0, float* m1,
+    float* v1, float* __restrict__ u, DevState* __restrict__ st, LambConsts c,
     const double* __restrict__ bc_table, int K, double* __restrict__ tile_part) {
-  if (st->local_flag) return;  // overflow: the step is skipped
+  if (st->local_flag) return;  // an earlier micro overflowed: the step is skipped
+  // double-buffered moments: read the current set, write the other one; the
+  // epilogue makes it current only if the step's overflow flag stays clear
+  const int par = st->parity;
+  const float* __restrict__ m = par ? m1 : m0;
+  const float* __restrict__ v = par ? v1 : v0;
+  float* __restrict__ mn = par ? m0 : m1;
+  float* __restrict__ vn = par ? v0 : v1;
   __shared__ double red[2][kP1Threads / 32];
   const double* bcp = bc_table + 4 * st->lamb_step;
   const double bc1 = bcp[0], bc2 = bcp[1], ibc1 = bcp[2], ibc2 = bcp[3];
@@ -114,11 +106,19 @@ __global__ void __launch_bounds__(kP1Threads, 2) k_lamb_p1(
     }
   }
   double wn = 0.0, un = 0.0;
+  bool bad = false;
 #pragma unroll
   for (int j = 0; j < 2; ++j) {
     const int e0 = 4 * (threadIdx.x + j * kP1Threads);
     if (e0 >= t.len) continue;
     const int n = min(4, t.len - e0);  // < 4 only in a tensor's last float4
+    // the sync micro's overflow check (micros 0..K-2: k_accumulate)
+    if (n == 4) {
+      bad |= pair_nonfinite(hv[j].x) | pair_nonfinite(hv[j].y);
+    } else {
+      const uint32_t hw[2] = {hv[j].x, hv[j].y};
+      for (int i = 0; i < n; ++i) bad |= ((hw[i >> 1] >> (16 * (i & 1))) & 0x7C00u) == 0x7C00u;
+    }
     const float hg[4] = {widen(static_cast<uint16_t>(hv[j].x & 0xFFFFu)),
                          widen(static_cast<uint16_t>(hv[j].x >> 16)),
                          widen(static_cast<uint16_t>(hv[j].y & 0xFFFFu)),
@@ -153,10 +153,11 @@ __global__ void __launch_bounds__(kP1Threads, 2) k_lamb_p1(
       }
     }
     const int64_t a = t.a0 + e0;
-    st4(m + a, mo, pf);
-    st4(v + a, vo, pf);
+    st4(mn + a, mo, pf);
+    st4(vn + a, vo, pf);
     st4(u + a, uo, pl);
   }
+  raise_flag(bad, st);
   wn = warp_sum(wn);
   un = warp_sum(un);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -265,6 +266,7 @@ __global__ void k_fused_epilogue(DevState* st, ScalerConsts sc) {
     st->skipped += 1;
   } else {
     st->lamb_step += 1;
+    st->parity ^= 1;  // the moments k_lamb_p1 wrote become current
   }
   if (sc.dynamic) {
     if (found) {
@@ -286,15 +288,10 @@ void check(bo_ctx* c, const char* what) {
 }  // namespace
 
 void run_fused_single_rank(bo_ctx* c, const PtrTable& tab) {
-  {
-    StageTimer timer(c, BO_STAGE_FLAG);
-    k_flag<<<c->n_acc_tiles, kThreads, 0, c->stream>>>(c->d_acc_tiles, tab, c->state);
-    check(c, "k_flag");
-  }
   StageTimer timer(c, BO_STAGE_LAMB_FUSED);
   k_lamb_p1<<<c->n_fused_tiles, kP1Threads, 0, c->stream>>>(
-      c->d_fused_tiles, tab, c->acc, c->w, c->m, c->v, c->u, c->state, c->lamb, c->bc_table,
-      c->cfg.accumulation, c->tile_part);
+      c->d_fused_tiles, tab, c->acc, c->w, c->m, c->v, c->m_alt, c->v_alt, c->u, c->state, c->lamb,
+      c->bc_table, c->cfg.accumulation, c->tile_part);
   check(c, "k_lamb_p1");
   k_lamb_trust<<<c->L.T, kThreads, 0, c->stream>>>(c->d_fused_tensor_tiles, c->tile_part, c->state,
                                                    c->lamb, c->trust);

@@ -52,6 +52,10 @@ inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 //   acc   : per-tensor fp32 accumulators at acc_off[p] (model order)
 struct Layout {
   int T = 0, B = 0, N = 1, rank = 0;
+  // Chunk index this rank owns in every bucket: r for the NCCL reduce-scatter,
+  // (r+1) % N for the reference ring, whose fold for chunk k ends on rank k-1
+  // (collective.hpp:65-80); the parameter push places it, so no hand-off hop.
+  int own = 0;
   std::vector<int64_t> numel;
   std::vector<int> bucket_of, ready;
   std::vector<int64_t> offset_of;
@@ -72,7 +76,7 @@ struct Layout {
   }
   int64_t shard_pos(int b, int p, int64_t a) const {
     return N == 1 ? flat_pos(b, p, a)
-                  : shoff[static_cast<size_t>(b)] + (a - rank * chunk[static_cast<size_t>(b)]);
+                  : shoff[static_cast<size_t>(b)] + (a - own * chunk[static_cast<size_t>(b)]);
   }
 };
 
@@ -87,11 +91,6 @@ struct LambTile {       // a slice of one tensor inside this rank's shard
   int64_t w0;           // flat index of the first element
   int32_t len;
   int32_t t;
-};
-struct HopTile {        // a slice of one bucket's chunk in shard space
-  int64_t s0;
-  int32_t len;
-  int32_t b;
 };
 // Ring hop with the finalize fused in: a slice of one tensor inside chunk q of
 // one bucket. x = (h + acc) * inv is computed on the fly from the caller's
@@ -130,7 +129,7 @@ struct DevState {
   int32_t found_inf;
   int32_t do_update;
   int32_t local_flag;   // set by LAMB phase 1 on this rank
-  int32_t pad;
+  int32_t parity;       // which moment buffer set is current (one rank: double-buffered)
   double bc1, bc2, ibc1, ibc2;   // bias corrections of the current LAMB step
 };
 
@@ -164,9 +163,6 @@ struct bo_ctx {
   bo::LambTile* d_lamb_tiles = nullptr;
   int n_lamb_tiles = 0;
   int* d_tensor_tile_begin = nullptr;   // [T+1] lamb-tile ranges per tensor
-  bo::HopTile* d_hop_tiles = nullptr;
-  int n_hop_tiles = 0;
-  int64_t* d_bucket_geo = nullptr;      // [3][B]: base, chunk, shoff
   bo::HopXTile* d_hopx_tiles = nullptr; // ring hops with fused finalize, grouped by chunk
   std::vector<int> hopx_begin;          // [N+1] tile range of chunk q
 
@@ -185,6 +181,14 @@ struct bo_ctx {
   float* w = nullptr;        // full parameter replica, flat layout
   float* m = nullptr;
   float* v = nullptr;
+  float* m_alt = nullptr;    // second moment buffer set (double-buffered moments)
+  float* v_alt = nullptr;
+  // world > 1: fp32 master copy of this rank's parameter shard (shard layout,
+  // aligned with m, v, u) and every rank's flat replica mapped through CUDA IPC
+  float* wsh = nullptr;
+  float** d_peer_w = nullptr;          // [world] device pointers to each rank's w
+  std::vector<void*> ipc_opened;       // peer mappings to close
+  int* d_barrier = nullptr;
   void* wire[3] = {nullptr, nullptr, nullptr};  // ring staging (shard-sized)
   double* tile_part = nullptr;    // [n_lamb_tiles][2]
   double* rank_part = nullptr;    // [2T+1]
@@ -220,7 +224,7 @@ void launch_accumulate(bo_ctx* c, int micro, const PtrTable& tab, bool vec_ok);
 void launch_finalize(bo_ctx* c, const PtrTable& tab);
 void run_reduce(bo_ctx* c, const PtrTable& tab);
 void run_lamb(bo_ctx* c);
-void run_allgather(bo_ctx* c);
+void gather_shard(bo_ctx* c);
 void run_fused_single_rank(bo_ctx* c, const PtrTable& tab);
 
 // Stage bracket: records events when profiling is on.

@@ -23,6 +23,7 @@ Layout Layout::build(int T, const int64_t* numel, const int32_t* firsts, uint64_
   L.T = T;
   L.N = world;
   L.rank = rank;
+  L.own = rank;
   L.numel.assign(numel, numel + T);
   for (int t = 0; t < T; ++t) {
     if (numel[t] <= 0) fail(BO_ERR_SHAPE_MISMATCH, "tensor " + std::to_string(t) + " is empty");

@@ -108,12 +108,6 @@ __global__ void __launch_bounds__(kThreads) k_finalize(const AccTile* __restrict
 }
 
 // --------------------------------------------------------------- ring hops
-struct BucketGeo {
-  const int64_t* base;
-  const int64_t* chunk;
-  const int64_t* shoff;
-};
-
 template <typename W>
 __device__ __forceinline__ W to_wire(float p);
 template <>
@@ -122,36 +116,6 @@ template <>
 __device__ __forceinline__ uint16_t to_wire<uint16_t>(float p) { return narrow(p); }
 __device__ __forceinline__ float from_wire(float w) { return w; }
 __device__ __forceinline__ float from_wire(uint16_t w) { return widen(w); }
-
-// combine == 0: out = wire(x[chunk q])                     (first send)
-// combine == 1: out = wire(from_wire(in) + x[chunk q])     (every later hop;
-//   the last one is the owner's re-rounded result, collective.cpp:205-209)
-template <typename W>
-__global__ void __launch_bounds__(kThreads) k_hop(const HopTile* __restrict__ tiles, BucketGeo geo,
-                                                  const float* __restrict__ x,
-                                                  const W* __restrict__ in, W* __restrict__ out,
-                                                  int q, int combine) {
-  const HopTile tile = tiles[blockIdx.x];
-  const int64_t src0 = geo.base[tile.b] + q * geo.chunk[tile.b] + (tile.s0 - geo.shoff[tile.b]);
-  constexpr int kPer = kTileElems / kThreads;
-#pragma unroll
-  for (int j = 0; j < kPer; ++j) {
-    const int e = threadIdx.x + j * kThreads;
-    if (e < tile.len) {
-      float p = __ldcs(x + src0 + e);
-      if (combine) p = __fadd_rn(from_wire(__ldcs(in + tile.s0 + e)), p);
-      out[tile.s0 + e] = to_wire<W>(p);
-    }
-  }
-}
-
-template <typename W>
-__global__ void __launch_bounds__(kThreads) k_unwire(const HopTile* __restrict__ tiles,
-                                                     const W* __restrict__ in,
-                                                     float* __restrict__ g) {
-  const HopTile tile = tiles[blockIdx.x];
-  for (int e = threadIdx.x; e < tile.len; e += kThreads) g[tile.s0 + e] = from_wire(in[tile.s0 + e]);
-}
 
 // Ring hop with flatten_param fused in (trainer.cpp:186-203 + collective.hpp:65-80
 // / collective.cpp:170-190): x = (h + acc) * inv for the elements of chunk q,
@@ -198,13 +162,15 @@ template <typename G>
 __global__ void __launch_bounds__(kThreads) k_lamb_norms(const LambTile* __restrict__ tiles,
                                                          const G* __restrict__ g,
                                                          const float* __restrict__ w,
-                                                         const float* __restrict__ m,
-                                                         const float* __restrict__ v,
+                                                         const float* m0, const float* v0,
+                                                         const float* m1, const float* v1,
                                                          DevState* __restrict__ st, LambConsts c,
                                                          const double* __restrict__ bc_table,
                                                          float invn, int scale_g,
                                                          double* __restrict__ tile_part) {
   const LambTile tile = tiles[blockIdx.x];
+  const float* __restrict__ m = st->parity ? m1 : m0;  // current moment buffers
+  const float* __restrict__ v = st->parity ? v1 : v0;
   __shared__ double bc[4];
   __shared__ double red[2][kThreads / 32];
   __shared__ int bad_any;
@@ -284,7 +250,8 @@ __global__ void __launch_bounds__(kThreads) k_norm_reduce(const int* __restrict_
 // loss-scaler state machine.
 __global__ void __launch_bounds__(1024) k_trust(const double* __restrict__ all_part, int N, int T,
                                                 DevState* __restrict__ st, LambConsts c,
-                                                ScalerConsts sc, float* __restrict__ trust) {
+                                                ScalerConsts sc, float* __restrict__ trust,
+                                                int flip_parity) {
   __shared__ int found;
   if (threadIdx.x == 0) {
     int f = 0;
@@ -316,6 +283,7 @@ __global__ void __launch_bounds__(1024) k_trust(const double* __restrict__ all_p
       st->skipped += 1;
     } else {
       st->lamb_step += 1;
+      if (flip_parity) st->parity ^= 1;  // double-buffered moments written by phase 1
     }
     if (sc.dynamic) {
       if (found) {
@@ -335,8 +303,8 @@ template <typename G>
 __global__ void __launch_bounds__(kThreads) k_lamb_update(const LambTile* __restrict__ tiles,
                                                           const G* __restrict__ g,
                                                           float* __restrict__ w,
-                                                          float* __restrict__ m,
-                                                          float* __restrict__ v,
+                                                          float* m0, float* v0, float* m1,
+                                                          float* v1,
                                                           const DevState* __restrict__ st,
                                                           LambConsts c,
                                                           const double* __restrict__ bc_table,
@@ -344,6 +312,8 @@ __global__ void __launch_bounds__(kThreads) k_lamb_update(const LambTile* __rest
                                                           const float* __restrict__ trust) {
   if (!st->do_update) return;
   const LambTile tile = tiles[blockIdx.x];
+  float* __restrict__ m = st->parity ? m1 : m0;  // current moment buffers (updated in place)
+  float* __restrict__ v = st->parity ? v1 : v0;
   __shared__ double bc[4];
   if (threadIdx.x < 4) bc[threadIdx.x] = bc_table[4 * (st->lamb_step - 1) + threadIdx.x];
   __syncthreads();
@@ -364,15 +334,156 @@ __global__ void __launch_bounds__(kThreads) k_lamb_update(const LambTile* __rest
   }
 }
 
+// ------------------------------------------------ sharded LAMB (world > 1)
+// All of g (the reduced shard, wire type G), wsh, m, v and u share the shard
+// layout, so a tile is split into a scalar head up to the next 16-byte
+// boundary, an aligned float4 body and a scalar tail.
+struct Split {
+  int head, nv, tail;
+};
+__device__ __forceinline__ Split split_tile(int64_t s0, int len) {
+  const int head = min(static_cast<int>((4 - (s0 & 3)) & 3), len);
+  return Split{head, (len - head) >> 2, (len - head) & 3};
+}
+__device__ __forceinline__ void load_g4(const float* p, float (&o)[4]) {
+  const float4 x = __ldcs(reinterpret_cast<const float4*>(p));
+  o[0] = x.x; o[1] = x.y; o[2] = x.z; o[3] = x.w;
+}
+__device__ __forceinline__ void load_g4(const uint16_t* p, float (&o)[4]) {
+  const uint2 x = __ldcs(reinterpret_cast<const uint2*>(p));
+  o[0] = widen(static_cast<uint16_t>(x.x & 0xFFFFu));
+  o[1] = widen(static_cast<uint16_t>(x.x >> 16));
+  o[2] = widen(static_cast<uint16_t>(x.y & 0xFFFFu));
+  o[3] = widen(static_cast<uint16_t>(x.y >> 16));
+}
+
+// Phase 1 on this rank's shard: g = reduced * (1/world) (trainer.cpp:212), the
+// NonFiniteGradient flag (lamb.cpp:179), m', v' into the other buffer set
+// (double-buffered: found_inf is global, known only after every rank's phase
+// 1), the update u, and per-tile fp64 partials of ||w||^2, ||u||^2.
+template <typename G>
+__global__ void __launch_bounds__(512, 2) k_shard_p1(const LambTile* __restrict__ tiles,
+                                                     const G* __restrict__ g, float invn,
+                                                     const float* __restrict__ wsh, float* m0,
+                                                     float* v0, float* m1, float* v1,
+                                                     float* __restrict__ u,
+                                                     DevState* __restrict__ st, LambConsts c,
+                                                     const double* __restrict__ bc_table,
+                                                     double* __restrict__ tile_part) {
+  const LambTile t = tiles[blockIdx.x];
+  const int par = st->parity;
+  const float* __restrict__ m = par ? m1 : m0;
+  const float* __restrict__ v = par ? v1 : v0;
+  float* __restrict__ mn = par ? m0 : m1;
+  float* __restrict__ vn = par ? v0 : v1;
+  const double* bcp = bc_table + 4 * st->lamb_step;
+  const double bc[4] = {bcp[0], bcp[1], bcp[2], bcp[3]};
+  const Split sp = split_tile(t.s0, t.len);
+  double wn = 0.0, un = 0.0;
+  bool bad = false;
+  auto scalar = [&](int e) {
+    const int64_t s = t.s0 + e;
+    const float gi = __fmul_rn(from_wire(g[s]), invn);
+    bad |= !finite(gi);
+    const float wi = wsh[s];
+    const Moments o = lamb_elem(gi, wi, m[s], v[s], c, bc);
+    mn[s] = o.m;
+    vn[s] = o.v;
+    u[s] = o.u;
+    wn = __dadd_rn(wn, __dmul_rn(static_cast<double>(wi), static_cast<double>(wi)));
+    un = __dadd_rn(un, __dmul_rn(static_cast<double>(o.u), static_cast<double>(o.u)));
+  };
+  if (threadIdx.x < sp.head) scalar(static_cast<int>(threadIdx.x));
+  if (threadIdx.x >= 32 && static_cast<int>(threadIdx.x) - 32 < sp.tail) {
+    scalar(sp.head + 4 * sp.nv + static_cast<int>(threadIdx.x) - 32);
+  }
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const int q = threadIdx.x + j * 512;
+    if (q < sp.nv) {
+      const int64_t s = t.s0 + sp.head + 4 * q;
+      float ga[4];
+      load_g4(g + s, ga);
+      const float4 w4 = __ldcs(reinterpret_cast<const float4*>(wsh + s));
+      const float4 m4 = __ldcs(reinterpret_cast<const float4*>(m + s));
+      const float4 v4 = __ldcs(reinterpret_cast<const float4*>(v + s));
+      const float wa[4] = {w4.x, w4.y, w4.z, w4.w};
+      const float ma[4] = {m4.x, m4.y, m4.z, m4.w};
+      const float va[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        ga[i] = __fmul_rn(ga[i], invn);
+        bad |= !finite(ga[i]);
+      }
+      const Lamb4 o = lamb_elem4(ga, wa, ma, va, c, bc[0], bc[1], bc[2], bc[3]);
+      __stcs(reinterpret_cast<float4*>(mn + s), make_float4(o.m[0], o.m[1], o.m[2], o.m[3]));
+      __stcs(reinterpret_cast<float4*>(vn + s), make_float4(o.v[0], o.v[1], o.v[2], o.v[3]));
+      *reinterpret_cast<float4*>(u + s) = make_float4(o.u[0], o.u[1], o.u[2], o.u[3]);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        wn = __dadd_rn(wn, __dmul_rn(static_cast<double>(wa[i]), static_cast<double>(wa[i])));
+        un = __dadd_rn(un, __dmul_rn(static_cast<double>(o.u[i]), static_cast<double>(o.u[i])));
+      }
+    }
+  }
+  raise_flag(bad, st);
+  wn = warp_sum(wn);
+  un = warp_sum(un);
+  __shared__ double red[2][16];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) {
+    red[0][wid] = wn;
+    red[1][wid] = un;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double A = 0.0, B = 0.0;
+    for (int i = 0; i < 16; ++i) {
+      A += red[0][i];
+      B += red[1][i];
+    }
+    tile_part[2 * blockIdx.x] = A;
+    tile_part[2 * blockIdx.x + 1] = B;
+  }
+}
+
+// Phase 2 fused with the parameter all-gather: w -= (lr * r) * u on the
+// master shard (lamb.cpp:197-198), and the new value stored straight into
+// every rank's flat parameter replica over NVLink (CUDA IPC mappings), at the
+// element's fusion-buffer position. Skipped steps exit.
+__global__ void __launch_bounds__(kThreads) k_shard_p2_push(const LambTile* __restrict__ tiles,
+                                                            float* __restrict__ wsh,
+                                                            const float* __restrict__ u,
+                                                            const DevState* __restrict__ st,
+                                                            LambConsts c,
+                                                            const float* __restrict__ trust,
+                                                            float* const* __restrict__ peer_w,
+                                                            int N) {
+  if (!st->do_update) return;
+  __shared__ float* dst[8];
+  if (threadIdx.x < N) dst[threadIdx.x] = peer_w[threadIdx.x];
+  __syncthreads();
+  const LambTile t = tiles[blockIdx.x];
+  const float step_scale = __fmul_rn(c.lr, trust[t.t]);
+  for (int e = threadIdx.x; e < t.len; e += kThreads) {
+    const int64_t s = t.s0 + e;
+    const float nw = __fsub_rn(wsh[s], __fmul_rn(step_scale, __ldcs(u + s)));
+    wsh[s] = nw;
+    for (int j = 0; j < N; ++j) __stcs(dst[j] + t.w0 + e, nw);
+  }
+}
+
+// Owned chunk positions of the flat replica -> the master shard (load time).
+__global__ void k_gather_shard(const LambTile* __restrict__ tiles, const float* __restrict__ w,
+                               float* __restrict__ wsh) {
+  const LambTile t = tiles[blockIdx.x];
+  for (int e = threadIdx.x; e < t.len; e += blockDim.x) wsh[t.s0 + e] = w[t.w0 + e];
+}
+
 void check_launch(bo_ctx* c, const char* what) {
   c->launches += 1;
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) fail(BO_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
-}
-
-BucketGeo geo_of(bo_ctx* c) {
-  const int64_t* p = c->d_bucket_geo;
-  return BucketGeo{p, p + c->L.B, p + 2 * c->L.B};
 }
 
 }  // namespace
@@ -425,14 +536,9 @@ static void ring_reduce_scatter(bo_ctx* c, const PtrTable& tab, ncclDataType_t d
     BO_NCCL(ncclGroupEnd());
     hop((r - s - 1 + 2 * N) % N, b, a, 1);  // chunk received at hop s (collective.hpp:70-71)
   }
-  // After N-1 hops rank r holds the finished chunk (r+1) % N (already
-  // wire-rounded: the owner re-round of collective.cpp:205-209). One more
-  // hop hands it to rank r+1, so rank r owns chunk r (the ncclAllGather
-  // placement). LAMB reads the wire buffer b directly.
-  BO_NCCL(ncclGroupStart());
-  BO_NCCL(ncclSend(a, S, dt, right, c->comm, c->stream));
-  BO_NCCL(ncclRecv(b, S, dt, left, c->comm, c->stream));
-  BO_NCCL(ncclGroupEnd());
+  // After N-1 hops buffer a holds the finished chunk (r+1) % N, already
+  // wire-rounded (the owner re-round of collective.cpp:205-209): the chunk
+  // this rank owns (Layout::own). LAMB reads it in place.
 }
 
 void run_reduce(bo_ctx* c, const PtrTable& tab) {
@@ -453,6 +559,8 @@ void run_reduce(bo_ctx* c, const PtrTable& tab) {
   }
 }
 
+// One rank's multi-kernel fallback (inputs not 16-byte aligned): recompute
+// LAMB in phase 2, moments updated in place.
 template <typename G>
 static void lamb_shard(bo_ctx* c, const G* g) {
   const int T = c->L.T;
@@ -461,6 +569,7 @@ static void lamb_shard(bo_ctx* c, const G* g) {
   {
   StageTimer timer(c, BO_STAGE_LAMB_NORMS);
   k_lamb_norms<G><<<c->n_lamb_tiles, kThreads, 0, c->stream>>>(c->d_lamb_tiles, g, c->w, c->m, c->v,
+                                                                c->m_alt, c->v_alt,
                                                                 c->state, c->lamb, c->bc_table, invn,
                                                                 scale_g, c->tile_part);
   check_launch(c, "k_lamb_norms");
@@ -470,45 +579,76 @@ static void lamb_shard(bo_ctx* c, const G* g) {
   k_norm_reduce<<<T, kThreads, 0, c->stream>>>(c->d_tensor_tile_begin, c->tile_part, c->state, T,
                                                 c->rank_part);
   check_launch(c, "k_norm_reduce");
-  if (c->world > 1) {
-    BO_NCCL(ncclAllGather(c->rank_part, c->all_part, static_cast<size_t>(2 * T + 1), ncclFloat64,
-                          c->comm, c->stream));
-  }
   k_trust<<<1, 1024, 0, c->stream>>>(c->all_part, c->world, T, c->state, c->lamb, c->scaler,
-                                     c->trust);
+                                     c->trust, 0);
   check_launch(c, "k_trust");
   }
   StageTimer timer(c, BO_STAGE_LAMB_UPDATE);
   k_lamb_update<G><<<c->n_lamb_tiles, kThreads, 0, c->stream>>>(c->d_lamb_tiles, g, c->w, c->m, c->v,
+                                                                 c->m_alt, c->v_alt,
                                                                  c->state, c->lamb, c->bc_table, invn,
                                                                  scale_g, c->trust);
   check_launch(c, "k_lamb_update");
 }
 
+// world > 1: phase 1 on the shard -> per-tensor partials -> all-gather of
+// the partials and flags (2T+1 doubles per rank, summed in rank order so all
+// ranks agree) -> trust ratios, found_inf, scaler -> phase 2 pushing the new
+// parameters into every rank's replica -> barrier.
+template <typename G>
+static void lamb_sharded(bo_ctx* c, const G* g) {
+  const int T = c->L.T;
+  const float invn = 1.0f / static_cast<float>(c->world);  // trainer.cpp:212
+  {
+  StageTimer timer(c, BO_STAGE_LAMB_NORMS);
+  k_shard_p1<G><<<c->n_lamb_tiles, 512, 0, c->stream>>>(c->d_lamb_tiles, g, invn, c->wsh, c->m, c->v,
+                                                         c->m_alt, c->v_alt, c->u, c->state, c->lamb,
+                                                         c->bc_table, c->tile_part);
+  check_launch(c, "k_shard_p1");
+  }
+  {
+  StageTimer timer(c, BO_STAGE_TRUST);
+  k_norm_reduce<<<T, kThreads, 0, c->stream>>>(c->d_tensor_tile_begin, c->tile_part, c->state, T,
+                                                c->rank_part);
+  check_launch(c, "k_norm_reduce");
+  BO_NCCL(ncclAllGather(c->rank_part, c->all_part, static_cast<size_t>(2 * T + 1), ncclFloat64,
+                        c->comm, c->stream));
+  k_trust<<<1, 1024, 0, c->stream>>>(c->all_part, c->world, T, c->state, c->lamb, c->scaler,
+                                     c->trust, 1);
+  check_launch(c, "k_trust");
+  }
+  {
+  StageTimer timer(c, BO_STAGE_LAMB_UPDATE);
+  k_shard_p2_push<<<c->n_lamb_tiles, kThreads, 0, c->stream>>>(c->d_lamb_tiles, c->wsh, c->u,
+                                                              c->state, c->lamb, c->trust,
+                                                              c->d_peer_w, c->world);
+  check_launch(c, "k_shard_p2_push");
+  }
+  // every rank's pushes into every replica have landed once all ranks are
+  // past their phase 2 (kernel completion flushes the NVLink stores)
+  StageTimer timer(c, BO_STAGE_ALLGATHER);
+  BO_NCCL(ncclAllReduce(c->d_barrier, c->d_barrier, 1, ncclInt32, ncclSum, c->comm, c->stream));
+}
+
 void run_lamb(bo_ctx* c) {
-  if (c->world > 1 && c->algo == BO_REDUCE_RING) {
+  if (c->world == 1) {
+    lamb_shard<float>(c, c->gshard);
+  } else if (c->algo == BO_REDUCE_RING) {
     // the reduced shard is the ring's final wire buffer (wire-exact values)
     if (c->cfg.f16_exchange) {
-      lamb_shard<uint16_t>(c, static_cast<const uint16_t*>(c->wire[1]));
+      lamb_sharded<uint16_t>(c, static_cast<const uint16_t*>(c->wire[0]));
     } else {
-      lamb_shard<float>(c, static_cast<const float*>(c->wire[1]));
+      lamb_sharded<float>(c, static_cast<const float*>(c->wire[0]));
     }
   } else {
-    lamb_shard<float>(c, c->gshard);
+    lamb_sharded<float>(c, c->gshard);
   }
 }
 
-void run_allgather(bo_ctx* c) {
+void gather_shard(bo_ctx* c) {
   if (c->world == 1) return;
-  StageTimer timer(c, BO_STAGE_ALLGATHER);
-  BO_NCCL(ncclGroupStart());
-  for (int b = 0; b < c->L.B; ++b) {
-    const size_t cb = static_cast<size_t>(c->L.chunk[b]);
-    float* base = c->w + c->L.base[b];
-    BO_NCCL(ncclAllGather(base + static_cast<size_t>(c->rank) * cb, base, cb, ncclFloat, c->comm,
-                          c->stream));
-  }
-  BO_NCCL(ncclGroupEnd());
+  k_gather_shard<<<c->n_lamb_tiles, kThreads, 0, c->stream>>>(c->d_lamb_tiles, c->w, c->wsh);
+  check_launch(c, "k_gather_shard");
 }
 
 }  // namespace bo
