@@ -42,11 +42,12 @@ BYTES_FINALIZE_K1 = 2 + 4
 BYTES_LAMB_NORMS = 4 * 4                # read g, w, m, v
 BYTES_LAMB_UPDATE = 4 * 4 + 3 * 4       # read g, w, m, v; write w, m, v
 BYTES_LAMB_ALGO = 28                    # single-pass LAMB (the algorithmic minimum)
-BYTES_LAMB_FUSED = 2 + 4 + 3 * 4 + 3 * 4  # one rank: read h, acc, w, m, v; write w, m, v
+# one rank, k_lamb_p1 (read h, acc, w, m, v; write m', v', u) + k_lamb_p2 (read w, u; write w)
+BYTES_LAMB_FUSED = (2 + 4 + 3 * 4 + 3 * 4) + (2 * 4 + 4)
 
 # index = BO_STAGE_* in include/bertopt_b200.h
 STAGES = ["accumulate", "finalize", "reduce", "lamb_norms", "trust", "lamb_update", "allgather",
-          "flag", "lamb_fused"]
+          "hop_kernels", "reserved"]
 
 MODELS = {"bert-large": "BERT_LARGE", "bert-large-128": "BERT_LARGE_PHASE1", "bert-base": "BERT_BASE",
           "bert-tiny": "BERT_TINY"}
@@ -302,12 +303,18 @@ def main_b200(args):
     hbm_bytes = {
         "accumulate": (BYTES_ACCUMULATE_FIRST + BYTES_ACCUMULATE * (K - 2)) * P / max(K - 1, 1),
         "finalize": (BYTES_FINALIZE if K > 1 else BYTES_FINALIZE_K1) * P,
-        "lamb_norms": BYTES_LAMB_NORMS * S_shard,
-        "lamb_update": BYTES_LAMB_UPDATE * S_shard,
-        "flag": 2 * P,
-        "lamb_fused": (BYTES_LAMB_FUSED if K > 1 else BYTES_LAMB_FUSED - 4) * P,
+        # LAMB phase 1: one rank k_lamb_p1 (h 2 + acc 4 + w, m, v read; m', v', u
+        # written), world > 1 k_shard_p1 (g wire E + wsh, m, v read; m', v', u);
+        # phase 2: k_lamb_p2 / k_shard_p2_push (w, u read; w written)
+        "lamb_norms": ((30 if K > 1 else 26) if world == 1 else E + 24) * S_shard,
+        "lamb_update": 12 * S_shard,
+        # ring hops (nested in "reduce"): h + acc read once per element over all
+        # hops, plus the wire in/out of every hop
+        "hop_kernels": (6 * P / world + (2 * E) * S_shard * (world - 1) / world),
     }
-    nvl_bytes = {"reduce": (world - 1) / world * E * P, "allgather": (world - 1) / world * 4 * P}
+    # NVLink bytes sent per rank: ring reduce-scatter; the parameter push
+    # (k_shard_p2_push stores every updated element into the N-1 other replicas)
+    nvl_bytes = {"reduce": (world - 1) / world * E * P, "lamb_update": (world - 1) * 4 * S_shard}
     stages = {}
     for i, name in enumerate(STAGES):
         if stage_n[i] == 0:
@@ -318,7 +325,7 @@ def main_b200(args):
             nbytes = hbm_bytes[name]
             gbs = nbytes / (avg * 1e-3) / 1e9
             entry.update({"bytes": int(nbytes), "GB/s": round(gbs, 1), "frac": round(gbs / hbm, 4)})
-        elif name in nvl_bytes and world > 1:
+        if name in nvl_bytes and world > 1:
             nbytes = nvl_bytes[name]
             gbs = nbytes / (avg * 1e-3) / 1e9
             entry.update({"nvlink_bytes": int(nbytes), "nvlink_GB/s": round(gbs, 1),
@@ -326,9 +333,9 @@ def main_b200(args):
         stages[name] = entry
     dom = max((n for n in stages if "bytes" in stages[n]),
               key=lambda n: stages[n]["ms"] * stages[n]["launches_per_step"])
-    kernel_names = {"accumulate": "k_accumulate", "finalize": "k_finalize", "flag": "k_flag",
-                    "lamb_norms": "k_lamb_norms", "lamb_update": "k_lamb_update",
-                    "lamb_fused": "k_lamb_fused"}
+    kernel_names = {"accumulate": "k_accumulate", "finalize": "k_finalize",
+                    "lamb_norms": "k_lamb_p1" if world == 1 else "k_shard_p1",
+                    "lamb_update": "k_lamb_p2" if world == 1 else "k_shard_p2_push"}
     roofline = {"kernel": kernel_names[dom], "bound": "hbm", "achieved": stages[dom]["GB/s"],
                 "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s", "frac": stages[dom]["frac"],
                 "traffic": traffic_from_profiles(kernel_names[dom]),

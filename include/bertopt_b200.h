@@ -184,14 +184,14 @@ bo_status bo_accumulate(bo_ctx* ctx, int32_t micro, const uint16_t* const* grads
 /* Stage timing with CUDA events recorded on the context stream around every
  * stage of bo_accumulate (off by default). Stages: */
 #define BO_STAGE_ACCUMULATE 0   /* micros 0..K-2 */
-#define BO_STAGE_FINALIZE 1     /* unscale + pack (sync micro) */
-#define BO_STAGE_REDUCE 2       /* reduce-scatter (ring hops or NCCL) */
-#define BO_STAGE_LAMB_NORMS 3   /* LAMB phase 1 */
+#define BO_STAGE_FINALIZE 1     /* unscale + pack into the fusion buffer (NCCL wire) */
+#define BO_STAGE_REDUCE 2       /* reduce-scatter (ring hops with fused finalize, or NCCL) */
+#define BO_STAGE_LAMB_NORMS 3   /* LAMB phase 1: moments, update, norm partials */
 #define BO_STAGE_TRUST 4        /* norm reduction, partials all-gather, trust/scaler */
-#define BO_STAGE_LAMB_UPDATE 5  /* LAMB phase 2 */
-#define BO_STAGE_ALLGATHER 6    /* parameter all-gather */
-#define BO_STAGE_FLAG 7         /* one rank: overflow pre-check of the sync micro */
-#define BO_STAGE_LAMB_FUSED 8   /* one rank: fused pipelined LAMB (k_lamb_fused + epilogue) */
+#define BO_STAGE_LAMB_UPDATE 5  /* LAMB phase 2 (world > 1: + parameter push to all replicas) */
+#define BO_STAGE_ALLGATHER 6    /* world > 1: replica-completion barrier */
+#define BO_STAGE_FLAG 7         /* ring hop kernels alone (nested inside REDUCE) */
+#define BO_STAGE_LAMB_FUSED 8   /* reserved */
 #define BO_NUM_STAGES 9
 bo_status bo_profile_enable(bo_ctx* ctx, int32_t enable);
 /* Total milliseconds and event count per stage since the last reset; syncs. */

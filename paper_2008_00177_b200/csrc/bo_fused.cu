@@ -288,17 +288,26 @@ void check(bo_ctx* c, const char* what) {
 }  // namespace
 
 void run_fused_single_rank(bo_ctx* c, const PtrTable& tab) {
-  StageTimer timer(c, BO_STAGE_LAMB_FUSED);
-  k_lamb_p1<<<c->n_fused_tiles, kP1Threads, 0, c->stream>>>(
-      c->d_fused_tiles, tab, c->acc, c->w, c->m, c->v, c->m_alt, c->v_alt, c->u, c->state, c->lamb,
-      c->bc_table, c->cfg.accumulation, c->tile_part);
-  check(c, "k_lamb_p1");
-  k_lamb_trust<<<c->L.T, kThreads, 0, c->stream>>>(c->d_fused_tensor_tiles, c->tile_part, c->state,
-                                                   c->lamb, c->trust);
-  check(c, "k_lamb_trust");
-  k_lamb_p2<<<c->n_fused_tiles, kP2Threads, 0, c->stream>>>(c->d_fused_tiles, c->n_fused_tiles, c->w,
-                                                            c->u, c->state, c->lamb, c->trust);
-  check(c, "k_lamb_p2");
+  {
+    StageTimer timer(c, BO_STAGE_LAMB_NORMS);
+    k_lamb_p1<<<c->n_fused_tiles, kP1Threads, 0, c->stream>>>(
+        c->d_fused_tiles, tab, c->acc, c->w, c->m, c->v, c->m_alt, c->v_alt, c->u, c->state, c->lamb,
+        c->bc_table, c->cfg.accumulation, c->tile_part);
+    check(c, "k_lamb_p1");
+  }
+  {
+    StageTimer timer(c, BO_STAGE_TRUST);
+    k_lamb_trust<<<c->L.T, kThreads, 0, c->stream>>>(c->d_fused_tensor_tiles, c->tile_part, c->state,
+                                                     c->lamb, c->trust);
+    check(c, "k_lamb_trust");
+  }
+  {
+    StageTimer timer(c, BO_STAGE_LAMB_UPDATE);
+    k_lamb_p2<<<c->n_fused_tiles, kP2Threads, 0, c->stream>>>(c->d_fused_tiles, c->n_fused_tiles,
+                                                              c->w, c->u, c->state, c->lamb, c->trust);
+    check(c, "k_lamb_p2");
+  }
+  StageTimer timer(c, BO_STAGE_TRUST);
   k_fused_epilogue<<<1, 1, 0, c->stream>>>(c->state, c->scaler);
   check(c, "k_fused_epilogue");
 }

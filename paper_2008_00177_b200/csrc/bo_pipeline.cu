@@ -523,6 +523,7 @@ static void ring_reduce_scatter(bo_ctx* c, const PtrTable& tab, ncclDataType_t d
   auto hop = [&](int q, const W* in, W* out, int combine) {
     const int t0 = c->hopx_begin[static_cast<size_t>(q)], t1 = c->hopx_begin[static_cast<size_t>(q) + 1];
     if (t1 > t0) {
+      StageTimer timer(c, BO_STAGE_FLAG);
       k_hopx<W><<<t1 - t0, kThreads, 0, c->stream>>>(c->d_hopx_tiles + t0, c->d_tensors, tab, c->acc,
                                                       c->state, K, in, out, combine);
       check_launch(c, "k_hopx");
