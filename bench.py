@@ -308,9 +308,9 @@ def main_b200(args):
         # phase 2: k_lamb_p2 / k_shard_p2_push (w, u read; w written)
         "lamb_norms": ((30 if K > 1 else 26) if world == 1 else E + 24) * S_shard,
         "lamb_update": 12 * S_shard,
-        # ring hops (nested in "reduce"): h + acc read once per element over all
-        # hops, plus the wire in/out of every hop
-        "hop_kernels": (6 * P / world + (2 * E) * S_shard * (world - 1) / world),
+        # one ring hop kernel (nested in "reduce"): h + acc of one chunk of every
+        # bucket, wire in and out
+        "hop_kernels": (6 + 2 * E) * S_shard,
     }
     # NVLink bytes sent per rank: ring reduce-scatter; the parameter push
     # (k_shard_p2_push stores every updated element into the N-1 other replicas)
