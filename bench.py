@@ -335,7 +335,8 @@ def main_b200(args):
               key=lambda n: stages[n]["ms"] * stages[n]["launches_per_step"])
     kernel_names = {"accumulate": "k_accumulate", "finalize": "k_finalize",
                     "lamb_norms": "k_lamb_p1" if world == 1 else "k_shard_p1",
-                    "lamb_update": "k_lamb_p2" if world == 1 else "k_shard_p2_push"}
+                    "lamb_update": "k_lamb_p2" if world == 1 else "k_shard_p2_push",
+                    "hop_kernels": "k_hopx"}
     roofline = {"kernel": kernel_names[dom], "bound": "hbm", "achieved": stages[dom]["GB/s"],
                 "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s", "frac": stages[dom]["frac"],
                 "traffic": traffic_from_profiles(kernel_names[dom]),

@@ -167,6 +167,14 @@ bo_status bo_read_params(bo_ctx* ctx, float* dst, int32_t dst_on_host);
  * flat arrays (elements owned by other ranks are left untouched). */
 bo_status bo_read_moments(bo_ctx* ctx, float* m, float* v, int32_t dst_on_host);
 bo_status bo_get_status(bo_ctx* ctx, bo_step_status* out);
+/* Checkpoint / resume of the device state (the reference
+ * BCKP checkpoint, model.cpp:360-425, keeps only parameters). The blob holds
+ * the parameter replica and the moments of the elements this rank owns (both
+ * in model order), the LAMB step and the loss-scaler state; every rank of a
+ * world exports / imports its own blob. bo_export_state(ctx, NULL, &n) returns
+ * the size. Import requires the same tensors, world and ownership. Syncs. */
+bo_status bo_export_state(bo_ctx* ctx, void* blob, uint64_t* nbytes);
+bo_status bo_import_state(bo_ctx* ctx, const void* blob, uint64_t nbytes);
 /* Per-tensor device pointer into the full-replica parameter buffer. */
 bo_status bo_param_ptr(bo_ctx* ctx, int32_t tensor, float** out);
 

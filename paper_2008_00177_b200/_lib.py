@@ -71,7 +71,9 @@ SIGNATURES = {
     "bo_read_params": (_i32, [_vp, _vp, _i32]),
     "bo_read_moments": (_i32, [_vp, _vp, _vp, _i32]),
     "bo_get_status": (_i32, [_vp, C.POINTER(StepStatusC)]),
-    "bo_param_ptr": (_i32, [_vp, _i32, C.POINTER(_vp)]),
+    "bo_export_state": (_i32, [_vp, _vp, C.POINTER(_u64)]),
+    "bo_import_state": (_i32, [_vp, _vp, _u64]),
+    "bo_param_ptr":(_i32, [_vp, _i32, C.POINTER(_vp)]),
     "bo_accumulate": (_i32, [_vp, _i32, C.POINTER(_vp)]),
     "bo_profile_enable": (_i32, [_vp, _i32]),
     "bo_profile_read": (_i32, [_vp, C.POINTER(C.c_double), C.POINTER(_i64), _i32]),

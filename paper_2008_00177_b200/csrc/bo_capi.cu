@@ -254,6 +254,30 @@ static void validate(const bo_trainer_config& c) {
   }
 }
 
+struct StateHeader {
+  char magic[4];
+  uint32_t version;
+  int32_t world, rank, own, T;
+  int64_t P;
+  uint64_t layout_hash;
+  DevState st;
+};
+
+// Owned (shard) pieces: (shard index, model-order index, length).
+template <typename F>
+static void for_owned(const Layout& L, F&& f) {
+  const int q = L.own;
+  for (int b = 0; b < L.B; ++b) {
+    const int64_t cb = L.chunk[static_cast<size_t>(b)];
+    const int64_t lo = q * cb, hi = std::min<int64_t>((q + 1) * cb, L.elems[static_cast<size_t>(b)]);
+    for (int p : L.buckets[static_cast<size_t>(b)]) {
+      const int64_t t0 = L.offset_of[static_cast<size_t>(p)], t1 = t0 + L.numel[static_cast<size_t>(p)];
+      const int64_t a = std::max(lo, t0), z = std::min(hi, t1);
+      if (a < z) f(L.shard_pos(b, p, a), L.model_off[static_cast<size_t>(p)] + (a - t0), z - a);
+    }
+  }
+}
+
 }  // namespace bo
 
 using namespace bo;
@@ -599,6 +623,76 @@ bo_status bo_read_moments(bo_ctx* c, float* m, float* v, int32_t on_host) {
     }
   }
   BO_CUDA(cudaStreamSynchronize(c->stream));
+  BO_GUARD_END
+}
+
+bo_status bo_export_state(bo_ctx* c, void* blob, uint64_t* nbytes) {
+  BO_GUARD_BEGIN
+  if (!c || !nbytes) fail(BO_ERR_INVALID_CONFIG, "null argument");
+  const uint64_t need = sizeof(StateHeader) + 3ull * static_cast<uint64_t>(c->L.P) * 4;
+  if (!blob) {
+    *nbytes = need;
+    return BO_OK;
+  }
+  if (*nbytes < need) fail(BO_ERR_LENGTH_MISMATCH, "state blob too small");
+  StateHeader h{};
+  std::memcpy(h.magic, "BOST", 4);
+  h.version = 1;
+  h.world = c->world;
+  h.rank = c->rank;
+  h.own = c->L.own;
+  h.T = c->L.T;
+  h.P = c->L.P;
+  h.layout_hash = c->L.hash;
+  BO_CUDA(cudaMemcpyAsync(&h.st, c->state, sizeof(DevState), cudaMemcpyDeviceToHost, c->stream));
+  BO_CUDA(cudaStreamSynchronize(c->stream));
+  auto* base = static_cast<uint8_t*>(blob);
+  std::memcpy(base, &h, sizeof(h));
+  float* w = reinterpret_cast<float*>(base + sizeof(h));
+  float* m = w + c->L.P;
+  float* v = m + c->L.P;
+  std::memset(m, 0, static_cast<size_t>(c->L.P) * 8);
+  bo_status s = bo_read_params(c, w, 1);
+  if (s != BO_OK) return s;
+  s = bo_read_moments(c, m, v, 1);
+  if (s != BO_OK) return s;
+  *nbytes = need;
+  BO_GUARD_END
+}
+
+bo_status bo_import_state(bo_ctx* c, const void* blob, uint64_t nbytes) {
+  BO_GUARD_BEGIN
+  if (!c || !blob) fail(BO_ERR_INVALID_CONFIG, "null argument");
+  StateHeader h;
+  if (nbytes < sizeof(h)) fail(BO_ERR_LENGTH_MISMATCH, "state blob truncated");
+  std::memcpy(&h, blob, sizeof(h));
+  if (std::memcmp(h.magic, "BOST", 4) != 0 || h.version != 1) {
+    fail(BO_ERR_INVALID_CONFIG, "not a bertopt_b200 state blob");
+  }
+  if (nbytes < sizeof(h) + 3ull * static_cast<uint64_t>(h.P) * 4) {
+    fail(BO_ERR_LENGTH_MISMATCH, "state blob truncated");
+  }
+  if (h.world != c->world || h.rank != c->rank || h.own != c->L.own || h.T != c->L.T ||
+      h.P != c->L.P || h.layout_hash != c->L.hash) {
+    fail(BO_ERR_BUCKET_LAYOUT_MISMATCH, "state blob was written by a different layout or rank");
+  }
+  const auto* base = static_cast<const uint8_t*>(blob);
+  const float* w = reinterpret_cast<const float*>(base + sizeof(h));
+  const float* m = w + h.P;
+  const float* v = m + h.P;
+  bo_status s = bo_load_params(c, w, 1);
+  if (s != BO_OK) return s;
+  for_owned(c->L, [&](int64_t sp, int64_t mp, int64_t n) {
+    BO_CUDA(cudaMemcpyAsync(c->m + sp, m + mp, static_cast<size_t>(n) * 4, cudaMemcpyHostToDevice, c->stream));
+    BO_CUDA(cudaMemcpyAsync(c->v + sp, v + mp, static_cast<size_t>(n) * 4, cudaMemcpyHostToDevice, c->stream));
+  });
+  DevState st = h.st;
+  st.parity = 0;  // moments were written into buffer set 0
+  st.local_flag = 0;
+  BO_CUDA(cudaMemcpyAsync(c->state, &st, sizeof(st), cudaMemcpyHostToDevice, c->stream));
+  BO_CUDA(cudaStreamSynchronize(c->stream));
+  grow_bc_table(c, st.lamb_step + 2);
+  c->calls = std::max<int64_t>(c->calls, st.steps);
   BO_GUARD_END
 }
 

@@ -259,6 +259,17 @@ class GradPipeline:
         return StepStatus(st.loss_scale, st.good_steps, st.lamb_step, st.steps, st.skipped_steps,
                           bool(st.found_inf))
 
+    def export_state(self) -> bytes:
+        """Checkpoint of this rank's device state (params, owned moments, step, scaler)."""
+        n = C.c_uint64()
+        _lib.check(self.lib.bo_export_state(self.ctx, None, C.byref(n)))
+        buf = C.create_string_buffer(n.value)
+        _lib.check(self.lib.bo_export_state(self.ctx, buf, C.byref(n)))
+        return buf.raw[:n.value]
+
+    def import_state(self, blob: bytes) -> None:
+        _lib.check(self.lib.bo_import_state(self.ctx, blob, len(blob)))
+
     def param_ptr(self, t: int) -> int:
         p = C.c_void_p()
         _lib.check(self.lib.bo_param_ptr(self.ctx, t, C.byref(p)))

@@ -60,8 +60,9 @@ class GradBuffers:
 
 
 def run_pipeline(spec, cfg, params0, steps, grad_seed=1, spike_ppm=0, spike_exp=1, injections=(),
-                 rank=0, world=1, aligned=True, pipe=None, device=0):
-    """Run `steps` optimizer steps; returns (pipe, scale_used, found_inf)."""
+                 rank=0, world=1, aligned=True, pipe=None, device=0, first_step=0):
+    """Run optimizer steps first_step .. first_step+steps-1 (the step index
+    seeds the synthetic gradients); returns (pipe, scale_used, found_inf)."""
     if pipe is None:
         pipe = GradPipeline(spec, cfg, device=device, rank=rank, world=world)
         pipe.load_params(np.asarray(params0, np.float32))
@@ -69,7 +70,7 @@ def run_pipeline(spec, cfg, params0, steps, grad_seed=1, spike_ppm=0, spike_exp=
     gb = GradBuffers(spec, K, device, aligned)
     scale_used, found = [], []
     torch.cuda.set_device(device)
-    for step in range(steps):
+    for step in range(first_step, first_step + steps):
         S = pipe.status().loss_scale
         scale_used.append(S)
         for k in range(K):

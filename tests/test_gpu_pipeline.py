@@ -156,3 +156,36 @@ def test_bert_large_config2_matches_oracle(torch_cuda, oracle):
     pipe, su, fi = run_pipeline(spec, cfg, p0, steps=1)
     ref = oracle.train(spec, p0, 1, 4, 4 << 20, False, OL(lr=1e-4), OS(), 1)
     _compare(pipe, ref, su, fi)
+
+
+def test_checkpoint_resume_is_bit_identical(torch_cuda, oracle):
+    """§8(f) row 2: export the device state after 3 steps, import it into a
+    fresh context, run 2 more: identical to 5 uninterrupted steps."""
+    from paper_2008_00177_b200.errors import BucketLayoutMismatch
+    from paper_2008_00177_b200.model_spec import BERT_TINY, bert_spec
+    from paper_2008_00177_b200.pipeline import (GradPipeline, LambConfig, ScalerConfig,
+                                                TrainerConfig)
+    from tests.harness import run_pipeline
+
+    spec = bert_spec(BERT_TINY)
+    p0 = oracle.build_params(spec, 13)
+    cfg = TrainerConfig(LambConfig(), 2, 8192, False, 0, ScalerConfig(init_scale=2.0 ** 14,
+                                                                       growth_interval=2))
+    kw = dict(spike_ppm=3, spike_exp=3)
+    ref, _, _ = run_pipeline(spec, cfg, p0, steps=5, **kw)
+    a, _, _ = run_pipeline(spec, cfg, p0, steps=3, **kw)
+    blob = a.export_state()
+    b = GradPipeline(spec, cfg)
+    b.import_state(blob)
+    b, _, _ = run_pipeline(spec, cfg, None, steps=2, pipe=b, first_step=3, **kw)
+    assert np.array_equal(b.read_params().view(np.uint32), ref.read_params().view(np.uint32))
+    mb, vb = b.read_moments()
+    mr, vr = ref.read_moments()
+    assert np.array_equal(mb.view(np.uint32), mr.view(np.uint32))
+    assert np.array_equal(vb.view(np.uint32), vr.view(np.uint32))
+    sb, sr = b.status(), ref.status()
+    assert (sb.lamb_step, sb.loss_scale, sb.good_steps, sb.steps) == \
+        (sr.lamb_step, sr.loss_scale, sr.good_steps, sr.steps)
+    other = GradPipeline(spec, TrainerConfig(LambConfig(), 2, 1 << 20))
+    with pytest.raises(BucketLayoutMismatch):
+        other.import_state(blob)
