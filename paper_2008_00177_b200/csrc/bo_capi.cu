@@ -385,6 +385,7 @@ bo_status bo_create(const bo_trainer_config* cfg, int32_t n_tensors, const int64
   c->rank = rank;
   c->world = world;
   if (const char* e = std::getenv("BO_UNFUSED")) c->force_unfused = std::strcmp(e, "0") != 0;
+  if (const char* e = std::getenv("BO_RING_NCCL")) c->ring_via_nccl = std::strcmp(e, "0") != 0;
   c->algo = cfg->reduce_algo == BO_REDUCE_AUTO ? (cfg->f16_exchange ? BO_REDUCE_RING : BO_REDUCE_NCCL)
                                                : cfg->reduce_algo;
   BO_CUDA(cudaSetDevice(device));
@@ -524,25 +525,42 @@ bo_status bo_comm_init(bo_ctx* c, const uint8_t* id128) {
   // Map every rank's flat parameter replica into this process (CUDA IPC over
   // NVLink/NVSwitch): LAMB phase 2 stores each updated shard element straight
   // into all replicas, which replaces the parameter all-gather.
+  // The ring's two staging buffers are mapped too: a hop reads the left
+  // neighbour's previous output in place over NVLink.
   static_assert(sizeof(cudaIpcMemHandle_t) == 64, "ipc handle size");
-  cudaIpcMemHandle_t mine;
-  BO_CUDA(cudaIpcGetMemHandle(&mine, c->w));
-  uint8_t* dh = static_cast<uint8_t*>(dev_alloc(c, static_cast<size_t>(c->world + 1) * 64));
-  BO_CUDA(cudaMemcpyAsync(dh, &mine, 64, cudaMemcpyHostToDevice, c->stream));
-  BO_NCCL(ncclAllGather(dh, dh + 64, 64, ncclUint8, c->comm, c->stream));
-  std::vector<cudaIpcMemHandle_t> handles(static_cast<size_t>(c->world));
-  BO_CUDA(cudaMemcpyAsync(handles.data(), dh + 64, handles.size() * 64, cudaMemcpyDeviceToHost, c->stream));
-  BO_CUDA(cudaStreamSynchronize(c->stream));
-  std::vector<float*> peers(static_cast<size_t>(c->world));
-  for (int j = 0; j < c->world; ++j) {
-    if (j == c->rank) {
-      peers[static_cast<size_t>(j)] = c->w;
-      continue;
+  const bool ring = c->algo == BO_REDUCE_RING;
+  auto map_all = [&](void* mine_ptr, std::vector<void*>& out) {
+    cudaIpcMemHandle_t mine;
+    BO_CUDA(cudaIpcGetMemHandle(&mine, mine_ptr));
+    uint8_t* dh = static_cast<uint8_t*>(dev_alloc(c, static_cast<size_t>(c->world + 1) * 64));
+    BO_CUDA(cudaMemcpyAsync(dh, &mine, 64, cudaMemcpyHostToDevice, c->stream));
+    BO_NCCL(ncclAllGather(dh, dh + 64, 64, ncclUint8, c->comm, c->stream));
+    std::vector<cudaIpcMemHandle_t> handles(static_cast<size_t>(c->world));
+    BO_CUDA(cudaMemcpyAsync(handles.data(), dh + 64, handles.size() * 64, cudaMemcpyDeviceToHost,
+                            c->stream));
+    BO_CUDA(cudaStreamSynchronize(c->stream));
+    out.assign(static_cast<size_t>(c->world), nullptr);
+    for (int j = 0; j < c->world; ++j) {
+      if (j == c->rank) {
+        out[static_cast<size_t>(j)] = mine_ptr;
+        continue;
+      }
+      void* p = nullptr;
+      BO_CUDA(cudaIpcOpenMemHandle(&p, handles[static_cast<size_t>(j)], cudaIpcMemLazyEnablePeerAccess));
+      c->ipc_opened.push_back(p);
+      out[static_cast<size_t>(j)] = p;
     }
-    void* p = nullptr;
-    BO_CUDA(cudaIpcOpenMemHandle(&p, handles[static_cast<size_t>(j)], cudaIpcMemLazyEnablePeerAccess));
-    c->ipc_opened.push_back(p);
-    peers[static_cast<size_t>(j)] = static_cast<float*>(p);
+  };
+  std::vector<void*> pw;
+  map_all(c->w, pw);
+  std::vector<float*> peers(pw.size());
+  for (size_t j = 0; j < pw.size(); ++j) peers[j] = static_cast<float*>(pw[j]);
+  if (ring) {
+    for (int k = 0; k < 2; ++k) {
+      std::vector<void*> pk;
+      map_all(c->wire[k], pk);
+      for (int j = 0; j < c->world; ++j) c->peer_wire[k][j] = pk[static_cast<size_t>(j)];
+    }
   }
   c->d_peer_w = static_cast<float**>(dev_alloc(c, peers.size() * sizeof(float*)));
   BO_CUDA(cudaMemcpyAsync(c->d_peer_w, peers.data(), peers.size() * sizeof(float*),

@@ -187,6 +187,9 @@ struct bo_ctx {
   // aligned with m, v, u) and every rank's flat replica mapped through CUDA IPC
   float* wsh = nullptr;
   float** d_peer_w = nullptr;          // [world] device pointers to each rank's w
+  void* peer_wire[2][8] = {};          // every rank's ring staging buffers (IPC), host-side
+  void* ring_result = nullptr;         // staging buffer holding the owned reduced chunk
+  bool ring_via_nccl = false;          // BO_RING_NCCL=1: hops over ncclSend/ncclRecv
   std::vector<void*> ipc_opened;       // peer mappings to close
   int* d_barrier = nullptr;
   void* wire[3] = {nullptr, nullptr, nullptr};  // ring staging (shard-sized)

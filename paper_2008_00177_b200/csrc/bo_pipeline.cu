@@ -132,6 +132,68 @@ __global__ void __launch_bounds__(kThreads) k_hopx(const HopXTile* __restrict__ 
   const float inv = __fdiv_rn(1.0f, __fmul_rn(static_cast<float>(K), st->scale));
   const uint16_t* __restrict__ h = tab.p[tile.t] + tile.e0;
   const float* __restrict__ a = acc + td[tile.t].acc_off + tile.e0;
+  // Vector path when the tensor side (h, acc) and the shard side (in, out)
+  // share their 4-element alignment (the common case: BERT tensor sizes and
+  // chunk lengths are multiples of 4): scalar head to the boundary, float4 /
+  // 4 x binary16 body, scalar tail. Caller slots are 16-byte aligned.
+  if (((tile.e0 - tile.s0) & 3) == 0 && (reinterpret_cast<uintptr_t>(tab.p[tile.t]) & 15) == 0) {
+    const int head = min(static_cast<int>((4 - (tile.s0 & 3)) & 3), tile.len);
+    const int nv = (tile.len - head) >> 2;
+    auto one = [&](int e) {
+      const float g = widen(h[e]);
+      float p = __fmul_rn(K > 1 ? __fadd_rn(g, a[e]) : g, inv);
+      if (combine) p = __fadd_rn(from_wire(in[tile.s0 + e]), p);
+      out[tile.s0 + e] = to_wire<W>(p);
+    };
+    if (threadIdx.x < head) one(threadIdx.x);
+    const int tail0 = head + 4 * nv;
+    if (threadIdx.x >= 32 && static_cast<int>(threadIdx.x) - 32 < tile.len - tail0) {
+      one(tail0 + static_cast<int>(threadIdx.x) - 32);
+    }
+#pragma unroll 4
+    for (int q = threadIdx.x; q < nv; q += kThreads) {
+      const int e = head + 4 * q;
+      const uint2 hv = __ldcs(reinterpret_cast<const uint2*>(h + e));
+      const float hg[4] = {widen(static_cast<uint16_t>(hv.x & 0xFFFFu)),
+                           widen(static_cast<uint16_t>(hv.x >> 16)),
+                           widen(static_cast<uint16_t>(hv.y & 0xFFFFu)),
+                           widen(static_cast<uint16_t>(hv.y >> 16))};
+      float av[4] = {0.f, 0.f, 0.f, 0.f};
+      if (K > 1) {
+        const float4 a4 = __ldcs(reinterpret_cast<const float4*>(a + e));
+        av[0] = a4.x; av[1] = a4.y; av[2] = a4.z; av[3] = a4.w;
+      }
+      float iv[4] = {0.f, 0.f, 0.f, 0.f};
+      if (combine) {
+        if constexpr (sizeof(W) == 2) {
+          const uint2 w2 = __ldcs(reinterpret_cast<const uint2*>(in + tile.s0 + e));
+          iv[0] = widen(static_cast<uint16_t>(w2.x & 0xFFFFu));
+          iv[1] = widen(static_cast<uint16_t>(w2.x >> 16));
+          iv[2] = widen(static_cast<uint16_t>(w2.y & 0xFFFFu));
+          iv[3] = widen(static_cast<uint16_t>(w2.y >> 16));
+        } else {
+          const float4 w4 = __ldcs(reinterpret_cast<const float4*>(in + tile.s0 + e));
+          iv[0] = w4.x; iv[1] = w4.y; iv[2] = w4.z; iv[3] = w4.w;
+        }
+      }
+      W o[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        float p = __fmul_rn(K > 1 ? __fadd_rn(hg[i], av[i]) : hg[i], inv);
+        if (combine) p = __fadd_rn(iv[i], p);
+        o[i] = to_wire<W>(p);
+      }
+      if constexpr (sizeof(W) == 2) {
+        uint2 w2;
+        w2.x = static_cast<uint32_t>(o[0]) | (static_cast<uint32_t>(o[1]) << 16);
+        w2.y = static_cast<uint32_t>(o[2]) | (static_cast<uint32_t>(o[3]) << 16);
+        *reinterpret_cast<uint2*>(out + tile.s0 + e) = w2;
+      } else {
+        *reinterpret_cast<float4*>(out + tile.s0 + e) = make_float4(o[0], o[1], o[2], o[3]);
+      }
+    }
+    return;
+  }
   constexpr int kPer = kTileElems / kThreads;
   float xv[kPer];
 #pragma unroll
@@ -530,16 +592,31 @@ static void ring_reduce_scatter(bo_ctx* c, const PtrTable& tab, ncclDataType_t d
     }
   };
   hop(r, nullptr, a, 0);  // hop 0 payload: this rank's own chunk r (collective.cpp:178)
-  for (int s = 0; s < N - 1; ++s) {
-    BO_NCCL(ncclGroupStart());
-    BO_NCCL(ncclSend(a, S, dt, right, c->comm, c->stream));
-    BO_NCCL(ncclRecv(b, S, dt, left, c->comm, c->stream));
-    BO_NCCL(ncclGroupEnd());
-    hop((r - s - 1 + 2 * N) % N, b, a, 1);  // chunk received at hop s (collective.hpp:70-71)
+  if (c->peer_wire[0][left] && !c->ring_via_nccl) {
+    // Peer-to-peer hops: hop s reads the left neighbour's hop s-1 output in
+    // place over NVLink (CUDA IPC mapping) and writes the other local buffer.
+    // A 4-byte all-reduce before each hop is the barrier that orders a
+    // buffer's writer before its reader and its reader before its next writer.
+    for (int s = 0; s < N - 1; ++s) {
+      BO_NCCL(ncclAllReduce(c->d_barrier, c->d_barrier, 1, ncclInt32, ncclSum, c->comm, c->stream));
+      const W* in = static_cast<const W*>(c->peer_wire[s % 2][left]);
+      W* out = static_cast<W*>(c->wire[(s + 1) % 2]);
+      hop((r - s - 1 + 2 * N) % N, in, out, 1);  // chunk added at hop s (collective.hpp:70-71)
+    }
+    c->ring_result = c->wire[(N - 1) % 2];
+  } else {
+    for (int s = 0; s < N - 1; ++s) {
+      BO_NCCL(ncclGroupStart());
+      BO_NCCL(ncclSend(a, S, dt, right, c->comm, c->stream));
+      BO_NCCL(ncclRecv(b, S, dt, left, c->comm, c->stream));
+      BO_NCCL(ncclGroupEnd());
+      hop((r - s - 1 + 2 * N) % N, b, a, 1);  // chunk received at hop s (collective.hpp:70-71)
+    }
+    c->ring_result = a;
   }
-  // After N-1 hops buffer a holds the finished chunk (r+1) % N, already
-  // wire-rounded (the owner re-round of collective.cpp:205-209): the chunk
-  // this rank owns (Layout::own). LAMB reads it in place.
+  // After N-1 hops the result buffer holds the finished chunk (r+1) % N,
+  // already wire-rounded (the owner re-round of collective.cpp:205-209): the
+  // chunk this rank owns (Layout::own). LAMB reads it in place.
 }
 
 void run_reduce(bo_ctx* c, const PtrTable& tab) {
@@ -637,9 +714,9 @@ void run_lamb(bo_ctx* c) {
   } else if (c->algo == BO_REDUCE_RING) {
     // the reduced shard is the ring's final wire buffer (wire-exact values)
     if (c->cfg.f16_exchange) {
-      lamb_sharded<uint16_t>(c, static_cast<const uint16_t*>(c->wire[0]));
+      lamb_sharded<uint16_t>(c, static_cast<const uint16_t*>(c->ring_result));
     } else {
-      lamb_sharded<float>(c, static_cast<const float*>(c->wire[0]));
+      lamb_sharded<float>(c, static_cast<const float*>(c->ring_result));
     }
   } else {
     lamb_sharded<float>(c, c->gshard);
