@@ -89,6 +89,30 @@ __global__ void __launch_bounds__(kThreads) k_finalize(const AccTile* __restrict
   const uint16_t* __restrict__ src = tab.p[tile.t] + tile.e0;
   const float* __restrict__ a = acc + td[tile.t].acc_off + tile.e0;
   float* __restrict__ dst = x + td[tile.t].flat_off + tile.e0;
+  if (((td[tile.t].flat_off & 3) | (reinterpret_cast<uintptr_t>(tab.p[tile.t]) & 15)) == 0) {
+    // the tensor's fusion-buffer offset is 16-byte aligned: float4 path
+    const int nv = tile.len >> 2;
+#pragma unroll 4
+    for (int q = threadIdx.x; q < nv; q += kThreads) {
+      const uint2 hv = __ldcs(reinterpret_cast<const uint2*>(src) + q);
+      float g[4] = {widen(static_cast<uint16_t>(hv.x & 0xFFFFu)), widen(static_cast<uint16_t>(hv.x >> 16)),
+                    widen(static_cast<uint16_t>(hv.y & 0xFFFFu)), widen(static_cast<uint16_t>(hv.y >> 16))};
+      if (K > 1) {
+        const float4 a4 = __ldcs(reinterpret_cast<const float4*>(a) + q);
+        g[0] = __fadd_rn(g[0], a4.x);
+        g[1] = __fadd_rn(g[1], a4.y);
+        g[2] = __fadd_rn(g[2], a4.z);
+        g[3] = __fadd_rn(g[3], a4.w);
+      }
+      reinterpret_cast<float4*>(dst)[q] = make_float4(__fmul_rn(g[0], inv), __fmul_rn(g[1], inv),
+                                                      __fmul_rn(g[2], inv), __fmul_rn(g[3], inv));
+    }
+    for (int e = 4 * nv + threadIdx.x; e < tile.len; e += kThreads) {
+      const float g = widen(src[e]);
+      dst[e] = __fmul_rn(K > 1 ? __fadd_rn(g, a[e]) : g, inv);
+    }
+    return;
+  }
   constexpr int kPer = kTileElems / kThreads;
   float gv[kPer];
 #pragma unroll

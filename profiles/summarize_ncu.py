@@ -29,7 +29,9 @@ def short(name: str) -> str:
 
 
 def launches(path: str, steps: int, out: str) -> None:
-    rows = [r for r in csv.DictReader(open(path)) if r.get("Metric Name") == "gpu__time_duration.sum"]
+    text = open(path).read().splitlines()
+    start = next(i for i, ln in enumerate(text) if ln.startswith('"ID"'))  # skip ==PROF== lines
+    rows = [r for r in csv.DictReader(text[start:]) if r.get("Metric Name") == "gpu__time_duration.sum"]
     per = collections.OrderedDict()
     for r in rows:
         k = short(r["Kernel Name"])
