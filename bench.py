@@ -299,14 +299,19 @@ def main_b200(args):
     S_shard = pipe.shard_elems()
     hbm, peak_kind = peaks()
     E = 2 if f16 else 4
+    path = pipe.path()
+    fused_last = "last_hop_fused" in path
     # algorithmic bytes per launch of each stage (HBM) / per rank (NVLink)
     hbm_bytes = {
         "accumulate": (BYTES_ACCUMULATE_FIRST + BYTES_ACCUMULATE * (K - 2)) * P / max(K - 1, 1),
         "finalize": (BYTES_FINALIZE if K > 1 else BYTES_FINALIZE_K1) * P,
         # LAMB phase 1: one rank k_lamb_p1 (h 2 + acc 4 + w, m, v read; m', v', u
-        # written), world > 1 k_shard_p1 (g wire E + wsh, m, v read; m', v', u);
-        # phase 2: k_lamb_p2 / k_shard_p2_push (w, u read; w written)
-        "lamb_norms": ((30 if K > 1 else 26) if world == 1 else E + 24) * S_shard,
+        # written); world > 1 k_p1w (reduced wire E or, with the last ring hop
+        # fused in, h 2 + acc 4 with the wire over NVLink; + wsh, m, v read;
+        # m', v', u written); phase 2: k_lamb_p2 / k_shard_p2_push (w, u read;
+        # w written)
+        "lamb_norms": ((30 if K > 1 else 26) if world == 1 else
+                       ((6 if K > 1 else 2) if fused_last else E) + 24) * S_shard,
         "lamb_update": 12 * S_shard,
         # one ring hop kernel (nested in "reduce"): h + acc of one chunk of every
         # bucket, wire in and out
@@ -315,6 +320,8 @@ def main_b200(args):
     # NVLink bytes sent per rank: ring reduce-scatter; the parameter push
     # (k_shard_p2_push stores every updated element into the N-1 other replicas)
     nvl_bytes = {"reduce": (world - 1) / world * E * P, "lamb_update": (world - 1) * 4 * S_shard}
+    if fused_last:
+        nvl_bytes["lamb_norms"] = E * S_shard  # the last hop's read of the left partial
     stages = {}
     for i, name in enumerate(STAGES):
         if stage_n[i] == 0:
@@ -334,7 +341,7 @@ def main_b200(args):
     dom = max((n for n in stages if "bytes" in stages[n]),
               key=lambda n: stages[n]["ms"] * stages[n]["launches_per_step"])
     kernel_names = {"accumulate": "k_accumulate", "finalize": "k_finalize",
-                    "lamb_norms": "k_lamb_p1" if world == 1 else "k_shard_p1",
+                    "lamb_norms": "k_lamb_p1" if world == 1 else "k_p1w",
                     "lamb_update": "k_lamb_p2" if world == 1 else "k_shard_p2_push",
                     "hop_kernels": "k_hopx"}
     roofline = {"kernel": kernel_names[dom], "bound": "hbm", "achieved": stages[dom]["GB/s"],
@@ -408,6 +415,7 @@ def main_b200(args):
                        "bucket_bytes": bucket_bytes, "buckets": pipe.num_buckets,
                        "wire": args.wire if world > 1 else None,
                        "reduce_algo": args.algo if world > 1 else None,
+                       "kernel_path": path,
                        "parallelism": f"dp{world} (reduce-scatter + sharded LAMB + all-gather)",
                        "l2": "inputs (K x 2 B x P) larger than L2, no flush"},
             "roofline": roofline, "step_roofline": step_roofline, "stages": stages,

@@ -206,6 +206,14 @@ bo_status bo_profile_enable(bo_ctx* ctx, int32_t enable);
 bo_status bo_profile_read(bo_ctx* ctx, double* stage_ms, int64_t* stage_count, int32_t reset);
 /* Kernels this library has launched on ctx (NCCL kernels not included). */
 int64_t bo_launch_count(const bo_ctx* ctx);
+/* Which implementation the last sync micro ran (bit set; 0 before the first). */
+#define BO_PATH_ONE_RANK_FUSED 1     /* one rank: k_lamb_p1 / k_lamb_trust / k_lamb_p2 */
+#define BO_PATH_ONE_RANK_STAGED 2    /* one rank: finalize + multi-kernel LAMB */
+#define BO_PATH_RING_P2P 4           /* ring hops reading the left neighbour over CUDA IPC */
+#define BO_PATH_RING_SENDRECV 8      /* ring hops over ncclSend/ncclRecv */
+#define BO_PATH_LAST_HOP_FUSED 16    /* the ring's last hop ran inside LAMB phase 1 */
+#define BO_PATH_NCCL_RS 32           /* ncclReduceScatter of the fusion buffer */
+int32_t bo_path_flags(const bo_ctx* ctx);
 
 /* ---- operator-level drop-ins -------------------------------------------- */
 /* lamb_step (lamb.cpp:140-201) over device tensors; exact reference numerics

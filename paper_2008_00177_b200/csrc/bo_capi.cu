@@ -386,9 +386,11 @@ bo_status bo_create(const bo_trainer_config* cfg, int32_t n_tensors, const int64
   c->world = world;
   if (const char* e = std::getenv("BO_UNFUSED")) c->force_unfused = std::strcmp(e, "0") != 0;
   if (const char* e = std::getenv("BO_RING_NCCL")) c->ring_via_nccl = std::strcmp(e, "0") != 0;
+  if (const char* e = std::getenv("BO_FUSE_LAST")) c->fuse_last_hop = std::strcmp(e, "0") != 0;
   c->algo = cfg->reduce_algo == BO_REDUCE_AUTO ? (cfg->f16_exchange ? BO_REDUCE_RING : BO_REDUCE_NCCL)
                                                : cfg->reduce_algo;
   BO_CUDA(cudaSetDevice(device));
+  BO_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
   BO_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   c->own_stream = true;
   c->L = Layout::build(n_tensors, numels, first_consumers, cfg->bucket_bytes, world, rank);
@@ -760,6 +762,8 @@ bo_status bo_profile_read(bo_ctx* c, double* stage_ms, int64_t* stage_count, int
 
 int64_t bo_launch_count(const bo_ctx* c) { return c ? c->launches : 0; }
 
+int32_t bo_path_flags(const bo_ctx* c) { return c ? c->path : 0; }
+
 bo_status bo_accumulate(bo_ctx* c, int32_t micro, const uint16_t* const* grads) {
   BO_GUARD_BEGIN
   if (!c || !grads) fail(BO_ERR_INVALID_CONFIG, "null argument");
@@ -778,13 +782,16 @@ bo_status bo_accumulate(bo_ctx* c, int32_t micro, const uint16_t* const* grads) 
     return BO_OK;
   }
   grow_bc_table(c, c->calls + 2);
+  c->path = 0;
   if (c->world == 1 && aligned && !c->force_unfused) {
+    c->path = BO_PATH_ONE_RANK_FUSED;
     run_fused_single_rank(c, tab);
   } else {
+    if (c->world == 1) c->path = BO_PATH_ONE_RANK_STAGED;
     // the ring fuses flatten_param into its hops; NCCL needs the fusion buffer
     if (c->world == 1 || c->algo == BO_REDUCE_NCCL) launch_finalize(c, tab);
     run_reduce(c, tab);
-    run_lamb(c);  // world > 1: includes the fused parameter all-gather (IPC push)
+    run_lamb(c, tab);  // world > 1: includes the fused parameter all-gather (IPC push)
   }
   c->calls += 1;
   BO_GUARD_END

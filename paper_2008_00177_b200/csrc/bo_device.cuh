@@ -76,6 +76,38 @@ __device__ __forceinline__ Lamb4 lamb_elem4(const float (&g)[4], const float (&w
   return o;
 }
 
+// The same with the exact-division operands read from memory only on the rare
+// path (bcp -> {bc1, bc2}), which keeps two doubles out of the register file.
+template <typename C>
+__device__ __forceinline__ Lamb4 lamb_elem4(const float (&g)[4], const float (&w)[4],
+                                            const float (&m)[4], const float (&v)[4], const C& c,
+                                            const double* bcp, double ibc1, double ibc2) {
+  Lamb4 o;
+  float mh[4], vh[4];
+  bool need = false;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    o.m[i] = __fadd_rn(__fmul_rn(c.beta1, m[i]), __fmul_rn(c.omb1, g[i]));
+    o.v[i] = __fadd_rn(__fmul_rn(c.beta2, v[i]), __fmul_rn(__fmul_rn(c.omb2, g[i]), g[i]));
+    mh[i] = div_to_float_fast(o.m[i], ibc1, need);
+    vh[i] = div_to_float_fast(o.v[i], ibc2, need);
+  }
+  if (__builtin_expect(need, 0)) {
+    const double bc1 = bcp[0], bc2 = bcp[1];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      mh[i] = __double2float_rn(__ddiv_rn(static_cast<double>(o.m[i]), bc1));
+      vh[i] = __double2float_rn(__ddiv_rn(static_cast<double>(o.v[i]), bc2));
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float den = __fadd_rn(__fsqrt_rn(vh[i]), c.eps);
+    o.u[i] = __fadd_rn(__fdiv_rn(mh[i], den), __fmul_rn(c.wd, w[i]));
+  }
+  return o;
+}
+
 struct Moments {
   float m, v, u;
 };
@@ -113,6 +145,43 @@ __device__ __forceinline__ bool pair_nonfinite(uint32_t x) {
 // (lamb.cpp:179) on a single rank.
 __device__ __forceinline__ void raise_flag(bool bad, DevState* st) {
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&st->local_flag, 1);
+}
+
+// Streaming accesses with explicit L2 eviction priority (no L1 allocation):
+// evict_first for data read once, evict_last for what the next pass re-reads.
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ float4 ld4(const float* p, uint64_t pol) {
+  float4 r;
+  asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "l"(p), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ uint2 ld2u(const uint16_t* p, uint64_t pol) {
+  uint2 r;
+  asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;"
+               : "=r"(r.x), "=r"(r.y)
+               : "l"(p), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ void st4(float* p, float4 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "f"(v.x),
+               "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol));
+}
+__device__ __forceinline__ void widen4(uint2 x, float (&o)[4]) {
+  o[0] = widen(static_cast<uint16_t>(x.x & 0xFFFFu));
+  o[1] = widen(static_cast<uint16_t>(x.x >> 16));
+  o[2] = widen(static_cast<uint16_t>(x.y & 0xFFFFu));
+  o[3] = widen(static_cast<uint16_t>(x.y >> 16));
 }
 
 }  // namespace bo

@@ -151,6 +151,7 @@ struct PtrTable {
 struct bo_ctx {
   bo_trainer_config cfg{};
   int device = 0, rank = 0, world = 1, algo = BO_REDUCE_NCCL;
+  int num_sms = 148;
   bo::Layout L;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
@@ -171,7 +172,7 @@ struct bo_ctx {
   int n_fused_tiles = 0;
   int* d_fused_tensor_tiles = nullptr;  // [T+1] fused-tile ranges per tensor
   float* u = nullptr;                   // LAMB update scratch
-  bool force_unfused = false;           // BO_UNFUSED=1: use the multi-kernel path on one rank
+  bool force_unfused = false;           // BO_UNFUSED=1: unfused kernels (one rank: multi-kernel LAMB; ring: staged last hop)
   unsigned long long fused_epoch = 0;
 
   // device buffers
@@ -189,6 +190,9 @@ struct bo_ctx {
   float** d_peer_w = nullptr;          // [world] device pointers to each rank's w
   void* peer_wire[2][8] = {};          // every rank's ring staging buffers (IPC), host-side
   void* ring_result = nullptr;         // staging buffer holding the owned reduced chunk
+  const void* ring_last_in = nullptr;  // last hop fused into LAMB phase 1: its input
+  int fuse_last_hop = -1;
+  int path = 0;                        // BO_PATH_* bits of the last sync micro              // BO_FUSE_LAST=0/1 overrides the per-world default
   bool ring_via_nccl = false;          // BO_RING_NCCL=1: hops over ncclSend/ncclRecv
   std::vector<void*> ipc_opened;       // peer mappings to close
   int* d_barrier = nullptr;
@@ -226,7 +230,7 @@ void grow_bc_table(bo_ctx* c, int64_t need);
 void launch_accumulate(bo_ctx* c, int micro, const PtrTable& tab, bool vec_ok);
 void launch_finalize(bo_ctx* c, const PtrTable& tab);
 void run_reduce(bo_ctx* c, const PtrTable& tab);
-void run_lamb(bo_ctx* c);
+void run_lamb(bo_ctx* c, const PtrTable& tab);
 void gather_shard(bo_ctx* c);
 void run_fused_single_rank(bo_ctx* c, const PtrTable& tab);
 

@@ -431,106 +431,186 @@ __device__ __forceinline__ Split split_tile(int64_t s0, int len) {
   const int head = min(static_cast<int>((4 - (s0 & 3)) & 3), len);
   return Split{head, (len - head) >> 2, (len - head) & 3};
 }
-__device__ __forceinline__ void load_g4(const float* p, float (&o)[4]) {
-  const float4 x = __ldcs(reinterpret_cast<const float4*>(p));
-  o[0] = x.x; o[1] = x.y; o[2] = x.z; o[3] = x.w;
-}
-__device__ __forceinline__ void load_g4(const uint16_t* p, float (&o)[4]) {
-  const uint2 x = __ldcs(reinterpret_cast<const uint2*>(p));
-  o[0] = widen(static_cast<uint16_t>(x.x & 0xFFFFu));
-  o[1] = widen(static_cast<uint16_t>(x.x >> 16));
-  o[2] = widen(static_cast<uint16_t>(x.y & 0xFFFFu));
-  o[3] = widen(static_cast<uint16_t>(x.y >> 16));
-}
+// ------------------------------------------------ phase 1 (world > 1)
+// Phase 1 on this rank's shard: the reduced gradient g (trainer.cpp:212
+// scaling), the NonFiniteGradient flag (lamb.cpp:179), m', v' into the other
+// moment buffer set (double-buffered: found_inf is global, known only after
+// every rank's phase 1), the update u, and per-tile fp64 partials of
+// ||w||^2 and ||u||^2 (lamb.cpp:176-190).
+struct P1Args {
+  const TensorDev* td;
+  const float* acc;
+  int K;
+  float invn;
+  const float* wsh;
+  float *m0, *v0, *m1, *v1, *u;
+  DevState* st;
+  LambConsts c;
+  const double* bc_table;
+  double* tile_part;
+};
 
-// Phase 1 on this rank's shard: g = reduced * (1/world) (trainer.cpp:212), the
-// NonFiniteGradient flag (lamb.cpp:179), m', v' into the other buffer set
-// (double-buffered: found_inf is global, known only after every rank's phase
-// 1), the update u, and per-tile fp64 partials of ||w||^2, ||u||^2.
-template <typename G>
-__global__ void __launch_bounds__(512, 2) k_shard_p1(const LambTile* __restrict__ tiles,
-                                                     const G* __restrict__ g, float invn,
-                                                     const float* __restrict__ wsh, float* m0,
-                                                     float* v0, float* m1, float* v1,
-                                                     float* __restrict__ u,
-                                                     DevState* __restrict__ st, LambConsts c,
-                                                     const double* __restrict__ bc_table,
-                                                     double* __restrict__ tile_part) {
-  const LambTile t = tiles[blockIdx.x];
+// Phase 1 with one WARP per tile (<= 4096 elements, up to 128 per lane): the
+// tile's setup, its norm reduction (one warp_sum, no block barrier) and the
+// flag are amortised over 16x more elements per thread than with a CTA per
+// tile, which at 8 elements per thread spent about a quarter of its
+// instructions on them (profiles/r01_notes.md).
+//   kIn && kX : the fused last ring hop, g = wire(in + x) / N
+//   kIn       : the staged ring / NCCL shard, g = in / N
+//   kX        : one rank, g = x
+// with x = (h + acc) * inv from the sync micro's binary16 gradient and the
+// accumulator (flatten_param, trainer.cpp:186-203).
+constexpr int kWarpTileCTA = 256;
+template <typename W, bool kIn, bool kX, int U = 2, int kMinBlocks = 4>
+__global__ void __launch_bounds__(kWarpTileCTA, kMinBlocks) k_p1w(const LambTile* __restrict__ tiles,
+                                                          int n_tiles,
+                                                          const __grid_constant__ PtrTable tab,
+                                                          const W* __restrict__ in, P1Args A) {
+  static_assert(kIn || kX, "a gradient source");
+  const int wt = static_cast<int>((blockIdx.x * kWarpTileCTA + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (wt >= n_tiles) return;
+  DevState* __restrict__ st = A.st;
+  // one rank: an earlier micro overflowed, the step is skipped
+  if constexpr (!kIn) {
+    if (st->local_flag) return;
+  }
+  const LambTile t = tiles[wt];
   const int par = st->parity;
-  const float* __restrict__ m = par ? m1 : m0;
-  const float* __restrict__ v = par ? v1 : v0;
-  float* __restrict__ mn = par ? m0 : m1;
-  float* __restrict__ vn = par ? v0 : v1;
-  const double* bcp = bc_table + 4 * st->lamb_step;
-  const double bc[4] = {bcp[0], bcp[1], bcp[2], bcp[3]};
-  const Split sp = split_tile(t.s0, t.len);
+  const float* __restrict__ m = par ? A.m1 : A.m0;
+  const float* __restrict__ v = par ? A.v1 : A.v0;
+  float* __restrict__ mn = par ? A.m0 : A.m1;
+  float* __restrict__ vn = par ? A.v0 : A.v1;
+  const float* __restrict__ wsh = A.wsh + t.s0;
+  float* __restrict__ u = A.u + t.s0;
+  m += t.s0;
+  v += t.s0;
+  mn += t.s0;
+  vn += t.s0;
+  const W* __restrict__ gin = kIn ? in + t.s0 : nullptr;
+  const double* bcp = A.bc_table + 4 * st->lamb_step;
+  const double ibc1 = bcp[2], ibc2 = bcp[3];
+  const int K = A.K;
+  const uint64_t pf = policy_evict_first(), pl = policy_evict_last();
+  const uint16_t* __restrict__ h = nullptr;
+  const float* __restrict__ a = nullptr;
+  float inv = 0.0f;
+  bool vec = true;
+  if constexpr (kX) {
+    const TensorDev d = A.td[t.t];
+    const int64_t e0 = t.w0 - d.flat_off;  // element offset inside the tensor
+    h = tab.p[t.t] + e0;
+    a = A.acc + d.acc_off + e0;
+    inv = __fdiv_rn(1.0f, __fmul_rn(static_cast<float>(K), st->scale));
+    vec = ((e0 - t.s0) & 3) == 0 && (reinterpret_cast<uintptr_t>(tab.p[t.t]) & 7) == 0;
+  }
+  auto grad = [&](float win, float hg, float ag) {
+    if constexpr (kX) {
+      const float x = __fmul_rn(K > 1 ? __fadd_rn(hg, ag) : hg, inv);
+      if constexpr (kIn) {
+        return __fmul_rn(from_wire(to_wire<W>(__fadd_rn(win, x))), A.invn);
+      } else {
+        return x;
+      }
+    } else {
+      return __fmul_rn(win, A.invn);
+    }
+  };
   double wn = 0.0, un = 0.0;
   bool bad = false;
   auto scalar = [&](int e) {
-    const int64_t s = t.s0 + e;
-    const float gi = __fmul_rn(from_wire(g[s]), invn);
+    float hg = 0.0f, ag = 0.0f, win = 0.0f;
+    if constexpr (kX) {
+      hg = widen(h[e]);
+      if (K > 1) ag = a[e];
+    }
+    if constexpr (kIn) win = from_wire(gin[e]);
+    const float gi = grad(win, hg, ag);
     bad |= !finite(gi);
-    const float wi = wsh[s];
-    const Moments o = lamb_elem(gi, wi, m[s], v[s], c, bc);
-    mn[s] = o.m;
-    vn[s] = o.v;
-    u[s] = o.u;
+    const float wi = wsh[e];
+    const Moments o = lamb_elem(gi, wi, m[e], v[e], A.c, bcp);
+    mn[e] = o.m;
+    vn[e] = o.v;
+    u[e] = o.u;
     wn = __dadd_rn(wn, __dmul_rn(static_cast<double>(wi), static_cast<double>(wi)));
     un = __dadd_rn(un, __dmul_rn(static_cast<double>(o.u), static_cast<double>(o.u)));
   };
-  if (threadIdx.x < sp.head) scalar(static_cast<int>(threadIdx.x));
-  if (threadIdx.x >= 32 && static_cast<int>(threadIdx.x) - 32 < sp.tail) {
-    scalar(sp.head + 4 * sp.nv + static_cast<int>(threadIdx.x) - 32);
-  }
+  if (!vec) {
+    for (int e = lane; e < t.len; e += 32) scalar(e);
+  } else {
+    const Split sp = split_tile(t.s0, t.len);
+    if (lane < sp.head) scalar(lane);
+    if (lane >= 8 && lane - 8 < sp.tail) scalar(sp.head + 4 * sp.nv + lane - 8);
+    for (int q0 = 0; q0 < sp.nv; q0 += 32 * U) {
+      float iv[U][4], av[U][4];
+      uint2 hv[U];
+      float4 wv[U], mv[U], vv[U];
 #pragma unroll
-  for (int j = 0; j < 2; ++j) {
-    const int q = threadIdx.x + j * 512;
-    if (q < sp.nv) {
-      const int64_t s = t.s0 + sp.head + 4 * q;
-      float ga[4];
-      load_g4(g + s, ga);
-      const float4 w4 = __ldcs(reinterpret_cast<const float4*>(wsh + s));
-      const float4 m4 = __ldcs(reinterpret_cast<const float4*>(m + s));
-      const float4 v4 = __ldcs(reinterpret_cast<const float4*>(v + s));
-      const float wa[4] = {w4.x, w4.y, w4.z, w4.w};
-      const float ma[4] = {m4.x, m4.y, m4.z, m4.w};
-      const float va[4] = {v4.x, v4.y, v4.z, v4.w};
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        ga[i] = __fmul_rn(ga[i], invn);
-        bad |= !finite(ga[i]);
+      for (int j = 0; j < U; ++j) {
+        const int q = q0 + lane + 32 * j;
+        if (q < sp.nv) {
+          const int e = sp.head + 4 * q;
+          if constexpr (kIn) {
+            if constexpr (sizeof(W) == 2) {
+              widen4(__ldcs(reinterpret_cast<const uint2*>(gin + e)), iv[j]);
+            } else {
+              const float4 x = __ldcs(reinterpret_cast<const float4*>(gin + e));
+              iv[j][0] = x.x; iv[j][1] = x.y; iv[j][2] = x.z; iv[j][3] = x.w;
+            }
+          }
+          if constexpr (kX) {
+            hv[j] = ld2u(h + e, pf);
+            if (K > 1) {
+              const float4 a4 = ld4(a + e, pf);
+              av[j][0] = a4.x; av[j][1] = a4.y; av[j][2] = a4.z; av[j][3] = a4.w;
+            }
+          }
+          wv[j] = ld4(wsh + e, pl);
+          mv[j] = ld4(m + e, pf);
+          vv[j] = ld4(v + e, pf);
+        }
       }
-      const Lamb4 o = lamb_elem4(ga, wa, ma, va, c, bc[0], bc[1], bc[2], bc[3]);
-      __stcs(reinterpret_cast<float4*>(mn + s), make_float4(o.m[0], o.m[1], o.m[2], o.m[3]));
-      __stcs(reinterpret_cast<float4*>(vn + s), make_float4(o.v[0], o.v[1], o.v[2], o.v[3]));
-      *reinterpret_cast<float4*>(u + s) = make_float4(o.u[0], o.u[1], o.u[2], o.u[3]);
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        wn = __dadd_rn(wn, __dmul_rn(static_cast<double>(wa[i]), static_cast<double>(wa[i])));
-        un = __dadd_rn(un, __dmul_rn(static_cast<double>(o.u[i]), static_cast<double>(o.u[i])));
+      for (int j = 0; j < U; ++j) {
+        const int q = q0 + lane + 32 * j;
+        if (q < sp.nv) {
+          const int e = sp.head + 4 * q;
+          const float wa[4] = {wv[j].x, wv[j].y, wv[j].z, wv[j].w};
+          const float ma[4] = {mv[j].x, mv[j].y, mv[j].z, mv[j].w};
+          const float va[4] = {vv[j].x, vv[j].y, vv[j].z, vv[j].w};
+          float ga[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            float hg = 0.0f, ag = 0.0f, win = 0.0f;
+            if constexpr (kX) {
+              const uint32_t hw = i < 2 ? hv[j].x : hv[j].y;
+              hg = widen(static_cast<uint16_t>(hw >> (16 * (i & 1))));
+              if (K > 1) ag = av[j][i];
+            }
+            if constexpr (kIn) win = iv[j][i];
+            ga[i] = grad(win, hg, ag);
+            bad |= !finite(ga[i]);
+          }
+          const Lamb4 o = lamb_elem4(ga, wa, ma, va, A.c, bcp, ibc1, ibc2);
+          st4(mn + e, make_float4(o.m[0], o.m[1], o.m[2], o.m[3]), pf);
+          st4(vn + e, make_float4(o.v[0], o.v[1], o.v[2], o.v[3]), pf);
+          st4(u + e, make_float4(o.u[0], o.u[1], o.u[2], o.u[3]), pl);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            wn = __dadd_rn(wn, __dmul_rn(static_cast<double>(wa[i]), static_cast<double>(wa[i])));
+            un = __dadd_rn(un, __dmul_rn(static_cast<double>(o.u[i]), static_cast<double>(o.u[i])));
+          }
+        }
       }
     }
   }
-  raise_flag(bad, st);
   wn = warp_sum(wn);
   un = warp_sum(un);
-  __shared__ double red[2][16];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   if (lane == 0) {
-    red[0][wid] = wn;
-    red[1][wid] = un;
+    A.tile_part[2 * wt] = wn;
+    A.tile_part[2 * wt + 1] = un;
   }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double A = 0.0, B = 0.0;
-    for (int i = 0; i < 16; ++i) {
-      A += red[0][i];
-      B += red[1][i];
-    }
-    tile_part[2 * blockIdx.x] = A;
-    tile_part[2 * blockIdx.x + 1] = B;
-  }
+  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(&st->local_flag, 1);
 }
 
 // Phase 2 fused with the parameter all-gather: w -= (lr * r) * u on the
@@ -615,8 +695,19 @@ static void ring_reduce_scatter(bo_ctx* c, const PtrTable& tab, ncclDataType_t d
       check_launch(c, "k_hopx");
     }
   };
+  // The last hop completes the owned chunk. It can run inside LAMB phase 1
+  // (k_p1w<W, true, true>), which then reads the left neighbour's partial
+  // directly: one staged write + read of the chunk less, but the NVLink
+  // latency is exposed inside an HBM-bound kernel. Measured on BERT-large
+  // (profiles/r01_notes.md): a net win at world 2 (1.10 vs 1.18 ms), a loss
+  // at world 4 (0.67 vs 0.62 ms), so the default fuses only at world 2.
+  const bool fuse_last = !c->force_unfused && (c->fuse_last_hop >= 0 ? c->fuse_last_hop != 0 : N == 2);
+  c->ring_last_in = nullptr;
+  c->ring_result = nullptr;
   hop(r, nullptr, a, 0);  // hop 0 payload: this rank's own chunk r (collective.cpp:178)
-  if (c->peer_wire[0][left] && !c->ring_via_nccl) {
+  const bool p2p = c->peer_wire[0][left] && !c->ring_via_nccl;
+  c->path |= p2p ? BO_PATH_RING_P2P : BO_PATH_RING_SENDRECV;
+  if (p2p) {
     // Peer-to-peer hops: hop s reads the left neighbour's hop s-1 output in
     // place over NVLink (CUDA IPC mapping) and writes the other local buffer.
     // A 4-byte all-reduce before each hop is the barrier that orders a
@@ -624,6 +715,11 @@ static void ring_reduce_scatter(bo_ctx* c, const PtrTable& tab, ncclDataType_t d
     for (int s = 0; s < N - 1; ++s) {
       BO_NCCL(ncclAllReduce(c->d_barrier, c->d_barrier, 1, ncclInt32, ncclSum, c->comm, c->stream));
       const W* in = static_cast<const W*>(c->peer_wire[s % 2][left]);
+      if (s == N - 2 && fuse_last) {
+        c->ring_last_in = in;  // the last hop runs inside LAMB phase 1
+        c->path |= BO_PATH_LAST_HOP_FUSED;
+        return;
+      }
       W* out = static_cast<W*>(c->wire[(s + 1) % 2]);
       hop((r - s - 1 + 2 * N) % N, in, out, 1);  // chunk added at hop s (collective.hpp:70-71)
     }
@@ -634,19 +730,26 @@ static void ring_reduce_scatter(bo_ctx* c, const PtrTable& tab, ncclDataType_t d
       BO_NCCL(ncclSend(a, S, dt, right, c->comm, c->stream));
       BO_NCCL(ncclRecv(b, S, dt, left, c->comm, c->stream));
       BO_NCCL(ncclGroupEnd());
+      if (s == N - 2 && fuse_last) {
+        c->ring_last_in = b;
+        c->path |= BO_PATH_LAST_HOP_FUSED;
+        return;
+      }
       hop((r - s - 1 + 2 * N) % N, b, a, 1);  // chunk received at hop s (collective.hpp:70-71)
     }
     c->ring_result = a;
   }
-  // After N-1 hops the result buffer holds the finished chunk (r+1) % N,
-  // already wire-rounded (the owner re-round of collective.cpp:205-209): the
-  // chunk this rank owns (Layout::own). LAMB reads it in place.
+  // Unfused: after N-1 hops the result buffer holds the finished chunk
+  // (r+1) % N, already wire-rounded (the owner re-round of
+  // collective.cpp:205-209): the chunk this rank owns (Layout::own). LAMB
+  // reads it in place.
 }
 
 void run_reduce(bo_ctx* c, const PtrTable& tab) {
   if (c->world == 1) return;
   StageTimer timer(c, BO_STAGE_REDUCE);
   if (c->algo == BO_REDUCE_NCCL) {
+    c->path |= BO_PATH_NCCL_RS;
     BO_NCCL(ncclGroupStart());
     for (int b = 0; b < c->L.B; ++b) {
       BO_NCCL(ncclReduceScatter(c->x + c->L.base[b], c->gshard + c->L.shoff[b],
@@ -697,16 +800,18 @@ static void lamb_shard(bo_ctx* c, const G* g) {
 // the partials and flags (2T+1 doubles per rank, summed in rank order so all
 // ranks agree) -> trust ratios, found_inf, scaler -> phase 2 pushing the new
 // parameters into every rank's replica -> barrier.
-template <typename G>
-static void lamb_sharded(bo_ctx* c, const G* g) {
+template <typename W, bool kHop>
+static void lamb_sharded(bo_ctx* c, const PtrTable& tab, const W* in) {
   const int T = c->L.T;
   const float invn = 1.0f / static_cast<float>(c->world);  // trainer.cpp:212
   {
   StageTimer timer(c, BO_STAGE_LAMB_NORMS);
-  k_shard_p1<G><<<c->n_lamb_tiles, 512, 0, c->stream>>>(c->d_lamb_tiles, g, invn, c->wsh, c->m, c->v,
-                                                         c->m_alt, c->v_alt, c->u, c->state, c->lamb,
-                                                         c->bc_table, c->tile_part);
-  check_launch(c, "k_shard_p1");
+  const P1Args A{c->d_tensors, c->acc, c->cfg.accumulation, invn, c->wsh, c->m, c->v,
+                 c->m_alt, c->v_alt, c->u, c->state, c->lamb, c->bc_table, c->tile_part};
+  const int grid = (c->n_lamb_tiles * 32 + kWarpTileCTA - 1) / kWarpTileCTA;
+  k_p1w<W, true, kHop, 1, 4><<<grid, kWarpTileCTA, 0, c->stream>>>(c->d_lamb_tiles, c->n_lamb_tiles,
+                                                                  tab, in, A);
+  check_launch(c, "k_p1w");
   }
   {
   StageTimer timer(c, BO_STAGE_TRUST);
@@ -732,18 +837,27 @@ static void lamb_sharded(bo_ctx* c, const G* g) {
   BO_NCCL(ncclAllReduce(c->d_barrier, c->d_barrier, 1, ncclInt32, ncclSum, c->comm, c->stream));
 }
 
-void run_lamb(bo_ctx* c) {
+void run_lamb(bo_ctx* c, const PtrTable& tab) {
   if (c->world == 1) {
     lamb_shard<float>(c, c->gshard);
   } else if (c->algo == BO_REDUCE_RING) {
-    // the reduced shard is the ring's final wire buffer (wire-exact values)
+    // the owned chunk: the left neighbour's last partial (last hop fused into
+    // phase 1) or the ring's final wire buffer (wire-exact values)
     if (c->cfg.f16_exchange) {
-      lamb_sharded<uint16_t>(c, static_cast<const uint16_t*>(c->ring_result));
+      if (c->ring_last_in) {
+        lamb_sharded<uint16_t, true>(c, tab, static_cast<const uint16_t*>(c->ring_last_in));
+      } else {
+        lamb_sharded<uint16_t, false>(c, tab, static_cast<const uint16_t*>(c->ring_result));
+      }
     } else {
-      lamb_sharded<float>(c, static_cast<const float*>(c->ring_result));
+      if (c->ring_last_in) {
+        lamb_sharded<float, true>(c, tab, static_cast<const float*>(c->ring_last_in));
+      } else {
+        lamb_sharded<float, false>(c, tab, static_cast<const float*>(c->ring_result));
+      }
     }
   } else {
-    lamb_sharded<float>(c, c->gshard);
+    lamb_sharded<float, false>(c, tab, c->gshard);
   }
 }
 

@@ -229,6 +229,18 @@ class GradPipeline:
     def synchronize(self) -> None:
         _lib.check(self.lib.bo_synchronize(self.ctx))
 
+    # -- introspection
+    PATH_NAMES = {1: "one_rank_fused", 2: "one_rank_staged", 4: "ring_p2p", 8: "ring_sendrecv",
+                  16: "last_hop_fused", 32: "nccl_reduce_scatter"}
+
+    def path(self) -> list[str]:
+        """Implementation the last sync micro ran (BO_PATH_* names)."""
+        f = int(self.lib.bo_path_flags(self.ctx))
+        return [n for b, n in self.PATH_NAMES.items() if f & b]
+
+    def launch_count(self) -> int:
+        return int(self.lib.bo_launch_count(self.ctx))
+
     # -- state
     def load_params(self, params) -> None:
         """params: flat float32 model-order array (numpy) or CUDA tensor."""

@@ -19,14 +19,15 @@ class GradBuffers:
 
     aligned=True gives every tensor a 256-byte aligned slot (vectorised
     accumulate path); aligned=False packs tensors back to back in model order
-    so that most slots are misaligned (scalar path).
+    starting one element into the buffer, so that the slots are misaligned
+    (scalar paths) whatever the tensor sizes.
     """
 
     def __init__(self, spec, K: int, device: int = 0, aligned: bool = True):
         self.spec = spec
         self.numels = spec.numels()
         self.model_off = np.concatenate([[0], np.cumsum(self.numels)[:-1]]).astype(np.int64)
-        offs, o = [], 0
+        offs, o = [], 0 if aligned else 1
         for n in self.numels:
             offs.append(o)
             o += (n + 127) // 128 * 128 if aligned else n
@@ -41,7 +42,7 @@ class GradBuffers:
              spike_exp=1) -> None:
         buf = self.bufs[k]
         if not self.aligned:
-            synth_grads(buf, 0, seed, rank, step, k, scale, spike_ppm, spike_exp)
+            synth_grads(buf[1:], 0, seed, rank, step, k, scale, spike_ppm, spike_exp)
             return
         for t, n in enumerate(self.numels):
             s = self.slot[t]

@@ -30,6 +30,9 @@ CASES = {
     "ring16_1bucket": (True, 1, 1, 1 << 30, dict(init_scale=4096.0), 0, 1, True),
     "ring16_tinybuckets": (True, 1, 2, 1, dict(init_scale=4096.0), 0, 1, True),
 }
+# "<case>_unfused" / "<case>_fused": the same case with the ring's last hop
+# staged (BO_UNFUSED=1) or fused into LAMB phase 1 (BO_FUSE_LAST=1) whatever
+# the world's default
 
 
 def main():
@@ -48,7 +51,14 @@ def main():
     from paper_2008_00177_b200.pipeline import GradPipeline, LambConfig, ScalerConfig, TrainerConfig
     from tests.harness import max_rel_or_abs, run_pipeline
 
-    f16, algo, K, bb, sc, ppm, sexp, exact = CASES[args.case]
+    case = args.case
+    if case.endswith("_unfused"):
+        os.environ["BO_UNFUSED"] = "1"
+        case = case[: -len("_unfused")]
+    elif case.endswith("_fused"):
+        os.environ["BO_FUSE_LAST"] = "1"
+        case = case[: -len("_fused")]
+    f16, algo, K, bb, sc, ppm, sexp, exact = CASES[case]
     if args.model == "tiny":
         spec = bert_spec(BERT_TINY)
     elif args.model == "ragged":
@@ -87,6 +97,7 @@ def main():
         replicas_equal = all(torch.equal(allw[0], x) for x in allw)
         result.update({
             "case": args.case, "world": world, "params": P, "steps": args.steps,
+            "path": pipe.path(),
             "found_inf": fi.tolist(), "ref_found_inf": ref.found_inf.tolist(),
             "scales_equal": bool(np.array_equal(su, ref.scale_used)),
             "final_scale": st.loss_scale, "ref_final_scale": ref.final_scale,

@@ -40,13 +40,18 @@ def run_case(case, nproc, model="tiny", steps=4):
 
 
 @pytest.mark.parametrize("case", ["ring16", "ring32", "nccl32", "ring16_1bucket",
-                                  "ring16_tinybuckets"])
+                                  "ring16_tinybuckets", "ring16_unfused", "ring32_unfused"])
 def test_two_gpus(case):
     if _ngpu() < 2:
         pytest.skip("needs 2 GPUs")
     res = run_case(case, 2)
     if case.startswith("ring"):
         assert res["m_bit_exact"] and res["v_bit_exact"]
+        assert "ring_p2p" in res["path"]
+        # world 2 runs the last hop inside LAMB phase 1 unless BO_UNFUSED is set
+        assert ("last_hop_fused" in res["path"]) == (not case.endswith("_unfused"))
+    else:
+        assert res["path"] == ["nccl_reduce_scatter"]
 
 
 @pytest.mark.parametrize("model", ["ragged", "small"])
@@ -60,5 +65,10 @@ def test_two_gpus_shapes(model):
 def test_more_gpus(n):
     if _ngpu() < n:
         pytest.skip(f"needs {n} GPUs")
-    run_case("ring16", n)
+    res = run_case("ring16", n)
+    assert res["m_bit_exact"] and res["v_bit_exact"]
+    assert res["path"] == ["ring_p2p"]  # staged last hop beyond world 2
+    res = run_case("ring16_fused", n)
+    assert res["m_bit_exact"] and res["v_bit_exact"]
+    assert "last_hop_fused" in res["path"]
     run_case("nccl32", n)

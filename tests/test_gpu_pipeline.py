@@ -59,6 +59,8 @@ def test_tiny_bert_matches_oracle(torch_cuda, oracle, K, aligned):
     w = _compare(pipe, ref, su, fi)
     # bit-exact in practice; record how close
     assert np.mean(w.view(np.uint32) == ref.params.view(np.uint32)) > 0.999
+    # 16-byte aligned gradient slots take the fused one-rank kernels
+    assert pipe.path() == (["one_rank_fused"] if aligned else ["one_rank_staged"])
 
 
 def test_dynamic_scaler_overflow_sequence(torch_cuda, oracle):
