@@ -614,29 +614,88 @@ __global__ void __launch_bounds__(kWarpTileCTA, kMinBlocks) k_p1w(const LambTile
 }
 
 // Phase 2 fused with the parameter all-gather: w -= (lr * r) * u on the
-// master shard (lamb.cpp:197-198), and the new value stored straight into
-// every rank's flat parameter replica over NVLink (CUDA IPC mappings), at the
-// element's fusion-buffer position. Skipped steps exit.
+// master shard (lamb.cpp:197-198), and the new value written into every
+// rank's flat parameter replica over NVLink (CUDA IPC mappings) at the
+// element's fusion-buffer position. The replica writes are bulk asynchronous
+// copies (cp.async.bulk, the TMA engine) from a shared-memory copy of the
+// tile, staged at its 16-byte phase in the flat replica: one bulk copy per
+// destination moves the aligned middle of the tile and the SMs only issue the
+// <= 3 + 3 edge elements. The arithmetic reads the shard with 16-byte loads.
+// Skipped steps exit.
+__device__ __forceinline__ void bulk_s2g(float* gdst, const float* ssrc, uint32_t bytes) {
+  const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(ssrc));
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(s), "r"(bytes)
+               : "memory");
+}
 __global__ void __launch_bounds__(kThreads) k_shard_p2_push(const LambTile* __restrict__ tiles,
                                                             float* __restrict__ wsh,
                                                             const float* __restrict__ u,
-                                                            const DevState* __restrict__ st,
-                                                            LambConsts c,
-                                                            const float* __restrict__ trust,
-                                                            float* const* __restrict__ peer_w,
-                                                            int N) {
+                                                                 const DevState* __restrict__ st,
+                                                                 LambConsts c,
+                                                                 const float* __restrict__ trust,
+                                                                 float* const* __restrict__ peer_w,
+                                                                 int N) {
   if (!st->do_update) return;
+  __shared__ __align__(128) float buf[kTileElems + 4];
   __shared__ float* dst[8];
   if (threadIdx.x < N) dst[threadIdx.x] = peer_w[threadIdx.x];
-  __syncthreads();
   const LambTile t = tiles[blockIdx.x];
   const float step_scale = __fmul_rn(c.lr, trust[t.t]);
-  for (int e = threadIdx.x; e < t.len; e += kThreads) {
+  const int off = static_cast<int>(t.w0 & 3);  // buf[off + e] <-> flat element w0 + e
+  const Split sp = split_tile(t.s0, t.len);
+  auto one = [&](int e) {
     const int64_t s = t.s0 + e;
-    const float nw = __fsub_rn(wsh[s], __fmul_rn(step_scale, __ldcs(u + s)));
+    const float nw = __fsub_rn(wsh[s], __fmul_rn(step_scale, u[s]));
     wsh[s] = nw;
-    for (int j = 0; j < N; ++j) __stcs(dst[j] + t.w0 + e, nw);
+    buf[off + e] = nw;
+  };
+  if (static_cast<int>(threadIdx.x) < sp.head) one(threadIdx.x);
+  if (threadIdx.x >= 32 && static_cast<int>(threadIdx.x) - 32 < sp.tail) {
+    one(sp.head + 4 * sp.nv + static_cast<int>(threadIdx.x) - 32);
   }
+  for (int q = threadIdx.x; q < sp.nv; q += kThreads) {
+    const int e = sp.head + 4 * q;
+    const int64_t s = t.s0 + e;
+    const float4 w4 = *reinterpret_cast<const float4*>(wsh + s);
+    const float4 u4 = __ldcs(reinterpret_cast<const float4*>(u + s));
+    const float4 n4 = make_float4(__fsub_rn(w4.x, __fmul_rn(step_scale, u4.x)),
+                                  __fsub_rn(w4.y, __fmul_rn(step_scale, u4.y)),
+                                  __fsub_rn(w4.z, __fmul_rn(step_scale, u4.z)),
+                                  __fsub_rn(w4.w, __fmul_rn(step_scale, u4.w)));
+    *reinterpret_cast<float4*>(wsh + s) = n4;
+    buf[off + e] = n4.x;
+    buf[off + e + 1] = n4.y;
+    buf[off + e + 2] = n4.z;
+    buf[off + e + 3] = n4.w;
+  }
+  // make the generic-proxy shared-memory writes visible to the bulk copies
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+  // flat elements [w0, w0 + len): aligned middle [a0, a1) by bulk copy
+  const int64_t a0 = (t.w0 + 3) & ~static_cast<int64_t>(3);
+  const int64_t a1 = (t.w0 + t.len) & ~static_cast<int64_t>(3);
+  if (a1 > a0) {
+    if (threadIdx.x == 0) {
+      for (int j = 0; j < N; ++j) {
+        bulk_s2g(dst[j] + a0, buf + off + (a0 - t.w0), static_cast<uint32_t>(a1 - a0) * 4u);
+      }
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+  }
+  // edges (and tiles shorter than one aligned 16-byte group)
+  const int nhead = static_cast<int>(a1 > a0 ? a0 - t.w0 : t.len);
+  const int ntail = static_cast<int>(a1 > a0 ? t.w0 + t.len - a1 : 0);
+  if (static_cast<int>(threadIdx.x) < nhead * N) {
+    const int e = threadIdx.x % nhead, j = threadIdx.x / nhead;
+    dst[j][t.w0 + e] = buf[off + e];
+  } else if (static_cast<int>(threadIdx.x) >= 128 && static_cast<int>(threadIdx.x) - 128 < ntail * N) {
+    const int i = static_cast<int>(threadIdx.x) - 128;
+    const int e = static_cast<int>(a1 - t.w0) + i % ntail, j = i / ntail;
+    dst[j][t.w0 + e] = buf[off + e];
+  }
+  // the shared-memory tile must outlive the copies; kernel completion then
+  // implies the replica writes are done
+  if (threadIdx.x == 0 && a1 > a0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 // Owned chunk positions of the flat replica -> the master shard (load time).

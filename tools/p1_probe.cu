@@ -100,7 +100,20 @@ int main(int argc, char** argv) {
   float** d_peer_w;
   CK(cudaMalloc(&d_peer_w, 8 * sizeof(float*)));
   std::vector<float*> pws(8, c->w);
-  for (int r = 0; r < world; ++r) pws[r] = (r == rank || !peer) ? c->w : pw;
+  // replicas of the other ranks on distinct GPUs where the box has them
+  for (int r = 0, j = 0; r < world; ++r) {
+    if (r == rank || !peer) continue;
+    const int dev = 1 + (j++ % (ndev - 1));
+    if (dev == 1) {
+      pws[r] = pw;
+    } else {
+      CK(cudaDeviceEnablePeerAccess(dev, 0));
+      CK(cudaSetDevice(dev));
+      CK(cudaDeviceEnablePeerAccess(0, 0));
+      CK(cudaMalloc(&pws[r], L.flat_total * 4));
+      CK(cudaSetDevice(0));
+    }
+  }
   CK(cudaMemcpy(d_peer_w, pws.data(), 8 * sizeof(float*), cudaMemcpyHostToDevice));
   DevState st{};
   CK(cudaMemcpy(&st, c->state, sizeof(st), cudaMemcpyDeviceToHost));
