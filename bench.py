@@ -41,7 +41,6 @@ BYTES_FINALIZE = 2 + 4 + 4              # read fp16 + acc, write fusion buffer (
 BYTES_FINALIZE_K1 = 2 + 4
 BYTES_LAMB_NORMS = 4 * 4                # read g, w, m, v
 BYTES_LAMB_UPDATE = 4 * 4 + 3 * 4       # read g, w, m, v; write w, m, v
-BYTES_LAMB_ALGO = 28                    # single-pass LAMB (the algorithmic minimum)
 # one rank, k_lamb_p1 (read h, acc, w, m, v; write m', v', u) + k_lamb_p2 (read w, u; write w)
 BYTES_LAMB_FUSED = (2 + 4 + 3 * 4 + 3 * 4) + (2 * 4 + 4)
 
@@ -344,25 +343,48 @@ def main_b200(args):
                     "lamb_norms": "k_lamb_p1" if world == 1 else "k_p1w",
                     "lamb_update": "k_lamb_p2" if world == 1 else "k_shard_p2_push",
                     "hop_kernels": "k_hopx"}
-    roofline = {"kernel": kernel_names[dom], "bound": "hbm", "achieved": stages[dom]["GB/s"],
-                "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s", "frac": stages[dom]["frac"],
-                "traffic": traffic_from_profiles(kernel_names[dom]),
-                "algorithmic_bytes_per_launch": stages[dom]["bytes"]}
+    st_dom = stages[dom]
+    if st_dom.get("nvlink_frac", 0.0) > st_dom["frac"]:
+        # the parameter push / ring hops at world > 1: NVLink is the bound
+        roofline = {"kernel": kernel_names[dom], "bound": "nvlink", "achieved": st_dom["nvlink_GB/s"],
+                    "peak": NVLINK_GBS, "peak_kind": "measured (B200_PROFILING.md peer copy)",
+                    "unit": "GB/s", "frac": st_dom["nvlink_frac"], "traffic": None,
+                    "algorithmic_bytes_per_launch": st_dom["nvlink_bytes"],
+                    "hbm_frac": st_dom["frac"]}
+    else:
+        roofline = {"kernel": kernel_names[dom], "bound": "hbm", "achieved": st_dom["GB/s"],
+                    "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s", "frac": st_dom["frac"],
+                    "traffic": traffic_from_profiles(kernel_names[dom]),
+                    "algorithmic_bytes_per_launch": st_dom["bytes"]}
+    if roofline["frac"] > 1.0:
+        roofline["note"] = ("the measured HBM peak is a 1:1 read:write copy; this kernel's "
+                            "read-heavy mix streams slightly above it")
 
-    # whole-step roofline: sum over stages of max(HBM, NVLink) time
+    # whole-step roofline: sum over stages of max(HBM, NVLink)
+    # time, with A = accumulate + finalize (36 B/param, 34 with the binary16
+    # wire: the fusion buffer element is E bytes), C = LAMB on the shard
+    # (24 + E B/param: g, w, m, v read; w, m, v written; one rank reads the
+    # fp32 fusion buffer), B = reduce-scatter, D = all-gather of fp32 weights;
+    # plus the stricter pipelined bound max(sum HBM / BW_hbm, sum NVL / BW_nvl)
     E = 2 if f16 else 4
-    hbm_a = (BYTES_ACCUMULATE_FIRST + BYTES_ACCUMULATE * (K - 2) + BYTES_FINALIZE) * P if K > 1 \
-        else BYTES_FINALIZE_K1 * P
-    hbm_c = BYTES_LAMB_ALGO * P / world
+    E_lamb = E if world > 1 else 4
+    hbm_a = (BYTES_ACCUMULATE_FIRST + BYTES_ACCUMULATE * (K - 2) + 2 + 4 + E) * P if K > 1 \
+        else (2 + E) * P
+    hbm_c = (24 + E_lamb) * P / world
     nvl_b = (world - 1) / world * E * P
     nvl_d = (world - 1) / world * 4 * P
     t_roof = hbm_a / (hbm * 1e9) + hbm_c / (hbm * 1e9) + nvl_b / (NVLINK_GBS * 1e9) + \
         nvl_d / (NVLINK_GBS * 1e9)
+    t_pipe = max((hbm_a + hbm_c) / (hbm * 1e9), (nvl_b + nvl_d) / (NVLINK_GBS * 1e9))
     step_roofline = {"t_roof_ms": round(t_roof * 1e3, 4), "frac": round(t_roof * 1e3 / ms, 4),
+                     "t_pipelined_ms": round(t_pipe * 1e3, 4),
+                     "pipelined_frac": round(t_pipe * 1e3 / ms, 4),
                      "hbm_bytes": int(hbm_a + hbm_c), "nvlink_bytes": int(nvl_b + nvl_d),
                      "hbm_gbs": hbm, "nvlink_gbs": NVLINK_GBS,
-                     "formula": "sum_stages max(HBM/BW_hbm, NVL/BW_nvl); A=acc+finalize, "
-                                "C=28 B/param LAMB on the shard, B=RS, D=AG"}
+                     "formula": "frac: sum over stages of max(HBM/BW_hbm, NVL/BW_nvl) with "
+                                "A=acc+finalize, C=LAMB on the shard, B=RS, D=AG (no overlap; "
+                                "> 1 when stages overlap, e.g. the fused last hop); "
+                                "pipelined_frac: max(sum HBM/BW_hbm, sum NVL/BW_nvl)"}
 
     # end to end through the public API with host buffers
     e2e = None
