@@ -154,9 +154,6 @@ int main(int argc, char** argv) {
                                                    c->v_alt, c->u, c->state, c->lamb, c->bc_table, 4,
                                                    c->tile_part);
     });
-    time("k_p1w<x> U2 B4 (one rank)", 30 * S, 0, [&] {
-      k_p1w<float, false, true, 2, 4><<<wgrid, kWarpTileCTA>>>(c->d_lamb_tiles, c->n_lamb_tiles, tab, nullptr, A);
-    });
     time("k_p1w<x> U1 B4 (one rank)", 30 * S, 0, [&] {
       k_p1w<float, false, true, 1, 4><<<wgrid, kWarpTileCTA>>>(c->d_lamb_tiles, c->n_lamb_tiles, tab, nullptr, A);
     });
@@ -168,32 +165,14 @@ int main(int argc, char** argv) {
     return 0;
   }
   const int t0 = c->hopx_begin[q], t1 = c->hopx_begin[q + 1];
-  time("k_p1w<f16,in> staged local", 26 * S, 0, [&] {
-    k_p1w<uint16_t, true, false><<<wgrid, kWarpTileCTA>>>(c->d_lamb_tiles, c->n_lamb_tiles, tab, lin, A);
-  });
-  time("k_p1w<f16,in,x> U2 B4 local", 30 * S + 2 * S, 0, [&] {
-    k_p1w<uint16_t, true, true, 2, 4><<<wgrid, kWarpTileCTA>>>(c->d_lamb_tiles, c->n_lamb_tiles, tab, lin, A);
-  });
-  time("k_p1w<f16,in,x> U2 B4 peer", 30 * S, 2 * S, [&] {
-    k_p1w<uint16_t, true, true, 2, 4><<<wgrid, kWarpTileCTA>>>(c->d_lamb_tiles, c->n_lamb_tiles, tab, pin, A);
-  });
-  time("k_p1w<f16,in,x> U2 B3 peer", 30 * S, 2 * S, [&] {
-    k_p1w<uint16_t, true, true, 2, 3><<<wgrid, kWarpTileCTA>>>(c->d_lamb_tiles, c->n_lamb_tiles, tab, pin, A);
+  time("k_p1w<f16,in,x> U1 B4 local", 30 * S + 2 * S, 0, [&] {
+    k_p1w<uint16_t, true, true, 1, 4><<<wgrid, kWarpTileCTA>>>(c->d_lamb_tiles, c->n_lamb_tiles, tab, lin, A);
   });
   time("k_p1w<f16,in,x> U1 B4 peer", 30 * S, 2 * S, [&] {
     k_p1w<uint16_t, true, true, 1, 4><<<wgrid, kWarpTileCTA>>>(c->d_lamb_tiles, c->n_lamb_tiles, tab, pin, A);
   });
-  time("k_p1w<f16,in,x> U1 B3 peer", 30 * S, 2 * S, [&] {
-    k_p1w<uint16_t, true, true, 1, 3><<<wgrid, kWarpTileCTA>>>(c->d_lamb_tiles, c->n_lamb_tiles, tab, pin, A);
-  });
   time("k_p1w<f16,in> U1 B4 staged local", 26 * S, 0, [&] {
     k_p1w<uint16_t, true, false, 1, 4><<<wgrid, kWarpTileCTA>>>(c->d_lamb_tiles, c->n_lamb_tiles, tab, lin, A);
-  });
-  time("k_p1w<f16,in,x> U1 B2 peer", 30 * S, 2 * S, [&] {
-    k_p1w<uint16_t, true, true, 1, 2><<<wgrid, kWarpTileCTA>>>(c->d_lamb_tiles, c->n_lamb_tiles, tab, pin, A);
-  });
-  time("k_p1w<f16,in,x> U2 B2 peer", 30 * S, 2 * S, [&] {
-    k_p1w<uint16_t, true, true, 2, 2><<<wgrid, kWarpTileCTA>>>(c->d_lamb_tiles, c->n_lamb_tiles, tab, pin, A);
   });
   time("k_hopx<f16> (own chunk) local", 10 * S, 0, [&] {
     k_hopx<uint16_t><<<t1 - t0, kThreads>>>(c->d_hopx_tiles + t0, c->d_tensors, tab, c->acc, c->state,
