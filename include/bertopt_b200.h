@@ -187,6 +187,17 @@ bo_status bo_param_ptr(bo_ctx* ctx, int32_t tensor, float** out);
  * ratio; skipped on overflow) -> loss-scaler update -> all-gather of the
  * updated parameters. Asynchronous on the context stream. */
 bo_status bo_accumulate(bo_ctx* ctx, int32_t micro, const uint16_t* const* grads);
+/* The sync micro with bucket-level overlap (TrainerConfig::overlap,
+ * trainer.cpp:247-348; readiness = Tape::backward's progress hook,
+ * tensor.hpp:94-106): deliver the sync micro's gradients as they become final,
+ * n tensors per call (tensor indices + device pointers, any chunking, each
+ * tensor once). Buckets are reduced in layout order, in communication groups
+ * of whole buckets, on an internal stream as soon as every tensor of the group
+ * has been delivered — overlapping the caller's remaining backward work on the
+ * context stream. The call that delivers the last tensor runs the rest of the
+ * step. Results are bit-identical to bo_accumulate(ctx, K-1, grads). Micros
+ * 0..K-2 still go through bo_accumulate. */
+bo_status bo_sync_ready(bo_ctx* ctx, int32_t n, const int32_t* tensors, const uint16_t* const* grads);
 
 /* ---- measurement ---------------------------------------------------------- */
 /* Stage timing with CUDA events recorded on the context stream around every
@@ -213,6 +224,7 @@ int64_t bo_launch_count(const bo_ctx* ctx);
 #define BO_PATH_RING_SENDRECV 8      /* ring hops over ncclSend/ncclRecv */
 #define BO_PATH_LAST_HOP_FUSED 16    /* the ring's last hop ran inside LAMB phase 1 */
 #define BO_PATH_NCCL_RS 32           /* ncclReduceScatter of the fusion buffer */
+#define BO_PATH_OVERLAP 64           /* sync micro delivered through bo_sync_ready */
 int32_t bo_path_flags(const bo_ctx* ctx);
 
 /* ---- operator-level drop-ins -------------------------------------------- */

@@ -101,9 +101,11 @@ void upload_tables(bo_ctx* c) {
     // boundaries, in shard order.
     std::vector<HopXTile> hx;
     c->hopx_begin.assign(static_cast<size_t>(c->world) + 1, 0);
+    c->hopx_bucket_begin.assign(static_cast<size_t>(c->world), std::vector<int>(static_cast<size_t>(L.B) + 1, 0));
     for (int qq = 0; qq < c->world; ++qq) {
       c->hopx_begin[static_cast<size_t>(qq)] = static_cast<int>(hx.size());
       for (int b = 0; b < L.B; ++b) {
+        c->hopx_bucket_begin[static_cast<size_t>(qq)][static_cast<size_t>(b)] = static_cast<int>(hx.size());
         const int64_t cb = L.chunk[static_cast<size_t>(b)];
         const int64_t lo = qq * cb;
         const int64_t hi = std::min<int64_t>((qq + 1) * cb, L.elems[static_cast<size_t>(b)]);
@@ -116,9 +118,49 @@ void upload_tables(bo_ctx* c) {
           }
         }
       }
+      c->hopx_bucket_begin[static_cast<size_t>(qq)][static_cast<size_t>(L.B)] = static_cast<int>(hx.size());
     }
     c->hopx_begin[static_cast<size_t>(c->world)] = static_cast<int>(hx.size());
     c->d_hopx_tiles = upload(c, hx);
+
+    // Communication groups for the overlapped sync micro: consecutive buckets
+    // (layout order = gradient-ready order) merged up to >= BO_COMM_GROUP_ELEMS
+    // elements (default 16 Mi = 64 MiB of fp32 gradient), so every group costs
+    // N - 1 hop barriers; a pure function of the layout and the environment,
+    // which must therefore match across ranks (it is part of the layout hash).
+    int64_t group_elems = 16ll << 20;
+    if (const char* e = std::getenv("BO_COMM_GROUP_ELEMS")) {
+      group_elems = std::max<int64_t>(1, std::atoll(e));
+    }
+    c->comm_groups.clear();
+    c->group_of_bucket.assign(static_cast<size_t>(L.B), 0);
+    std::vector<AccTile> gacc;
+    std::vector<int> first_acc_tile(static_cast<size_t>(L.T) + 1, 0);
+    for (int t = 0, i = 0; t < L.T; ++t) {
+      first_acc_tile[static_cast<size_t>(t)] = i;
+      i += static_cast<int>((L.numel[static_cast<size_t>(t)] + kTileElems - 1) / kTileElems);
+    }
+    int b0 = 0;
+    int64_t n = 0;
+    for (int b = 0; b < L.B; ++b) {
+      n += L.elems[static_cast<size_t>(b)];
+      if (n >= group_elems || b == L.B - 1) {
+        bo_ctx::CommGroup g{b0, b + 1, 0, static_cast<int>(gacc.size()), 0};
+        for (int bb = b0; bb <= b; ++bb) {
+          c->group_of_bucket[static_cast<size_t>(bb)] = static_cast<int>(c->comm_groups.size());
+          for (int p : L.buckets[static_cast<size_t>(bb)]) {
+            g.pending0 += 1;
+            const int64_t nt = (L.numel[static_cast<size_t>(p)] + kTileElems - 1) / kTileElems;
+            for (int64_t k = 0; k < nt; ++k) gacc.push_back(acc_tiles[static_cast<size_t>(first_acc_tile[static_cast<size_t>(p)] + k)]);
+          }
+        }
+        g.acc1 = static_cast<int>(gacc.size());
+        c->comm_groups.push_back(g);
+        b0 = b + 1;
+        n = 0;
+      }
+    }
+    c->d_group_acc_tiles = upload(c, gacc);
   }
   c->d_tensors = upload(c, td);
   c->d_acc_tiles = upload(c, acc_tiles);
@@ -166,20 +208,23 @@ static cudaEvent_t take_event(bo_ctx* c) {
   return e;
 }
 
-StageTimer::StageTimer(bo_ctx* ctx, int s) : c(ctx), stage(s) {
+StageTimer::StageTimer(bo_ctx* ctx, int s) : StageTimer(ctx, s, ctx->stream) {}
+
+StageTimer::StageTimer(bo_ctx* ctx, int s, cudaStream_t on) : c(ctx), stage(s), stream(on) {
   if (!c->profiling) return;
   b = take_event(c);
-  BO_CUDA(cudaEventRecord(b, c->stream));
+  BO_CUDA(cudaEventRecord(b, stream));
 }
 
 StageTimer::~StageTimer() {
   if (!c->profiling || !b) return;
   cudaEvent_t e = take_event(c);
-  if (cudaEventRecord(e, c->stream) == cudaSuccess) c->marks.push_back({stage, b, e});
+  if (cudaEventRecord(e, stream) == cudaSuccess) c->marks.push_back({stage, b, e});
 }
 
 static void drain_marks(bo_ctx* c) {
   BO_CUDA(cudaStreamSynchronize(c->stream));
+  if (c->comm_stream) BO_CUDA(cudaStreamSynchronize(c->comm_stream));
   for (const auto& mk : c->marks) {
     float ms = 0.0f;
     BO_CUDA(cudaEventElapsedTime(&ms, mk.a, mk.b));
@@ -417,7 +462,12 @@ bo_status bo_create(const bo_trainer_config* cfg, int32_t n_tensors, const int64
   // step's overflow flag is final (DevState::parity picks the current set)
   c->m_alt = static_cast<float*>(dev_alloc(c, static_cast<size_t>(L.shard_total) * 4));
   c->v_alt = static_cast<float*>(dev_alloc(c, static_cast<size_t>(L.shard_total) * 4));
+  c->sync_tab = new PtrTable{};
+  c->delivered.assign(static_cast<size_t>(L.T), 0);
   if (world > 1) {
+    BO_CUDA(cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));
+    BO_CUDA(cudaEventCreateWithFlags(&c->comm_ready, cudaEventDisableTiming));
+    BO_CUDA(cudaEventCreateWithFlags(&c->comm_done, cudaEventDisableTiming));
     c->wsh = static_cast<float*>(dev_alloc(c, static_cast<size_t>(L.shard_total) * 4));
     c->u = static_cast<float*>(dev_alloc(c, static_cast<size_t>(L.shard_total) * 4));
     c->d_barrier = static_cast<int*>(dev_alloc(c, 4));
@@ -460,6 +510,11 @@ void bo_destroy(bo_ctx* c) {
     cudaEventDestroy(mk.b);
   }
   for (cudaEvent_t e : c->event_pool) cudaEventDestroy(e);
+  if (c->comm_stream) cudaStreamSynchronize(c->comm_stream);
+  if (c->comm_ready) cudaEventDestroy(c->comm_ready);
+  if (c->comm_done) cudaEventDestroy(c->comm_done);
+  if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+  delete c->sync_tab;
   for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
   if (c->comm) ncclCommDestroy(c->comm);
   for (void* p : c->allocations) cudaFree(p);
@@ -511,17 +566,34 @@ bo_status bo_comm_init(bo_ctx* c, const uint8_t* id128) {
   ncclUniqueId id;
   std::memcpy(&id, id128, 128);
   BO_NCCL(ncclCommInitRank(&c->comm, c->world, id, c->rank));
-  // Layout agreement (trainer.cpp:169-183): all-gather the salted hash.
-  uint64_t* d = static_cast<uint64_t*>(dev_alloc(c, static_cast<size_t>(c->world + 1) * 8));
-  BO_CUDA(cudaMemcpyAsync(d, &c->L.hash, 8, cudaMemcpyHostToDevice, c->stream));
-  BO_NCCL(ncclAllGather(d, d + 1, 1, ncclUint64, c->comm, c->stream));
-  std::vector<uint64_t> all(static_cast<size_t>(c->world));
-  BO_CUDA(cudaMemcpyAsync(all.data(), d + 1, all.size() * 8, cudaMemcpyDeviceToHost, c->stream));
+  // Layout agreement (trainer.cpp:169-183): all-gather the salted hash, and
+  // a hash of the settings that shape the collective call sequence (reduce
+  // algorithm, ring transport, communication groups of the overlapped sync
+  // micro) so that ranks started with different BO_* environments fail here
+  // instead of deadlocking later.
+  uint64_t mine[2] = {c->L.hash, 1469598103934665603ull};
+  auto mix = [&](uint64_t v) {
+    for (int i = 0; i < 8; ++i) mine[1] = (mine[1] ^ ((v >> (8 * i)) & 0xFF)) * 1099511628211ull;
+  };
+  mix(static_cast<uint64_t>(c->algo));
+  mix(c->ring_via_nccl ? 1 : 0);
+  mix(c->comm_groups.size());
+  for (const auto& g : c->comm_groups) mix(static_cast<uint64_t>(g.b1));
+  uint64_t* d = static_cast<uint64_t*>(dev_alloc(c, static_cast<size_t>(2 * c->world + 2) * 8));
+  BO_CUDA(cudaMemcpyAsync(d, mine, 16, cudaMemcpyHostToDevice, c->stream));
+  BO_NCCL(ncclAllGather(d, d + 2, 2, ncclUint64, c->comm, c->stream));
+  std::vector<uint64_t> all(static_cast<size_t>(2 * c->world));
+  BO_CUDA(cudaMemcpyAsync(all.data(), d + 2, all.size() * 8, cudaMemcpyDeviceToHost, c->stream));
   BO_CUDA(cudaStreamSynchronize(c->stream));
-  for (uint64_t h : all) {
-    if (h != c->L.hash) {
+  for (int r = 0; r < c->world; ++r) {
+    if (all[static_cast<size_t>(2 * r)] != mine[0]) {
       fail(BO_ERR_BUCKET_LAYOUT_MISMATCH,
            "rank " + std::to_string(c->rank) + " bucket layout disagrees with peers");
+    }
+    if (all[static_cast<size_t>(2 * r + 1)] != mine[1]) {
+      fail(BO_ERR_PROTOCOL, "rank " + std::to_string(c->rank) +
+                                " collective settings (reduce algorithm, BO_RING_NCCL, "
+                                "BO_COMM_GROUP_ELEMS) disagree with peers");
     }
   }
   // Map every rank's flat parameter replica into this process (CUDA IPC over
@@ -777,6 +849,7 @@ bo_status bo_accumulate(bo_ctx* c, int32_t micro, const uint16_t* const* grads) 
     if (!grads[t]) fail(BO_ERR_SHAPE_MISMATCH, "null gradient for tensor " + std::to_string(t));
     aligned &= (reinterpret_cast<uintptr_t>(grads[t]) & 15u) == 0;
   }
+  if (c->sync_open) fail(BO_ERR_PROTOCOL, "an overlapped sync micro (bo_sync_ready) is in progress");
   if (micro + 1 < K) {
     launch_accumulate(c, micro, tab, aligned);
     return BO_OK;
@@ -792,6 +865,76 @@ bo_status bo_accumulate(bo_ctx* c, int32_t micro, const uint16_t* const* grads) 
     if (c->world == 1 || c->algo == BO_REDUCE_NCCL) launch_finalize(c, tab);
     run_reduce(c, tab);
     run_lamb(c, tab);  // world > 1: includes the fused parameter all-gather (IPC push)
+  }
+  c->calls += 1;
+  BO_GUARD_END
+}
+
+bo_status bo_sync_ready(bo_ctx* c, int32_t n, const int32_t* tensors, const uint16_t* const* grads) {
+  BO_GUARD_BEGIN
+  if (!c || (n > 0 && (!tensors || !grads))) fail(BO_ERR_INVALID_CONFIG, "null argument");
+  if (c->world > 1 && !c->comm) fail(BO_ERR_INVALID_CONFIG, "bo_comm_init has not run");
+  const Layout& L = c->L;
+  if (!c->sync_open) {
+    c->sync_open = true;
+    c->n_delivered = 0;
+    c->next_group = 0;
+    c->sync_aligned = true;
+    std::fill(c->delivered.begin(), c->delivered.end(), 0);
+    c->group_pending.clear();
+    for (const auto& g : c->comm_groups) c->group_pending.push_back(g.pending0);
+    c->path = BO_PATH_OVERLAP;
+    c->ring_last_in = nullptr;
+    c->ring_result = nullptr;
+  }
+  for (int i = 0; i < n; ++i) {
+    const int t = tensors[i];
+    if (t < 0 || t >= L.T) fail(BO_ERR_SHAPE_MISMATCH, "tensor index out of range");
+    if (!grads[i]) fail(BO_ERR_SHAPE_MISMATCH, "null gradient for tensor " + std::to_string(t));
+    if (c->delivered[static_cast<size_t>(t)]) {
+      fail(BO_ERR_PROTOCOL, "tensor " + std::to_string(t) + " delivered twice in one sync micro");
+    }
+    c->delivered[static_cast<size_t>(t)] = 1;
+    c->sync_tab->p[t] = grads[i];
+    c->sync_aligned &= (reinterpret_cast<uintptr_t>(grads[i]) & 15u) == 0;
+    c->n_delivered += 1;
+    if (c->world > 1) {
+      c->group_pending[static_cast<size_t>(c->group_of_bucket[static_cast<size_t>(L.bucket_of[static_cast<size_t>(t)])])] -= 1;
+    }
+  }
+  // reduce every group whose tensors are all final, in layout order (the
+  // reference's comm thread, trainer.cpp:301-327), on the communication
+  // stream after the caller's work so far (the gradients' producer)
+  if (c->world > 1) {
+    const int G = static_cast<int>(c->comm_groups.size());
+    if (c->next_group < G && c->group_pending[static_cast<size_t>(c->next_group)] == 0) {
+      BO_CUDA(cudaEventRecord(c->comm_ready, c->stream));
+      BO_CUDA(cudaStreamWaitEvent(c->comm_stream, c->comm_ready, 0));
+    }
+    while (c->next_group < G && c->group_pending[static_cast<size_t>(c->next_group)] == 0) {
+      const auto& g = c->comm_groups[static_cast<size_t>(c->next_group)];
+      run_reduce_group(c, *c->sync_tab, g.b0, g.b1, g.acc0, g.acc1, c->comm_stream);
+      c->next_group += 1;
+    }
+  }
+  if (c->n_delivered < L.T) return BO_OK;
+  // every gradient delivered: the rest of the step on the caller's stream
+  c->sync_open = false;
+  grow_bc_table(c, c->calls + 2);
+  if (c->world == 1) {
+    if (c->sync_aligned && !c->force_unfused) {
+      c->path |= BO_PATH_ONE_RANK_FUSED;
+      run_fused_single_rank(c, *c->sync_tab);
+    } else {
+      c->path |= BO_PATH_ONE_RANK_STAGED;
+      launch_finalize(c, *c->sync_tab);
+      run_reduce(c, *c->sync_tab);
+      run_lamb(c, *c->sync_tab);
+    }
+  } else {
+    BO_CUDA(cudaEventRecord(c->comm_done, c->comm_stream));
+    BO_CUDA(cudaStreamWaitEvent(c->stream, c->comm_done, 0));
+    run_lamb(c, *c->sync_tab);
   }
   c->calls += 1;
   BO_GUARD_END

@@ -166,6 +166,28 @@ struct bo_ctx {
   int* d_tensor_tile_begin = nullptr;   // [T+1] lamb-tile ranges per tensor
   bo::HopXTile* d_hopx_tiles = nullptr; // ring hops with fused finalize, grouped by chunk
   std::vector<int> hopx_begin;          // [N+1] tile range of chunk q
+  std::vector<std::vector<int>> hopx_bucket_begin;  // [N][B+1] first tile of chunk q, bucket b
+
+  // Overlapped sync micro (bo_sync_ready; trainer.cpp:247-348 with overlap):
+  // buckets reduced in layout order, in communication groups of whole buckets
+  // (deterministic, identical on every rank), on comm_stream as soon as every
+  // tensor of the group has been delivered.
+  struct CommGroup {
+    int b0, b1;      // bucket range
+    int pending0;    // tensors in the group
+    int acc0, acc1;  // NCCL wire: range in d_group_acc_tiles (finalize of the group's tensors)
+  };
+  std::vector<CommGroup> comm_groups;
+  std::vector<int> group_of_bucket;
+  bo::AccTile* d_group_acc_tiles = nullptr;
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t comm_ready = nullptr, comm_done = nullptr;
+  bool sync_open = false;
+  bo::PtrTable* sync_tab = nullptr;     // host copy of the delivered pointers
+  std::vector<uint8_t> delivered;
+  std::vector<int> group_pending;
+  int n_delivered = 0, next_group = 0;
+  bool sync_aligned = true;
 
   // single-rank fused LAMB (world == 1)
   bo::FusedTile* d_fused_tiles = nullptr;
@@ -230,6 +252,9 @@ void grow_bc_table(bo_ctx* c, int64_t need);
 void launch_accumulate(bo_ctx* c, int micro, const PtrTable& tab, bool vec_ok);
 void launch_finalize(bo_ctx* c, const PtrTable& tab);
 void run_reduce(bo_ctx* c, const PtrTable& tab);
+// one communication group of buckets [b0, b1) on `stream` (overlap mode)
+void run_reduce_group(bo_ctx* c, const PtrTable& tab, int b0, int b1, int acc0, int acc1,
+                      cudaStream_t stream);
 void run_lamb(bo_ctx* c, const PtrTable& tab);
 void gather_shard(bo_ctx* c);
 void run_fused_single_rank(bo_ctx* c, const PtrTable& tab);
@@ -239,7 +264,9 @@ struct StageTimer {
   bo_ctx* c;
   int stage;
   cudaEvent_t b = nullptr;
+  cudaStream_t stream;
   StageTimer(bo_ctx* ctx, int s);
+  StageTimer(bo_ctx* ctx, int s, cudaStream_t on);
   ~StageTimer();
 };
 }  // namespace bo

@@ -733,24 +733,27 @@ void launch_finalize(bo_ctx* c, const PtrTable& tab) {
 }
 
 // The reference ring's reduce-scatter phase (collective.hpp:65-80, binary16
-// wire collective.cpp:170-190) with flatten_param fused into every hop: the
-// local addend x of chunk q is computed from the sync micro's binary16 input
-// and the accumulator as the hop needs it. One grouped ncclSend/ncclRecv of
-// one contiguous message (all buckets' current chunks) per hop.
+// wire collective.cpp:170-190) over buckets [b0, b1), with flatten_param fused
+// into every hop: the local addend x of chunk q is computed from the sync
+// micro's binary16 input and the accumulator as the hop needs it.
 template <typename W>
-static void ring_reduce_scatter(bo_ctx* c, const PtrTable& tab, ncclDataType_t dt) {
+static void ring_reduce_scatter(bo_ctx* c, const PtrTable& tab, ncclDataType_t dt, int b0, int b1,
+                                cudaStream_t st) {
   const int N = c->world, r = c->rank;
   const int right = (r + 1) % N, left = (r - 1 + N) % N;
-  const size_t S = static_cast<size_t>(c->L.shard_total);
+  const Layout& L = c->L;
+  const int64_t sh0 = L.shoff[static_cast<size_t>(b0)];
+  const int64_t sh1 = b1 < L.B ? L.shoff[static_cast<size_t>(b1)] : L.shard_total;
   W* a = static_cast<W*>(c->wire[0]);
   W* b = static_cast<W*>(c->wire[1]);
   const int K = c->cfg.accumulation;
   auto hop = [&](int q, const W* in, W* out, int combine) {
-    const int t0 = c->hopx_begin[static_cast<size_t>(q)], t1 = c->hopx_begin[static_cast<size_t>(q) + 1];
+    const std::vector<int>& qb = c->hopx_bucket_begin[static_cast<size_t>(q)];
+    const int t0 = qb[static_cast<size_t>(b0)], t1 = qb[static_cast<size_t>(b1)];
     if (t1 > t0) {
-      StageTimer timer(c, BO_STAGE_FLAG);
-      k_hopx<W><<<t1 - t0, kThreads, 0, c->stream>>>(c->d_hopx_tiles + t0, c->d_tensors, tab, c->acc,
-                                                      c->state, K, in, out, combine);
+      StageTimer timer(c, BO_STAGE_FLAG, st);
+      k_hopx<W><<<t1 - t0, kThreads, 0, st>>>(c->d_hopx_tiles + t0, c->d_tensors, tab, c->acc, c->state, K,
+                                               in, out, combine);
       check_launch(c, "k_hopx");
     }
   };
@@ -759,10 +762,11 @@ static void ring_reduce_scatter(bo_ctx* c, const PtrTable& tab, ncclDataType_t d
   // directly: one staged write + read of the chunk less, but the NVLink
   // latency is exposed inside an HBM-bound kernel. Measured on BERT-large
   // (profiles/r01_notes.md): a net win at world 2 (1.10 vs 1.18 ms), a loss
-  // at world 4 (0.67 vs 0.62 ms), so the default fuses only at world 2.
-  const bool fuse_last = !c->force_unfused && (c->fuse_last_hop >= 0 ? c->fuse_last_hop != 0 : N == 2);
-  c->ring_last_in = nullptr;
-  c->ring_result = nullptr;
+  // at world 4 (0.67 vs 0.62 ms), so the default fuses only at world 2 —
+  // and never in the overlapped sync micro, where a staged last hop runs
+  // under the caller's backward instead of inside the exposed LAMB.
+  const bool fuse_last = !c->force_unfused &&
+                         (c->fuse_last_hop >= 0 ? c->fuse_last_hop != 0 : (N == 2 && !c->sync_open));
   hop(r, nullptr, a, 0);  // hop 0 payload: this rank's own chunk r (collective.cpp:178)
   const bool p2p = c->peer_wire[0][left] && !c->ring_via_nccl;
   c->path |= p2p ? BO_PATH_RING_P2P : BO_PATH_RING_SENDRECV;
@@ -770,9 +774,10 @@ static void ring_reduce_scatter(bo_ctx* c, const PtrTable& tab, ncclDataType_t d
     // Peer-to-peer hops: hop s reads the left neighbour's hop s-1 output in
     // place over NVLink (CUDA IPC mapping) and writes the other local buffer.
     // A 4-byte all-reduce before each hop is the barrier that orders a
-    // buffer's writer before its reader and its reader before its next writer.
+    // buffer's writer before its reader and its reader before its next writer
+    // (buckets of different groups occupy disjoint positions).
     for (int s = 0; s < N - 1; ++s) {
-      BO_NCCL(ncclAllReduce(c->d_barrier, c->d_barrier, 1, ncclInt32, ncclSum, c->comm, c->stream));
+      BO_NCCL(ncclAllReduce(c->d_barrier, c->d_barrier, 1, ncclInt32, ncclSum, c->comm, st));
       const W* in = static_cast<const W*>(c->peer_wire[s % 2][left]);
       if (s == N - 2 && fuse_last) {
         c->ring_last_in = in;  // the last hop runs inside LAMB phase 1
@@ -786,8 +791,8 @@ static void ring_reduce_scatter(bo_ctx* c, const PtrTable& tab, ncclDataType_t d
   } else {
     for (int s = 0; s < N - 1; ++s) {
       BO_NCCL(ncclGroupStart());
-      BO_NCCL(ncclSend(a, S, dt, right, c->comm, c->stream));
-      BO_NCCL(ncclRecv(b, S, dt, left, c->comm, c->stream));
+      BO_NCCL(ncclSend(a + sh0, static_cast<size_t>(sh1 - sh0), dt, right, c->comm, st));
+      BO_NCCL(ncclRecv(b + sh0, static_cast<size_t>(sh1 - sh0), dt, left, c->comm, st));
       BO_NCCL(ncclGroupEnd());
       if (s == N - 2 && fuse_last) {
         c->ring_last_in = b;
@@ -804,22 +809,46 @@ static void ring_reduce_scatter(bo_ctx* c, const PtrTable& tab, ncclDataType_t d
   // reads it in place.
 }
 
+static void nccl_reduce_scatter(bo_ctx* c, int b0, int b1, cudaStream_t st) {
+  c->path |= BO_PATH_NCCL_RS;
+  BO_NCCL(ncclGroupStart());
+  for (int b = b0; b < b1; ++b) {
+    BO_NCCL(ncclReduceScatter(c->x + c->L.base[static_cast<size_t>(b)], c->gshard + c->L.shoff[static_cast<size_t>(b)],
+                              static_cast<size_t>(c->L.chunk[static_cast<size_t>(b)]), ncclFloat, ncclSum,
+                              c->comm, st));
+  }
+  BO_NCCL(ncclGroupEnd());
+}
+
 void run_reduce(bo_ctx* c, const PtrTable& tab) {
   if (c->world == 1) return;
   StageTimer timer(c, BO_STAGE_REDUCE);
+  c->ring_last_in = nullptr;
+  c->ring_result = nullptr;
   if (c->algo == BO_REDUCE_NCCL) {
-    c->path |= BO_PATH_NCCL_RS;
-    BO_NCCL(ncclGroupStart());
-    for (int b = 0; b < c->L.B; ++b) {
-      BO_NCCL(ncclReduceScatter(c->x + c->L.base[b], c->gshard + c->L.shoff[b],
-                                static_cast<size_t>(c->L.chunk[b]), ncclFloat, ncclSum, c->comm,
-                                c->stream));
-    }
-    BO_NCCL(ncclGroupEnd());
+    nccl_reduce_scatter(c, 0, c->L.B, c->stream);
   } else if (c->cfg.f16_exchange) {
-    ring_reduce_scatter<uint16_t>(c, tab, ncclFloat16);
+    ring_reduce_scatter<uint16_t>(c, tab, ncclFloat16, 0, c->L.B, c->stream);
   } else {
-    ring_reduce_scatter<float>(c, tab, ncclFloat32);
+    ring_reduce_scatter<float>(c, tab, ncclFloat32, 0, c->L.B, c->stream);
+  }
+}
+
+void run_reduce_group(bo_ctx* c, const PtrTable& tab, int b0, int b1, int acc0, int acc1,
+                      cudaStream_t stream) {
+  StageTimer timer(c, BO_STAGE_REDUCE, stream);
+  if (c->algo == BO_REDUCE_NCCL) {
+    if (acc1 > acc0) {
+      StageTimer t2(c, BO_STAGE_FINALIZE, stream);
+      k_finalize<<<acc1 - acc0, kThreads, 0, stream>>>(c->d_group_acc_tiles + acc0, c->d_tensors, tab, c->acc,
+                                                        c->x, c->state, c->cfg.accumulation);
+      check_launch(c, "k_finalize");
+    }
+    nccl_reduce_scatter(c, b0, b1, stream);
+  } else if (c->cfg.f16_exchange) {
+    ring_reduce_scatter<uint16_t>(c, tab, ncclFloat16, b0, b1, stream);
+  } else {
+    ring_reduce_scatter<float>(c, tab, ncclFloat32, b0, b1, stream);
   }
 }
 

@@ -231,7 +231,7 @@ class GradPipeline:
 
     # -- introspection
     PATH_NAMES = {1: "one_rank_fused", 2: "one_rank_staged", 4: "ring_p2p", 8: "ring_sendrecv",
-                  16: "last_hop_fused", 32: "nccl_reduce_scatter"}
+                  16: "last_hop_fused", 32: "nccl_reduce_scatter", 64: "overlap"}
 
     def path(self) -> list[str]:
         """Implementation the last sync micro ran (BO_PATH_* names)."""
@@ -303,6 +303,22 @@ class GradPipeline:
     @staticmethod
     def make_ptr_array(ptrs) -> C.Array:
         return _ptr_array(ptrs)
+
+    def sync_ready(self, tensors, grads) -> None:
+        """Overlapped sync micro (TrainerConfig.overlap): deliver the sync
+        micro's gradients of `tensors` (indices) as they become final; buckets
+        are reduced in layout order as soon as their communication group is
+        complete; the call delivering the last tensor finishes the step."""
+        tensors = [int(t) for t in tensors]
+        if len(tensors) != len(grads):
+            raise ShapeMismatch("ShapeMismatch: tensors and grads differ in length")
+        ptrs = [g if isinstance(g, int) else g.data_ptr() for g in grads]
+        ids = (C.c_int32 * max(1, len(tensors)))(*tensors)
+        _lib.check(self.lib.bo_sync_ready(self.ctx, len(tensors), ids, _ptr_array(ptrs)))
+
+    def ready_order(self) -> list[int]:
+        """Tensor indices in gradient-ready order (BucketLayout::ready_order)."""
+        return [int(t) for t in self.layout()[2]]
 
     def train_step(self, micro_grads) -> None:
         """All K micro-batches of one optimizer step (the train_step analog)."""

@@ -61,9 +61,13 @@ class GradBuffers:
 
 
 def run_pipeline(spec, cfg, params0, steps, grad_seed=1, spike_ppm=0, spike_exp=1, injections=(),
-                 rank=0, world=1, aligned=True, pipe=None, device=0, first_step=0):
+                 rank=0, world=1, aligned=True, pipe=None, device=0, first_step=0, overlap=None):
     """Run optimizer steps first_step .. first_step+steps-1 (the step index
-    seeds the synthetic gradients); returns (pipe, scale_used, found_inf)."""
+    seeds the synthetic gradients); returns (pipe, scale_used, found_inf).
+
+    overlap: None (the sync micro through bo_accumulate) or a list of chunk
+    sizes: the sync micro is then delivered through bo_sync_ready in the
+    layout's ready order, in chunks of these sizes (cycled)."""
     if pipe is None:
         pipe = GradPipeline(spec, cfg, device=device, rank=rank, world=world)
         pipe.load_params(np.asarray(params0, np.float32))
@@ -80,7 +84,17 @@ def run_pipeline(spec, cfg, params0, steps, grad_seed=1, spike_ppm=0, spike_exp=
                 if st == step and r == rank and mk == k:
                     gb.inject(k, idx, bits)
             torch.cuda.synchronize()
-            pipe.accumulate(k, gb.ptrs[k])
+            if overlap is None or k < K - 1:
+                pipe.accumulate(k, gb.ptrs[k])
+            else:
+                order = pipe.ready_order()
+                i = j = 0
+                while i < len(order):
+                    n = max(1, overlap[j % len(overlap)])
+                    ids = order[i:i + n]
+                    pipe.sync_ready(ids, [gb.ptrs[k][t] for t in ids])
+                    i += n
+                    j += 1
         pipe.synchronize()
         found.append(int(pipe.status().found_inf))
     return pipe, np.array(scale_used, np.float32), np.array(found, np.int32)

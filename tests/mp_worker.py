@@ -32,7 +32,8 @@ CASES = {
 }
 # "<case>_unfused" / "<case>_fused": the same case with the ring's last hop
 # staged (BO_UNFUSED=1) or fused into LAMB phase 1 (BO_FUSE_LAST=1) whatever
-# the world's default
+# the world's default; "<case>_overlap": the sync micro delivered through
+# bo_sync_ready (bucket-level overlap)
 
 
 def main():
@@ -52,6 +53,13 @@ def main():
     from tests.harness import max_rel_or_abs, run_pipeline
 
     case = args.case
+    overlap = None
+    if case.endswith("_overlap"):
+        # the sync micro delivered through bo_sync_ready in ragged chunks,
+        # with communication groups of ~20k elements (several per step)
+        os.environ["BO_COMM_GROUP_ELEMS"] = "20000"
+        overlap = [1, 5, 2, 17]
+        case = case[: -len("_overlap")]
     if case.endswith("_unfused"):
         os.environ["BO_UNFUSED"] = "1"
         case = case[: -len("_unfused")]
@@ -75,7 +83,7 @@ def main():
     pipe.comm_init_torch()
     pipe, su, fi = run_pipeline(spec, cfg, None, args.steps, grad_seed=9, spike_ppm=ppm,
                                 spike_exp=sexp, injections=inj, rank=rank, world=world, pipe=pipe,
-                                device=local)
+                                device=local, overlap=overlap)
     w = pipe.read_params()
     m = np.zeros(P, np.float32)
     v = np.zeros(P, np.float32)

@@ -31,7 +31,12 @@ def run_case(case, nproc, model="tiny", steps=4):
            "--master-addr", "127.0.0.1", f"--master-port={_port()}",
            os.path.join(ROOT, "tests", "mp_worker.py"), "--case", case, "--steps", str(steps),
            "--model", model]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    for _attempt in range(3):
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+        if "EADDRINUSE" not in r.stderr:
+            break
+        # the rendezvous port was taken between probing and binding: new port
+        cmd[cmd.index(next(a for a in cmd if a.startswith("--master-port=")))] = f"--master-port={_port()}"
     lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
     assert lines, r.stdout[-3000:] + r.stderr[-3000:]
     res = json.loads(lines[-1])
@@ -40,7 +45,8 @@ def run_case(case, nproc, model="tiny", steps=4):
 
 
 @pytest.mark.parametrize("case", ["ring16", "ring32", "nccl32", "ring16_1bucket",
-                                  "ring16_tinybuckets", "ring16_unfused", "ring32_unfused"])
+                                  "ring16_tinybuckets", "ring16_unfused", "ring32_unfused",
+                                  "ring16_overlap", "ring32_unfused_overlap", "nccl32_overlap"])
 def test_two_gpus(case):
     if _ngpu() < 2:
         pytest.skip("needs 2 GPUs")
@@ -49,9 +55,11 @@ def test_two_gpus(case):
         assert res["m_bit_exact"] and res["v_bit_exact"]
         assert "ring_p2p" in res["path"]
         # world 2 runs the last hop inside LAMB phase 1 unless BO_UNFUSED is set
-        assert ("last_hop_fused" in res["path"]) == (not case.endswith("_unfused"))
+        # (and never in the overlapped sync micro)
+        assert ("last_hop_fused" in res["path"]) == ("_unfused" not in case and "_overlap" not in case)
     else:
-        assert res["path"] == ["nccl_reduce_scatter"]
+        assert "nccl_reduce_scatter" in res["path"]
+    assert ("overlap" in res["path"]) == case.endswith("_overlap")
 
 
 @pytest.mark.parametrize("model", ["ragged", "small"])

@@ -191,3 +191,53 @@ def test_checkpoint_resume_is_bit_identical(torch_cuda, oracle):
     other = GradPipeline(spec, TrainerConfig(LambConfig(), 2, 1 << 20))
     with pytest.raises(BucketLayoutMismatch):
         other.import_state(blob)
+
+
+@pytest.mark.parametrize("aligned", [True, False])
+def test_overlapped_sync_micro_bit_identical(torch_cuda, oracle, aligned):
+    """bo_sync_ready (bucket-level overlap, trainer.cpp:247-348) gives the same
+    bits as bo_accumulate for the sync micro, overflow steps included."""
+    from paper_2008_00177_b200.model_spec import BERT_TINY, bert_spec
+    from paper_2008_00177_b200.pipeline import LambConfig, ScalerConfig, TrainerConfig
+    from tests.harness import run_pipeline
+
+    spec = bert_spec(BERT_TINY)
+    P = spec.param_count()
+    p0 = oracle.build_params(spec, 5)
+    cfg = TrainerConfig(LambConfig(lr=1e-2), 3, 4096, False, 0,
+                        ScalerConfig(init_scale=2.0 ** 14, growth_interval=3))
+    inj = [(2, 0, 2, P // 2, 0x7C00)]
+    base, su0, fi0 = run_pipeline(spec, cfg, p0, steps=6, spike_ppm=3, spike_exp=3, injections=inj,
+                                  aligned=aligned)
+    ovl, su1, fi1 = run_pipeline(spec, cfg, p0, steps=6, spike_ppm=3, spike_exp=3, injections=inj,
+                                 aligned=aligned, overlap=[1, 7, 3, 40])
+    assert "overlap" in ovl.path()
+    assert np.array_equal(su0, su1) and np.array_equal(fi0, fi1) and fi0.any()
+    assert np.array_equal(base.read_params().view(np.uint32), ovl.read_params().view(np.uint32))
+    m0, v0, m1, v1 = (np.zeros(P, np.float32) for _ in range(4))
+    base.read_moments(m0, v0)
+    ovl.read_moments(m1, v1)
+    assert np.array_equal(m0.view(np.uint32), m1.view(np.uint32))
+    assert np.array_equal(v0.view(np.uint32), v1.view(np.uint32))
+
+
+def test_sync_ready_protocol_errors(torch_cuda, oracle):
+    from paper_2008_00177_b200.errors import BertoptError
+    from paper_2008_00177_b200.model_spec import BERT_TINY, bert_spec
+    from paper_2008_00177_b200.pipeline import GradPipeline, LambConfig, ScalerConfig, TrainerConfig
+    from tests.harness import GradBuffers
+
+    spec = bert_spec(BERT_TINY)
+    cfg = TrainerConfig(LambConfig(), 1, 4096, False, 0, ScalerConfig())
+    pipe = GradPipeline(spec, cfg, device=0)
+    pipe.load_params(oracle.build_params(spec, 1))
+    gb = GradBuffers(spec, 1, 0, True)
+    pipe.sync_ready([0], [gb.ptrs[0][0]])
+    with pytest.raises(BertoptError):
+        pipe.sync_ready([0], [gb.ptrs[0][0]])  # delivered twice
+    with pytest.raises(BertoptError):
+        pipe.accumulate(0, gb.ptrs[0])  # bo_accumulate while a sync micro is open
+    rest = [t for t in range(spec.n_tensors) if t != 0]
+    pipe.sync_ready(rest, [gb.ptrs[0][t] for t in rest])
+    pipe.synchronize()
+    assert pipe.status().lamb_step == 1
