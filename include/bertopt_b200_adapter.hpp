@@ -186,6 +186,12 @@ class GradPipeline {
   void accumulate(int micro, const std::vector<const uint16_t*>& device_grads) {
     check(bo_accumulate(ctx_, micro, device_grads.data()));
   }
+  // TrainerConfig::overlap: the sync micro's gradients as they become final
+  // (call from Tape::backward's progress hook, in ready order).
+  void sync_ready(const std::vector<int32_t>& params, const std::vector<const uint16_t*>& device_grads) {
+    if (params.size() != device_grads.size()) throw ShapeMismatch("sync_ready: sizes differ");
+    check(bo_sync_ready(ctx_, static_cast<int32_t>(params.size()), params.data(), device_grads.data()));
+  }
   void read_params(Model& model) {
     std::vector<float> flat(static_cast<size_t>(model.param_count()));
     check(bo_read_params(ctx_, flat.data(), 1));
