@@ -211,7 +211,7 @@ static cudaEvent_t take_event(bo_ctx* c) {
 StageTimer::StageTimer(bo_ctx* ctx, int s) : StageTimer(ctx, s, ctx->stream) {}
 
 StageTimer::StageTimer(bo_ctx* ctx, int s, cudaStream_t on) : c(ctx), stage(s), stream(on) {
-  if (!c->profiling) return;
+  if (!c->profiling || !((c->profile_mask >> s) & 1)) return;
   b = take_event(c);
   BO_CUDA(cudaEventRecord(b, stream));
 }
@@ -814,6 +814,10 @@ bo_status bo_profile_enable(bo_ctx* c, int32_t enable) {
   BO_GUARD_BEGIN
   if (!c) fail(BO_ERR_INVALID_CONFIG, "null ctx");
   c->profiling = enable != 0;
+  // BO_PROFILE_STAGES: bit mask of the stages to bracket (default all); timing
+  // one stage alone shows what the events between all stages cost
+  c->profile_mask = ~0u;
+  if (const char* e = std::getenv("BO_PROFILE_STAGES")) c->profile_mask = static_cast<unsigned>(std::strtoul(e, nullptr, 0));
   BO_GUARD_END
 }
 

@@ -234,6 +234,7 @@ struct bo_ctx {
   std::vector<void*> allocations;
   // measurement
   bool profiling = false;
+  unsigned profile_mask = ~0u;
   int64_t launches = 0;
   struct Mark { int stage; cudaEvent_t a, b; };
   std::vector<Mark> marks;

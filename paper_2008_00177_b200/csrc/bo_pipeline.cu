@@ -29,8 +29,11 @@ __global__ void __launch_bounds__(kThreads) k_accumulate(const AccTile* __restri
                                                          const TensorDev* __restrict__ td,
                                                          const __grid_constant__ PtrTable tab,
                                                          float* __restrict__ acc, int first,
-                                                         DevState* __restrict__ st) {
-  const AccTile tile = tiles[blockIdx.x];
+                                                         DevState* __restrict__ st, int reverse) {
+  // reverse: the last micro before the sync micro walks the tiles backwards,
+  // so the accumulator lines still in L2 when it ends are the ones the sync
+  // micro's first CTAs read (and then drop from L2, see k_lamb_p1)
+  const AccTile tile = tiles[reverse ? gridDim.x - 1 - blockIdx.x : blockIdx.x];
   const uint16_t* __restrict__ src = tab.p[tile.t] + tile.e0;
   float* __restrict__ dst = acc + td[tile.t].acc_off + tile.e0;
   const int len = tile.len;
@@ -715,12 +718,15 @@ void check_launch(bo_ctx* c, const char* what) {
 
 void launch_accumulate(bo_ctx* c, int micro, const PtrTable& tab, bool vec_ok) {
   StageTimer timer(c, BO_STAGE_ACCUMULATE);
+  const int reverse = micro == c->cfg.accumulation - 2;
   if (vec_ok) {
     k_accumulate<true><<<c->n_acc_tiles, kThreads, 0, c->stream>>>(c->d_acc_tiles, c->d_tensors,
-                                                                    tab, c->acc, micro == 0, c->state);
+                                                                    tab, c->acc, micro == 0, c->state,
+                                                                    reverse);
   } else {
     k_accumulate<false><<<c->n_acc_tiles, kThreads, 0, c->stream>>>(c->d_acc_tiles, c->d_tensors,
-                                                                     tab, c->acc, micro == 0, c->state);
+                                                                     tab, c->acc, micro == 0, c->state,
+                                                                     reverse);
   }
   check_launch(c, "k_accumulate");
 }

@@ -157,6 +157,28 @@ int main(int argc, char** argv) {
     time("k_p1w<x> U1 B4 (one rank)", 30 * S, 0, [&] {
       k_p1w<float, false, true, 1, 4><<<wgrid, kWarpTileCTA>>>(c->d_lamb_tiles, c->n_lamb_tiles, tab, nullptr, A);
     });
+    {  // p1 right after the last accumulate micro (the pipeline's order)
+      cudaEvent_t x0, x1, y0;
+      cudaEventCreate(&x0); cudaEventCreate(&x1); cudaEventCreate(&y0);
+      float tot = 0.0f, tacc = 0.0f;
+      for (int i = 0; i < reps; ++i) {
+        cudaEventRecord(y0);
+        k_accumulate<true><<<c->n_acc_tiles, kThreads>>>(c->d_acc_tiles, c->d_tensors, tab, c->acc, 0, c->state, 1);
+        cudaEventRecord(x0);
+        k_lamb_p1<<<c->n_fused_tiles, kP1Threads>>>(c->d_fused_tiles, tab, c->acc, c->w, c->m, c->v, c->m_alt,
+                                                     c->v_alt, c->u, c->state, c->lamb, c->bc_table, 4,
+                                                     c->tile_part);
+        cudaEventRecord(x1);
+        cudaEventSynchronize(x1);
+        float a, b;
+        cudaEventElapsedTime(&a, y0, x0);
+        cudaEventElapsedTime(&b, x0, x1);
+        tacc += a;
+        tot += b;
+      }
+      printf("%-34s %8.3f ms  (accumulate before it %.3f ms)\n", "k_lamb_p1 after k_accumulate", tot / reps,
+             tacc / reps);
+    }
     time("k_lamb_p2 (one rank)", 12 * S, 0, [&] {
       k_lamb_p2<<<c->n_fused_tiles, kP2Threads>>>(c->d_fused_tiles, c->n_fused_tiles, c->w, c->u, c->state,
                                                   c->lamb, c->trust);
