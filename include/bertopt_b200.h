@@ -245,6 +245,19 @@ bo_status bo_unscale_gradients(float* grads, size_t n, float scale, int32_t enab
                                void* stream);
 bo_status bo_narrow_f16(const float* src, uint16_t* dst, size_t n, void* stream);
 bo_status bo_widen_f16(const uint16_t* src, float* dst, size_t n, void* stream);
+/* SURVEY §8(f) rank 4, the paper's fused elementwise optimizer: the
+ * Adam-form FusedKernel fused_optimizer_step(lr, beta1, beta2, eps,
+ * weight_decay, step) (graph.cpp:458-487) as run_fused_kernel executes it on
+ * (w, g, m, v) -> (w', m', v') in fp32 (apply_block, graph.cpp:296-347: every
+ * attribute a double rounded to float, one rounding per instruction), applied
+ * in place over n_tensors device tensors. */
+bo_status bo_fused_optimizer_step(int32_t n_tensors, const int64_t* numels, float* const* params,
+                                  const float* const* grads, float* const* m, float* const* v,
+                                  float lr, float beta1, float beta2, float eps,
+                                  float weight_decay, int32_t step, void* stream);
+/* The AMP cast (Tape::cast to f16, ops.cpp:655-668 -> quantize_inplace):
+ * x = binary16_RNE(x) in place (f16_round, half.cpp:59-62). */
+bo_status bo_f16_round(float* x, size_t n, void* stream);
 float bo_scale_loss(float loss, float scale, int32_t enabled);
 
 /* ---- device memory for hosts without the CUDA toolkit (cgo / JNI / C++) -- */

@@ -266,6 +266,54 @@ uint64_t or_layout_hash(int T, const char* const* names, const int* ndims, const
   return h;
 }
 
+// fused_optimizer_step (graph.cpp:458-487) as run_fused_kernel executes it:
+// apply_block (graph.cpp:296-347) rounds every attribute to float
+// (`const float c = static_cast<float>(attr)`) and each of the 17 body
+// instructions to fp32, in body order. In place on n elements of (w, g, m, v).
+// Parity: graph.cpp needs Eigen (absent), so this restatement is pinned by the
+// reference's own tests (test_graph.cpp:395-452, restated in
+// tests/test_fused_optimizer.py), not by the compiled reference.
+void or_fused_optimizer_step(int64_t n, float* w, const float* g, float* m, float* v, float lr,
+                             float beta1, float beta2, float eps, float weight_decay, int step) {
+  const double bc1 = 1.0 / (1.0 - std::pow(static_cast<double>(beta1), step));
+  const double bc2 = 1.0 / (1.0 - std::pow(static_cast<double>(beta2), step));
+  const float c_b1 = static_cast<float>(static_cast<double>(beta1));
+  const float c_omb1 = static_cast<float>(1.0 - static_cast<double>(beta1));
+  const float c_b2 = static_cast<float>(static_cast<double>(beta2));
+  const float c_omb2 = static_cast<float>(1.0 - static_cast<double>(beta2));
+  const float c_bc1 = static_cast<float>(bc1), c_bc2 = static_cast<float>(bc2);
+  const float c_eps = static_cast<float>(static_cast<double>(eps));
+  const float c_wd = static_cast<float>(static_cast<double>(weight_decay));
+  const float c_nlr = static_cast<float>(-static_cast<double>(lr));
+  for (int64_t i = 0; i < n; ++i) {
+    const float r4 = c_b1 * m[i];           // kScalarMul m, beta1
+    const float r5 = c_omb1 * g[i];         // kScalarMul g, 1 - beta1
+    const float r6 = r4 + r5;               // m'
+    const float r7 = g[i] * g[i];           // kMul g, g
+    const float r8 = c_b2 * v[i];
+    const float r9 = c_omb2 * r7;
+    const float r10 = r8 + r9;              // v'
+    const float r11 = c_bc1 * r6;
+    const float r12 = c_bc2 * r10;
+    const float r13 = std::sqrt(r12);
+    const float r14 = r13 + c_eps;
+    const float r15 = 1.0f / r14;
+    const float r16 = r11 * r15;
+    const float r17 = c_wd * w[i];
+    const float r18 = r16 + r17;            // u
+    const float r19 = c_nlr * r18;
+    const float r20 = w[i] + r19;           // w'
+    w[i] = r20;
+    m[i] = r6;
+    v[i] = r10;
+  }
+}
+
+// quantize_inplace of a binary16 tensor: f16_round = widen(narrow(x)) RNE.
+void or_f16_round(float* x, size_t n) {
+  for (size_t i = 0; i < n; ++i) x[i] = f16_to_f32(f32_to_f16(x[i]));
+}
+
 int or_lamb_step(int T, const int64_t* numel, float* w, const float* g, float* m, float* v,
                  int64_t* step, const float* lamb6) {
   return lamb_step(T, numel, w, g, m, v, step, lamb_from(lamb6));

@@ -122,6 +122,9 @@ class Oracle:
                                      C.c_int, _i32p, _i64p]
         L.or_layout_hash.restype = C.c_uint64
         L.or_lamb_step.argtypes = [C.c_int, _i64p, _f32p, _f32p, _f32p, _f32p, _i64p, _f32p]
+        L.or_fused_optimizer_step.argtypes = [C.c_int64, _f32p, _f32p, _f32p, _f32p, C.c_float,
+                                              C.c_float, C.c_float, C.c_float, C.c_float, C.c_int]
+        L.or_f16_round.argtypes = [_f32p, C.c_size_t]
         L.or_ring_allreduce.argtypes = [C.c_int, C.c_size_t, C.c_void_p, C.c_int]
         L.or_build_params.argtypes = [C.c_int, _i64p, _i32p, C.c_uint64, _f32p]
         L.or_synth_grads.argtypes = [C.c_int64, C.c_uint64, C.c_int, C.c_int, C.c_int, C.c_float,
@@ -191,6 +194,15 @@ class Oracle:
         d = np.ascontiguousarray(data).copy()
         self.lib.or_ring_allreduce(d.shape[0], d.shape[1], d.ctypes.data, kind)
         return d
+
+    def fused_optimizer_step(self, w, g, m, v, lr, beta1, beta2, eps, weight_decay, step):
+        """fused_optimizer_step (graph.cpp:458-487) in place on float32 arrays."""
+        self.lib.or_fused_optimizer_step(w.size, _ptr(w, _f32p), _ptr(g, _f32p), _ptr(m, _f32p),
+                                         _ptr(v, _f32p), lr, beta1, beta2, eps, weight_decay, step)
+
+    def f16_round(self, x):
+        """quantize_inplace of a binary16 tensor, in place on a float32 array."""
+        self.lib.or_f16_round(_ptr(x, _f32p), x.size)
 
     def build_params(self, spec, seed: int) -> np.ndarray:
         nm = np.asarray(spec.numels(), np.int64)

@@ -87,6 +87,10 @@ SIGNATURES = {
     "bo_unscale_gradients": (_i32, [_vp, _sz, C.c_float, _i32, _vp]),
     "bo_narrow_f16": (_i32, [_vp, _vp, _sz, _vp]),
     "bo_widen_f16": (_i32, [_vp, _vp, _sz, _vp]),
+    "bo_fused_optimizer_step": (_i32, [_i32, C.POINTER(_i64), C.POINTER(_vp), C.POINTER(_vp),
+                                       C.POINTER(_vp), C.POINTER(_vp), C.c_float, C.c_float,
+                                       C.c_float, C.c_float, C.c_float, _i32, _vp]),
+    "bo_f16_round": (_i32, [_vp, _sz, _vp]),
     "bo_scale_loss": (C.c_float, [C.c_float, C.c_float, _i32]),
     "bo_malloc": (_i32, [C.POINTER(_vp), _sz, _i32]),
     "bo_free": (_i32, [_vp]),

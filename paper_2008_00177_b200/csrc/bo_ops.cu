@@ -7,8 +7,13 @@
 //   bo_ring_allreduce_f16_wire ring_allreduce_f16_wire collective.cpp:163-212
 //   bo_unscale_gradients       unscale_gradients      half.cpp:105-115
 //   bo_narrow_f16/bo_widen_f16 narrow/widen_f16_block graph.cpp:176-199
+//   bo_fused_optimizer_step    fused_optimizer_step   graph.cpp:458-487 run by
+//                              run_fused_kernel (apply_block, graph.cpp:296-347)
+//   bo_f16_round               quantize_inplace of a binary16 tensor (Tape::cast,
+//                              ops.cpp:655-668; f16_round, half.cpp:59-62)
 #include <cmath>
 #include <cstring>
+#include <memory>
 
 #include "bo_device.cuh"
 #include "bo_internal.hpp"
@@ -147,6 +152,95 @@ __global__ void k_ring_add(const W* in, float* mine, size_t n) {
     float w;
     if constexpr (sizeof(W) == 2) w = widen(in[i]); else w = in[i];
     mine[i] = __fadd_rn(w, mine[i]);
+  }
+}
+
+// fused_optimizer_step's constants exactly as apply_block sees them: every
+// attribute is a double cast to float at use (graph.cpp:297).
+struct AdamConsts {
+  float b1, omb1, b2, omb2, bc1, bc2, eps, wd, nlr;
+};
+
+struct AdamTensor {
+  float* w;
+  const float* g;
+  float* m;
+  float* v;
+  int64_t n;
+  int32_t vec;  // all four arrays 16-byte aligned
+};
+
+// The 17 instructions of the fused kernel body in order, each rounded to
+// fp32 (no contraction): m' = b1 m + (1-b1) g; v' = b2 v + (1-b2) g g;
+// u = (bc1 m') * (1 / (sqrt(bc2 v') + eps)) + wd w; w' = w + (-lr) u.
+__device__ __forceinline__ void adam_elem(const AdamConsts& k, float w, float g, float m, float v,
+                                          float& wo, float& mo, float& vo) {
+  mo = __fadd_rn(__fmul_rn(k.b1, m), __fmul_rn(k.omb1, g));
+  vo = __fadd_rn(__fmul_rn(k.b2, v), __fmul_rn(k.omb2, __fmul_rn(g, g)));
+  const float re = __fdiv_rn(1.0f, __fadd_rn(__fsqrt_rn(__fmul_rn(k.bc2, vo)), k.eps));
+  const float u = __fadd_rn(__fmul_rn(__fmul_rn(k.bc1, mo), re), __fmul_rn(k.wd, w));
+  wo = __fadd_rn(w, __fmul_rn(k.nlr, u));
+}
+
+// The tensor table travels as a kernel parameter (CUDA 12.1+: up to 32 KB),
+// so calls need no device scratch and no synchronisation; larger lists are
+// processed in batches of kAdamBatch tensors.
+constexpr int kAdamBatch = 512;
+struct AdamTable {
+  AdamTensor t[kAdamBatch];
+  int64_t cstart[kAdamBatch + 1];  // first chunk of each tensor; cstart[T] = total
+  int T;
+};
+static_assert(sizeof(AdamTable) + sizeof(AdamConsts) < 32000, "kernel parameter limit");
+
+// One CTA per 4096-element chunk of one tensor, grid-stride over the chunks
+// of all tensors; chunk c belongs to the tensor t with cstart[t] <= c <
+// cstart[t + 1] (binary search).
+__global__ void __launch_bounds__(kThreads) k_fused_adam(const __grid_constant__ AdamTable tab,
+                                                         AdamConsts k) {
+  const int T = tab.T;
+  const int64_t total = tab.cstart[T];
+  for (int64_t c = blockIdx.x; c < total; c += gridDim.x) {
+    int lo = 0, hi = T - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (tab.cstart[mid] <= c) lo = mid; else hi = mid - 1;
+    }
+    const AdamTensor Tn = tab.t[lo];
+    const int64_t e0 = (c - tab.cstart[lo]) * kTileElems;
+    const int64_t rem = Tn.n - e0;
+    const int len = static_cast<int>(rem < kTileElems ? rem : kTileElems);
+    float* __restrict__ w = Tn.w + e0;
+    const float* __restrict__ g = Tn.g + e0;
+    float* __restrict__ m = Tn.m + e0;
+    float* __restrict__ v = Tn.v + e0;
+    int done = 0;
+    if (Tn.vec) {  // e0 is a multiple of 4096: 16-byte aligned like the tensor
+      const int nv = len >> 2;
+#pragma unroll 2
+      for (int q = threadIdx.x; q < nv; q += kThreads) {
+        const float4 w4 = __ldcs(reinterpret_cast<const float4*>(w) + q);
+        const float4 g4 = __ldcs(reinterpret_cast<const float4*>(g) + q);
+        const float4 m4 = __ldcs(reinterpret_cast<const float4*>(m) + q);
+        const float4 v4 = __ldcs(reinterpret_cast<const float4*>(v) + q);
+        float4 wo, mo, vo;
+        adam_elem(k, w4.x, g4.x, m4.x, v4.x, wo.x, mo.x, vo.x);
+        adam_elem(k, w4.y, g4.y, m4.y, v4.y, wo.y, mo.y, vo.y);
+        adam_elem(k, w4.z, g4.z, m4.z, v4.z, wo.z, mo.z, vo.z);
+        adam_elem(k, w4.w, g4.w, m4.w, v4.w, wo.w, mo.w, vo.w);
+        __stcs(reinterpret_cast<float4*>(w) + q, wo);
+        __stcs(reinterpret_cast<float4*>(m) + q, mo);
+        __stcs(reinterpret_cast<float4*>(v) + q, vo);
+      }
+      done = nv << 2;
+    }
+    for (int e = done + threadIdx.x; e < len; e += kThreads) {
+      float wo, mo, vo;
+      adam_elem(k, w[e], g[e], m[e], v[e], wo, mo, vo);
+      w[e] = wo;
+      m[e] = mo;
+      v[e] = vo;
+    }
   }
 }
 
@@ -336,6 +430,63 @@ bo_status bo_lamb_step(int32_t T, const int64_t* numels, float* const* params,
   BO_CUDA(cudaStreamSynchronize(s));
   if (limit_t < T) {
     fail(BO_ERR_NON_FINITE_GRADIENT, "non-finite gradient in tensor " + std::to_string(limit_t));
+  }
+  BO_OP_END
+}
+
+bo_status bo_fused_optimizer_step(int32_t T, const int64_t* numels, float* const* params,
+                                  const float* const* grads, float* const* m, float* const* v,
+                                  float lr, float beta1, float beta2, float eps,
+                                  float weight_decay, int32_t step, void* stream) {
+  BO_OP_BEGIN
+  if (T < 0 || (T > 0 && (!numels || !params || !grads || !m || !v))) {
+    fail(BO_ERR_SHAPE_MISMATCH, "fused_optimizer_step: null argument");
+  }
+  if (T == 0) return BO_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // graph.cpp:460-462 and the attributes of the body (graph.cpp:468-483)
+  const double bc1 = 1.0 / (1.0 - std::pow(static_cast<double>(beta1), step));
+  const double bc2 = 1.0 / (1.0 - std::pow(static_cast<double>(beta2), step));
+  const AdamConsts k{static_cast<float>(static_cast<double>(beta1)),
+                     static_cast<float>(1.0 - static_cast<double>(beta1)),
+                     static_cast<float>(static_cast<double>(beta2)),
+                     static_cast<float>(1.0 - static_cast<double>(beta2)),
+                     static_cast<float>(bc1), static_cast<float>(bc2),
+                     static_cast<float>(static_cast<double>(eps)),
+                     static_cast<float>(static_cast<double>(weight_decay)),
+                     static_cast<float>(-static_cast<double>(lr))};
+  int device = 0;
+  BO_CUDA(cudaGetDevice(&device));
+  int sms = 148;
+  BO_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  auto tab = std::make_unique<AdamTable>();
+  for (int base = 0; base < T; base += kAdamBatch) {
+    const int nb = std::min(kAdamBatch, T - base);
+    tab->T = nb;
+    tab->cstart[0] = 0;
+    for (int j = 0; j < nb; ++j) {
+      const int i = base + j;
+      if (numels[i] < 0) fail(BO_ERR_SHAPE_MISMATCH, "fused_optimizer_step: negative size");
+      const bool vec = ((reinterpret_cast<uintptr_t>(params[i]) | reinterpret_cast<uintptr_t>(grads[i]) |
+                         reinterpret_cast<uintptr_t>(m[i]) | reinterpret_cast<uintptr_t>(v[i])) & 15u) == 0;
+      tab->t[j] = AdamTensor{params[i], grads[i], m[i], v[i], numels[i], vec ? 1 : 0};
+      tab->cstart[j + 1] = tab->cstart[j] + (numels[i] + kTileElems - 1) / kTileElems;
+    }
+    if (tab->cstart[nb] == 0) continue;
+    const int grid = static_cast<int>(std::min<int64_t>(tab->cstart[nb], static_cast<int64_t>(sms) * 8));
+    k_fused_adam<<<grid, kThreads, 0, s>>>(*tab, k);
+    check("k_fused_adam");
+  }
+  BO_OP_END
+}
+
+bo_status bo_f16_round(float* x, size_t n, void* stream) {
+  BO_OP_BEGIN
+  if (!x && n) fail(BO_ERR_SHAPE_MISMATCH, "f16_round: null argument");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (n) {
+    k_round_f16<<<grid_for(n), kThreads, 0, s>>>(x, n);
+    check("k_round_f16");
   }
   BO_OP_END
 }

@@ -372,6 +372,32 @@ def lamb_step(params, grads, state: dict, cfg: LambConfig, stream=None) -> None:
     _lib.check(st)
 
 
+def fused_optimizer_step(params, grads, m, v, lr: float, beta1: float, beta2: float, eps: float,
+                         weight_decay: float, step: int, stream=None) -> None:
+    """The paper's fused Adam-form optimizer kernel, ``run_fused_kernel(
+    fused_optimizer_step(lr, beta1, beta2, eps, weight_decay, step), {w, g, m, v})``
+    (graph.cpp:458-487), in place on lists of contiguous CUDA fp32 tensors."""
+    lib = _lib.load()
+    n = len(params)
+    if not (len(grads) == len(m) == len(v) == n):
+        raise ShapeMismatch("ShapeMismatch: fused_optimizer_step expects 4 equal-length lists")
+    for i in range(n):
+        if not (params[i].shape == grads[i].shape == m[i].shape == v[i].shape):
+            raise ShapeMismatch(f"ShapeMismatch: fused_optimizer_step: shapes differ at tensor {i}")
+    numels = (C.c_int64 * max(n, 1))(*[p.numel() for p in params])
+    _lib.check(lib.bo_fused_optimizer_step(
+        n, numels, _ptr_array([t.data_ptr() for t in params]), _ptr_array([t.data_ptr() for t in grads]),
+        _ptr_array([t.data_ptr() for t in m]), _ptr_array([t.data_ptr() for t in v]), lr, beta1, beta2,
+        eps, weight_decay, step, _stream(stream)))
+
+
+def f16_round(x, stream=None) -> None:
+    """In-place binary16 round trip of a contiguous CUDA fp32 tensor (the AMP
+    cast, Tape::cast -> quantize_inplace, ops.cpp:655-668)."""
+    lib = _lib.load()
+    _lib.check(lib.bo_f16_round(x.data_ptr(), x.numel(), _stream(stream)))
+
+
 def unscale_gradients(grads, scale: float, enabled: bool = True, stream=None) -> None:
     """In place on a contiguous CUDA fp32 tensor (half.cpp:105-115)."""
     lib = _lib.load()

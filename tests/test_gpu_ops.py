@@ -226,3 +226,66 @@ def test_lamb_error_conditions(torch):
     bad[2] = float("inf")
     with pytest.raises(NonFiniteGradient):
         lamb_step(params, [bad], {}, LambConfig())
+
+
+@pytest.mark.parametrize("step", [1, 7, 1000])
+def test_fused_optimizer_step_bit_exact(torch, oracle, step):
+    """bo_fused_optimizer_step vs the oracle restatement of
+    fused_optimizer_step (graph.cpp:458-487): bit for bit, over ragged and
+    misaligned tensors (the scalar path) and aligned ones (float4 path)."""
+    from paper_2008_00177_b200.pipeline import fused_optimizer_step
+
+    rng = np.random.default_rng(step)
+    sizes = [1, 7, 4099, 130001, 4096 * 3]
+    host = []
+    for n in sizes:
+        w = rng.uniform(-1.0, 1.0, n).astype(np.float32)
+        g = rng.uniform(-0.2, 0.2, n).astype(np.float32)
+        m = rng.uniform(-0.05, 0.05, n).astype(np.float32)
+        v = (rng.uniform(0.0, 0.1, n) ** 2).astype(np.float32)
+        host.append([w, g, m, v])
+    # device copies; the second tensor set lives one element into a buffer
+    dev = []
+    for i, arrs in enumerate(host):
+        off = 1 if i % 2 else 0
+        ts = []
+        for a in arrs:
+            buf = torch.zeros(a.size + off, dtype=torch.float32, device="cuda")
+            buf[off:] = torch.from_numpy(a).cuda()
+            ts.append(buf[off:])
+        dev.append(ts)
+    args = (1e-3, 0.9, 0.999, 1e-6, 0.01, step)
+    fused_optimizer_step([d[0] for d in dev], [d[1] for d in dev], [d[2] for d in dev],
+                         [d[3] for d in dev], *args)
+    torch.cuda.synchronize()
+    for (w, g, m, v), d in zip(host, dev):
+        oracle.fused_optimizer_step(w, g, m, v, *args)
+        for want, got in ((w, d[0]), (m, d[2]), (v, d[3])):
+            assert np.array_equal(got.cpu().numpy().view(np.uint32), want.view(np.uint32))
+
+
+def test_fused_optimizer_zero_gradient_is_noop(torch):
+    """test_graph.cpp:439-452 on the device."""
+    from paper_2008_00177_b200.pipeline import fused_optimizer_step
+
+    w = (torch.rand(5000, device="cuda") * 4 - 2)
+    w0 = w.clone()
+    z = [torch.zeros(5000, device="cuda") for _ in range(3)]
+    fused_optimizer_step([w], [z[0]], [z[1]], [z[2]], 1e-2, 0.9, 0.999, 1e-6, 0.0, 1)
+    torch.cuda.synchronize()
+    assert torch.equal(w, w0) and not z[1].any() and not z[2].any()
+
+
+def test_f16_round_matches_oracle(torch, oracle):
+    from paper_2008_00177_b200.pipeline import f16_round
+
+    rng = np.random.default_rng(5)
+    x = np.concatenate([rng.standard_normal(1 << 20).astype(np.float32) * 100,
+                        np.array([65504, 65519.99, 65520, 2.0 ** -24, 2.0 ** -25, 2.0 ** -25 * 1.01,
+                                  -0.0, np.inf, -np.inf], np.float32)])
+    d = torch.from_numpy(x.copy()).cuda()
+    f16_round(d)
+    torch.cuda.synchronize()
+    want = x.copy()
+    oracle.f16_round(want)
+    assert np.array_equal(d.cpu().numpy().view(np.uint32), want.view(np.uint32))
