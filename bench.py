@@ -462,7 +462,10 @@ def main_reference(args):
     steps = max(1, min(args.steps, 10))
     cpu = run_cpu_reference(spec, world, K, bucket_bytes, f16, max(1, min(args.warmup, 2)), steps)
     line = {"metric": METRIC, "value": cpu["value"], "unit": UNIT, "n_gpus": world,
-            "steps": steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+            "steps": steps, "warmup": args.warmup,
+            # the full workload (world x P parameters) at the sample's throughput
+            "ms_per_step": round(world * spec.param_count() / cpu["value"] * 1e3, 3),
+            "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "impl": "reference",
             "config": {"workload": f"{args.model} optimizer step (reference CPU path, sample)",
