@@ -69,6 +69,9 @@ def main():
     f16, algo, K, bb, sc, ppm, sexp, exact = CASES[case]
     if args.model == "tiny":
         spec = bert_spec(BERT_TINY)
+    elif args.model == "bert-large":
+        from paper_2008_00177_b200.model_spec import BERT_LARGE
+        spec = bert_spec(BERT_LARGE)
     elif args.model == "ragged":
         spec = flat_spec([1, 7, 4099, 13, 2, 30000, 3], first_use=[3, 0, 6, 1, 5, 2, 4])
     else:

@@ -69,6 +69,16 @@ def test_two_gpus_shapes(model):
     run_case("ring16", 2, model=model)
 
 
+@pytest.mark.slow
+def test_two_gpus_bert_large_full_size():
+    """Config 3 at full size: BERT-large (336M) on two GPUs, binary16 ring,
+    against the oracle's emulation of the same world; moments bit-exact."""
+    if _ngpu() < 2:
+        pytest.skip("needs 2 GPUs")
+    res = run_case("ring16", 2, model="bert-large", steps=2)
+    assert res["m_bit_exact"] and res["v_bit_exact"] and res["replicas_identical"]
+
+
 @pytest.mark.parametrize("n", [4, 8])
 def test_more_gpus(n):
     if _ngpu() < n:
