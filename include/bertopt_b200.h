@@ -158,6 +158,16 @@ bo_status bo_comm_init(bo_ctx* ctx, const uint8_t* id128);
 bo_status bo_set_stream(bo_ctx* ctx, void* cuda_stream);
 void* bo_get_stream(const bo_ctx* ctx);
 bo_status bo_synchronize(bo_ctx* ctx);
+/* Watchdog wait (the reference's transport watchdog, transport.cpp:113-132 /
+ * 336-383): block until the context's queued work has completed, at most
+ * timeout_ms milliseconds (< 0: no limit). BO_ERR_PEER_DISCONNECTED when the
+ * communicator reports a remote failure (ncclCommGetAsyncError),
+ * BO_ERR_WATCHDOG_TIMEOUT when the work is still pending at the deadline (a
+ * stalled or dead peer keeps a collective from completing). Nothing is
+ * cancelled: the caller decides whether to keep waiting or to tear the rank
+ * down (the reference's run_data_parallel then reports the root cause,
+ * trainer.cpp:473-487). */
+bo_status bo_wait(bo_ctx* ctx, int64_t timeout_ms);
 
 /* ---- state ------------------------------------------------------------- */
 /* Parameters in model order, flat (all tensors concatenated). */

@@ -67,6 +67,7 @@ SIGNATURES = {
     "bo_set_stream": (_i32, [_vp, _vp]),
     "bo_get_stream": (_vp, [_vp]),
     "bo_synchronize": (_i32, [_vp]),
+    "bo_wait": (_i32, [_vp, _i64]),
     "bo_load_params": (_i32, [_vp, _vp, _i32]),
     "bo_read_params": (_i32, [_vp, _vp, _i32]),
     "bo_read_moments": (_i32, [_vp, _vp, _vp, _i32]),

@@ -1,6 +1,8 @@
 // C ABI of the pipeline context: creation, layout, communication, state, and
 // the hot-path entry point bo_accumulate (see include/bertopt_b200.h).
 #include <algorithm>
+#include <chrono>
+#include <thread>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -663,6 +665,43 @@ void* bo_get_stream(const bo_ctx* c) { return c ? c->stream : nullptr; }
 bo_status bo_synchronize(bo_ctx* c) {
   BO_GUARD_BEGIN
   BO_CUDA(cudaStreamSynchronize(c->stream));
+  BO_GUARD_END
+}
+
+bo_status bo_wait(bo_ctx* c, int64_t timeout_ms) {
+  BO_GUARD_BEGIN
+  if (!c) fail(BO_ERR_INVALID_CONFIG, "null ctx");
+  BO_CUDA(cudaSetDevice(c->device));
+  const auto t0 = std::chrono::steady_clock::now();
+  const cudaStream_t streams[2] = {c->stream, c->comm_stream};
+  for (;;) {
+    bool pending = false;
+    for (cudaStream_t s : streams) {
+      if (!s) continue;
+      const cudaError_t e = cudaStreamQuery(s);
+      if (e == cudaErrorNotReady) {
+        pending = true;
+      } else if (e != cudaSuccess) {
+        fail(BO_ERR_CUDA, std::string("bo_wait: ") + cudaGetErrorString(e));
+      }
+    }
+    if (!pending) break;
+    if (c->comm) {
+      ncclResult_t async = ncclSuccess;
+      BO_NCCL(ncclCommGetAsyncError(c->comm, &async));
+      if (async != ncclSuccess) {
+        fail(BO_ERR_PEER_DISCONNECTED, std::string("rank ") + std::to_string(c->rank) +
+                                           ": communicator failed: " + ncclGetErrorString(async));
+      }
+    }
+    const auto waited = std::chrono::duration_cast<std::chrono::milliseconds>(
+        std::chrono::steady_clock::now() - t0).count();
+    if (timeout_ms >= 0 && waited >= timeout_ms) {
+      fail(BO_ERR_WATCHDOG_TIMEOUT, "rank " + std::to_string(c->rank) + ": step still pending after " +
+                                        std::to_string(waited) + " ms");
+    }
+    std::this_thread::sleep_for(std::chrono::microseconds(200));
+  }
   BO_GUARD_END
 }
 

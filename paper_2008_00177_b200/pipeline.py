@@ -229,6 +229,12 @@ class GradPipeline:
     def synchronize(self) -> None:
         _lib.check(self.lib.bo_synchronize(self.ctx))
 
+    def wait(self, timeout_ms: int = -1) -> None:
+        """Watchdog wait: raises WatchdogTimeout if the queued step has not
+        completed within timeout_ms, PeerDisconnected on a communicator
+        failure (transport.cpp:113-132)."""
+        _lib.check(self.lib.bo_wait(self.ctx, int(timeout_ms)))
+
     # -- introspection
     PATH_NAMES = {1: "one_rank_fused", 2: "one_rank_staged", 4: "ring_p2p", 8: "ring_sendrecv",
                   16: "last_hop_fused", 32: "nccl_reduce_scatter", 64: "overlap"}

@@ -241,3 +241,25 @@ def test_sync_ready_protocol_errors(torch_cuda, oracle):
     pipe.sync_ready(rest, [gb.ptrs[0][t] for t in rest])
     pipe.synchronize()
     assert pipe.status().lamb_step == 1
+
+
+def test_watchdog_wait(torch_cuda, oracle):
+    """bo_wait: WatchdogTimeout while the context stream is still busy,
+    success once it drains (transport.cpp:113-132 semantics)."""
+    import torch
+
+    from paper_2008_00177_b200.errors import WatchdogTimeout
+    from paper_2008_00177_b200.model_spec import BERT_TINY, bert_spec
+    from paper_2008_00177_b200.pipeline import GradPipeline, LambConfig, ScalerConfig, TrainerConfig
+
+    spec = bert_spec(BERT_TINY)
+    pipe = GradPipeline(spec, TrainerConfig(LambConfig(), 1, 4096, False, 0, ScalerConfig()))
+    pipe.load_params(oracle.build_params(spec, 1))
+    s = torch.cuda.Stream()
+    pipe.set_stream(s)
+    with torch.cuda.stream(s):
+        torch.cuda._sleep(int(1.5e9))  # ~0.8 s of device time queued on the context stream
+    with pytest.raises(WatchdogTimeout):
+        pipe.wait(20)
+    pipe.wait(-1)
+    pipe.wait(0)  # nothing pending: immediate success
