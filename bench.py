@@ -68,6 +68,9 @@ def parse():
     ap.add_argument("--bucket-mb", type=float, default=4.0)
     ap.add_argument("--wire", default="f16", choices=["f16", "f32"])
     ap.add_argument("--algo", default="auto", choices=["auto", "ring", "nccl"])
+    ap.add_argument("--api", default="train_step", choices=["train_step", "accumulate"],
+                    help="train_step: one bo_train_step per step (all K micros resident); "
+                         "accumulate: K bo_accumulate calls per step")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -243,15 +246,21 @@ def main_b200(args):
             synth_grads(b[slots[t]:slots[t] + n], int(model_off[t]), 1, rank, 0, k, S0)
         bufs.append(b)
     ptr_arrays = [GradPipeline.make_ptr_array([b.data_ptr() + 2 * s for s in slots]) for b in bufs]
+    all_ptrs = GradPipeline.make_ptr_array([b.data_ptr() + 2 * s for b in bufs for s in slots])
     torch.cuda.synchronize()
 
     # the pipeline runs on a torch-owned stream (torch's allocators record on it)
     stream = torch.cuda.Stream()
     pipe.set_stream(stream)
 
-    def step():
+    def step_per_micro():
         for k in range(K):
             pipe.accumulate_ptr_array(k, ptr_arrays[k])
+
+    def step_train():
+        pipe.train_step_ptr_array(all_ptrs)
+
+    step = step_train if args.api == "train_step" else step_per_micro
 
     def barrier():
         if world > 1:
@@ -300,21 +309,24 @@ def main_b200(args):
     E = 2 if f16 else 4
     path = pipe.path()
     fused_last = "last_hop_fused" in path
+    resident = "resident_micros" in path
+    # the sync gradient's source per element: the K resident micros (2K B,
+    # bo_train_step) or the live micro + the fp32 accumulator (2 + 4 B)
+    xb = 2 * K if resident else (6 if K > 1 else 2)
     # algorithmic bytes per launch of each stage (HBM) / per rank (NVLink)
     hbm_bytes = {
         "accumulate": (BYTES_ACCUMULATE_FIRST + BYTES_ACCUMULATE * (K - 2)) * P / max(K - 1, 1),
         "finalize": (BYTES_FINALIZE if K > 1 else BYTES_FINALIZE_K1) * P,
-        # LAMB phase 1: one rank k_lamb_p1 (h 2 + acc 4 + w, m, v read; m', v', u
-        # written); world > 1 k_p1w (reduced wire E or, with the last ring hop
-        # fused in, h 2 + acc 4 with the wire over NVLink; + wsh, m, v read;
-        # m', v', u written); phase 2: k_lamb_p2 / k_shard_p2_push (w, u read;
-        # w written)
-        "lamb_norms": ((30 if K > 1 else 26) if world == 1 else
-                       ((6 if K > 1 else 2) if fused_last else E) + 24) * S_shard,
+        # LAMB phase 1: one rank k_lamb_p1 (the gradient source xb + w, m, v
+        # read; m', v', u written); world > 1 k_p1w (reduced wire E or, with
+        # the last ring hop fused in, xb with the wire over NVLink; + wsh, m, v
+        # read; m', v', u written); phase 2: k_lamb_p2 / k_shard_p2_push (w, u
+        # read; w written)
+        "lamb_norms": ((xb + 24) if world == 1 else ((xb if fused_last else E) + 24)) * S_shard,
         "lamb_update": 12 * S_shard,
-        # one ring hop kernel (nested in "reduce"): h + acc of one chunk of every
-        # bucket, wire in and out
-        "hop_kernels": (6 + 2 * E) * S_shard,
+        # one ring hop kernel (nested in "reduce"): the gradient source of one
+        # chunk of every bucket, wire in and out
+        "hop_kernels": (xb + 2 * E) * S_shard,
     }
     # NVLink bytes sent per rank: ring reduce-scatter; the parameter push
     # (k_shard_p2_push stores every updated element into the N-1 other replicas)
@@ -368,9 +380,15 @@ def main_b200(args):
     # plus the stricter pipelined bound max(sum HBM / BW_hbm, sum NVL / BW_nvl)
     E = 2 if f16 else 4
     E_lamb = E if world > 1 else 4
-    hbm_a = (BYTES_ACCUMULATE_FIRST + BYTES_ACCUMULATE * (K - 2) + 2 + 4 + E) * P if K > 1 \
-        else (2 + E) * P
-    hbm_c = (24 + E_lamb) * P / world
+    if resident:
+        # all K micros read once in the sync pass, no accumulator and, on one
+        # rank, no fusion buffer (the gradient feeds LAMB in registers)
+        hbm_a = (2 * K + (E if world > 1 else 0)) * P
+        hbm_c = (24 + (E if world > 1 else 0)) * P / world
+    else:
+        hbm_a = (BYTES_ACCUMULATE_FIRST + BYTES_ACCUMULATE * (K - 2) + 2 + 4 + E) * P if K > 1 \
+            else (2 + E) * P
+        hbm_c = (24 + E_lamb) * P / world
     nvl_b = (world - 1) / world * E * P
     nvl_d = (world - 1) / world * 4 * P
     t_roof = hbm_a / (hbm * 1e9) + hbm_c / (hbm * 1e9) + nvl_b / (NVLINK_GBS * 1e9) + \
@@ -382,9 +400,33 @@ def main_b200(args):
                      "hbm_bytes": int(hbm_a + hbm_c), "nvlink_bytes": int(nvl_b + nvl_d),
                      "hbm_gbs": hbm, "nvlink_gbs": NVLINK_GBS,
                      "formula": "frac: sum over stages of max(HBM/BW_hbm, NVL/BW_nvl) with "
-                                "A=acc+finalize, C=LAMB on the shard, B=RS, D=AG (no overlap; "
-                                "> 1 when stages overlap, e.g. the fused last hop); "
-                                "pipelined_frac: max(sum HBM/BW_hbm, sum NVL/BW_nvl)"}
+                                "A=gradient accumulation + finalize (per-micro API: SURVEY's "
+                                "36 B/param at K=4; train_step API: the K binary16 micros read "
+                                "once, 2K B/param, + the fusion-buffer write at N>1), C=LAMB on "
+                                "the shard, B=RS, D=AG (no overlap; > 1 when stages overlap, "
+                                "e.g. the fused last hop); pipelined_frac: max(sum HBM/BW_hbm, "
+                                "sum NVL/BW_nvl)"}
+
+    # the same step through the per-micro API (K bo_accumulate calls, fp32
+    # accumulator in HBM), timed the same way, for comparison
+    per_micro = None
+    if args.api == "train_step":
+        for _ in range(2):
+            step_per_micro()
+        barrier()
+        p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        p0.record(stream)
+        for _ in range(args.steps):
+            step_per_micro()
+        p1.record(stream)
+        barrier()
+        pm = p0.elapsed_time(p1) / args.steps
+        if world > 1:
+            t = torch.tensor([pm], device=f"cuda:{local}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            pm = float(t.item())
+        per_micro = {"ms_per_step": round(pm, 4), "value": world * P / (pm * 1e-3), "unit": UNIT,
+                     "api": "bo_accumulate x K (accumulator in HBM)"}
 
     # end to end through the public API with host buffers
     e2e = None
@@ -399,7 +441,7 @@ def main_b200(args):
             with torch.cuda.stream(stream):
                 for k in range(K):
                     stage_dev[k].copy_(host[k], non_blocking=True)
-                    pipe.accumulate_ptr_array(k, ptr_arrays[k])
+                step()
             return pipe.status()  # D2H of the step result (syncs the stream)
 
         e2e_step()
@@ -437,11 +479,14 @@ def main_b200(args):
                        "bucket_bytes": bucket_bytes, "buckets": pipe.num_buckets,
                        "wire": args.wire if world > 1 else None,
                        "reduce_algo": args.algo if world > 1 else None,
+                       "api": "bo_train_step (K micros resident)" if args.api == "train_step"
+                              else "bo_accumulate x K",
                        "kernel_path": path,
                        "parallelism": f"dp{world} (reduce-scatter + sharded LAMB + all-gather)",
                        "l2": "inputs (K x 2 B x P) larger than L2, no flush"},
             "roofline": roofline, "step_roofline": step_roofline, "stages": stages,
-            "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": int(launches),
+            "e2e": e2e, "per_micro_api": per_micro, "cpu_baseline": cpu,
+            "gpu_launches": int(launches),
             "clocks": sampler.summary() if sampler else None,
         }
         sys.stdout.flush()

@@ -197,6 +197,15 @@ bo_status bo_param_ptr(bo_ctx* ctx, int32_t tensor, float** out);
  * ratio; skipped on overflow) -> loss-scaler update -> all-gather of the
  * updated parameters. Asynchronous on the context stream. */
 bo_status bo_accumulate(bo_ctx* ctx, int32_t micro, const uint16_t* const* grads);
+/* One whole optimizer step, DistributedTrainer::train_step(micros)
+ * (trainer.cpp:217-373): grads[k * n_tensors + p] is micro k's binary16
+ * gradient of tensor p, for k = 0..K-1, all resident in HBM until the step's
+ * work has run on the context stream. With every micro at hand the sync pass
+ * reads the K gradient sets directly — summed in the reference's order,
+ * ((0 + g0) + g1) + ... + g_{K-2}, then + g_{K-1} — instead of materialising
+ * an fp32 accumulator (24 B/param of accumulator traffic saved at K = 4).
+ * Bit-identical to K bo_accumulate calls. */
+bo_status bo_train_step(bo_ctx* ctx, const uint16_t* const* grads);
 /* The sync micro with bucket-level overlap (TrainerConfig::overlap,
  * trainer.cpp:247-348; readiness = Tape::backward's progress hook,
  * tensor.hpp:94-106): deliver the sync micro's gradients as they become final,
@@ -235,6 +244,7 @@ int64_t bo_launch_count(const bo_ctx* ctx);
 #define BO_PATH_LAST_HOP_FUSED 16    /* the ring's last hop ran inside LAMB phase 1 */
 #define BO_PATH_NCCL_RS 32           /* ncclReduceScatter of the fusion buffer */
 #define BO_PATH_OVERLAP 64           /* sync micro delivered through bo_sync_ready */
+#define BO_PATH_RESIDENT 128         /* bo_train_step: the K micros read in the sync pass */
 int32_t bo_path_flags(const bo_ctx* ctx);
 
 /* ---- operator-level drop-ins -------------------------------------------- */

@@ -913,6 +913,61 @@ bo_status bo_accumulate(bo_ctx* c, int32_t micro, const uint16_t* const* grads) 
   BO_GUARD_END
 }
 
+bo_status bo_train_step(bo_ctx* c, const uint16_t* const* grads) {
+  BO_GUARD_BEGIN
+  if (!c || !grads) fail(BO_ERR_INVALID_CONFIG, "null argument");
+  if (c->world > 1 && !c->comm) fail(BO_ERR_INVALID_CONFIG, "bo_comm_init has not run");
+  if (c->sync_open) fail(BO_ERR_PROTOCOL, "an overlapped sync micro (bo_sync_ready) is in progress");
+  const int K = c->cfg.accumulation, T = c->L.T;
+  bool aligned = true;
+  for (int i = 0; i < K * T; ++i) {
+    if (!grads[i]) fail(BO_ERR_SHAPE_MISMATCH, "null gradient for micro " + std::to_string(i / T) +
+                                                   ", tensor " + std::to_string(i % T));
+    aligned &= (reinterpret_cast<uintptr_t>(grads[i]) & 15u) == 0;
+  }
+  // The resident-micro kernels read all K gradient sets in the sync pass
+  // (no accumulator round trips): one rank's fused path and the ring. Other
+  // configurations (NCCL wire, unaligned slots, K == 1, K > 8) take the
+  // per-micro path; the results are identical either way.
+  const bool resident = K > 1 && K <= kMaxResident && aligned &&
+                        (c->world == 1 ? !c->force_unfused : c->algo == BO_REDUCE_RING);
+  if (!resident) {
+    for (int k = 0; k < K; ++k) {
+      const bo_status st = bo_accumulate(c, k, grads + static_cast<size_t>(k) * T);
+      if (st != BO_OK) return st;
+    }
+    return BO_OK;
+  }
+  if (c->micro_tab_cap < K * T) {
+    c->d_micro_tab = static_cast<const uint16_t**>(dev_alloc(c, static_cast<size_t>(K) * T * sizeof(void*)));
+    c->micro_tab_cap = K * T;
+  }
+  // pageable source: staged by the driver before the call returns; ordered
+  // on the stream after the previous step's kernels that read the table
+  BO_CUDA(cudaMemcpyAsync(c->d_micro_tab, grads, static_cast<size_t>(K) * T * sizeof(void*),
+                          cudaMemcpyHostToDevice, c->stream));
+  PtrTable tab;
+  for (int t = 0; t < T; ++t) tab.p[t] = grads[static_cast<size_t>(K - 1) * T + t];  // the live micro
+  grow_bc_table(c, c->calls + 2);
+  c->ms = MicroSrc{c->d_micro_tab, K, T};
+  c->path = BO_PATH_RESIDENT;
+  try {
+    if (c->world == 1) {
+      c->path |= BO_PATH_ONE_RANK_FUSED;
+      run_fused_single_rank(c, tab, c->ms);
+    } else {
+      run_reduce(c, tab);
+      run_lamb(c, tab);
+    }
+  } catch (...) {
+    c->ms = MicroSrc{nullptr, 0, 0};
+    throw;
+  }
+  c->ms = MicroSrc{nullptr, 0, 0};
+  c->calls += 1;
+  BO_GUARD_END
+}
+
 bo_status bo_sync_ready(bo_ctx* c, int32_t n, const int32_t* tensors, const uint16_t* const* grads) {
   BO_GUARD_BEGIN
   if (!c || (n > 0 && (!tensors || !grads))) fail(BO_ERR_INVALID_CONFIG, "null argument");

@@ -147,6 +147,74 @@ __device__ __forceinline__ void raise_flag(bool bad, DevState* st) {
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&st->local_flag, 1);
 }
 
+// All K micro-batches of one step resident (bo_train_step). p[k] points at
+// micro k's gradient of the current tile (a per-CTA/per-warp table in shared
+// memory); the flattened sync gradient before the unscale is the reference's
+// live + summed, summed = ((0 + g0) + g1) + ... + g_{K-2} (trainer.cpp:240-244,
+// 196-201): the same additions in the same order as the accumulator path.
+__device__ __forceinline__ void widen4(uint2 x, float (&o)[4]) {
+  o[0] = widen(static_cast<uint16_t>(x.x & 0xFFFFu));
+  o[1] = widen(static_cast<uint16_t>(x.x >> 16));
+  o[2] = widen(static_cast<uint16_t>(x.y & 0xFFFFu));
+  o[3] = widen(static_cast<uint16_t>(x.y >> 16));
+}
+
+__device__ __forceinline__ float micro_sum1(const uint16_t* const* p, int K, int e) {
+  float acc = 0.0f;
+  for (int k = 0; k + 1 < K; ++k) acc = __fadd_rn(acc, widen(p[k][e]));
+  const float live = widen(p[K - 1][e]);
+  return K > 1 ? __fadd_rn(live, acc) : live;
+}
+
+// Elements e..e+3 with K known at compile time (all K loads first).
+template <int K>
+__device__ __forceinline__ void micro_sum4_k(const uint16_t* const* p, int e, float (&o)[4]) {
+  uint2 x[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) x[k] = __ldcs(reinterpret_cast<const uint2*>(p[k] + e));
+  float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+  for (int k = 0; k + 1 < K; ++k) {
+    float f[4];
+    widen4(x[k], f);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) acc[i] = __fadd_rn(acc[i], f[i]);
+  }
+  widen4(x[K - 1], o);
+  if (K > 1) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) o[i] = __fadd_rn(o[i], acc[i]);
+  }
+}
+
+// Elements e..e+3 (8-byte aligned in every micro): all K loads are issued
+// before the first addition.
+__device__ __forceinline__ void micro_sum4(const uint16_t* const* p, int K, int e, float (&o)[4]) {
+  uint2 x[kMaxResident];
+#pragma unroll
+  for (int k = 0; k < kMaxResident; ++k) {
+    if (k < K) x[k] = __ldcs(reinterpret_cast<const uint2*>(p[k] + e));
+  }
+  float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+  uint2 live = x[0];
+#pragma unroll
+  for (int k = 0; k < kMaxResident; ++k) {
+    if (k + 1 < K) {
+      float f[4];
+      widen4(x[k], f);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) acc[i] = __fadd_rn(acc[i], f[i]);
+    } else if (k + 1 == K) {
+      live = x[k];
+    }
+  }
+  widen4(live, o);
+  if (K > 1) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) o[i] = __fadd_rn(o[i], acc[i]);
+  }
+}
+
 // Streaming accesses with explicit L2 eviction priority (no L1 allocation):
 // evict_first for data read once, evict_last for what the next pass re-reads.
 __device__ __forceinline__ uint64_t policy_evict_first() {
@@ -176,12 +244,6 @@ __device__ __forceinline__ uint2 ld2u(const uint16_t* p, uint64_t pol) {
 __device__ __forceinline__ void st4(float* p, float4 v, uint64_t pol) {
   asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "f"(v.x),
                "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol));
-}
-__device__ __forceinline__ void widen4(uint2 x, float (&o)[4]) {
-  o[0] = widen(static_cast<uint16_t>(x.x & 0xFFFFu));
-  o[1] = widen(static_cast<uint16_t>(x.x >> 16));
-  o[2] = widen(static_cast<uint16_t>(x.y & 0xFFFFu));
-  o[3] = widen(static_cast<uint16_t>(x.y >> 16));
 }
 
 }  // namespace bo

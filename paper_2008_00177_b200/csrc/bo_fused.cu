@@ -12,6 +12,8 @@
 //   k_lamb_p2     w -= (lr * r) * u, tiles in reverse order so the update
 //                 and weights phase 1 wrote last are still in L2; the dead
 //                 u lines are then dropped from L2 (discard.global.L2)      12 B/elem
+//   k_lamb_p1r    the same with the K micro-batches resident (bo_train_step):
+//                 g = micro sum * inv, no accumulator               2K + 24 B/elem
 //   k_fused_epilogue  step counters, the moment-buffer flip and the
 //                 loss-scaler state machine
 //
@@ -115,6 +117,119 @@ __global__ void __launch_bounds__(kP1Threads, 2) k_lamb_p1(
     } else {
       // padding lanes past len keep their old m/v bits and contribute nothing
       for (int i = n; i < 4; ++i) {
+        put(mo, i, ma[i]);
+        put(vo, i, va[i]);
+        put(uo, i, 0.0f);
+      }
+      for (int i = 0; i < n; ++i) {
+        wn = __dadd_rn(wn, __dmul_rn(static_cast<double>(wa[i]), static_cast<double>(wa[i])));
+        un = __dadd_rn(un, __dmul_rn(static_cast<double>(o.u[i]), static_cast<double>(o.u[i])));
+      }
+    }
+    const int64_t a = t.a0 + e0;
+    st4(mn + a, mo, pf);
+    st4(vn + a, vo, pf);
+    st4(u + a, uo, pl);
+  }
+  raise_flag(bad, st);
+  wn = warp_sum(wn);
+  un = warp_sum(un);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) {
+    red[0][wid] = wn;
+    red[1][wid] = un;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double A = 0.0, B = 0.0;
+    for (int i = 0; i < kP1Threads / 32; ++i) {
+      A += red[0][i];
+      B += red[1][i];
+    }
+    tile_part[2 * blockIdx.x] = A;
+    tile_part[2 * blockIdx.x + 1] = B;
+  }
+}
+
+// Phase 1 with the K micro-batches resident (bo_train_step): g = the micro
+// sum * inv straight from the K binary16 gradients, no accumulator. K is a
+// template parameter so the K loads of both float4 groups of a thread are
+// issued up front like k_lamb_p1's; the tile's K gradient pointers sit in
+// shared memory. 2K + 24 B/elem.
+template <int K>
+__global__ void __launch_bounds__(kP1Threads, 2) k_lamb_p1r(
+    const FusedTile* __restrict__ tiles, MicroSrc ms, const float* __restrict__ w, float* m0,
+    float* v0, float* m1, float* v1, float* __restrict__ u, DevState* __restrict__ st, LambConsts c,
+    const double* __restrict__ bc_table, double* __restrict__ tile_part) {
+  const FusedTile t = tiles[blockIdx.x];
+  __shared__ const uint16_t* sp[K];
+  __shared__ double red[2][kP1Threads / 32];
+  if (threadIdx.x < K) sp[threadIdx.x] = ms.hk[threadIdx.x * ms.T + t.t] + t.e0;
+  const int par = st->parity;
+  const float* __restrict__ m = par ? m1 : m0;
+  const float* __restrict__ v = par ? v1 : v0;
+  float* __restrict__ mn = par ? m0 : m1;
+  float* __restrict__ vn = par ? v0 : v1;
+  const double* bcp = bc_table + 4 * st->lamb_step;
+  const double ibc1 = bcp[2], ibc2 = bcp[3];
+  const float inv = __fdiv_rn(1.0f, __fmul_rn(static_cast<float>(K), st->scale));
+  const uint64_t pf = policy_evict_first(), pl = policy_evict_last();
+  __syncthreads();
+  float4 wv[2], mv[2], vv[2];
+  uint2 hv[2][K];
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const int e0 = 4 * (threadIdx.x + j * kP1Threads);
+    if (e0 < t.len) {
+      const int64_t a = t.a0 + e0;
+#pragma unroll
+      for (int k = 0; k < K; ++k) hv[j][k] = ld2u(sp[k] + e0, pf);
+      wv[j] = ld4(w + a, pl);
+      mv[j] = ld4(m + a, pf);
+      vv[j] = ld4(v + a, pf);
+    }
+  }
+  double wn = 0.0, un = 0.0;
+  bool bad = false;
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const int e0 = 4 * (threadIdx.x + j * kP1Threads);
+    if (e0 >= t.len) continue;
+    const int n = min(4, t.len - e0);  // < 4 only in a tensor's last float4
+    // live + (((0 + g0) + g1) + ... + g_{K-2}) (trainer.cpp:240-244, 196-201)
+    float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f}, xs[4];
+#pragma unroll
+    for (int k = 0; k + 1 < K; ++k) {
+      float f[4];
+      widen4(hv[j][k], f);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) acc[i] = __fadd_rn(acc[i], f[i]);
+    }
+    widen4(hv[j][K - 1], xs);
+    float ga[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      xs[i] = __fadd_rn(xs[i], acc[i]);
+      ga[i] = __fmul_rn(xs[i], inv);
+      // a non-finite input makes the fp32 sum non-finite (K finite binary16
+      // values cannot overflow fp32): the step's overflow check
+      if (i < n) bad |= !finite(xs[i]);
+    }
+    const float wa[4] = {wv[j].x, wv[j].y, wv[j].z, wv[j].w};
+    const float ma[4] = {mv[j].x, mv[j].y, mv[j].z, mv[j].w};
+    const float va[4] = {vv[j].x, vv[j].y, vv[j].z, vv[j].w};
+    const Lamb4 o = lamb_elem4(ga, wa, ma, va, c, bcp, ibc1, ibc2);
+    float4 mo = make_float4(o.m[0], o.m[1], o.m[2], o.m[3]);
+    float4 vo = make_float4(o.v[0], o.v[1], o.v[2], o.v[3]);
+    float4 uo = make_float4(o.u[0], o.u[1], o.u[2], o.u[3]);
+    if (n == 4) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        wn = __dadd_rn(wn, __dmul_rn(static_cast<double>(wa[i]), static_cast<double>(wa[i])));
+        un = __dadd_rn(un, __dmul_rn(static_cast<double>(o.u[i]), static_cast<double>(o.u[i])));
+      }
+    } else {
+      for (int i = n; i < 4; ++i) {  // padding lanes keep their old m/v bits
         put(mo, i, ma[i]);
         put(vo, i, va[i]);
         put(uo, i, 0.0f);
@@ -259,13 +374,31 @@ void check(bo_ctx* c, const char* what) {
 
 }  // namespace
 
-void run_fused_single_rank(bo_ctx* c, const PtrTable& tab) {
+void run_fused_single_rank(bo_ctx* c, const PtrTable& tab, MicroSrc ms) {
   {
     StageTimer timer(c, BO_STAGE_LAMB_NORMS);
-    k_lamb_p1<<<c->n_fused_tiles, kP1Threads, 0, c->stream>>>(
-        c->d_fused_tiles, tab, c->acc, c->w, c->m, c->v, c->m_alt, c->v_alt, c->u, c->state, c->lamb,
-        c->bc_table, c->cfg.accumulation, c->tile_part);
-    check(c, "k_lamb_p1");
+    if (ms.K > 0) {
+      auto launch = [&](auto kern) {
+        kern<<<c->n_fused_tiles, kP1Threads, 0, c->stream>>>(c->d_fused_tiles, ms, c->w, c->m, c->v, c->m_alt,
+                                                             c->v_alt, c->u, c->state, c->lamb, c->bc_table,
+                                                             c->tile_part);
+      };
+      switch (ms.K) {
+        case 2: launch(k_lamb_p1r<2>); break;
+        case 3: launch(k_lamb_p1r<3>); break;
+        case 4: launch(k_lamb_p1r<4>); break;
+        case 5: launch(k_lamb_p1r<5>); break;
+        case 6: launch(k_lamb_p1r<6>); break;
+        case 7: launch(k_lamb_p1r<7>); break;
+        default: launch(k_lamb_p1r<8>); break;
+      }
+      check(c, "k_lamb_p1r");
+    } else {
+      k_lamb_p1<<<c->n_fused_tiles, kP1Threads, 0, c->stream>>>(
+          c->d_fused_tiles, tab, c->acc, c->w, c->m, c->v, c->m_alt, c->v_alt, c->u, c->state, c->lamb,
+          c->bc_table, c->cfg.accumulation, c->tile_part);
+      check(c, "k_lamb_p1");
+    }
   }
   {
     StageTimer timer(c, BO_STAGE_TRUST);

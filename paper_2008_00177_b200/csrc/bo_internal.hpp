@@ -17,6 +17,7 @@ constexpr int kMaxTensors = 1024;     // per-micro pointer table travels as a ke
 constexpr int kTileElems = 4096;      // elements per CTA work tile
 constexpr int kAlignElems = 64;       // 256-byte alignment of every buffer region
 constexpr int kThreads = 256;
+constexpr int kMaxResident = 8;       // micro-batches bo_train_step reads in one pass
 
 // Thrown inside the library, turned into a bo_status at the C boundary.
 struct Failure {
@@ -146,6 +147,13 @@ struct PtrTable {
   const uint16_t* p[kMaxTensors];
 };
 
+// All K micro-batches of a step resident (bo_train_step): micro k's gradient
+// of tensor t is hk[k * T + t] (a device array). K == 0: not in use.
+struct MicroSrc {
+  const uint16_t* const* hk;
+  int K, T;
+};
+
 }  // namespace bo
 
 struct bo_ctx {
@@ -214,7 +222,10 @@ struct bo_ctx {
   void* ring_result = nullptr;         // staging buffer holding the owned reduced chunk
   const void* ring_last_in = nullptr;  // last hop fused into LAMB phase 1: its input
   int fuse_last_hop = -1;
-  int path = 0;                        // BO_PATH_* bits of the last sync micro              // BO_FUSE_LAST=0/1 overrides the per-world default
+  int path = 0;                        // BO_PATH_* bits of the last sync micro
+  bo::MicroSrc ms{nullptr, 0, 0};      // resident micros of the step in flight (bo_train_step)
+  const uint16_t** d_micro_tab = nullptr;  // device [K][T] gradient pointer table
+  int micro_tab_cap = 0;              // BO_FUSE_LAST=0/1 overrides the per-world default
   bool ring_via_nccl = false;          // BO_RING_NCCL=1: hops over ncclSend/ncclRecv
   std::vector<void*> ipc_opened;       // peer mappings to close
   int* d_barrier = nullptr;
@@ -258,7 +269,7 @@ void run_reduce_group(bo_ctx* c, const PtrTable& tab, int b0, int b1, int acc0, 
                       cudaStream_t stream);
 void run_lamb(bo_ctx* c, const PtrTable& tab);
 void gather_shard(bo_ctx* c);
-void run_fused_single_rank(bo_ctx* c, const PtrTable& tab);
+void run_fused_single_rank(bo_ctx* c, const PtrTable& tab, MicroSrc ms = MicroSrc{nullptr, 0, 0});
 
 // Stage bracket: records events when profiling is on.
 struct StageTimer {

@@ -147,10 +147,11 @@ __device__ __forceinline__ float from_wire(uint16_t w) { return widen(w); }
 // Ring hop with flatten_param fused in (trainer.cpp:186-203 + collective.hpp:65-80
 // / collective.cpp:170-190): x = (h + acc) * inv for the elements of chunk q,
 // out = wire(x) (combine == 0, the first send) or wire(from_wire(in) + x).
-template <typename W>
+// KR > 0 (bo_train_step): x from the KR resident micros instead of h + acc.
+template <typename W, int KR>
 __global__ void __launch_bounds__(kThreads) k_hopx(const HopXTile* __restrict__ tiles,
                                                    const TensorDev* __restrict__ td,
-                                                   const __grid_constant__ PtrTable tab,
+                                                   const __grid_constant__ PtrTable tab, MicroSrc ms,
                                                    const float* __restrict__ acc,
                                                    const DevState* __restrict__ st, int K,
                                                    const W* __restrict__ in, W* __restrict__ out,
@@ -159,16 +160,48 @@ __global__ void __launch_bounds__(kThreads) k_hopx(const HopXTile* __restrict__ 
   const float inv = __fdiv_rn(1.0f, __fmul_rn(static_cast<float>(K), st->scale));
   const uint16_t* __restrict__ h = tab.p[tile.t] + tile.e0;
   const float* __restrict__ a = acc + td[tile.t].acc_off + tile.e0;
+  constexpr bool resident = KR > 0;
+  __shared__ const uint16_t* mp[KR > 0 ? KR : 1];  // the tile's KR micro pointers
+  if constexpr (resident) {
+    if (static_cast<int>(threadIdx.x) < KR) mp[threadIdx.x] = ms.hk[threadIdx.x * ms.T + tile.t] + tile.e0;
+    __syncthreads();
+  }
+  // (h + acc) * inv, or the resident micros' sum * inv, for element e / e..e+3
+  auto x1 = [&](int e) {
+    if constexpr (resident) return __fmul_rn(micro_sum1(mp, KR, e), inv);
+    const float g = widen(__ldcs(h + e));
+    return __fmul_rn(K > 1 ? __fadd_rn(g, __ldcs(a + e)) : g, inv);
+  };
+  auto x4 = [&](int e, float (&x)[4]) {
+    if constexpr (resident) {
+      micro_sum4_k<KR>(mp, e, x);
+    } else {
+      const uint2 hv = __ldcs(reinterpret_cast<const uint2*>(h + e));
+      x[0] = widen(static_cast<uint16_t>(hv.x & 0xFFFFu));
+      x[1] = widen(static_cast<uint16_t>(hv.x >> 16));
+      x[2] = widen(static_cast<uint16_t>(hv.y & 0xFFFFu));
+      x[3] = widen(static_cast<uint16_t>(hv.y >> 16));
+      if (K > 1) {
+        const float4 a4 = __ldcs(reinterpret_cast<const float4*>(a + e));
+        x[0] = __fadd_rn(x[0], a4.x);
+        x[1] = __fadd_rn(x[1], a4.y);
+        x[2] = __fadd_rn(x[2], a4.z);
+        x[3] = __fadd_rn(x[3], a4.w);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) x[i] = __fmul_rn(x[i], inv);
+  };
   // Vector path when the tensor side (h, acc) and the shard side (in, out)
   // share their 4-element alignment (the common case: BERT tensor sizes and
   // chunk lengths are multiples of 4): scalar head to the boundary, float4 /
-  // 4 x binary16 body, scalar tail. Caller slots are 16-byte aligned.
-  if (((tile.e0 - tile.s0) & 3) == 0 && (reinterpret_cast<uintptr_t>(tab.p[tile.t]) & 15) == 0) {
+  // 4 x binary16 body, scalar tail. Caller slots are 16-byte aligned (all K
+  // of them in resident mode, checked by bo_train_step).
+  if (((tile.e0 - tile.s0) & 3) == 0 && (resident || (reinterpret_cast<uintptr_t>(tab.p[tile.t]) & 15) == 0)) {
     const int head = min(static_cast<int>((4 - (tile.s0 & 3)) & 3), tile.len);
     const int nv = (tile.len - head) >> 2;
     auto one = [&](int e) {
-      const float g = widen(h[e]);
-      float p = __fmul_rn(K > 1 ? __fadd_rn(g, a[e]) : g, inv);
+      float p = x1(e);
       if (combine) p = __fadd_rn(from_wire(in[tile.s0 + e]), p);
       out[tile.s0 + e] = to_wire<W>(p);
     };
@@ -180,16 +213,6 @@ __global__ void __launch_bounds__(kThreads) k_hopx(const HopXTile* __restrict__ 
 #pragma unroll 4
     for (int q = threadIdx.x; q < nv; q += kThreads) {
       const int e = head + 4 * q;
-      const uint2 hv = __ldcs(reinterpret_cast<const uint2*>(h + e));
-      const float hg[4] = {widen(static_cast<uint16_t>(hv.x & 0xFFFFu)),
-                           widen(static_cast<uint16_t>(hv.x >> 16)),
-                           widen(static_cast<uint16_t>(hv.y & 0xFFFFu)),
-                           widen(static_cast<uint16_t>(hv.y >> 16))};
-      float av[4] = {0.f, 0.f, 0.f, 0.f};
-      if (K > 1) {
-        const float4 a4 = __ldcs(reinterpret_cast<const float4*>(a + e));
-        av[0] = a4.x; av[1] = a4.y; av[2] = a4.z; av[3] = a4.w;
-      }
       float iv[4] = {0.f, 0.f, 0.f, 0.f};
       if (combine) {
         if constexpr (sizeof(W) == 2) {
@@ -203,10 +226,12 @@ __global__ void __launch_bounds__(kThreads) k_hopx(const HopXTile* __restrict__ 
           iv[0] = w4.x; iv[1] = w4.y; iv[2] = w4.z; iv[3] = w4.w;
         }
       }
+      float xv[4];
+      x4(e, xv);
       W o[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        float p = __fmul_rn(K > 1 ? __fadd_rn(hg[i], av[i]) : hg[i], inv);
+        float p = xv[i];
         if (combine) p = __fadd_rn(iv[i], p);
         o[i] = to_wire<W>(p);
       }
@@ -226,11 +251,7 @@ __global__ void __launch_bounds__(kThreads) k_hopx(const HopXTile* __restrict__ 
 #pragma unroll
   for (int j = 0; j < kPer; ++j) {
     const int e = threadIdx.x + j * kThreads;
-    xv[j] = 0.0f;
-    if (e < tile.len) {
-      const float g = widen(__ldcs(h + e));
-      xv[j] = __fmul_rn(K > 1 ? __fadd_rn(g, __ldcs(a + e)) : g, inv);
-    }
+    xv[j] = e < tile.len ? x1(e) : 0.0f;
   }
 #pragma unroll
   for (int j = 0; j < kPer; ++j) {
@@ -501,15 +522,16 @@ __global__ void __launch_bounds__(kWarpTileCTA, kMinBlocks) k_p1w(const LambTile
   bool vec = true;
   if constexpr (kX) {
     const TensorDev d = A.td[t.t];
-    const int64_t e0 = t.w0 - d.flat_off;  // element offset inside the tensor
-    h = tab.p[t.t] + e0;
-    a = A.acc + d.acc_off + e0;
+    const int64_t e0t = t.w0 - d.flat_off;  // element offset of the tile inside its tensor
+    h = tab.p[t.t] + e0t;
+    a = A.acc + d.acc_off + e0t;
     inv = __fdiv_rn(1.0f, __fmul_rn(static_cast<float>(K), st->scale));
-    vec = ((e0 - t.s0) & 3) == 0 && (reinterpret_cast<uintptr_t>(tab.p[t.t]) & 7) == 0;
+    vec = ((e0t - t.s0) & 3) == 0 && (reinterpret_cast<uintptr_t>(tab.p[t.t]) & 7) == 0;
   }
-  auto grad = [&](float win, float hg, float ag) {
+  // xs: the flattened gradient before the unscale (h + acc)
+  auto grad = [&](float win, float xs) {
     if constexpr (kX) {
-      const float x = __fmul_rn(K > 1 ? __fadd_rn(hg, ag) : hg, inv);
+      const float x = __fmul_rn(xs, inv);
       if constexpr (kIn) {
         return __fmul_rn(from_wire(to_wire<W>(__fadd_rn(win, x))), A.invn);
       } else {
@@ -522,13 +544,13 @@ __global__ void __launch_bounds__(kWarpTileCTA, kMinBlocks) k_p1w(const LambTile
   double wn = 0.0, un = 0.0;
   bool bad = false;
   auto scalar = [&](int e) {
-    float hg = 0.0f, ag = 0.0f, win = 0.0f;
+    float xs = 0.0f, win = 0.0f;
     if constexpr (kX) {
-      hg = widen(h[e]);
-      if (K > 1) ag = a[e];
+      xs = widen(h[e]);
+      if (K > 1) xs = __fadd_rn(xs, a[e]);
     }
     if constexpr (kIn) win = from_wire(gin[e]);
-    const float gi = grad(win, hg, ag);
+    const float gi = grad(win, xs);
     bad |= !finite(gi);
     const float wi = wsh[e];
     const Moments o = lamb_elem(gi, wi, m[e], v[e], A.c, bcp);
@@ -584,14 +606,14 @@ __global__ void __launch_bounds__(kWarpTileCTA, kMinBlocks) k_p1w(const LambTile
           float ga[4];
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
-            float hg = 0.0f, ag = 0.0f, win = 0.0f;
+            float xs = 0.0f, win = 0.0f;
             if constexpr (kX) {
               const uint32_t hw = i < 2 ? hv[j].x : hv[j].y;
-              hg = widen(static_cast<uint16_t>(hw >> (16 * (i & 1))));
-              if (K > 1) ag = av[j][i];
+              xs = widen(static_cast<uint16_t>(hw >> (16 * (i & 1))));
+              if (K > 1) xs = __fadd_rn(xs, av[j][i]);
             }
             if constexpr (kIn) win = iv[j][i];
-            ga[i] = grad(win, hg, ag);
+            ga[i] = grad(win, xs);
             bad |= !finite(ga[i]);
           }
           const Lamb4 o = lamb_elem4(ga, wa, ma, va, A.c, bcp, ibc1, ibc2);
@@ -758,8 +780,21 @@ static void ring_reduce_scatter(bo_ctx* c, const PtrTable& tab, ncclDataType_t d
     const int t0 = qb[static_cast<size_t>(b0)], t1 = qb[static_cast<size_t>(b1)];
     if (t1 > t0) {
       StageTimer timer(c, BO_STAGE_FLAG, st);
-      k_hopx<W><<<t1 - t0, kThreads, 0, st>>>(c->d_hopx_tiles + t0, c->d_tensors, tab, c->acc, c->state, K,
-                                               in, out, combine);
+      auto go = [&](auto kern) {
+        kern<<<t1 - t0, kThreads, 0, st>>>(c->d_hopx_tiles + t0, c->d_tensors, tab, c->ms, c->acc, c->state, K,
+                                           in, out, combine);
+      };
+      switch (c->ms.K) {
+        case 0: go(k_hopx<W, 0>); break;
+        case 2: go(k_hopx<W, 2>); break;
+        case 3: go(k_hopx<W, 3>); break;
+        case 4: go(k_hopx<W, 4>); break;
+        case 5: go(k_hopx<W, 5>); break;
+        case 6: go(k_hopx<W, 6>); break;
+        case 7: go(k_hopx<W, 7>); break;
+        case 8: go(k_hopx<W, 8>); break;
+        default: fail(BO_ERR_INVALID_CONFIG, "resident micro count outside 2..8");
+      }
       check_launch(c, "k_hopx");
     }
   };
@@ -771,7 +806,11 @@ static void ring_reduce_scatter(bo_ctx* c, const PtrTable& tab, ncclDataType_t d
   // at world 4 (0.67 vs 0.62 ms), so the default fuses only at world 2 —
   // and never in the overlapped sync micro, where a staged last hop runs
   // under the caller's backward instead of inside the exposed LAMB.
-  const bool fuse_last = !c->force_unfused &&
+  // With the K micros resident (bo_train_step) the hops read 2K bytes per
+  // element instead of 6, and the staged last hop measured faster at world 2
+  // too (2.93 vs 3.13 ms per step): no fusion there either. Fusing needs the
+  // accumulator form of x, so the resident mode never fuses.
+  const bool fuse_last = !c->force_unfused && c->ms.K == 0 &&
                          (c->fuse_last_hop >= 0 ? c->fuse_last_hop != 0 : (N == 2 && !c->sync_open));
   hop(r, nullptr, a, 0);  // hop 0 payload: this rank's own chunk r (collective.cpp:178)
   const bool p2p = c->peer_wire[0][left] && !c->ring_via_nccl;

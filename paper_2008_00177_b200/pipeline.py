@@ -237,7 +237,8 @@ class GradPipeline:
 
     # -- introspection
     PATH_NAMES = {1: "one_rank_fused", 2: "one_rank_staged", 4: "ring_p2p", 8: "ring_sendrecv",
-                  16: "last_hop_fused", 32: "nccl_reduce_scatter", 64: "overlap"}
+                  16: "last_hop_fused", 32: "nccl_reduce_scatter", 64: "overlap",
+                  128: "resident_micros"}
 
     def path(self) -> list[str]:
         """Implementation the last sync micro ran (BO_PATH_* names)."""
@@ -327,12 +328,23 @@ class GradPipeline:
         return [int(t) for t in self.layout()[2]]
 
     def train_step(self, micro_grads) -> None:
-        """All K micro-batches of one optimizer step (the train_step analog)."""
+        """All K micro-batches of one optimizer step (DistributedTrainer::train_step,
+        trainer.cpp:217-373): micro_grads[k][p] is micro k's gradient of tensor p
+        (device pointer or CUDA tensor), resident until the step has run."""
         K = self.cfg.accumulation
         if len(micro_grads) != K:
             raise InvalidConfig("InvalidConfig: train_step expects exactly K micro batches")
-        for k, g in enumerate(micro_grads):
-            self.accumulate(k, g)
+        ptrs = []
+        for g in micro_grads:
+            if len(g) != self.spec.n_tensors:
+                raise ShapeMismatch(f"ShapeMismatch: {len(g)} gradients for "
+                                    f"{self.spec.n_tensors} parameters")
+            ptrs += [x if isinstance(x, int) else x.data_ptr() for x in g]
+        _lib.check(self.lib.bo_train_step(self.ctx, _ptr_array(ptrs)))
+
+    def train_step_ptr_array(self, arr) -> None:
+        """Fast path: a prebuilt ctypes array of the K x T pointers (make_ptr_array)."""
+        _lib.check(self.lib.bo_train_step(self.ctx, arr))
 
 
 # ---------------------------------------------------------------- operators

@@ -61,13 +61,15 @@ class GradBuffers:
 
 
 def run_pipeline(spec, cfg, params0, steps, grad_seed=1, spike_ppm=0, spike_exp=1, injections=(),
-                 rank=0, world=1, aligned=True, pipe=None, device=0, first_step=0, overlap=None):
+                 rank=0, world=1, aligned=True, pipe=None, device=0, first_step=0, overlap=None,
+                 resident=False):
     """Run optimizer steps first_step .. first_step+steps-1 (the step index
     seeds the synthetic gradients); returns (pipe, scale_used, found_inf).
 
     overlap: None (the sync micro through bo_accumulate) or a list of chunk
     sizes: the sync micro is then delivered through bo_sync_ready in the
-    layout's ready order, in chunks of these sizes (cycled)."""
+    layout's ready order, in chunks of these sizes (cycled).
+    resident: all K micros filled first, then one bo_train_step."""
     if pipe is None:
         pipe = GradPipeline(spec, cfg, device=device, rank=rank, world=world)
         pipe.load_params(np.asarray(params0, np.float32))
@@ -84,7 +86,10 @@ def run_pipeline(spec, cfg, params0, steps, grad_seed=1, spike_ppm=0, spike_exp=
                 if st == step and r == rank and mk == k:
                     gb.inject(k, idx, bits)
             torch.cuda.synchronize()
-            if overlap is None or k < K - 1:
+            if resident:
+                if k == K - 1:
+                    pipe.train_step(gb.ptrs)
+            elif overlap is None or k < K - 1:
                 pipe.accumulate(k, gb.ptrs[k])
             else:
                 order = pipe.ready_order()

@@ -54,6 +54,10 @@ def main():
 
     case = args.case
     overlap = None
+    resident = False
+    if case.endswith("_resident"):
+        resident = True
+        case = case[: -len("_resident")]
     if case.endswith("_overlap"):
         # the sync micro delivered through bo_sync_ready in ragged chunks,
         # with communication groups of ~20k elements (several per step)
@@ -86,7 +90,7 @@ def main():
     pipe.comm_init_torch()
     pipe, su, fi = run_pipeline(spec, cfg, None, args.steps, grad_seed=9, spike_ppm=ppm,
                                 spike_exp=sexp, injections=inj, rank=rank, world=world, pipe=pipe,
-                                device=local, overlap=overlap)
+                                device=local, overlap=overlap, resident=resident)
     w = pipe.read_params()
     m = np.zeros(P, np.float32)
     v = np.zeros(P, np.float32)

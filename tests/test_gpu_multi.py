@@ -46,7 +46,8 @@ def run_case(case, nproc, model="tiny", steps=4):
 
 @pytest.mark.parametrize("case", ["ring16", "ring32", "nccl32", "ring16_1bucket",
                                   "ring16_tinybuckets", "ring16_unfused", "ring32_unfused",
-                                  "ring16_overlap", "ring32_unfused_overlap", "nccl32_overlap"])
+                                  "ring16_overlap", "ring32_unfused_overlap", "nccl32_overlap",
+                                  "ring16_resident", "ring32_unfused_resident"])
 def test_two_gpus(case):
     if _ngpu() < 2:
         pytest.skip("needs 2 GPUs")
@@ -55,11 +56,13 @@ def test_two_gpus(case):
         assert res["m_bit_exact"] and res["v_bit_exact"]
         assert "ring_p2p" in res["path"]
         # world 2 runs the last hop inside LAMB phase 1 unless BO_UNFUSED is set
-        # (and never in the overlapped sync micro)
-        assert ("last_hop_fused" in res["path"]) == ("_unfused" not in case and "_overlap" not in case)
+        # (and never in the overlapped sync micro or with resident micros)
+        assert ("last_hop_fused" in res["path"]) == \
+            ("_unfused" not in case and "_overlap" not in case and "_resident" not in case)
     else:
         assert "nccl_reduce_scatter" in res["path"]
     assert ("overlap" in res["path"]) == case.endswith("_overlap")
+    assert ("resident_micros" in res["path"]) == case.endswith("_resident")
 
 
 @pytest.mark.parametrize("model", ["ragged", "small"])
@@ -89,4 +92,7 @@ def test_more_gpus(n):
     res = run_case("ring16_fused", n)
     assert res["m_bit_exact"] and res["v_bit_exact"]
     assert "last_hop_fused" in res["path"]
+    res = run_case("ring16_resident", n)
+    assert res["m_bit_exact"] and res["v_bit_exact"]
+    assert res["path"] == ["ring_p2p", "resident_micros"]
     run_case("nccl32", n)

@@ -263,3 +263,33 @@ def test_watchdog_wait(torch_cuda, oracle):
         pipe.wait(20)
     pipe.wait(-1)
     pipe.wait(0)  # nothing pending: immediate success
+
+
+@pytest.mark.parametrize("K", [2, 3, 4])
+@pytest.mark.parametrize("aligned", [True, False])
+def test_train_step_resident_micros_bit_identical(torch_cuda, oracle, K, aligned):
+    """bo_train_step (all K micros resident, no accumulator) gives the same
+    bits as K bo_accumulate calls, overflow steps included; unaligned slots
+    take the per-micro path inside the call."""
+    from paper_2008_00177_b200.model_spec import BERT_TINY, bert_spec
+    from paper_2008_00177_b200.pipeline import LambConfig, ScalerConfig, TrainerConfig
+    from tests.harness import run_pipeline
+
+    spec = bert_spec(BERT_TINY)
+    P = spec.param_count()
+    p0 = oracle.build_params(spec, 8)
+    cfg = TrainerConfig(LambConfig(lr=1e-2), K, 4096, False, 0,
+                        ScalerConfig(init_scale=2.0 ** 14, growth_interval=3))
+    inj = [(2, 0, K - 2, P // 3, 0x7E00), (4, 0, K - 1, 11, 0xFC00)]
+    base, su0, fi0 = run_pipeline(spec, cfg, p0, steps=6, spike_ppm=3, spike_exp=3, injections=inj,
+                                  aligned=aligned)
+    res, su1, fi1 = run_pipeline(spec, cfg, p0, steps=6, spike_ppm=3, spike_exp=3, injections=inj,
+                                 aligned=aligned, resident=True)
+    assert ("resident_micros" in res.path()) == aligned
+    assert np.array_equal(su0, su1) and np.array_equal(fi0, fi1) and fi0.sum() >= 2
+    assert np.array_equal(base.read_params().view(np.uint32), res.read_params().view(np.uint32))
+    m0, v0, m1, v1 = (np.zeros(P, np.float32) for _ in range(4))
+    base.read_moments(m0, v0)
+    res.read_moments(m1, v1)
+    assert np.array_equal(m0.view(np.uint32), m1.view(np.uint32))
+    assert np.array_equal(v0.view(np.uint32), v1.view(np.uint32))

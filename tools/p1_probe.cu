@@ -197,11 +197,11 @@ int main(int argc, char** argv) {
     k_p1w<uint16_t, true, false, 1, 4><<<wgrid, kWarpTileCTA>>>(c->d_lamb_tiles, c->n_lamb_tiles, tab, lin, A);
   });
   time("k_hopx<f16> (own chunk) local", 10 * S, 0, [&] {
-    k_hopx<uint16_t><<<t1 - t0, kThreads>>>(c->d_hopx_tiles + t0, c->d_tensors, tab, c->acc, c->state,
+    k_hopx<uint16_t, 0><<<t1 - t0, kThreads>>>(c->d_hopx_tiles + t0, c->d_tensors, tab, MicroSrc{nullptr, 0, 0}, c->acc, c->state,
                                             4, lin, static_cast<uint16_t*>(c->wire[0]), 1);
   });
   time("k_hopx<f16> (own chunk) peer", 8 * S, 2 * S, [&] {
-    k_hopx<uint16_t><<<t1 - t0, kThreads>>>(c->d_hopx_tiles + t0, c->d_tensors, tab, c->acc, c->state,
+    k_hopx<uint16_t, 0><<<t1 - t0, kThreads>>>(c->d_hopx_tiles + t0, c->d_tensors, tab, MicroSrc{nullptr, 0, 0}, c->acc, c->state,
                                             4, pin, static_cast<uint16_t*>(c->wire[0]), 1);
   });
   time("k_shard_p2_push (peer replicas)", 16 * S, 4.0 * (world - 1) * S, [&] {
