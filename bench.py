@@ -352,7 +352,7 @@ def main_b200(args):
     dom = max((n for n in stages if "bytes" in stages[n]),
               key=lambda n: stages[n]["ms"] * stages[n]["launches_per_step"])
     kernel_names = {"accumulate": "k_accumulate", "finalize": "k_finalize",
-                    "lamb_norms": "k_lamb_p1" if world == 1 else "k_p1w",
+                    "lamb_norms": ("k_lamb_p1r" if resident else "k_lamb_p1") if world == 1 else "k_p1w",
                     "lamb_update": "k_lamb_p2" if world == 1 else "k_shard_p2_push",
                     "hop_kernels": "k_hopx"}
     st_dom = stages[dom]
