@@ -187,34 +187,6 @@ __device__ __forceinline__ void micro_sum4_k(const uint16_t* const* p, int e, fl
   }
 }
 
-// Elements e..e+3 (8-byte aligned in every micro): all K loads are issued
-// before the first addition.
-__device__ __forceinline__ void micro_sum4(const uint16_t* const* p, int K, int e, float (&o)[4]) {
-  uint2 x[kMaxResident];
-#pragma unroll
-  for (int k = 0; k < kMaxResident; ++k) {
-    if (k < K) x[k] = __ldcs(reinterpret_cast<const uint2*>(p[k] + e));
-  }
-  float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-  uint2 live = x[0];
-#pragma unroll
-  for (int k = 0; k < kMaxResident; ++k) {
-    if (k + 1 < K) {
-      float f[4];
-      widen4(x[k], f);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) acc[i] = __fadd_rn(acc[i], f[i]);
-    } else if (k + 1 == K) {
-      live = x[k];
-    }
-  }
-  widen4(live, o);
-  if (K > 1) {
-#pragma unroll
-    for (int i = 0; i < 4; ++i) o[i] = __fadd_rn(o[i], acc[i]);
-  }
-}
-
 // Streaming accesses with explicit L2 eviction priority (no L1 allocation):
 // evict_first for data read once, evict_last for what the next pass re-reads.
 __device__ __forceinline__ uint64_t policy_evict_first() {

@@ -47,7 +47,7 @@ def run_case(case, nproc, model="tiny", steps=4):
 @pytest.mark.parametrize("case", ["ring16", "ring32", "nccl32", "ring16_1bucket",
                                   "ring16_tinybuckets", "ring16_unfused", "ring32_unfused",
                                   "ring16_overlap", "ring32_unfused_overlap", "nccl32_overlap",
-                                  "ring16_resident", "ring32_unfused_resident"])
+                                  "ring16_resident", "ring32_unfused_resident", "nccl32_resident"])
 def test_two_gpus(case):
     if _ngpu() < 2:
         pytest.skip("needs 2 GPUs")
@@ -62,7 +62,9 @@ def test_two_gpus(case):
     else:
         assert "nccl_reduce_scatter" in res["path"]
     assert ("overlap" in res["path"]) == case.endswith("_overlap")
-    assert ("resident_micros" in res["path"]) == case.endswith("_resident")
+    # bo_train_step reads the resident micros on the ring; the NCCL wire takes
+    # the per-micro path inside the call (same results)
+    assert ("resident_micros" in res["path"]) == (case.endswith("_resident") and case.startswith("ring"))
 
 
 @pytest.mark.parametrize("model", ["ragged", "small"])
