@@ -824,6 +824,7 @@ bo_status bo_import_state(bo_ctx* c, const void* blob, uint64_t nbytes) {
   BO_CUDA(cudaStreamSynchronize(c->stream));
   grow_bc_table(c, st.lamb_step + 2);
   c->calls = std::max<int64_t>(c->calls, st.steps);
+  c->next_micro = 0;
   BO_GUARD_END
 }
 
@@ -893,10 +894,16 @@ bo_status bo_accumulate(bo_ctx* c, int32_t micro, const uint16_t* const* grads) 
     aligned &= (reinterpret_cast<uintptr_t>(grads[t]) & 15u) == 0;
   }
   if (c->sync_open) fail(BO_ERR_PROTOCOL, "an overlapped sync micro (bo_sync_ready) is in progress");
+  if (micro != c->next_micro) {
+    fail(BO_ERR_PROTOCOL, "micro " + std::to_string(micro) + " out of order (expected " +
+                              std::to_string(c->next_micro) + ")");
+  }
   if (micro + 1 < K) {
     launch_accumulate(c, micro, tab, aligned);
+    c->next_micro = micro + 1;
     return BO_OK;
   }
+  c->next_micro = 0;
   grow_bc_table(c, c->calls + 2);
   c->path = 0;
   if (c->world == 1 && aligned && !c->force_unfused) {
@@ -918,6 +925,7 @@ bo_status bo_train_step(bo_ctx* c, const uint16_t* const* grads) {
   if (!c || !grads) fail(BO_ERR_INVALID_CONFIG, "null argument");
   if (c->world > 1 && !c->comm) fail(BO_ERR_INVALID_CONFIG, "bo_comm_init has not run");
   if (c->sync_open) fail(BO_ERR_PROTOCOL, "an overlapped sync micro (bo_sync_ready) is in progress");
+  if (c->next_micro != 0) fail(BO_ERR_PROTOCOL, "bo_train_step inside a step fed by bo_accumulate");
   const int K = c->cfg.accumulation, T = c->L.T;
   bool aligned = true;
   for (int i = 0; i < K * T; ++i) {
@@ -974,6 +982,10 @@ bo_status bo_sync_ready(bo_ctx* c, int32_t n, const int32_t* tensors, const uint
   if (c->world > 1 && !c->comm) fail(BO_ERR_INVALID_CONFIG, "bo_comm_init has not run");
   const Layout& L = c->L;
   if (!c->sync_open) {
+    if (c->next_micro != c->cfg.accumulation - 1) {
+      fail(BO_ERR_PROTOCOL, "bo_sync_ready before micros 0.." + std::to_string(c->cfg.accumulation - 2) +
+                                " went through bo_accumulate");
+    }
     c->sync_open = true;
     c->n_delivered = 0;
     c->next_group = 0;
@@ -1018,6 +1030,7 @@ bo_status bo_sync_ready(bo_ctx* c, int32_t n, const int32_t* tensors, const uint
   if (c->n_delivered < L.T) return BO_OK;
   // every gradient delivered: the rest of the step on the caller's stream
   c->sync_open = false;
+  c->next_micro = 0;
   grow_bc_table(c, c->calls + 2);
   if (c->world == 1) {
     if (c->sync_aligned && !c->force_unfused) {

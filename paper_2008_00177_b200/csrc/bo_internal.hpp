@@ -238,6 +238,7 @@ struct bo_ctx {
   double* bc_table = nullptr;     // [bc_cap][4] (bc1, bc2, 1/bc1, 1/bc2) for steps 1..cap
   int64_t bc_cap = 0;
   int64_t calls = 0;              // sync micros issued (upper bound of lamb_step)
+  int next_micro = 0;             // the micro bo_accumulate expects next (0..K-1)
   uint64_t device_bytes = 0;
 
   bo::LambConsts lamb{};

@@ -293,3 +293,27 @@ def test_train_step_resident_micros_bit_identical(torch_cuda, oracle, K, aligned
     res.read_moments(m1, v1)
     assert np.array_equal(m0.view(np.uint32), m1.view(np.uint32))
     assert np.array_equal(v0.view(np.uint32), v1.view(np.uint32))
+
+
+def test_micro_order_protocol(torch_cuda, oracle):
+    """Micros must arrive 0..K-1; bo_train_step cannot start inside a step fed
+    by bo_accumulate (ProtocolError, the reference's protocol-violation class)."""
+    from paper_2008_00177_b200.errors import ProtocolError
+    from paper_2008_00177_b200.model_spec import BERT_TINY, bert_spec
+    from paper_2008_00177_b200.pipeline import GradPipeline, LambConfig, ScalerConfig, TrainerConfig
+    from tests.harness import GradBuffers
+
+    spec = bert_spec(BERT_TINY)
+    pipe = GradPipeline(spec, TrainerConfig(LambConfig(), 3, 4096, False, 0, ScalerConfig()))
+    pipe.load_params(oracle.build_params(spec, 1))
+    gb = GradBuffers(spec, 3, 0, True)
+    with pytest.raises(ProtocolError):
+        pipe.accumulate(1, gb.ptrs[1])
+    pipe.accumulate(0, gb.ptrs[0])
+    with pytest.raises(ProtocolError):
+        pipe.train_step(gb.ptrs)
+    pipe.accumulate(1, gb.ptrs[1])
+    pipe.accumulate(2, gb.ptrs[2])
+    pipe.train_step(gb.ptrs)  # a fresh step
+    pipe.synchronize()
+    assert pipe.status().lamb_step == 2
