@@ -145,8 +145,10 @@ def test_bert_base_config1_matches_oracle(torch_cuda, oracle):
 
 
 @pytest.mark.slow
-def test_bert_large_config2_matches_oracle(torch_cuda, oracle):
-    """Config 2 at full size: BERT-large (336M), K=4, one optimizer step."""
+@pytest.mark.parametrize("resident", [False, True])
+def test_bert_large_config2_matches_oracle(torch_cuda, oracle, resident):
+    """Config 2 at full size: BERT-large (336M), K=4, one optimizer step,
+    through the per-micro API and through bo_train_step."""
     from oracle.oracle import LambConfig as OL, ScalerConfig as OS
     from paper_2008_00177_b200.model_spec import BERT_LARGE, bert_spec
     from paper_2008_00177_b200.pipeline import LambConfig, ScalerConfig, TrainerConfig
@@ -155,7 +157,8 @@ def test_bert_large_config2_matches_oracle(torch_cuda, oracle):
     spec = bert_spec(BERT_LARGE)
     p0 = oracle.build_params(spec, 1)
     cfg = TrainerConfig(LambConfig(lr=1e-4), 4, 4 << 20, False, 0, ScalerConfig())
-    pipe, su, fi = run_pipeline(spec, cfg, p0, steps=1)
+    pipe, su, fi = run_pipeline(spec, cfg, p0, steps=1, resident=resident)
+    assert ("resident_micros" in pipe.path()) == resident
     ref = oracle.train(spec, p0, 1, 4, 4 << 20, False, OL(lr=1e-4), OS(), 1)
     _compare(pipe, ref, su, fi)
 
