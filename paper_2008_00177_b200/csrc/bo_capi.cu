@@ -1,5 +1,6 @@
-// C ABI of the pipeline context: creation, layout, communication, state, and
-// the hot-path entry point bo_accumulate (see include/bertopt_b200.h).
+// C ABI of the pipeline context: creation, layout, communication, state,
+// profiling (see include/bertopt_b200.h); the hot-path entry points are in
+// bo_step.cu, the work tables in bo_tables.cu.
 #include <algorithm>
 #include <chrono>
 #include <thread>
@@ -27,176 +28,6 @@ void* dev_alloc(bo_ctx* c, size_t bytes) {
   c->allocations.push_back(p);
   c->device_bytes += bytes;
   return p;
-}
-
-template <typename T>
-static T* upload(bo_ctx* c, const std::vector<T>& v) {
-  T* d = static_cast<T*>(dev_alloc(c, v.size() * sizeof(T)));
-  if (!v.empty()) {
-    BO_CUDA(cudaMemcpyAsync(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, c->stream));
-  }
-  return d;
-}
-
-// Work tables: accumulate/finalize tiles over tensors, LAMB tiles over this
-// rank's shard (split at tensor boundaries), ring tiles over the shard.
-void upload_tables(bo_ctx* c) {
-  const Layout& L = c->L;
-  std::vector<TensorDev> td(static_cast<size_t>(L.T));
-  std::vector<AccTile> acc_tiles;
-  for (int t = 0; t < L.T; ++t) {
-    td[static_cast<size_t>(t)] = TensorDev{L.acc_off[static_cast<size_t>(t)], L.flat_off[static_cast<size_t>(t)]};
-    for (int64_t e = 0; e < L.numel[static_cast<size_t>(t)]; e += kTileElems) {
-      const int64_t len = std::min<int64_t>(kTileElems, L.numel[static_cast<size_t>(t)] - e);
-      acc_tiles.push_back(AccTile{t, static_cast<int32_t>(len), e});
-    }
-  }
-  std::vector<LambTile> lamb_tiles;
-  std::vector<int> tile_begin(static_cast<size_t>(L.T) + 1, 0);
-  std::vector<std::vector<LambTile>> per_tensor(static_cast<size_t>(L.T));
-  const int q = L.own;  // owned chunk
-  for (int b = 0; b < L.B; ++b) {
-    const int64_t cb = L.chunk[static_cast<size_t>(b)];
-    const int64_t lo = q * cb;
-    const int64_t hi = std::min<int64_t>((q + 1) * cb, L.elems[static_cast<size_t>(b)]);
-    for (int p : L.buckets[static_cast<size_t>(b)]) {
-      const int64_t t0 = L.offset_of[static_cast<size_t>(p)];
-      const int64_t t1 = t0 + L.numel[static_cast<size_t>(p)];
-      const int64_t a = std::max(lo, t0), z = std::min(hi, t1);
-      for (int64_t e = a; e < z; e += kTileElems) {
-        const int64_t len = std::min<int64_t>(kTileElems, z - e);
-        per_tensor[static_cast<size_t>(p)].push_back(
-            LambTile{L.shard_pos(b, p, e), L.flat_pos(b, p, e), static_cast<int32_t>(len), p});
-      }
-    }
-  }
-  // Tiles grouped per tensor so each tensor's partials are contiguous; within
-  // a tensor, shard order.
-  for (int t = 0; t < L.T; ++t) {
-    tile_begin[static_cast<size_t>(t)] = static_cast<int>(lamb_tiles.size());
-    for (const LambTile& lt : per_tensor[static_cast<size_t>(t)]) lamb_tiles.push_back(lt);
-  }
-  tile_begin[static_cast<size_t>(L.T)] = static_cast<int>(lamb_tiles.size());
-
-  if (c->world == 1) {
-    // Single-rank LAMB (bo_fused.cu): tiles of <= kTileElems elements of one
-    // tensor, model order, in the aligned tensor layout; per-tensor tile
-    // ranges for the fixed-order norm reduction.
-    std::vector<FusedTile> ft;
-    std::vector<int> ttiles(static_cast<size_t>(L.T) + 1);
-    for (int t = 0; t < L.T; ++t) {
-      const int64_t n = L.numel[static_cast<size_t>(t)];
-      ttiles[static_cast<size_t>(t)] = static_cast<int>(ft.size());
-      for (int64_t e = 0; e < n; e += kTileElems) {
-        ft.push_back(FusedTile{L.acc_off[static_cast<size_t>(t)] + e, e,
-                               static_cast<int32_t>(std::min<int64_t>(kTileElems, n - e)), t});
-      }
-    }
-    ttiles[static_cast<size_t>(L.T)] = static_cast<int>(ft.size());
-    c->d_fused_tiles = upload(c, ft);
-    c->n_fused_tiles = static_cast<int>(ft.size());
-    c->d_fused_tensor_tiles = upload(c, ttiles);
-  }
-  if (c->world > 1) {
-    // Ring hops with the finalize fused in: for every chunk index q, the
-    // valid (non-padding) elements of chunk q of every bucket, split at tensor
-    // boundaries, in shard order.
-    std::vector<HopXTile> hx;
-    c->hopx_begin.assign(static_cast<size_t>(c->world) + 1, 0);
-    c->hopx_bucket_begin.assign(static_cast<size_t>(c->world), std::vector<int>(static_cast<size_t>(L.B) + 1, 0));
-    for (int qq = 0; qq < c->world; ++qq) {
-      c->hopx_begin[static_cast<size_t>(qq)] = static_cast<int>(hx.size());
-      for (int b = 0; b < L.B; ++b) {
-        c->hopx_bucket_begin[static_cast<size_t>(qq)][static_cast<size_t>(b)] = static_cast<int>(hx.size());
-        const int64_t cb = L.chunk[static_cast<size_t>(b)];
-        const int64_t lo = qq * cb;
-        const int64_t hi = std::min<int64_t>((qq + 1) * cb, L.elems[static_cast<size_t>(b)]);
-        for (int p : L.buckets[static_cast<size_t>(b)]) {
-          const int64_t t0 = L.offset_of[static_cast<size_t>(p)];
-          const int64_t a = std::max(lo, t0), z = std::min(hi, t0 + L.numel[static_cast<size_t>(p)]);
-          for (int64_t e = a; e < z; e += kTileElems) {
-            hx.push_back(HopXTile{L.shoff[static_cast<size_t>(b)] + (e - lo), e - t0,
-                                  static_cast<int32_t>(std::min<int64_t>(kTileElems, z - e)), p});
-          }
-        }
-      }
-      c->hopx_bucket_begin[static_cast<size_t>(qq)][static_cast<size_t>(L.B)] = static_cast<int>(hx.size());
-    }
-    c->hopx_begin[static_cast<size_t>(c->world)] = static_cast<int>(hx.size());
-    c->d_hopx_tiles = upload(c, hx);
-
-    // Communication groups for the overlapped sync micro: consecutive buckets
-    // (layout order = gradient-ready order) merged up to >= BO_COMM_GROUP_ELEMS
-    // elements (default 16 Mi = 64 MiB of fp32 gradient), so every group costs
-    // N - 1 hop barriers; a pure function of the layout and the environment,
-    // which must therefore match across ranks (it is part of the layout hash).
-    int64_t group_elems = 16ll << 20;
-    if (const char* e = std::getenv("BO_COMM_GROUP_ELEMS")) {
-      group_elems = std::max<int64_t>(1, std::atoll(e));
-    }
-    c->comm_groups.clear();
-    c->group_of_bucket.assign(static_cast<size_t>(L.B), 0);
-    std::vector<AccTile> gacc;
-    std::vector<int> first_acc_tile(static_cast<size_t>(L.T) + 1, 0);
-    for (int t = 0, i = 0; t < L.T; ++t) {
-      first_acc_tile[static_cast<size_t>(t)] = i;
-      i += static_cast<int>((L.numel[static_cast<size_t>(t)] + kTileElems - 1) / kTileElems);
-    }
-    int b0 = 0;
-    int64_t n = 0;
-    for (int b = 0; b < L.B; ++b) {
-      n += L.elems[static_cast<size_t>(b)];
-      if (n >= group_elems || b == L.B - 1) {
-        bo_ctx::CommGroup g{b0, b + 1, 0, static_cast<int>(gacc.size()), 0};
-        for (int bb = b0; bb <= b; ++bb) {
-          c->group_of_bucket[static_cast<size_t>(bb)] = static_cast<int>(c->comm_groups.size());
-          for (int p : L.buckets[static_cast<size_t>(bb)]) {
-            g.pending0 += 1;
-            const int64_t nt = (L.numel[static_cast<size_t>(p)] + kTileElems - 1) / kTileElems;
-            for (int64_t k = 0; k < nt; ++k) gacc.push_back(acc_tiles[static_cast<size_t>(first_acc_tile[static_cast<size_t>(p)] + k)]);
-          }
-        }
-        g.acc1 = static_cast<int>(gacc.size());
-        c->comm_groups.push_back(g);
-        b0 = b + 1;
-        n = 0;
-      }
-    }
-    c->d_group_acc_tiles = upload(c, gacc);
-  }
-  c->d_tensors = upload(c, td);
-  c->d_acc_tiles = upload(c, acc_tiles);
-  c->n_acc_tiles = static_cast<int>(acc_tiles.size());
-  c->d_lamb_tiles = upload(c, lamb_tiles);
-  c->n_lamb_tiles = static_cast<int>(lamb_tiles.size());
-  c->d_tensor_tile_begin = upload(c, tile_begin);
-}
-
-// Bias corrections bc_t = 1 - pow(double(beta), double(t)) evaluated on the
-// host with the same libm the reference uses (lamb.cpp:158-161), with their
-// reciprocals; the device indexes the table by its own step counter.
-void grow_bc_table(bo_ctx* c, int64_t need) {
-  if (need <= c->bc_cap) return;
-  int64_t cap = std::max<int64_t>(4096, c->bc_cap * 2);
-  while (cap < need) cap *= 2;
-  std::vector<double> tab(static_cast<size_t>(cap) * 4);
-  for (int64_t i = 0; i < cap; ++i) {
-    const double t = static_cast<double>(i + 1);
-    const double bc1 = 1.0 - std::pow(static_cast<double>(c->cfg.lamb.beta1), t);
-    const double bc2 = 1.0 - std::pow(static_cast<double>(c->cfg.lamb.beta2), t);
-    tab[static_cast<size_t>(4 * i)] = bc1;
-    tab[static_cast<size_t>(4 * i + 1)] = bc2;
-    tab[static_cast<size_t>(4 * i + 2)] = 1.0 / bc1;
-    tab[static_cast<size_t>(4 * i + 3)] = 1.0 / bc2;
-  }
-  double* d = nullptr;
-  BO_CUDA(cudaMalloc(&d, tab.size() * sizeof(double)));
-  BO_CUDA(cudaMemcpyAsync(d, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-  // The old table may still be read by queued kernels: keep it alive.
-  if (c->bc_table) c->allocations.push_back(c->bc_table);
-  BO_CUDA(cudaStreamSynchronize(c->stream));  // tab is pageable host memory
-  c->bc_table = d;
-  c->bc_cap = cap;
 }
 
 static cudaEvent_t take_event(bo_ctx* c) {
@@ -328,19 +159,6 @@ static void for_owned(const Layout& L, F&& f) {
 }  // namespace bo
 
 using namespace bo;
-
-#define BO_GUARD_BEGIN try {
-#define BO_GUARD_END                          \
-  }                                           \
-  catch (const Failure& f) {                  \
-    set_thread_error(f.msg);                  \
-    return f.code;                            \
-  }                                           \
-  catch (const std::exception& e) {           \
-    set_thread_error(e.what());               \
-    return BO_ERR_CUDA;                       \
-  }                                           \
-  return BO_OK;
 
 extern "C" {
 
@@ -879,176 +697,5 @@ bo_status bo_profile_read(bo_ctx* c, double* stage_ms, int64_t* stage_count, int
 int64_t bo_launch_count(const bo_ctx* c) { return c ? c->launches : 0; }
 
 int32_t bo_path_flags(const bo_ctx* c) { return c ? c->path : 0; }
-
-bo_status bo_accumulate(bo_ctx* c, int32_t micro, const uint16_t* const* grads) {
-  BO_GUARD_BEGIN
-  if (!c || !grads) fail(BO_ERR_INVALID_CONFIG, "null argument");
-  const int K = c->cfg.accumulation;
-  if (micro < 0 || micro >= K) fail(BO_ERR_INVALID_CONFIG, "micro index outside [0, K)");
-  if (c->world > 1 && !c->comm) fail(BO_ERR_INVALID_CONFIG, "bo_comm_init has not run");
-  PtrTable tab;
-  bool aligned = true;
-  for (int t = 0; t < c->L.T; ++t) {
-    tab.p[t] = grads[t];
-    if (!grads[t]) fail(BO_ERR_SHAPE_MISMATCH, "null gradient for tensor " + std::to_string(t));
-    aligned &= (reinterpret_cast<uintptr_t>(grads[t]) & 15u) == 0;
-  }
-  if (c->sync_open) fail(BO_ERR_PROTOCOL, "an overlapped sync micro (bo_sync_ready) is in progress");
-  if (micro != c->next_micro) {
-    fail(BO_ERR_PROTOCOL, "micro " + std::to_string(micro) + " out of order (expected " +
-                              std::to_string(c->next_micro) + ")");
-  }
-  if (micro + 1 < K) {
-    launch_accumulate(c, micro, tab, aligned);
-    c->next_micro = micro + 1;
-    return BO_OK;
-  }
-  c->next_micro = 0;
-  grow_bc_table(c, c->calls + 2);
-  c->path = 0;
-  if (c->world == 1 && aligned && !c->force_unfused) {
-    c->path = BO_PATH_ONE_RANK_FUSED;
-    run_fused_single_rank(c, tab);
-  } else {
-    if (c->world == 1) c->path = BO_PATH_ONE_RANK_STAGED;
-    // the ring fuses flatten_param into its hops; NCCL needs the fusion buffer
-    if (c->world == 1 || c->algo == BO_REDUCE_NCCL) launch_finalize(c, tab);
-    run_reduce(c, tab);
-    run_lamb(c, tab);  // world > 1: includes the fused parameter all-gather (IPC push)
-  }
-  c->calls += 1;
-  BO_GUARD_END
-}
-
-bo_status bo_train_step(bo_ctx* c, const uint16_t* const* grads) {
-  BO_GUARD_BEGIN
-  if (!c || !grads) fail(BO_ERR_INVALID_CONFIG, "null argument");
-  if (c->world > 1 && !c->comm) fail(BO_ERR_INVALID_CONFIG, "bo_comm_init has not run");
-  if (c->sync_open) fail(BO_ERR_PROTOCOL, "an overlapped sync micro (bo_sync_ready) is in progress");
-  if (c->next_micro != 0) fail(BO_ERR_PROTOCOL, "bo_train_step inside a step fed by bo_accumulate");
-  const int K = c->cfg.accumulation, T = c->L.T;
-  bool aligned = true;
-  for (int i = 0; i < K * T; ++i) {
-    if (!grads[i]) fail(BO_ERR_SHAPE_MISMATCH, "null gradient for micro " + std::to_string(i / T) +
-                                                   ", tensor " + std::to_string(i % T));
-    aligned &= (reinterpret_cast<uintptr_t>(grads[i]) & 15u) == 0;
-  }
-  // The resident-micro kernels read all K gradient sets in the sync pass
-  // (no accumulator round trips): one rank's fused path and the ring. Other
-  // configurations (NCCL wire, unaligned slots, K == 1, K > 8) take the
-  // per-micro path; the results are identical either way.
-  const bool resident = K > 1 && K <= kMaxResident && aligned &&
-                        (c->world == 1 ? !c->force_unfused : c->algo == BO_REDUCE_RING);
-  if (!resident) {
-    for (int k = 0; k < K; ++k) {
-      const bo_status st = bo_accumulate(c, k, grads + static_cast<size_t>(k) * T);
-      if (st != BO_OK) return st;
-    }
-    return BO_OK;
-  }
-  if (c->micro_tab_cap < K * T) {
-    c->d_micro_tab = static_cast<const uint16_t**>(dev_alloc(c, static_cast<size_t>(K) * T * sizeof(void*)));
-    c->micro_tab_cap = K * T;
-  }
-  // pageable source: staged by the driver before the call returns; ordered
-  // on the stream after the previous step's kernels that read the table
-  BO_CUDA(cudaMemcpyAsync(c->d_micro_tab, grads, static_cast<size_t>(K) * T * sizeof(void*),
-                          cudaMemcpyHostToDevice, c->stream));
-  PtrTable tab;
-  for (int t = 0; t < T; ++t) tab.p[t] = grads[static_cast<size_t>(K - 1) * T + t];  // the live micro
-  grow_bc_table(c, c->calls + 2);
-  c->ms = MicroSrc{c->d_micro_tab, K, T};
-  c->path = BO_PATH_RESIDENT;
-  try {
-    if (c->world == 1) {
-      c->path |= BO_PATH_ONE_RANK_FUSED;
-      run_fused_single_rank(c, tab, c->ms);
-    } else {
-      run_reduce(c, tab);
-      run_lamb(c, tab);
-    }
-  } catch (...) {
-    c->ms = MicroSrc{nullptr, 0, 0};
-    throw;
-  }
-  c->ms = MicroSrc{nullptr, 0, 0};
-  c->calls += 1;
-  BO_GUARD_END
-}
-
-bo_status bo_sync_ready(bo_ctx* c, int32_t n, const int32_t* tensors, const uint16_t* const* grads) {
-  BO_GUARD_BEGIN
-  if (!c || (n > 0 && (!tensors || !grads))) fail(BO_ERR_INVALID_CONFIG, "null argument");
-  if (c->world > 1 && !c->comm) fail(BO_ERR_INVALID_CONFIG, "bo_comm_init has not run");
-  const Layout& L = c->L;
-  if (!c->sync_open) {
-    if (c->next_micro != c->cfg.accumulation - 1) {
-      fail(BO_ERR_PROTOCOL, "bo_sync_ready before micros 0.." + std::to_string(c->cfg.accumulation - 2) +
-                                " went through bo_accumulate");
-    }
-    c->sync_open = true;
-    c->n_delivered = 0;
-    c->next_group = 0;
-    c->sync_aligned = true;
-    std::fill(c->delivered.begin(), c->delivered.end(), 0);
-    c->group_pending.clear();
-    for (const auto& g : c->comm_groups) c->group_pending.push_back(g.pending0);
-    c->path = BO_PATH_OVERLAP;
-    c->ring_last_in = nullptr;
-    c->ring_result = nullptr;
-  }
-  for (int i = 0; i < n; ++i) {
-    const int t = tensors[i];
-    if (t < 0 || t >= L.T) fail(BO_ERR_SHAPE_MISMATCH, "tensor index out of range");
-    if (!grads[i]) fail(BO_ERR_SHAPE_MISMATCH, "null gradient for tensor " + std::to_string(t));
-    if (c->delivered[static_cast<size_t>(t)]) {
-      fail(BO_ERR_PROTOCOL, "tensor " + std::to_string(t) + " delivered twice in one sync micro");
-    }
-    c->delivered[static_cast<size_t>(t)] = 1;
-    c->sync_tab->p[t] = grads[i];
-    c->sync_aligned &= (reinterpret_cast<uintptr_t>(grads[i]) & 15u) == 0;
-    c->n_delivered += 1;
-    if (c->world > 1) {
-      c->group_pending[static_cast<size_t>(c->group_of_bucket[static_cast<size_t>(L.bucket_of[static_cast<size_t>(t)])])] -= 1;
-    }
-  }
-  // reduce every group whose tensors are all final, in layout order (the
-  // reference's comm thread, trainer.cpp:301-327), on the communication
-  // stream after the caller's work so far (the gradients' producer)
-  if (c->world > 1) {
-    const int G = static_cast<int>(c->comm_groups.size());
-    if (c->next_group < G && c->group_pending[static_cast<size_t>(c->next_group)] == 0) {
-      BO_CUDA(cudaEventRecord(c->comm_ready, c->stream));
-      BO_CUDA(cudaStreamWaitEvent(c->comm_stream, c->comm_ready, 0));
-    }
-    while (c->next_group < G && c->group_pending[static_cast<size_t>(c->next_group)] == 0) {
-      const auto& g = c->comm_groups[static_cast<size_t>(c->next_group)];
-      run_reduce_group(c, *c->sync_tab, g.b0, g.b1, g.acc0, g.acc1, c->comm_stream);
-      c->next_group += 1;
-    }
-  }
-  if (c->n_delivered < L.T) return BO_OK;
-  // every gradient delivered: the rest of the step on the caller's stream
-  c->sync_open = false;
-  c->next_micro = 0;
-  grow_bc_table(c, c->calls + 2);
-  if (c->world == 1) {
-    if (c->sync_aligned && !c->force_unfused) {
-      c->path |= BO_PATH_ONE_RANK_FUSED;
-      run_fused_single_rank(c, *c->sync_tab);
-    } else {
-      c->path |= BO_PATH_ONE_RANK_STAGED;
-      launch_finalize(c, *c->sync_tab);
-      run_reduce(c, *c->sync_tab);
-      run_lamb(c, *c->sync_tab);
-    }
-  } else {
-    BO_CUDA(cudaEventRecord(c->comm_done, c->comm_stream));
-    BO_CUDA(cudaStreamWaitEvent(c->stream, c->comm_done, 0));
-    run_lamb(c, *c->sync_tab);
-  }
-  c->calls += 1;
-  BO_GUARD_END
-}
 
 }  // extern "C"

@@ -187,6 +187,16 @@ __device__ __forceinline__ void micro_sum4_k(const uint16_t* const* p, int e, fl
   }
 }
 
+// Ring wire element type W (float or binary16 bits).
+template <typename W>
+__device__ __forceinline__ W to_wire(float p);
+template <>
+__device__ __forceinline__ float to_wire<float>(float p) { return p; }
+template <>
+__device__ __forceinline__ uint16_t to_wire<uint16_t>(float p) { return narrow(p); }
+__device__ __forceinline__ float from_wire(float w) { return w; }
+__device__ __forceinline__ float from_wire(uint16_t w) { return widen(w); }
+
 // Streaming accesses with explicit L2 eviction priority (no L1 allocation):
 // evict_first for data read once, evict_last for what the next pass re-reads.
 __device__ __forceinline__ uint64_t policy_evict_first() {

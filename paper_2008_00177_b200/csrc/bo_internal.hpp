@@ -256,6 +256,21 @@ struct bo_ctx {
   std::vector<bool> ptr_aligned_cache;
 };
 
+// Every C entry point: library failures become a bo_status plus the thread's
+// last-error message.
+#define BO_GUARD_BEGIN try {
+#define BO_GUARD_END                          \
+  }                                           \
+  catch (const Failure& f) {                  \
+    set_thread_error(f.msg);                  \
+    return f.code;                            \
+  }                                           \
+  catch (const std::exception& e) {           \
+    set_thread_error(e.what());               \
+    return BO_ERR_CUDA;                       \
+  }                                           \
+  return BO_OK;
+
 namespace bo {
 void* dev_alloc(bo_ctx* c, size_t bytes);
 void upload_tables(bo_ctx* c);
@@ -264,6 +279,9 @@ void grow_bc_table(bo_ctx* c, int64_t need);
 // kernels / pipeline stages (bo_pipeline.cu)
 void launch_accumulate(bo_ctx* c, int micro, const PtrTable& tab, bool vec_ok);
 void launch_finalize(bo_ctx* c, const PtrTable& tab);
+void launch_finalize_tiles(bo_ctx* c, const AccTile* tiles, int n, const PtrTable& tab,
+                           cudaStream_t stream);
+void check_launch(bo_ctx* c, const char* what);  // counts the launch, raises on a launch error
 void run_reduce(bo_ctx* c, const PtrTable& tab);
 // one communication group of buckets [b0, b1) on `stream` (overlap mode)
 void run_reduce_group(bo_ctx* c, const PtrTable& tab, int b0, int b1, int acc0, int acc1,

@@ -1,13 +1,17 @@
-// B200 gradient-to-update pipeline: device kernels and stage orchestration.
+// B200 gradient-to-update pipeline: accumulate / finalize kernels and the
+// sharded (world > 1) LAMB with the fused parameter all-gather.
 //
 // Stage map onto the reference (proj/core/src, read-only):
-//   k_accumulate   accum_[p][i] += g[i]                  trainer.cpp:240-244
-//   k_finalize     flatten_param: (live + accum) * inv   trainer.cpp:186-203
-//   ring hops      ring_allreduce RS phase, fold order   collective.hpp:65-80
-//                  and the binary16 wire semantics       collective.cpp:170-190, 205-209
-//   k_lamb_norms   lamb_step moments + fp64 norms        lamb.cpp:176-190
-//   k_trust        trust ratio (lamb.cpp:192-196) + found_inf + loss-scaler
-//   k_lamb_update  w -= (lr * r) * u                      lamb.cpp:197-198
+//   k_accumulate     accum_[p][i] += g[i]                trainer.cpp:240-244
+//   k_finalize       flatten_param: (live + accum) * inv trainer.cpp:186-203
+//   (ring hops: bo_ring.cu; one rank's fused LAMB: bo_fused.cu)
+//   k_p1w            lamb_step moments, u + fp64 norm partials on the shard
+//                                                        lamb.cpp:176-190
+//   k_norm_reduce / k_trust  trust ratio (lamb.cpp:192-196), found_inf and
+//                    the loss scaler
+//   k_shard_p2_push  w -= (lr * r) * u (lamb.cpp:197-198) + the push into
+//                    every replica (the all-gather)
+//   k_lamb_norms / k_lamb_update  one rank with unaligned inputs
 //
 // Bit-level contract: every float operation uses an
 // explicit round-to-nearest intrinsic and the file is compiled with
@@ -131,136 +135,6 @@ __global__ void __launch_bounds__(kThreads) k_finalize(const AccTile* __restrict
   for (int j = 0; j < kPer; ++j) {
     const int e = threadIdx.x + j * kThreads;
     if (e < tile.len) dst[e] = __fmul_rn(gv[j], inv);
-  }
-}
-
-// --------------------------------------------------------------- ring hops
-template <typename W>
-__device__ __forceinline__ W to_wire(float p);
-template <>
-__device__ __forceinline__ float to_wire<float>(float p) { return p; }
-template <>
-__device__ __forceinline__ uint16_t to_wire<uint16_t>(float p) { return narrow(p); }
-__device__ __forceinline__ float from_wire(float w) { return w; }
-__device__ __forceinline__ float from_wire(uint16_t w) { return widen(w); }
-
-// Ring hop with flatten_param fused in (trainer.cpp:186-203 + collective.hpp:65-80
-// / collective.cpp:170-190): x = (h + acc) * inv for the elements of chunk q,
-// out = wire(x) (combine == 0, the first send) or wire(from_wire(in) + x).
-// KR > 0 (bo_train_step): x from the KR resident micros instead of h + acc.
-template <typename W, int KR>
-__global__ void __launch_bounds__(kThreads) k_hopx(const HopXTile* __restrict__ tiles,
-                                                   const TensorDev* __restrict__ td,
-                                                   const __grid_constant__ PtrTable tab, MicroSrc ms,
-                                                   const float* __restrict__ acc,
-                                                   const DevState* __restrict__ st, int K,
-                                                   const W* __restrict__ in, W* __restrict__ out,
-                                                   int combine) {
-  const HopXTile tile = tiles[blockIdx.x];
-  const float inv = __fdiv_rn(1.0f, __fmul_rn(static_cast<float>(K), st->scale));
-  const uint16_t* __restrict__ h = tab.p[tile.t] + tile.e0;
-  const float* __restrict__ a = acc + td[tile.t].acc_off + tile.e0;
-  constexpr bool resident = KR > 0;
-  __shared__ const uint16_t* mp[KR > 0 ? KR : 1];  // the tile's KR micro pointers
-  if constexpr (resident) {
-    if (static_cast<int>(threadIdx.x) < KR) mp[threadIdx.x] = ms.hk[threadIdx.x * ms.T + tile.t] + tile.e0;
-    __syncthreads();
-  }
-  // (h + acc) * inv, or the resident micros' sum * inv, for element e / e..e+3
-  auto x1 = [&](int e) {
-    if constexpr (resident) return __fmul_rn(micro_sum1(mp, KR, e), inv);
-    const float g = widen(__ldcs(h + e));
-    return __fmul_rn(K > 1 ? __fadd_rn(g, __ldcs(a + e)) : g, inv);
-  };
-  auto x4 = [&](int e, float (&x)[4]) {
-    if constexpr (resident) {
-      micro_sum4_k<KR>(mp, e, x);
-    } else {
-      const uint2 hv = __ldcs(reinterpret_cast<const uint2*>(h + e));
-      x[0] = widen(static_cast<uint16_t>(hv.x & 0xFFFFu));
-      x[1] = widen(static_cast<uint16_t>(hv.x >> 16));
-      x[2] = widen(static_cast<uint16_t>(hv.y & 0xFFFFu));
-      x[3] = widen(static_cast<uint16_t>(hv.y >> 16));
-      if (K > 1) {
-        const float4 a4 = __ldcs(reinterpret_cast<const float4*>(a + e));
-        x[0] = __fadd_rn(x[0], a4.x);
-        x[1] = __fadd_rn(x[1], a4.y);
-        x[2] = __fadd_rn(x[2], a4.z);
-        x[3] = __fadd_rn(x[3], a4.w);
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < 4; ++i) x[i] = __fmul_rn(x[i], inv);
-  };
-  // Vector path when the tensor side (h, acc) and the shard side (in, out)
-  // share their 4-element alignment (the common case: BERT tensor sizes and
-  // chunk lengths are multiples of 4): scalar head to the boundary, float4 /
-  // 4 x binary16 body, scalar tail. Caller slots are 16-byte aligned (all K
-  // of them in resident mode, checked by bo_train_step).
-  if (((tile.e0 - tile.s0) & 3) == 0 && (resident || (reinterpret_cast<uintptr_t>(tab.p[tile.t]) & 15) == 0)) {
-    const int head = min(static_cast<int>((4 - (tile.s0 & 3)) & 3), tile.len);
-    const int nv = (tile.len - head) >> 2;
-    auto one = [&](int e) {
-      float p = x1(e);
-      if (combine) p = __fadd_rn(from_wire(in[tile.s0 + e]), p);
-      out[tile.s0 + e] = to_wire<W>(p);
-    };
-    if (threadIdx.x < head) one(threadIdx.x);
-    const int tail0 = head + 4 * nv;
-    if (threadIdx.x >= 32 && static_cast<int>(threadIdx.x) - 32 < tile.len - tail0) {
-      one(tail0 + static_cast<int>(threadIdx.x) - 32);
-    }
-#pragma unroll 4
-    for (int q = threadIdx.x; q < nv; q += kThreads) {
-      const int e = head + 4 * q;
-      float iv[4] = {0.f, 0.f, 0.f, 0.f};
-      if (combine) {
-        if constexpr (sizeof(W) == 2) {
-          const uint2 w2 = __ldcs(reinterpret_cast<const uint2*>(in + tile.s0 + e));
-          iv[0] = widen(static_cast<uint16_t>(w2.x & 0xFFFFu));
-          iv[1] = widen(static_cast<uint16_t>(w2.x >> 16));
-          iv[2] = widen(static_cast<uint16_t>(w2.y & 0xFFFFu));
-          iv[3] = widen(static_cast<uint16_t>(w2.y >> 16));
-        } else {
-          const float4 w4 = __ldcs(reinterpret_cast<const float4*>(in + tile.s0 + e));
-          iv[0] = w4.x; iv[1] = w4.y; iv[2] = w4.z; iv[3] = w4.w;
-        }
-      }
-      float xv[4];
-      x4(e, xv);
-      W o[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        float p = xv[i];
-        if (combine) p = __fadd_rn(iv[i], p);
-        o[i] = to_wire<W>(p);
-      }
-      if constexpr (sizeof(W) == 2) {
-        uint2 w2;
-        w2.x = static_cast<uint32_t>(o[0]) | (static_cast<uint32_t>(o[1]) << 16);
-        w2.y = static_cast<uint32_t>(o[2]) | (static_cast<uint32_t>(o[3]) << 16);
-        *reinterpret_cast<uint2*>(out + tile.s0 + e) = w2;
-      } else {
-        *reinterpret_cast<float4*>(out + tile.s0 + e) = make_float4(o[0], o[1], o[2], o[3]);
-      }
-    }
-    return;
-  }
-  constexpr int kPer = kTileElems / kThreads;
-  float xv[kPer];
-#pragma unroll
-  for (int j = 0; j < kPer; ++j) {
-    const int e = threadIdx.x + j * kThreads;
-    xv[j] = e < tile.len ? x1(e) : 0.0f;
-  }
-#pragma unroll
-  for (int j = 0; j < kPer; ++j) {
-    const int e = threadIdx.x + j * kThreads;
-    if (e < tile.len) {
-      float p = xv[j];
-      if (combine) p = __fadd_rn(from_wire(__ldcs(in + tile.s0 + e)), p);
-      out[tile.s0 + e] = to_wire<W>(p);
-    }
   }
 }
 
@@ -730,13 +604,14 @@ __global__ void k_gather_shard(const LambTile* __restrict__ tiles, const float* 
   for (int e = threadIdx.x; e < t.len; e += blockDim.x) wsh[t.s0 + e] = w[t.w0 + e];
 }
 
+}  // namespace
+
 void check_launch(bo_ctx* c, const char* what) {
   c->launches += 1;
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) fail(BO_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
-}  // namespace
 
 void launch_accumulate(bo_ctx* c, int micro, const PtrTable& tab, bool vec_ok) {
   StageTimer timer(c, BO_STAGE_ACCUMULATE);
@@ -753,148 +628,17 @@ void launch_accumulate(bo_ctx* c, int micro, const PtrTable& tab, bool vec_ok) {
   check_launch(c, "k_accumulate");
 }
 
-void launch_finalize(bo_ctx* c, const PtrTable& tab) {
-  StageTimer timer(c, BO_STAGE_FINALIZE);
-  k_finalize<<<c->n_acc_tiles, kThreads, 0, c->stream>>>(c->d_acc_tiles, c->d_tensors, tab, c->acc,
-                                                          c->x, c->state, c->cfg.accumulation);
+void launch_finalize_tiles(bo_ctx* c, const AccTile* tiles, int n, const PtrTable& tab,
+                           cudaStream_t stream) {
+  if (n == 0) return;
+  StageTimer timer(c, BO_STAGE_FINALIZE, stream);
+  k_finalize<<<n, kThreads, 0, stream>>>(tiles, c->d_tensors, tab, c->acc, c->x, c->state,
+                                         c->cfg.accumulation);
   check_launch(c, "k_finalize");
 }
 
-// The reference ring's reduce-scatter phase (collective.hpp:65-80, binary16
-// wire collective.cpp:170-190) over buckets [b0, b1), with flatten_param fused
-// into every hop: the local addend x of chunk q is computed from the sync
-// micro's binary16 input and the accumulator as the hop needs it.
-template <typename W>
-static void ring_reduce_scatter(bo_ctx* c, const PtrTable& tab, ncclDataType_t dt, int b0, int b1,
-                                cudaStream_t st) {
-  const int N = c->world, r = c->rank;
-  const int right = (r + 1) % N, left = (r - 1 + N) % N;
-  const Layout& L = c->L;
-  const int64_t sh0 = L.shoff[static_cast<size_t>(b0)];
-  const int64_t sh1 = b1 < L.B ? L.shoff[static_cast<size_t>(b1)] : L.shard_total;
-  W* a = static_cast<W*>(c->wire[0]);
-  W* b = static_cast<W*>(c->wire[1]);
-  const int K = c->cfg.accumulation;
-  auto hop = [&](int q, const W* in, W* out, int combine) {
-    const std::vector<int>& qb = c->hopx_bucket_begin[static_cast<size_t>(q)];
-    const int t0 = qb[static_cast<size_t>(b0)], t1 = qb[static_cast<size_t>(b1)];
-    if (t1 > t0) {
-      StageTimer timer(c, BO_STAGE_FLAG, st);
-      auto go = [&](auto kern) {
-        kern<<<t1 - t0, kThreads, 0, st>>>(c->d_hopx_tiles + t0, c->d_tensors, tab, c->ms, c->acc, c->state, K,
-                                           in, out, combine);
-      };
-      switch (c->ms.K) {
-        case 0: go(k_hopx<W, 0>); break;
-        case 2: go(k_hopx<W, 2>); break;
-        case 3: go(k_hopx<W, 3>); break;
-        case 4: go(k_hopx<W, 4>); break;
-        case 5: go(k_hopx<W, 5>); break;
-        case 6: go(k_hopx<W, 6>); break;
-        case 7: go(k_hopx<W, 7>); break;
-        case 8: go(k_hopx<W, 8>); break;
-        default: fail(BO_ERR_INVALID_CONFIG, "resident micro count outside 2..8");
-      }
-      check_launch(c, "k_hopx");
-    }
-  };
-  // The last hop completes the owned chunk. It can run inside LAMB phase 1
-  // (k_p1w<W, true, true>), which then reads the left neighbour's partial
-  // directly: one staged write + read of the chunk less, but the NVLink
-  // latency is exposed inside an HBM-bound kernel. Measured on BERT-large
-  // (profiles/r01_notes.md): a net win at world 2 (1.10 vs 1.18 ms), a loss
-  // at world 4 (0.67 vs 0.62 ms), so the default fuses only at world 2 —
-  // and never in the overlapped sync micro, where a staged last hop runs
-  // under the caller's backward instead of inside the exposed LAMB.
-  // With the K micros resident (bo_train_step) the hops read 2K bytes per
-  // element instead of 6, and the staged last hop measured faster at world 2
-  // too (2.93 vs 3.13 ms per step): no fusion there either. Fusing needs the
-  // accumulator form of x, so the resident mode never fuses.
-  const bool fuse_last = !c->force_unfused && c->ms.K == 0 &&
-                         (c->fuse_last_hop >= 0 ? c->fuse_last_hop != 0 : (N == 2 && !c->sync_open));
-  hop(r, nullptr, a, 0);  // hop 0 payload: this rank's own chunk r (collective.cpp:178)
-  const bool p2p = c->peer_wire[0][left] && !c->ring_via_nccl;
-  c->path |= p2p ? BO_PATH_RING_P2P : BO_PATH_RING_SENDRECV;
-  if (p2p) {
-    // Peer-to-peer hops: hop s reads the left neighbour's hop s-1 output in
-    // place over NVLink (CUDA IPC mapping) and writes the other local buffer.
-    // A 4-byte all-reduce before each hop is the barrier that orders a
-    // buffer's writer before its reader and its reader before its next writer
-    // (buckets of different groups occupy disjoint positions).
-    for (int s = 0; s < N - 1; ++s) {
-      BO_NCCL(ncclAllReduce(c->d_barrier, c->d_barrier, 1, ncclInt32, ncclSum, c->comm, st));
-      const W* in = static_cast<const W*>(c->peer_wire[s % 2][left]);
-      if (s == N - 2 && fuse_last) {
-        c->ring_last_in = in;  // the last hop runs inside LAMB phase 1
-        c->path |= BO_PATH_LAST_HOP_FUSED;
-        return;
-      }
-      W* out = static_cast<W*>(c->wire[(s + 1) % 2]);
-      hop((r - s - 1 + 2 * N) % N, in, out, 1);  // chunk added at hop s (collective.hpp:70-71)
-    }
-    c->ring_result = c->wire[(N - 1) % 2];
-  } else {
-    for (int s = 0; s < N - 1; ++s) {
-      BO_NCCL(ncclGroupStart());
-      BO_NCCL(ncclSend(a + sh0, static_cast<size_t>(sh1 - sh0), dt, right, c->comm, st));
-      BO_NCCL(ncclRecv(b + sh0, static_cast<size_t>(sh1 - sh0), dt, left, c->comm, st));
-      BO_NCCL(ncclGroupEnd());
-      if (s == N - 2 && fuse_last) {
-        c->ring_last_in = b;
-        c->path |= BO_PATH_LAST_HOP_FUSED;
-        return;
-      }
-      hop((r - s - 1 + 2 * N) % N, b, a, 1);  // chunk received at hop s (collective.hpp:70-71)
-    }
-    c->ring_result = a;
-  }
-  // Unfused: after N-1 hops the result buffer holds the finished chunk
-  // (r+1) % N, already wire-rounded (the owner re-round of
-  // collective.cpp:205-209): the chunk this rank owns (Layout::own). LAMB
-  // reads it in place.
-}
-
-static void nccl_reduce_scatter(bo_ctx* c, int b0, int b1, cudaStream_t st) {
-  c->path |= BO_PATH_NCCL_RS;
-  BO_NCCL(ncclGroupStart());
-  for (int b = b0; b < b1; ++b) {
-    BO_NCCL(ncclReduceScatter(c->x + c->L.base[static_cast<size_t>(b)], c->gshard + c->L.shoff[static_cast<size_t>(b)],
-                              static_cast<size_t>(c->L.chunk[static_cast<size_t>(b)]), ncclFloat, ncclSum,
-                              c->comm, st));
-  }
-  BO_NCCL(ncclGroupEnd());
-}
-
-void run_reduce(bo_ctx* c, const PtrTable& tab) {
-  if (c->world == 1) return;
-  StageTimer timer(c, BO_STAGE_REDUCE);
-  c->ring_last_in = nullptr;
-  c->ring_result = nullptr;
-  if (c->algo == BO_REDUCE_NCCL) {
-    nccl_reduce_scatter(c, 0, c->L.B, c->stream);
-  } else if (c->cfg.f16_exchange) {
-    ring_reduce_scatter<uint16_t>(c, tab, ncclFloat16, 0, c->L.B, c->stream);
-  } else {
-    ring_reduce_scatter<float>(c, tab, ncclFloat32, 0, c->L.B, c->stream);
-  }
-}
-
-void run_reduce_group(bo_ctx* c, const PtrTable& tab, int b0, int b1, int acc0, int acc1,
-                      cudaStream_t stream) {
-  StageTimer timer(c, BO_STAGE_REDUCE, stream);
-  if (c->algo == BO_REDUCE_NCCL) {
-    if (acc1 > acc0) {
-      StageTimer t2(c, BO_STAGE_FINALIZE, stream);
-      k_finalize<<<acc1 - acc0, kThreads, 0, stream>>>(c->d_group_acc_tiles + acc0, c->d_tensors, tab, c->acc,
-                                                        c->x, c->state, c->cfg.accumulation);
-      check_launch(c, "k_finalize");
-    }
-    nccl_reduce_scatter(c, b0, b1, stream);
-  } else if (c->cfg.f16_exchange) {
-    ring_reduce_scatter<uint16_t>(c, tab, ncclFloat16, b0, b1, stream);
-  } else {
-    ring_reduce_scatter<float>(c, tab, ncclFloat32, b0, b1, stream);
-  }
+void launch_finalize(bo_ctx* c, const PtrTable& tab) {
+  launch_finalize_tiles(c, c->d_acc_tiles, c->n_acc_tiles, tab, c->stream);
 }
 
 // One rank's multi-kernel fallback (inputs not 16-byte aligned): recompute

@@ -6,6 +6,7 @@
 //   make -C tools p1_probe && tools/p1_probe tools/bert_large.txt 2 0
 #include "../paper_2008_00177_b200/csrc/bo_pipeline.cu"
 #include "../paper_2008_00177_b200/csrc/bo_fused.cu"
+#include "../paper_2008_00177_b200/csrc/bo_ring.cu"
 
 #include <cstdio>
 #include <fstream>
