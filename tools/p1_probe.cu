@@ -205,6 +205,31 @@ int main(int argc, char** argv) {
     k_hopx<uint16_t, 0><<<t1 - t0, kThreads>>>(c->d_hopx_tiles + t0, c->d_tensors, tab, MicroSrc{nullptr, 0, 0}, c->acc, c->state,
                                             4, pin, static_cast<uint16_t*>(c->wire[0]), 1);
   });
+  // resident micros (bo_train_step): K = 4 binary16 gradient sets
+  std::vector<const uint16_t*> mt(4 * static_cast<size_t>(T));
+  for (int k = 0; k < 4; ++k) {
+    uint16_t* gk;
+    CK(cudaMalloc(&gk, tot * 2));
+    fill_f16<<<1024, 256>>>(gk, tot, 4096.0f * 0.01f, 10 + k);
+    int64_t o = 0;
+    for (int t = 0; t < T; ++t) { mt[static_cast<size_t>(k) * T + t] = gk + o; o += align_up(numel[t], 64); }
+  }
+  const uint16_t** dmt;
+  CK(cudaMalloc(&dmt, mt.size() * sizeof(void*)));
+  CK(cudaMemcpy(dmt, mt.data(), mt.size() * sizeof(void*), cudaMemcpyHostToDevice));
+  const MicroSrc ms4{dmt, 4, T};
+  time("k_hopx<f16, K=4> pack (own chunk)", 10 * S, 0, [&] {
+    k_hopx<uint16_t, 4><<<t1 - t0, kThreads>>>(c->d_hopx_tiles + t0, c->d_tensors, tab, ms4, c->acc, c->state,
+                                              4, nullptr, static_cast<uint16_t*>(c->wire[0]), 0);
+  });
+  time("k_hopx<f16, K=4> (own chunk) peer", 10 * S, 2 * S, [&] {
+    k_hopx<uint16_t, 4><<<t1 - t0, kThreads>>>(c->d_hopx_tiles + t0, c->d_tensors, tab, ms4, c->acc, c->state,
+                                              4, pin, static_cast<uint16_t*>(c->wire[0]), 1);
+  });
+  time("k_hopx<f16> pack (own chunk)", 8 * S, 0, [&] {
+    k_hopx<uint16_t, 0><<<t1 - t0, kThreads>>>(c->d_hopx_tiles + t0, c->d_tensors, tab, MicroSrc{nullptr, 0, 0}, c->acc, c->state,
+                                            4, nullptr, static_cast<uint16_t*>(c->wire[0]), 0);
+  });
   time("k_shard_p2_push (peer replicas)", 16 * S, 4.0 * (world - 1) * S, [&] {
     k_shard_p2_push<<<c->n_lamb_tiles, kThreads>>>(c->d_lamb_tiles, c->wsh, c->u, c->state, c->lamb,
                                                    c->trust, d_peer_w, world);
