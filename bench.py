@@ -118,7 +118,9 @@ def run_cpu_reference(spec, world, K, bucket_bytes, f16, warmup, steps, groups=N
     numels, firsts, sample = cpu_sample(spec)
     ncpu = os.cpu_count() or 1
     if groups is None:
-        groups = max(1, min(ncpu // max(world, 1), 16))
+        # every host core (one rank thread each); ~0.6 GB of host memory per
+        # replica group bounds it on very large hosts
+        groups = max(1, min(ncpu // max(world, 1), 96))
     if orc.reference_available():
         ref = orc.Reference()
         secs, stages = ref.stage_bench(numels, firsts, world, K, bucket_bytes, f16, groups, warmup,
