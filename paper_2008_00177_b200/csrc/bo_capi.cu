@@ -251,6 +251,7 @@ bo_status bo_create(const bo_trainer_config* cfg, int32_t n_tensors, const int64
   c->world = world;
   if (const char* e = std::getenv("BO_UNFUSED")) c->force_unfused = std::strcmp(e, "0") != 0;
   if (const char* e = std::getenv("BO_RING_NCCL")) c->ring_via_nccl = std::strcmp(e, "0") != 0;
+  if (const char* e = std::getenv("BO_RING_PUSH")) c->ring_push = std::strcmp(e, "0") != 0;
   if (const char* e = std::getenv("BO_FUSE_LAST")) c->fuse_last_hop = std::strcmp(e, "0") != 0;
   c->algo = cfg->reduce_algo == BO_REDUCE_AUTO ? (cfg->f16_exchange ? BO_REDUCE_RING : BO_REDUCE_NCCL)
                                                : cfg->reduce_algo;
@@ -397,6 +398,7 @@ bo_status bo_comm_init(bo_ctx* c, const uint8_t* id128) {
   };
   mix(static_cast<uint64_t>(c->algo));
   mix(c->ring_via_nccl ? 1 : 0);
+  mix(c->ring_push ? 1 : 0);
   mix(c->comm_groups.size());
   for (const auto& g : c->comm_groups) mix(static_cast<uint64_t>(g.b1));
   uint64_t* d = static_cast<uint64_t*>(dev_alloc(c, static_cast<size_t>(2 * c->world + 2) * 8));

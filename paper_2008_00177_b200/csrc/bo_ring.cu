@@ -188,9 +188,29 @@ static void ring_reduce_scatter(bo_ctx* c, const PtrTable& tab, ncclDataType_t d
   // accumulator form of x, so the resident mode never fuses.
   const bool fuse_last = !c->force_unfused && c->ms.K == 0 &&
                          (c->fuse_last_hop >= 0 ? c->fuse_last_hop != 0 : (N == 2 && !c->sync_open));
-  hop(r, nullptr, a, 0);  // hop 0 payload: this rank's own chunk r (collective.cpp:178)
   const bool p2p = c->peer_wire[0][left] && !c->ring_via_nccl;
   c->path |= p2p ? BO_PATH_RING_P2P : BO_PATH_RING_SENDRECV;
+  if (p2p && c->ring_push && !fuse_last) {
+    // Push form: every hop writes its output straight into the RIGHT
+    // neighbour's staging buffer over NVLink and reads its input locally
+    // (what the left neighbour pushed). With every rank sending and
+    // receiving at once, NVLink stores sustain ~700 GB/s per direction where
+    // remote reads (the pull form below) stall at ~540 GB/s. The barrier
+    // before each hop orders the pushes into a buffer before its reader and
+    // its reader before the next push into it; the last hop completes this
+    // rank's owned chunk locally.
+    hop(r, nullptr, static_cast<W*>(c->peer_wire[0][right]), 0);
+    for (int s = 0; s < N - 1; ++s) {
+      BO_NCCL(ncclAllReduce(c->d_barrier, c->d_barrier, 1, ncclInt32, ncclSum, c->comm, st));
+      const W* in = static_cast<const W*>(c->wire[s % 2]);
+      W* out = s == N - 2 ? static_cast<W*>(c->wire[(s + 1) % 2]) : static_cast<W*>(c->peer_wire[(s + 1) % 2][right]);
+      hop((r - s - 1 + 2 * N) % N, in, out, 1);  // chunk added at hop s (collective.hpp:70-71)
+    }
+    c->path |= BO_PATH_RING_PUSH;
+    c->ring_result = c->wire[(N - 1) % 2];
+    return;
+  }
+  hop(r, nullptr, a, 0);  // hop 0 payload: this rank's own chunk r (collective.cpp:178)
   if (p2p) {
     // Peer-to-peer hops: hop s reads the left neighbour's hop s-1 output in
     // place over NVLink (CUDA IPC mapping) and writes the other local buffer.

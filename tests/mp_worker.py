@@ -58,6 +58,10 @@ def main():
     if case.endswith("_resident"):
         resident = True
         case = case[: -len("_resident")]
+    if case.endswith("_pull"):
+        # ring hops reading the left neighbour's buffer instead of pushing
+        os.environ["BO_RING_PUSH"] = "0"
+        case = case[: -len("_pull")]
     if case.endswith("_overlap"):
         # the sync micro delivered through bo_sync_ready in ragged chunks,
         # with communication groups of ~20k elements (several per step)

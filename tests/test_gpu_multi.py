@@ -47,7 +47,8 @@ def run_case(case, nproc, model="tiny", steps=4):
 @pytest.mark.parametrize("case", ["ring16", "ring32", "nccl32", "ring16_1bucket",
                                   "ring16_tinybuckets", "ring16_unfused", "ring32_unfused",
                                   "ring16_overlap", "ring32_unfused_overlap", "nccl32_overlap",
-                                  "ring16_resident", "ring32_unfused_resident", "nccl32_resident"])
+                                  "ring16_resident", "ring32_unfused_resident", "nccl32_resident",
+                                  "ring16_pull_resident", "ring32_unfused_pull"])
 def test_two_gpus(case):
     if _ngpu() < 2:
         pytest.skip("needs 2 GPUs")
@@ -65,6 +66,10 @@ def test_two_gpus(case):
     # bo_train_step reads the resident micros on the ring; the NCCL wire takes
     # the per-micro path inside the call (same results)
     assert ("resident_micros" in res["path"]) == (case.endswith("_resident") and case.startswith("ring"))
+    # staged hops push into the right neighbour's buffer unless BO_RING_PUSH=0;
+    # a last hop fused into LAMB phase 1 reads the left neighbour in place
+    pushed = case.startswith("ring") and "_pull" not in case and "last_hop_fused" not in res["path"]
+    assert ("ring_push" in res["path"]) == pushed
 
 
 @pytest.mark.parametrize("model", ["ragged", "small"])
@@ -90,11 +95,14 @@ def test_more_gpus(n):
         pytest.skip(f"needs {n} GPUs")
     res = run_case("ring16", n)
     assert res["m_bit_exact"] and res["v_bit_exact"]
-    assert res["path"] == ["ring_p2p"]  # staged last hop beyond world 2
+    assert res["path"] == ["ring_p2p", "ring_push"]  # staged last hop beyond world 2
     res = run_case("ring16_fused", n)
     assert res["m_bit_exact"] and res["v_bit_exact"]
     assert "last_hop_fused" in res["path"]
     res = run_case("ring16_resident", n)
+    assert res["m_bit_exact"] and res["v_bit_exact"]
+    assert res["path"] == ["ring_p2p", "resident_micros", "ring_push"]
+    res = run_case("ring16_pull_resident", n)
     assert res["m_bit_exact"] and res["v_bit_exact"]
     assert res["path"] == ["ring_p2p", "resident_micros"]
     run_case("nccl32", n)
