@@ -318,7 +318,8 @@ def main_b200(args):
     # algorithmic bytes per launch of each stage (HBM) / per rank (NVLink)
     hbm_bytes = {
         "accumulate": (BYTES_ACCUMULATE_FIRST + BYTES_ACCUMULATE * (K - 2)) * P / max(K - 1, 1),
-        "finalize": (BYTES_FINALIZE if K > 1 else BYTES_FINALIZE_K1) * P,
+        # (resident micros, NCCL wire: the K micros read, the fp32 fusion buffer written)
+        "finalize": ((2 * K + 4) if resident else (BYTES_FINALIZE if K > 1 else BYTES_FINALIZE_K1)) * P,
         # LAMB phase 1: one rank k_lamb_p1 (the gradient source xb + w, m, v
         # read; m', v', u written); world > 1 k_p1w (reduced wire E or, with
         # the last ring hop fused in, xb with the wire over NVLink; + wsh, m, v

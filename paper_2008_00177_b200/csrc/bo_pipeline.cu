@@ -85,9 +85,12 @@ __global__ void __launch_bounds__(kThreads) k_accumulate(const AccTile* __restri
 // The sync micro's flatten_param (trainer.cpp:186-203): v = live (+ summed),
 // dst = v * inv with inv = 1/(K*S) in float, S the current (device) scale.
 // Writes the fusion-buffer position of every element (the packer).
+// KR > 0 (bo_train_step): v = the KR resident micros' sum in the reference's
+// order (live + ((0 + g0) + ... + g_{K-2})), no accumulator.
+template <int KR>
 __global__ void __launch_bounds__(kThreads) k_finalize(const AccTile* __restrict__ tiles,
                                                        const TensorDev* __restrict__ td,
-                                                       const __grid_constant__ PtrTable tab,
+                                                       const __grid_constant__ PtrTable tab, MicroSrc ms,
                                                        const float* __restrict__ acc,
                                                        float* __restrict__ x,
                                                        const DevState* __restrict__ st, int K) {
@@ -96,6 +99,25 @@ __global__ void __launch_bounds__(kThreads) k_finalize(const AccTile* __restrict
   const uint16_t* __restrict__ src = tab.p[tile.t] + tile.e0;
   const float* __restrict__ a = acc + td[tile.t].acc_off + tile.e0;
   float* __restrict__ dst = x + td[tile.t].flat_off + tile.e0;
+  if constexpr (KR > 0) {
+    __shared__ const uint16_t* mp[KR];
+    if (static_cast<int>(threadIdx.x) < KR) mp[threadIdx.x] = ms.hk[threadIdx.x * ms.T + tile.t] + tile.e0;
+    __syncthreads();
+    if ((td[tile.t].flat_off & 3) == 0) {  // resident slots are 16-byte aligned (bo_train_step)
+      const int nv = tile.len >> 2;
+#pragma unroll 2
+      for (int q = threadIdx.x; q < nv; q += kThreads) {
+        float g[4];
+        micro_sum4_k<KR>(mp, 4 * q, g);
+        reinterpret_cast<float4*>(dst)[q] = make_float4(__fmul_rn(g[0], inv), __fmul_rn(g[1], inv),
+                                                        __fmul_rn(g[2], inv), __fmul_rn(g[3], inv));
+      }
+      for (int e = 4 * nv + threadIdx.x; e < tile.len; e += kThreads) dst[e] = __fmul_rn(micro_sum1(mp, KR, e), inv);
+    } else {
+      for (int e = threadIdx.x; e < tile.len; e += kThreads) dst[e] = __fmul_rn(micro_sum1(mp, KR, e), inv);
+    }
+    return;
+  }
   if (((td[tile.t].flat_off & 3) | (reinterpret_cast<uintptr_t>(tab.p[tile.t]) & 15)) == 0) {
     // the tensor's fusion-buffer offset is 16-byte aligned: float4 path
     const int nv = tile.len >> 2;
@@ -632,8 +654,20 @@ void launch_finalize_tiles(bo_ctx* c, const AccTile* tiles, int n, const PtrTabl
                            cudaStream_t stream) {
   if (n == 0) return;
   StageTimer timer(c, BO_STAGE_FINALIZE, stream);
-  k_finalize<<<n, kThreads, 0, stream>>>(tiles, c->d_tensors, tab, c->acc, c->x, c->state,
-                                         c->cfg.accumulation);
+  auto go = [&](auto kern) {
+    kern<<<n, kThreads, 0, stream>>>(tiles, c->d_tensors, tab, c->ms, c->acc, c->x, c->state, c->cfg.accumulation);
+  };
+  switch (c->ms.K) {
+    case 0: go(k_finalize<0>); break;
+    case 2: go(k_finalize<2>); break;
+    case 3: go(k_finalize<3>); break;
+    case 4: go(k_finalize<4>); break;
+    case 5: go(k_finalize<5>); break;
+    case 6: go(k_finalize<6>); break;
+    case 7: go(k_finalize<7>); break;
+    case 8: go(k_finalize<8>); break;
+    default: fail(BO_ERR_INVALID_CONFIG, "resident micro count outside 2..8");
+  }
   check_launch(c, "k_finalize");
 }
 

@@ -67,11 +67,11 @@ bo_status bo_train_step(bo_ctx* c, const uint16_t* const* grads) {
     aligned &= (reinterpret_cast<uintptr_t>(grads[i]) & 15u) == 0;
   }
   // The resident-micro kernels read all K gradient sets in the sync pass
-  // (no accumulator round trips): one rank's fused path and the ring. Other
-  // configurations (NCCL wire, unaligned slots, K == 1, K > 8) take the
-  // per-micro path; the results are identical either way.
-  const bool resident = K > 1 && K <= kMaxResident && aligned &&
-                        (c->world == 1 ? !c->force_unfused : c->algo == BO_REDUCE_RING);
+  // (no accumulator round trips): one rank's fused path, the ring hops, the
+  // NCCL wire's finalize. Other configurations (unaligned slots, K == 1,
+  // K > 8, the one-rank staged fallback) take the per-micro path; the
+  // results are identical either way.
+  const bool resident = K > 1 && K <= kMaxResident && aligned && (c->world > 1 || !c->force_unfused);
   if (!resident) {
     for (int k = 0; k < K; ++k) {
       const bo_status st = bo_accumulate(c, k, grads + static_cast<size_t>(k) * T);
@@ -97,6 +97,7 @@ bo_status bo_train_step(bo_ctx* c, const uint16_t* const* grads) {
       c->path |= BO_PATH_ONE_RANK_FUSED;
       run_fused_single_rank(c, tab, c->ms);
     } else {
+      if (c->algo == BO_REDUCE_NCCL) launch_finalize(c, tab);  // the fusion buffer from the K micros
       run_reduce(c, tab);
       run_lamb(c, tab);
     }

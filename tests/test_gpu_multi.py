@@ -63,9 +63,8 @@ def test_two_gpus(case):
     else:
         assert "nccl_reduce_scatter" in res["path"]
     assert ("overlap" in res["path"]) == case.endswith("_overlap")
-    # bo_train_step reads the resident micros on the ring; the NCCL wire takes
-    # the per-micro path inside the call (same results)
-    assert ("resident_micros" in res["path"]) == (case.endswith("_resident") and case.startswith("ring"))
+    # bo_train_step reads the resident micros (ring hops, NCCL-wire finalize)
+    assert ("resident_micros" in res["path"]) == case.endswith("_resident")
     # staged hops push into the right neighbour's buffer unless BO_RING_PUSH=0;
     # a last hop fused into LAMB phase 1 reads the left neighbour in place
     pushed = case.startswith("ring") and "_pull" not in case and "last_hop_fused" not in res["path"]
