@@ -80,6 +80,8 @@ def main():
     elif args.model == "bert-large":
         from paper_2008_00177_b200.model_spec import BERT_LARGE
         spec = bert_spec(BERT_LARGE)
+    elif args.model == "empty":
+        spec = flat_spec([0, 5, 4097, 0, 3, 1, 8191], first_use=[2, 0, 1, 4, 3, 6, 5])
     elif args.model == "ragged":
         spec = flat_spec([1, 7, 4099, 13, 2, 30000, 3], first_use=[3, 0, 6, 1, 5, 2, 4])
     else:

@@ -71,11 +71,12 @@ def test_two_gpus(case):
     assert ("ring_push" in res["path"]) == pushed
 
 
-@pytest.mark.parametrize("model", ["ragged", "small"])
+@pytest.mark.parametrize("model", ["ragged", "small", "empty"])
 def test_two_gpus_shapes(model):
     if _ngpu() < 2:
         pytest.skip("needs 2 GPUs")
     run_case("ring16", 2, model=model)
+    run_case("ring16_resident", 2, model=model)
 
 
 @pytest.mark.slow

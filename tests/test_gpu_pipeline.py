@@ -63,6 +63,29 @@ def test_tiny_bert_matches_oracle(torch_cuda, oracle, K, aligned):
     assert pipe.path() == (["one_rank_fused"] if aligned else ["one_rank_staged"])
 
 
+@pytest.mark.parametrize("resident", [False, True])
+def test_empty_and_ragged_tensors_match_oracle(torch_cuda, oracle, resident):
+    """Zero-element and ragged tensors (sizes 0, 1, primes, one past a tile)
+    through both step APIs, overflow injected: scale sequence and moments
+    bit-exact, params within the north-star tolerance."""
+    from oracle.oracle import LambConfig as OL, ScalerConfig as OS
+    from paper_2008_00177_b200.model_spec import flat_spec
+    from paper_2008_00177_b200.pipeline import LambConfig, ScalerConfig, TrainerConfig
+    from tests.harness import run_pipeline
+
+    spec = flat_spec([0, 5, 4097, 0, 3, 1, 8191], first_use=[2, 0, 1, 4, 3, 6, 5])
+    P = spec.param_count()
+    p0 = oracle.build_params(spec, 5)
+    inj = [(1, 0, 2, P - 1, 0x7C00)]
+    cfg = TrainerConfig(LambConfig(), 3, 4096, False, 0, ScalerConfig(init_scale=4096.0, growth_interval=2))
+    pipe, su, fi = run_pipeline(spec, cfg, p0, steps=4, injections=inj, resident=resident)
+    ref = oracle.train(spec, p0, 1, 3, 4096, False, OL(), OS(init_scale=4096.0, growth_interval=2), 4,
+                       injections=inj)
+    _compare(pipe, ref, su, fi)
+    assert fi.tolist() == [0, 1, 0, 0]
+    assert ("resident_micros" in pipe.path()) == resident
+
+
 def test_dynamic_scaler_overflow_sequence(torch_cuda, oracle):
     """Config 4 at desk scale: injected inf/NaN plus natural spikes, growth every 4."""
     from oracle.oracle import LambConfig as OL, ScalerConfig as OS

@@ -112,3 +112,15 @@ def test_flat_spec_tensor_boundaries(oracle, reference):
         a = oracle.train(spec, p0, world, 2, 64, f16, LambConfig(), ScalerConfig(), 3)
         b = reference.train(spec, 2, world, 2, 64, f16, LambConfig(), ScalerConfig(), 3)
         assert np.array_equal(a.params.view(np.uint32), b.params.view(np.uint32))
+
+
+def test_empty_tensors(oracle, reference):
+    """Zero-element tensors (an empty bucket member, W = U = 0 -> trust 1)
+    next to ragged ones, worlds 1-4, both wires."""
+    spec = flat_spec([0, 5, 4097, 0, 3], first_use=[2, 0, 1, 4, 3])
+    p0 = oracle.build_params(spec, 3)
+    for world, f16 in ((1, False), (2, True), (3, False), (4, True)):
+        a = oracle.train(spec, p0, world, 2, 4096, f16, LambConfig(), ScalerConfig(), 3)
+        b = reference.train(spec, 3, world, 2, 4096, f16, LambConfig(), ScalerConfig(), 3)
+        assert np.array_equal(a.params.view(np.uint32), b.params.view(np.uint32))
+        assert np.array_equal(a.m.view(np.uint32), b.m.view(np.uint32))
