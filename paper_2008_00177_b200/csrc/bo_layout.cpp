@@ -25,9 +25,15 @@ Layout Layout::build(int T, const int64_t* numel, const int32_t* firsts, uint64_
   L.rank = rank;
   L.own = rank;
   L.numel.assign(numel, numel + T);
+  // Zero-element tensors are legal (the reference's Tensor allows them:
+  // they join a bucket with 0 bytes, own no tiles and get trust ratio 1); a
+  // model without any element is not.
+  int64_t total = 0;
   for (int t = 0; t < T; ++t) {
-    if (numel[t] <= 0) fail(BO_ERR_SHAPE_MISMATCH, "tensor " + std::to_string(t) + " is empty");
+    if (numel[t] < 0) fail(BO_ERR_SHAPE_MISMATCH, "tensor " + std::to_string(t) + " has a negative size");
+    total += numel[t];
   }
+  if (total == 0) fail(BO_ERR_SHAPE_MISMATCH, "the model has no parameter elements");
   L.ready.resize(static_cast<size_t>(T));
   std::iota(L.ready.begin(), L.ready.end(), 0);
   std::stable_sort(L.ready.begin(), L.ready.end(),

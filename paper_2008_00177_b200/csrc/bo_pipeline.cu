@@ -720,6 +720,7 @@ static void lamb_sharded(bo_ctx* c, const PtrTable& tab, const W* in) {
   const P1Args A{c->d_tensors, c->acc, c->cfg.accumulation, invn, c->wsh, c->m, c->v,
                  c->m_alt, c->v_alt, c->u, c->state, c->lamb, c->bc_table, c->tile_part};
   const int grid = (c->n_lamb_tiles * 32 + kWarpTileCTA - 1) / kWarpTileCTA;
+  if (c->n_lamb_tiles > 0)  // a rank of a tiny model can own no element
   k_p1w<W, true, kHop, 1, 4><<<grid, kWarpTileCTA, 0, c->stream>>>(c->d_lamb_tiles, c->n_lamb_tiles,
                                                                   tab, in, A);
   check_launch(c, "k_p1w");
@@ -737,6 +738,7 @@ static void lamb_sharded(bo_ctx* c, const PtrTable& tab, const W* in) {
   }
   {
   StageTimer timer(c, BO_STAGE_LAMB_UPDATE);
+  if (c->n_lamb_tiles > 0)
   k_shard_p2_push<<<c->n_lamb_tiles, kThreads, 0, c->stream>>>(c->d_lamb_tiles, c->wsh, c->u,
                                                               c->state, c->lamb, c->trust,
                                                               c->d_peer_w, c->world);
@@ -774,6 +776,7 @@ void run_lamb(bo_ctx* c, const PtrTable& tab) {
 
 void gather_shard(bo_ctx* c) {
   if (c->world == 1) return;
+  if (c->n_lamb_tiles == 0) return;
   k_gather_shard<<<c->n_lamb_tiles, kThreads, 0, c->stream>>>(c->d_lamb_tiles, c->w, c->wsh);
   check_launch(c, "k_gather_shard");
 }

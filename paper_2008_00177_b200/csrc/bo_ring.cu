@@ -254,6 +254,7 @@ static void nccl_reduce_scatter(bo_ctx* c, int b0, int b1, cudaStream_t st) {
   c->path |= BO_PATH_NCCL_RS;
   BO_NCCL(ncclGroupStart());
   for (int b = b0; b < b1; ++b) {
+    if (c->L.chunk[static_cast<size_t>(b)] == 0) continue;  // a bucket of empty tensors
     BO_NCCL(ncclReduceScatter(c->x + c->L.base[static_cast<size_t>(b)], c->gshard + c->L.shoff[static_cast<size_t>(b)],
                               static_cast<size_t>(c->L.chunk[static_cast<size_t>(b)]), ncclFloat, ncclSum,
                               c->comm, st));

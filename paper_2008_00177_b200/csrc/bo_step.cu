@@ -23,7 +23,9 @@ bo_status bo_accumulate(bo_ctx* c, int32_t micro, const uint16_t* const* grads) 
   bool aligned = true;
   for (int t = 0; t < c->L.T; ++t) {
     tab.p[t] = grads[t];
-    if (!grads[t]) fail(BO_ERR_SHAPE_MISMATCH, "null gradient for tensor " + std::to_string(t));
+    if (!grads[t] && c->L.numel[static_cast<size_t>(t)] > 0) {
+      fail(BO_ERR_SHAPE_MISMATCH, "null gradient for tensor " + std::to_string(t));
+    }
     aligned &= (reinterpret_cast<uintptr_t>(grads[t]) & 15u) == 0;
   }
   if (c->sync_open) fail(BO_ERR_PROTOCOL, "an overlapped sync micro (bo_sync_ready) is in progress");
@@ -62,7 +64,7 @@ bo_status bo_train_step(bo_ctx* c, const uint16_t* const* grads) {
   const int K = c->cfg.accumulation, T = c->L.T;
   bool aligned = true;
   for (int i = 0; i < K * T; ++i) {
-    if (!grads[i]) fail(BO_ERR_SHAPE_MISMATCH, "null gradient for micro " + std::to_string(i / T) +
+    if (!grads[i] && c->L.numel[static_cast<size_t>(i % T)] > 0) fail(BO_ERR_SHAPE_MISMATCH, "null gradient for micro " + std::to_string(i / T) +
                                                    ", tensor " + std::to_string(i % T));
     aligned &= (reinterpret_cast<uintptr_t>(grads[i]) & 15u) == 0;
   }
@@ -134,7 +136,9 @@ bo_status bo_sync_ready(bo_ctx* c, int32_t n, const int32_t* tensors, const uint
   for (int i = 0; i < n; ++i) {
     const int t = tensors[i];
     if (t < 0 || t >= L.T) fail(BO_ERR_SHAPE_MISMATCH, "tensor index out of range");
-    if (!grads[i]) fail(BO_ERR_SHAPE_MISMATCH, "null gradient for tensor " + std::to_string(t));
+    if (!grads[i] && L.numel[static_cast<size_t>(t)] > 0) {
+      fail(BO_ERR_SHAPE_MISMATCH, "null gradient for tensor " + std::to_string(t));
+    }
     if (c->delivered[static_cast<size_t>(t)]) {
       fail(BO_ERR_PROTOCOL, "tensor " + std::to_string(t) + " delivered twice in one sync micro");
     }

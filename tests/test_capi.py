@@ -106,3 +106,25 @@ def test_create_without_device_fails_loudly():
 
     with pytest.raises(NoDevice):
         GradPipeline(bert_spec(BERT_TINY), TrainerConfig())
+
+
+def test_bucket_layout_with_empty_tensors_matches_reference():
+    """Zero-element tensors join the current bucket with 0 bytes, exactly as
+    BucketLayout::build does (trainer.cpp:100-114); a model with no element
+    at all is rejected."""
+    from oracle import oracle as o
+    from paper_2008_00177_b200.model_spec import flat_spec
+
+    spec = flat_spec([0, 5, 4097, 0, 3, 1, 8191], first_use=[2, 0, 1, 4, 3, 6, 5])
+    for bb in (4, 64, 16384, 1 << 20):
+        L = BucketLayout.build(spec, bb)
+        bo, off, ro, be = o.Oracle().bucket_layout(spec.numels(), spec.first_consumer_ids(), bb)
+        assert np.array_equal(L.bucket_of, bo) and np.array_equal(L.offset_of, off)
+        assert np.array_equal(L.ready_order, ro) and np.array_equal(L.bucket_elems, be)
+        if o.reference_available():
+            bo2, off2, ro2, be2, _h = o.Reference().bucket_layout(spec, spec.first_consumer_ids(), bb)
+            assert np.array_equal(L.bucket_of, bo2) and np.array_equal(L.bucket_elems, be2)
+    from paper_2008_00177_b200.errors import ShapeMismatch
+
+    with pytest.raises(ShapeMismatch):
+        BucketLayout.build(flat_spec([0, 0]), 64)
