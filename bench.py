@@ -71,7 +71,7 @@ def parse():
     ap.add_argument("--api", default="train_step", choices=["train_step", "accumulate"],
                     help="train_step: one bo_train_step per step (all K micros resident); "
                          "accumulate: K bo_accumulate calls per step")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=6)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-steps", type=int, default=3)
@@ -439,6 +439,7 @@ def main_b200(args):
             host[k].copy_(bufs[k])
         stage_dev = bufs  # reuse the device slots as the H2D destination
         n_e2e = max(1, min(args.e2e_steps, args.steps))
+        pipelined = args.api == "train_step"
 
         def e2e_step():
             with torch.cuda.stream(stream):
@@ -447,11 +448,44 @@ def main_b200(args):
                 step()
             return pipe.status()  # D2H of the step result (syncs the stream)
 
-        e2e_step()
+        if pipelined:
+            # A training loop that prefetches: step i+1's micro-batches are
+            # copied (own stream, second device slot set) while step i
+            # computes; every step still copies all its inputs from pinned
+            # host memory and reads its result back.
+            bufs2 = [torch.empty(total, dtype=torch.int16, device=f"cuda:{local}") for _ in range(K)]
+            ptrs2 = GradPipeline.make_ptr_array([b.data_ptr() + 2 * s for b in bufs2 for s in slots])
+            sets = [(bufs, all_ptrs), (bufs2, ptrs2)]
+            copy_stream = torch.cuda.Stream()
+            ready = [torch.cuda.Event(), torch.cuda.Event()]
+            free = [torch.cuda.Event(), torch.cuda.Event()]
+
+            def issue_copy(j):
+                with torch.cuda.stream(copy_stream):
+                    copy_stream.wait_event(free[j])  # the step that last read slot set j is done
+                    for k in range(K):
+                        sets[j][0][k].copy_(host[k], non_blocking=True)
+                    ready[j].record(copy_stream)
+
+            def e2e_run(n):
+                issue_copy(0)
+                for i in range(n):
+                    j = i % 2
+                    stream.wait_event(ready[j])
+                    pipe.train_step_ptr_array(sets[j][1])
+                    free[j].record(stream)
+                    if i + 1 < n:
+                        issue_copy(1 - j)
+                    pipe.status()  # D2H of step i's result (syncs the pipeline stream only)
+        else:
+            def e2e_run(n):
+                for _ in range(n):
+                    e2e_step()
+
+        e2e_run(1)
         barrier()
         t0 = time.perf_counter()
-        for _ in range(n_e2e):
-            e2e_step()
+        e2e_run(n_e2e)
         barrier()
         e2e_s = (time.perf_counter() - t0) / n_e2e
         if world > 1:
@@ -460,7 +494,9 @@ def main_b200(args):
             e2e_s = float(t.item())
         e2e = {"value": world * P / e2e_s, "unit": UNIT, "ms_per_step": round(e2e_s * 1e3, 3),
                "h2d_bytes_per_step": int(K * total * 2),
-               "d2h_bytes_per_step": int(C.sizeof(C.c_int64) * 5), "steps": n_e2e}
+               "d2h_bytes_per_step": int(C.sizeof(C.c_int64) * 5), "steps": n_e2e,
+               "pipelined": "inputs of step i+1 copied on a second stream into a second slot set "
+                            "while step i computes" if pipelined else None}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
