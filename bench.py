@@ -72,6 +72,8 @@ def parse():
                     help="train_step: one bo_train_step per step (all K micros resident); "
                          "accumulate: K bo_accumulate calls per step")
     ap.add_argument("--e2e-steps", type=int, default=6)
+    ap.add_argument("--e2e-serial", action="store_true",
+                    help="e2e: copy each step's inputs, then compute (no prefetch of the next step)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-steps", type=int, default=3)
@@ -439,7 +441,7 @@ def main_b200(args):
             host[k].copy_(bufs[k])
         stage_dev = bufs  # reuse the device slots as the H2D destination
         n_e2e = max(1, min(args.e2e_steps, args.steps))
-        pipelined = args.api == "train_step"
+        pipelined = args.api == "train_step" and not args.e2e_serial
 
         def e2e_step():
             with torch.cuda.stream(stream):

@@ -228,6 +228,7 @@ struct bo_ctx {
   int micro_tab_cap = 0;              // BO_FUSE_LAST=0/1 overrides the per-world default
   bool ring_via_nccl = false;          // BO_RING_NCCL=1: hops over ncclSend/ncclRecv
   bool ring_push = true;               // BO_RING_PUSH=0: hops pull the left neighbour's buffer
+  bool fuse_push_default = true;       // push form: fuse the (local) last hop into phase 1 by default
   std::vector<void*> ipc_opened;       // peer mappings to close
   int* d_barrier = nullptr;
   void* wire[3] = {nullptr, nullptr, nullptr};  // ring staging (shard-sized)

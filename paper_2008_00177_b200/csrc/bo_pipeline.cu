@@ -368,6 +368,7 @@ struct P1Args {
   LambConsts c;
   const double* bc_table;
   double* tile_part;
+  MicroSrc ms;  // KR > 0: the resident micros (bo_train_step)
 };
 
 // Phase 1 with one WARP per tile (<= 4096 elements, up to 128 per lane): the
@@ -381,7 +382,9 @@ struct P1Args {
 // with x = (h + acc) * inv from the sync micro's binary16 gradient and the
 // accumulator (flatten_param, trainer.cpp:186-203).
 constexpr int kWarpTileCTA = 256;
-template <typename W, bool kIn, bool kX, int U = 2, int kMinBlocks = 4>
+// KR > 0 (with kX): x from the KR resident micros in the reference's order
+// instead of h + acc.
+template <typename W, bool kIn, bool kX, int U = 2, int kMinBlocks = 4, int KR = 0>
 __global__ void __launch_bounds__(kWarpTileCTA, kMinBlocks) k_p1w(const LambTile* __restrict__ tiles,
                                                           int n_tiles,
                                                           const __grid_constant__ PtrTable tab,
@@ -416,6 +419,7 @@ __global__ void __launch_bounds__(kWarpTileCTA, kMinBlocks) k_p1w(const LambTile
   const float* __restrict__ a = nullptr;
   float inv = 0.0f;
   bool vec = true;
+  const uint16_t* hk[KR > 0 ? KR : 1];
   if constexpr (kX) {
     const TensorDev d = A.td[t.t];
     const int64_t e0t = t.w0 - d.flat_off;  // element offset of the tile inside its tensor
@@ -423,6 +427,11 @@ __global__ void __launch_bounds__(kWarpTileCTA, kMinBlocks) k_p1w(const LambTile
     a = A.acc + d.acc_off + e0t;
     inv = __fdiv_rn(1.0f, __fmul_rn(static_cast<float>(K), st->scale));
     vec = ((e0t - t.s0) & 3) == 0 && (reinterpret_cast<uintptr_t>(tab.p[t.t]) & 7) == 0;
+    if constexpr (KR > 0) {
+#pragma unroll
+      for (int k = 0; k < KR; ++k) hk[k] = A.ms.hk[k * A.ms.T + t.t] + e0t;
+      vec = ((e0t - t.s0) & 3) == 0;  // resident slots are 16-byte aligned (bo_train_step)
+    }
   }
   // xs: the flattened gradient before the unscale (h + acc)
   auto grad = [&](float win, float xs) {
@@ -441,7 +450,9 @@ __global__ void __launch_bounds__(kWarpTileCTA, kMinBlocks) k_p1w(const LambTile
   bool bad = false;
   auto scalar = [&](int e) {
     float xs = 0.0f, win = 0.0f;
-    if constexpr (kX) {
+    if constexpr (kX && KR > 0) {
+      xs = micro_sum1(hk, KR, e);
+    } else if constexpr (kX) {
       xs = widen(h[e]);
       if (K > 1) xs = __fadd_rn(xs, a[e]);
     }
@@ -465,6 +476,7 @@ __global__ void __launch_bounds__(kWarpTileCTA, kMinBlocks) k_p1w(const LambTile
     for (int q0 = 0; q0 < sp.nv; q0 += 32 * U) {
       float iv[U][4], av[U][4];
       uint2 hv[U];
+      uint2 hr[U][KR > 0 ? KR : 1];
       float4 wv[U], mv[U], vv[U];
 #pragma unroll
       for (int j = 0; j < U; ++j) {
@@ -479,7 +491,10 @@ __global__ void __launch_bounds__(kWarpTileCTA, kMinBlocks) k_p1w(const LambTile
               iv[j][0] = x.x; iv[j][1] = x.y; iv[j][2] = x.z; iv[j][3] = x.w;
             }
           }
-          if constexpr (kX) {
+          if constexpr (kX && KR > 0) {
+#pragma unroll
+            for (int k = 0; k < KR; ++k) hr[j][k] = ld2u(hk[k] + e, pf);
+          } else if constexpr (kX) {
             hv[j] = ld2u(h + e, pf);
             if (K > 1) {
               const float4 a4 = ld4(a + e, pf);
@@ -500,10 +515,27 @@ __global__ void __launch_bounds__(kWarpTileCTA, kMinBlocks) k_p1w(const LambTile
           const float ma[4] = {mv[j].x, mv[j].y, mv[j].z, mv[j].w};
           const float va[4] = {vv[j].x, vv[j].y, vv[j].z, vv[j].w};
           float ga[4];
+          float xr[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+          if constexpr (kX && KR > 0) {
+            // live + (((0 + g0) + g1) + ... + g_{K-2}) (trainer.cpp:240-244, 196-201)
+            float acc4[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+            for (int k = 0; k + 1 < KR; ++k) {
+              float f[4];
+              widen4(hr[j][k], f);
+#pragma unroll
+              for (int i = 0; i < 4; ++i) acc4[i] = __fadd_rn(acc4[i], f[i]);
+            }
+            widen4(hr[j][KR - 1], xr);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) xr[i] = __fadd_rn(xr[i], acc4[i]);
+          }
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
             float xs = 0.0f, win = 0.0f;
-            if constexpr (kX) {
+            if constexpr (kX && KR > 0) {
+              xs = xr[i];
+            } else if constexpr (kX) {
               const uint32_t hw = i < 2 ? hv[j].x : hv[j].y;
               xs = widen(static_cast<uint16_t>(hw >> (16 * (i & 1))));
               if (K > 1) xs = __fadd_rn(xs, av[j][i]);
@@ -718,11 +750,24 @@ static void lamb_sharded(bo_ctx* c, const PtrTable& tab, const W* in) {
   {
   StageTimer timer(c, BO_STAGE_LAMB_NORMS);
   const P1Args A{c->d_tensors, c->acc, c->cfg.accumulation, invn, c->wsh, c->m, c->v,
-                 c->m_alt, c->v_alt, c->u, c->state, c->lamb, c->bc_table, c->tile_part};
+                 c->m_alt, c->v_alt, c->u, c->state, c->lamb, c->bc_table, c->tile_part, c->ms};
   const int grid = (c->n_lamb_tiles * 32 + kWarpTileCTA - 1) / kWarpTileCTA;
-  if (c->n_lamb_tiles > 0)  // a rank of a tiny model can own no element
-  k_p1w<W, true, kHop, 1, 4><<<grid, kWarpTileCTA, 0, c->stream>>>(c->d_lamb_tiles, c->n_lamb_tiles,
-                                                                  tab, in, A);
+  auto go = [&](auto kern) {
+    kern<<<grid, kWarpTileCTA, 0, c->stream>>>(c->d_lamb_tiles, c->n_lamb_tiles, tab, in, A);
+  };
+  if (c->n_lamb_tiles > 0) {  // a rank of a tiny model can own no element
+    if constexpr (!kHop) {
+      go(k_p1w<W, true, false, 1, 4>);
+    } else if (c->ms.K == 0) {
+      go(k_p1w<W, true, true, 1, 4>);
+    } else if (c->ms.K == 2) {  // the last ring hop fused in, x from the resident micros
+      go(k_p1w<W, true, true, 1, 4, 2>);
+    } else if (c->ms.K == 4) {
+      go(k_p1w<W, true, true, 1, 4, 4>);
+    } else {
+      fail(BO_ERR_INVALID_CONFIG, "fused last hop with resident micros: K must be 2 or 4");
+    }
+  }
   check_launch(c, "k_p1w");
   }
   {

@@ -186,11 +186,17 @@ static void ring_reduce_scatter(bo_ctx* c, const PtrTable& tab, ncclDataType_t d
   // element instead of 6, and the staged last hop measured faster at world 2
   // too (2.93 vs 3.13 ms per step): no fusion there either. Fusing needs the
   // accumulator form of x, so the resident mode never fuses.
-  const bool fuse_last = !c->force_unfused && c->ms.K == 0 &&
-                         (c->fuse_last_hop >= 0 ? c->fuse_last_hop != 0 : (N == 2 && !c->sync_open));
   const bool p2p = c->peer_wire[0][left] && !c->ring_via_nccl;
+  const bool push = p2p && c->ring_push;
+  // Push form: the last hop's input is local (what the left neighbour
+  // pushed), so fusing it into phase 1 costs no NVLink latency there; it is
+  // fused with the per-micro accumulator or K = 2 / 4 resident micros.
+  const bool fuse_ok = push ? (c->ms.K == 0 || c->ms.K == 2 || c->ms.K == 4) : c->ms.K == 0;
+  const bool fuse_default = push ? c->fuse_push_default : N == 2;
+  const bool fuse_last = !c->force_unfused && fuse_ok &&
+                         (c->fuse_last_hop >= 0 ? c->fuse_last_hop != 0 : (fuse_default && !c->sync_open));
   c->path |= p2p ? BO_PATH_RING_P2P : BO_PATH_RING_SENDRECV;
-  if (p2p && c->ring_push && !fuse_last) {
+  if (push) {
     // Push form: every hop writes its output straight into the RIGHT
     // neighbour's staging buffer over NVLink and reads its input locally
     // (what the left neighbour pushed). With every rank sending and
@@ -200,13 +206,18 @@ static void ring_reduce_scatter(bo_ctx* c, const PtrTable& tab, ncclDataType_t d
     // its reader before the next push into it; the last hop completes this
     // rank's owned chunk locally.
     hop(r, nullptr, static_cast<W*>(c->peer_wire[0][right]), 0);
+    c->path |= BO_PATH_RING_PUSH;
     for (int s = 0; s < N - 1; ++s) {
       BO_NCCL(ncclAllReduce(c->d_barrier, c->d_barrier, 1, ncclInt32, ncclSum, c->comm, st));
       const W* in = static_cast<const W*>(c->wire[s % 2]);
+      if (s == N - 2 && fuse_last) {
+        c->ring_last_in = in;  // the last hop runs inside LAMB phase 1, reading locally
+        c->path |= BO_PATH_LAST_HOP_FUSED;
+        return;
+      }
       W* out = s == N - 2 ? static_cast<W*>(c->wire[(s + 1) % 2]) : static_cast<W*>(c->peer_wire[(s + 1) % 2][right]);
       hop((r - s - 1 + 2 * N) % N, in, out, 1);  // chunk added at hop s (collective.hpp:70-71)
     }
-    c->path |= BO_PATH_RING_PUSH;
     c->ring_result = c->wire[(N - 1) % 2];
     return;
   }

@@ -55,25 +55,29 @@ def main():
     case = args.case
     overlap = None
     resident = False
-    if case.endswith("_resident"):
-        resident = True
-        case = case[: -len("_resident")]
-    if case.endswith("_pull"):
-        # ring hops reading the left neighbour's buffer instead of pushing
-        os.environ["BO_RING_PUSH"] = "0"
-        case = case[: -len("_pull")]
-    if case.endswith("_overlap"):
-        # the sync micro delivered through bo_sync_ready in ragged chunks,
-        # with communication groups of ~20k elements (several per step)
-        os.environ["BO_COMM_GROUP_ELEMS"] = "20000"
-        overlap = [1, 5, 2, 17]
-        case = case[: -len("_overlap")]
-    if case.endswith("_unfused"):
-        os.environ["BO_UNFUSED"] = "1"
-        case = case[: -len("_unfused")]
-    elif case.endswith("_fused"):
-        os.environ["BO_FUSE_LAST"] = "1"
-        case = case[: -len("_fused")]
+    # "<case>_<suffix>..." in any order: strip known suffixes until a base case remains
+    while case not in CASES:
+        if case.endswith("_resident"):
+            resident = True
+            case = case[: -len("_resident")]
+        elif case.endswith("_pull"):
+            # ring hops reading the left neighbour's buffer instead of pushing
+            os.environ["BO_RING_PUSH"] = "0"
+            case = case[: -len("_pull")]
+        elif case.endswith("_overlap"):
+            # the sync micro delivered through bo_sync_ready in ragged chunks,
+            # with communication groups of ~20k elements (several per step)
+            os.environ["BO_COMM_GROUP_ELEMS"] = "20000"
+            overlap = [1, 5, 2, 17]
+            case = case[: -len("_overlap")]
+        elif case.endswith("_unfused"):
+            os.environ["BO_UNFUSED"] = "1"
+            case = case[: -len("_unfused")]
+        elif case.endswith("_fused"):
+            os.environ["BO_FUSE_LAST"] = "1"
+            case = case[: -len("_fused")]
+        else:
+            raise SystemExit(f"unknown case {args.case}")
     f16, algo, K, bb, sc, ppm, sexp, exact = CASES[case]
     if args.model == "tiny":
         spec = bert_spec(BERT_TINY)

@@ -48,7 +48,8 @@ def run_case(case, nproc, model="tiny", steps=4):
                                   "ring16_tinybuckets", "ring16_unfused", "ring32_unfused",
                                   "ring16_overlap", "ring32_unfused_overlap", "nccl32_overlap",
                                   "ring16_resident", "ring32_unfused_resident", "nccl32_resident",
-                                  "ring16_pull_resident", "ring32_unfused_pull"])
+                                  "ring16_pull_resident", "ring32_unfused_pull", "ring32_resident",
+                                  "ring16_pull"])
 def test_two_gpus(case):
     if _ngpu() < 2:
         pytest.skip("needs 2 GPUs")
@@ -56,19 +57,22 @@ def test_two_gpus(case):
     if case.startswith("ring"):
         assert res["m_bit_exact"] and res["v_bit_exact"]
         assert "ring_p2p" in res["path"]
-        # world 2 runs the last hop inside LAMB phase 1 unless BO_UNFUSED is set
-        # (and never in the overlapped sync micro or with resident micros)
-        assert ("last_hop_fused" in res["path"]) == \
-            ("_unfused" not in case and "_overlap" not in case and "_resident" not in case)
+        # the last hop runs inside LAMB phase 1 unless BO_UNFUSED is set or the
+        # sync micro is overlapped; push form (default): per-micro or K = 2 / 4
+        # resident micros (ring16: K = 2, ring32: K = 3); pull form: world 2,
+        # per-micro only
+        resident = case.endswith("_resident")
+        k_ok = (not resident) or case.startswith("ring16")
+        fused = "_unfused" not in case and "_overlap" not in case and \
+            (k_ok if "_pull" not in case else not resident)
+        assert ("last_hop_fused" in res["path"]) == fused
     else:
         assert "nccl_reduce_scatter" in res["path"]
     assert ("overlap" in res["path"]) == case.endswith("_overlap")
     # bo_train_step reads the resident micros (ring hops, NCCL-wire finalize)
     assert ("resident_micros" in res["path"]) == case.endswith("_resident")
-    # staged hops push into the right neighbour's buffer unless BO_RING_PUSH=0;
-    # a last hop fused into LAMB phase 1 reads the left neighbour in place
-    pushed = case.startswith("ring") and "_pull" not in case and "last_hop_fused" not in res["path"]
-    assert ("ring_push" in res["path"]) == pushed
+    # hops push into the right neighbour's buffer unless BO_RING_PUSH=0
+    assert ("ring_push" in res["path"]) == (case.startswith("ring") and "_pull" not in case)
 
 
 @pytest.mark.parametrize("model", ["ragged", "small", "empty"])
@@ -93,16 +97,17 @@ def test_two_gpus_bert_large_full_size():
 def test_more_gpus(n):
     if _ngpu() < n:
         pytest.skip(f"needs {n} GPUs")
-    res = run_case("ring16", n)
-    assert res["m_bit_exact"] and res["v_bit_exact"]
-    assert res["path"] == ["ring_p2p", "ring_push"]  # staged last hop beyond world 2
-    res = run_case("ring16_fused", n)
-    assert res["m_bit_exact"] and res["v_bit_exact"]
-    assert "last_hop_fused" in res["path"]
-    res = run_case("ring16_resident", n)
-    assert res["m_bit_exact"] and res["v_bit_exact"]
-    assert res["path"] == ["ring_p2p", "resident_micros", "ring_push"]
-    res = run_case("ring16_pull_resident", n)
-    assert res["m_bit_exact"] and res["v_bit_exact"]
-    assert res["path"] == ["ring_p2p", "resident_micros"]
+    expect = {
+        "ring16": ["ring_p2p", "last_hop_fused", "ring_push"],
+        "ring16_unfused": ["ring_p2p", "ring_push"],
+        "ring16_resident": ["ring_p2p", "last_hop_fused", "resident_micros", "ring_push"],
+        "ring32_resident": ["ring_p2p", "resident_micros", "ring_push"],  # K = 3: staged last hop
+        "ring16_pull_resident": ["ring_p2p", "resident_micros"],
+        "ring16_pull": ["ring_p2p"],  # pull form: staged last hop beyond world 2
+        "ring16_pull_fused": ["ring_p2p", "last_hop_fused"],
+    }
+    for case, path in expect.items():
+        res = run_case(case, n)
+        assert res["m_bit_exact"] and res["v_bit_exact"], case
+        assert res["path"] == path, (case, res["path"])
     run_case("nccl32", n)
