@@ -336,8 +336,10 @@ def main_b200(args):
     # NVLink bytes sent per rank: ring reduce-scatter; the parameter push
     # (k_shard_p2_push stores every updated element into the N-1 other replicas)
     nvl_bytes = {"reduce": (world - 1) / world * E * P, "lamb_update": (world - 1) * 4 * S_shard}
-    if fused_last:
-        nvl_bytes["lamb_norms"] = E * S_shard  # the last hop's read of the left partial
+    if fused_last and "ring_push" not in path:
+        # pull form: the fused last hop reads the left neighbour's partial over
+        # NVLink (push form: it was pushed here by the previous hop; local read)
+        nvl_bytes["lamb_norms"] = E * S_shard
     stages = {}
     for i, name in enumerate(STAGES):
         if stage_n[i] == 0:
