@@ -252,6 +252,7 @@ bo_status bo_create(const bo_trainer_config* cfg, int32_t n_tensors, const int64
   if (const char* e = std::getenv("BO_UNFUSED")) c->force_unfused = std::strcmp(e, "0") != 0;
   if (const char* e = std::getenv("BO_RING_NCCL")) c->ring_via_nccl = std::strcmp(e, "0") != 0;
   if (const char* e = std::getenv("BO_RING_PUSH")) c->ring_push = std::strcmp(e, "0") != 0;
+  if (const char* e = std::getenv("BO_RING_BARRIER")) c->nb_barrier = std::strcmp(e, "nccl") != 0;
   if (const char* e = std::getenv("BO_FUSE_LAST")) c->fuse_last_hop = std::strcmp(e, "0") != 0;
   c->algo = cfg->reduce_algo == BO_REDUCE_AUTO ? (cfg->f16_exchange ? BO_REDUCE_RING : BO_REDUCE_NCCL)
                                                : cfg->reduce_algo;
@@ -399,6 +400,7 @@ bo_status bo_comm_init(bo_ctx* c, const uint8_t* id128) {
   mix(static_cast<uint64_t>(c->algo));
   mix(c->ring_via_nccl ? 1 : 0);
   mix(c->ring_push ? 1 : 0);
+  mix(c->nb_barrier ? 1 : 0);
   mix(c->comm_groups.size());
   for (const auto& g : c->comm_groups) mix(static_cast<uint64_t>(g.b1));
   uint64_t* d = static_cast<uint64_t*>(dev_alloc(c, static_cast<size_t>(2 * c->world + 2) * 8));
@@ -457,6 +459,16 @@ bo_status bo_comm_init(bo_ctx* c, const uint8_t* id128) {
       map_all(c->wire[k], pk);
       for (int j = 0; j < c->world; ++j) c->peer_wire[k][j] = pk[static_cast<size_t>(j)];
     }
+  }
+  if (ring && c->nb_barrier) {
+    // neighbour flags for the barrier between ring hops
+    void* f = dev_alloc(c, 256);
+    std::vector<void*> pf;
+    map_all(f, pf);
+    const int left = (c->rank - 1 + c->world) % c->world, right = (c->rank + 1) % c->world;
+    c->nb_flags = static_cast<unsigned*>(f);
+    c->nb_left_from_right = static_cast<unsigned*>(pf[static_cast<size_t>(left)]) + 1;
+    c->nb_right_from_left = static_cast<unsigned*>(pf[static_cast<size_t>(right)]);
   }
   c->d_peer_w = static_cast<float**>(dev_alloc(c, peers.size() * sizeof(float*)));
   BO_CUDA(cudaMemcpyAsync(c->d_peer_w, peers.data(), peers.size() * sizeof(float*),
@@ -521,6 +533,15 @@ bo_status bo_wait(bo_ctx* c, int64_t timeout_ms) {
                                         std::to_string(waited) + " ms");
     }
     std::this_thread::sleep_for(std::chrono::microseconds(200));
+  }
+  if (c->nb_flags) {
+    // a ring-neighbour barrier gave up waiting (its step was skipped)
+    int32_t timed_out = 0;
+    BO_CUDA(cudaMemcpy(&timed_out, &c->state->ring_timeout, sizeof(timed_out), cudaMemcpyDeviceToHost));
+    if (timed_out) {
+      fail(BO_ERR_PEER_DISCONNECTED, "rank " + std::to_string(c->rank) +
+                                         ": a ring neighbour did not reach the hop barrier");
+    }
   }
   BO_GUARD_END
 }

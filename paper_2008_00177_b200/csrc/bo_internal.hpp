@@ -131,6 +131,7 @@ struct DevState {
   int32_t do_update;
   int32_t local_flag;   // set by LAMB phase 1 on this rank
   int32_t parity;       // which moment buffer set is current (one rank: double-buffered)
+  int32_t ring_timeout; // a ring-neighbour barrier timed out (peer gone)
   double bc1, bc2, ibc1, ibc2;   // bias corrections of the current LAMB step
 };
 
@@ -231,6 +232,13 @@ struct bo_ctx {
   bool fuse_push_default = true;       // push form: fuse the (local) last hop into phase 1 by default
   std::vector<void*> ipc_opened;       // peer mappings to close
   int* d_barrier = nullptr;
+  // ring-neighbour barrier (bo_ring.cu k_ring_barrier): this rank's two flags
+  // [from left, from right] and the matching slots in the neighbours' memory
+  unsigned* nb_flags = nullptr;
+  unsigned* nb_left_from_right = nullptr;
+  unsigned* nb_right_from_left = nullptr;
+  uint64_t nb_epoch = 0;
+  bool nb_barrier = true;              // BO_RING_BARRIER=nccl: 4-byte NCCL all-reduce instead
   void* wire[3] = {nullptr, nullptr, nullptr};  // ring staging (shard-sized)
   double* tile_part = nullptr;    // [n_lamb_tiles][2]
   double* rank_part = nullptr;    // [2T+1]

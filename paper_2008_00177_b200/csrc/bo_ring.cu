@@ -134,12 +134,54 @@ __global__ void __launch_bounds__(kThreads) k_hopx(const HopXTile* __restrict__ 
   }
 }
 
+// Neighbour barrier between ring hops: this rank's previous hop kernel has
+// completed (stream order), so its stores — including the NVLink pushes — are
+// performed; publish that to both ring neighbours (a flag in each of their
+// memories) and wait until both have published the same epoch. A hop only
+// exchanges data with its neighbours (reads what the left pushed, pushes into
+// the right's buffer after the right read it), so this replaces a global
+// barrier. The wait is bounded: a peer that never arrives raises the step's
+// overflow flag (the step is skipped, no hang) and bo_wait reports it.
+__global__ void k_ring_barrier(unsigned* left_from_right, unsigned* right_from_left, const unsigned* mine,
+                               unsigned epoch, DevState* st) {
+  __threadfence_system();
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(left_from_right), "r"(epoch) : "memory");
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(right_from_left), "r"(epoch) : "memory");
+  const long long t0 = clock64();
+  for (int i = 0; i < 2; ++i) {
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(mine + i) : "memory");
+      if (static_cast<int>(v - epoch) >= 0) break;
+      __nanosleep(64);
+    } while (clock64() - t0 < (1ll << 33));  // ~4 s
+    if (static_cast<int>(v - epoch) < 0) {
+      atomicOr(&st->local_flag, 1);
+      st->ring_timeout = 1;
+      return;
+    }
+  }
+}
+
 }  // namespace
 
 // The reference ring's reduce-scatter phase (collective.hpp:65-80, binary16
 // wire collective.cpp:170-190) over buckets [b0, b1), with flatten_param fused
 // into every hop: the local addend x of chunk q is computed from the sync
 // micro's binary16 input and the accumulator as the hop needs it.
+// Barrier before a ring hop: the neighbour flags when mapped, else a 4-byte
+// NCCL all-reduce.
+static void hop_barrier(bo_ctx* c, cudaStream_t st) {
+  if (c->nb_flags) {
+    c->nb_epoch += 1;
+    k_ring_barrier<<<1, 1, 0, st>>>(c->nb_left_from_right, c->nb_right_from_left, c->nb_flags,
+                                    static_cast<unsigned>(c->nb_epoch), c->state);
+    check_launch(c, "k_ring_barrier");
+  } else {
+    BO_NCCL(ncclAllReduce(c->d_barrier, c->d_barrier, 1, ncclInt32, ncclSum, c->comm, st));
+  }
+}
+
 template <typename W>
 static void ring_reduce_scatter(bo_ctx* c, const PtrTable& tab, ncclDataType_t dt, int b0, int b1,
                                 cudaStream_t st) {
@@ -208,7 +250,7 @@ static void ring_reduce_scatter(bo_ctx* c, const PtrTable& tab, ncclDataType_t d
     hop(r, nullptr, static_cast<W*>(c->peer_wire[0][right]), 0);
     c->path |= BO_PATH_RING_PUSH;
     for (int s = 0; s < N - 1; ++s) {
-      BO_NCCL(ncclAllReduce(c->d_barrier, c->d_barrier, 1, ncclInt32, ncclSum, c->comm, st));
+      hop_barrier(c, st);
       const W* in = static_cast<const W*>(c->wire[s % 2]);
       if (s == N - 2 && fuse_last) {
         c->ring_last_in = in;  // the last hop runs inside LAMB phase 1, reading locally
@@ -229,7 +271,7 @@ static void ring_reduce_scatter(bo_ctx* c, const PtrTable& tab, ncclDataType_t d
     // buffer's writer before its reader and its reader before its next writer
     // (buckets of different groups occupy disjoint positions).
     for (int s = 0; s < N - 1; ++s) {
-      BO_NCCL(ncclAllReduce(c->d_barrier, c->d_barrier, 1, ncclInt32, ncclSum, c->comm, st));
+      hop_barrier(c, st);
       const W* in = static_cast<const W*>(c->peer_wire[s % 2][left]);
       if (s == N - 2 && fuse_last) {
         c->ring_last_in = in;  // the last hop runs inside LAMB phase 1

@@ -60,6 +60,10 @@ def main():
         if case.endswith("_resident"):
             resident = True
             case = case[: -len("_resident")]
+        elif case.endswith("_ncclbar"):
+            # a 4-byte NCCL all-reduce between ring hops instead of the neighbour flags
+            os.environ["BO_RING_BARRIER"] = "nccl"
+            case = case[: -len("_ncclbar")]
         elif case.endswith("_pull"):
             # ring hops reading the left neighbour's buffer instead of pushing
             os.environ["BO_RING_PUSH"] = "0"

@@ -49,7 +49,7 @@ def run_case(case, nproc, model="tiny", steps=4):
                                   "ring16_overlap", "ring32_unfused_overlap", "nccl32_overlap",
                                   "ring16_resident", "ring32_unfused_resident", "nccl32_resident",
                                   "ring16_pull_resident", "ring32_unfused_pull", "ring32_resident",
-                                  "ring16_pull"])
+                                  "ring16_pull", "ring16_ncclbar_resident"])
 def test_two_gpus(case):
     if _ngpu() < 2:
         pytest.skip("needs 2 GPUs")
