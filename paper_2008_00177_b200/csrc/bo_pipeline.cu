@@ -629,7 +629,10 @@ __global__ void __launch_bounds__(kThreads) k_shard_p2_push(const LambTile* __re
   const int64_t a1 = (t.w0 + t.len) & ~static_cast<int64_t>(3);
   if (a1 > a0) {
     if (threadIdx.x == 0) {
-      for (int j = 0; j < N; ++j) {
+      // destinations in a per-tile rotated order, so the CTAs of all ranks
+      // spread their pushes over every peer's NVLink ingress at any moment
+      for (int i = 0; i < N; ++i) {
+        const int j = (static_cast<int>(blockIdx.x) + i) % N;
         bulk_s2g(dst[j] + a0, buf + off + (a0 - t.w0), static_cast<uint32_t>(a1 - a0) * 4u);
       }
       asm volatile("cp.async.bulk.commit_group;" ::: "memory");
