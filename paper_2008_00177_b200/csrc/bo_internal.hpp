@@ -204,7 +204,6 @@ struct bo_ctx {
   int* d_fused_tensor_tiles = nullptr;  // [T+1] fused-tile ranges per tensor
   float* u = nullptr;                   // LAMB update scratch
   bool force_unfused = false;           // BO_UNFUSED=1: unfused kernels (one rank: multi-kernel LAMB; ring: staged last hop)
-  unsigned long long fused_epoch = 0;
 
   // device buffers
   float* acc = nullptr;
