@@ -224,10 +224,10 @@ static void ring_reduce_scatter(bo_ctx* c, const PtrTable& tab, ncclDataType_t d
   // at world 4 (0.67 vs 0.62 ms), so the default fuses only at world 2 —
   // and never in the overlapped sync micro, where a staged last hop runs
   // under the caller's backward instead of inside the exposed LAMB.
-  // With the K micros resident (bo_train_step) the hops read 2K bytes per
-  // element instead of 6, and the staged last hop measured faster at world 2
-  // too (2.93 vs 3.13 ms per step): no fusion there either. Fusing needs the
-  // accumulator form of x, so the resident mode never fuses.
+  // That is the pull form (BO_RING_PUSH=0), where it also never fuses with
+  // resident micros (staged measured 2.93 vs 3.13 ms per step at world 2).
+  // The push form (default) fuses at every world size, resident micros
+  // included (world 2: 2.50 vs 2.65 ms, world 4: 2.84 vs 2.89 ms).
   const bool p2p = c->peer_wire[0][left] && !c->ring_via_nccl;
   const bool push = p2p && c->ring_push;
   // Push form: the last hop's input is local (what the left neighbour
