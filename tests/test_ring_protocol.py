@@ -102,3 +102,36 @@ def test_waiting_for_the_left_neighbour_alone_would_race(N):
              and not (a[0] == b[0] and a[1] == b[1] and a[2] == b[2])
              and not (ordered_left_only(a, b) or ordered_left_only(b, a))]
     assert races and all({a[5], b[5]} == {"r", "w"} for a, b in races)
+
+
+def accesses_pull(N, fuse_last):
+    """The pull form (BO_RING_PUSH=0): hop 0 packs into the own buffer 0; hop s
+    reads the LEFT neighbour's buffer s % 2 in place and writes its own
+    buffer (s+1) % 2; a fused last hop reads the left's buffer inside phase 1."""
+    acc = []
+    for r in range(N):
+        left = (r - 1) % N
+        order = 0
+        acc.append((r, 0, order, r, 0, "w"))
+        for s in range(N - 1):
+            seg = s + 1
+            order += 1
+            acc.append((r, seg, order, left, s % 2, "r"))
+            if s == N - 2 and fuse_last:
+                continue
+            acc.append((r, seg, order, r, (s + 1) % 2, "w"))
+        if not fuse_last:
+            acc.append((r, N - 1, order + 1, r, (N - 1) % 2, "r"))
+    return acc
+
+
+@pytest.mark.parametrize("N", range(2, 9))
+@pytest.mark.parametrize("fuse_last", [False, True])
+def test_pull_ring_buffers_race_free(N, fuse_last):
+    acc = accesses_pull(N, fuse_last)
+    for a, b in itertools.combinations(acc, 2):
+        if (a[3], a[4]) != (b[3], b[4]) or (a[5] == "r" and b[5] == "r"):
+            continue
+        if a[0] == b[0] and a[1] == b[1] and a[2] == b[2]:
+            continue
+        assert ordered(a, b, N) or ordered(b, a, N), (N, fuse_last, a, b)
