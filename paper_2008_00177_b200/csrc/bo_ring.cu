@@ -154,7 +154,7 @@ __global__ void k_ring_barrier(unsigned* left_from_right, unsigned* right_from_l
       asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(mine + i) : "memory");
       if (static_cast<int>(v - epoch) >= 0) break;
       __nanosleep(64);
-    } while (clock64() - t0 < (1ll << 33));  // ~4 s
+    } while (clock64() - t0 < (1ll << 36));  // ~35 s at the SM clock
     if (static_cast<int>(v - epoch) < 0) {
       atomicOr(&st->local_flag, 1);
       st->ring_timeout = 1;
