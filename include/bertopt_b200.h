@@ -161,7 +161,8 @@ bo_status bo_synchronize(bo_ctx* ctx);
 /* Watchdog wait (the reference's transport watchdog, transport.cpp:113-132 /
  * 336-383): block until the context's queued work has completed, at most
  * timeout_ms milliseconds (< 0: no limit). BO_ERR_PEER_DISCONNECTED when the
- * communicator reports a remote failure (ncclCommGetAsyncError),
+ * communicator reports a remote failure (ncclCommGetAsyncError) or a ring
+ * neighbour never reached a hop barrier (its step was then skipped),
  * BO_ERR_WATCHDOG_TIMEOUT when the work is still pending at the deadline (a
  * stalled or dead peer keeps a collective from completing). Nothing is
  * cancelled: the caller decides whether to keep waiting or to tear the rank
