@@ -86,8 +86,10 @@ def test_empty_and_ragged_tensors_match_oracle(torch_cuda, oracle, resident):
     assert ("resident_micros" in pipe.path()) == resident
 
 
-def test_dynamic_scaler_overflow_sequence(torch_cuda, oracle):
-    """Config 4 at desk scale: injected inf/NaN plus natural spikes, growth every 4."""
+@pytest.mark.parametrize("resident", [False, True])
+def test_dynamic_scaler_overflow_sequence(torch_cuda, oracle, resident):
+    """Config 4 at desk scale: injected inf/NaN plus natural spikes, growth
+    every 4, 24 steps, through the per-micro API and bo_train_step."""
     from oracle.oracle import LambConfig as OL, ScalerConfig as OS
     from paper_2008_00177_b200.model_spec import BERT_TINY, bert_spec
     from paper_2008_00177_b200.pipeline import LambConfig, ScalerConfig, TrainerConfig
@@ -102,7 +104,8 @@ def test_dynamic_scaler_overflow_sequence(torch_cuda, oracle):
     cfg = TrainerConfig(LambConfig(lr=1e-2), 3, 4096, False, 0, ScalerConfig(**sc))
     # spike exponent 3: |g| = 8..16, overflows binary16 whenever S >= 2^13
     pipe, su, fi = run_pipeline(spec, cfg, p0, steps=24, spike_ppm=3, spike_exp=3,
-                                injections=inj)
+                                injections=inj, resident=resident)
+    assert ("resident_micros" in pipe.path()) == resident
     ref = oracle.train(spec, p0, 1, 3, 4096, False, OL(lr=1e-2), OS(**sc), 24, spike_ppm=3,
                        spike_exp=3, injections=inj)
     assert ref.found_inf.sum() >= 4 and ref.found_inf.sum() < 20
