@@ -83,6 +83,19 @@ def test_two_gpus_shapes(model):
     run_case("ring16_resident", 2, model=model)
 
 
+@pytest.mark.parametrize("case", ["ring16_resident", "ring16"])
+def test_two_gpus_config4_long_run(case):
+    """Config 4 across ranks over 24 steps: natural binary16 overflows (spikes
+    at S = 2^13, growth every 3 steps) and an injected +inf; found_inf, the
+    scale sequence, moments (bit-exact) and parameters (1e-5) against the
+    oracle's world emulation."""
+    if _ngpu() < 2:
+        pytest.skip("needs 2 GPUs")
+    res = run_case(case, 2, steps=24)
+    assert res["m_bit_exact"] and res["v_bit_exact"]
+    assert sum(res["found_inf"]) >= 2 and sum(res["found_inf"]) < 24
+
+
 @pytest.mark.slow
 def test_two_gpus_bert_large_full_size():
     """Config 3 at full size: BERT-large (336M) on two GPUs, binary16 ring,
