@@ -33,6 +33,11 @@ def build(force: bool = False) -> None:
         subprocess.run(["make", "-s", "-C", HERE, "liboracle.so"], check=True)
     if os.path.isdir(REFERENCE_SRC):
         subprocess.run(["make", "-s", "-C", os.path.join(HERE, "ref")], check=True)
+        # the C++ adapter test binary links the product library: build it when
+        # that exists (tests/test_gpu_adapter.py runs it on a GPU box)
+        product = os.path.join(os.path.dirname(HERE), "paper_2008_00177_b200", "libbertopt_b200.so")
+        if os.path.exists(product):
+            subprocess.run(["make", "-s", "-C", os.path.join(HERE, "ref"), "adapter_test"], check=True)
 
 
 @dataclass
