@@ -165,10 +165,6 @@ __global__ void k_ring_barrier(unsigned* left_from_right, unsigned* right_from_l
 
 }  // namespace
 
-// The reference ring's reduce-scatter phase (collective.hpp:65-80, binary16
-// wire collective.cpp:170-190) over buckets [b0, b1), with flatten_param fused
-// into every hop: the local addend x of chunk q is computed from the sync
-// micro's binary16 input and the accumulator as the hop needs it.
 // Barrier before a ring hop: the neighbour flags when mapped, else a 4-byte
 // NCCL all-reduce.
 static void hop_barrier(bo_ctx* c, cudaStream_t st) {
@@ -182,6 +178,10 @@ static void hop_barrier(bo_ctx* c, cudaStream_t st) {
   }
 }
 
+// The reference ring's reduce-scatter phase (collective.hpp:65-80, binary16
+// wire collective.cpp:170-190) over buckets [b0, b1), with flatten_param fused
+// into every hop: the local addend x of chunk q is computed from the sync
+// micro's binary16 input and the accumulator as the hop needs it.
 template <typename W>
 static void ring_reduce_scatter(bo_ctx* c, const PtrTable& tab, ncclDataType_t dt, int b0, int b1,
                                 cudaStream_t st) {
