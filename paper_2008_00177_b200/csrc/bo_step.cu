@@ -64,8 +64,10 @@ bo_status bo_train_step(bo_ctx* c, const uint16_t* const* grads) {
   const int K = c->cfg.accumulation, T = c->L.T;
   bool aligned = true;
   for (int i = 0; i < K * T; ++i) {
-    if (!grads[i] && c->L.numel[static_cast<size_t>(i % T)] > 0) fail(BO_ERR_SHAPE_MISMATCH, "null gradient for micro " + std::to_string(i / T) +
-                                                   ", tensor " + std::to_string(i % T));
+    if (!grads[i] && c->L.numel[static_cast<size_t>(i % T)] > 0) {
+      fail(BO_ERR_SHAPE_MISMATCH,
+           "null gradient for micro " + std::to_string(i / T) + ", tensor " + std::to_string(i % T));
+    }
     aligned &= (reinterpret_cast<uintptr_t>(grads[i]) & 15u) == 0;
   }
   // The resident-micro kernels read all K gradient sets in the sync pass
