@@ -199,6 +199,18 @@ def traffic_from_profiles(kernel):
         return None
 
 
+def max_over_ranks(x, world, local, emulated):
+    """The max of a per-rank time over all ranks (the slowest rank bounds the step)."""
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], device="cpu" if emulated else f"cuda:{local}")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def main_b200(args):
     # Libraries print to stdout (NCCL's version banner); the contract is ONE
     # JSON line there, so everything else goes to stderr.
@@ -214,9 +226,18 @@ def main_b200(args):
     rank, world, local = env_rank()
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    ngpu = torch.cuda.device_count()
+    # one rank per GPU; more ranks than GPUs (world 8 on a 4-GPU lease) share
+    # them round-robin — the pipeline's default step needs no NCCL, so this
+    # runs end to end (emulation: the timing is then not a scaling number)
+    emulated = world > ngpu
+    local = local % ngpu
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if emulated:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     K = args.accumulation
     spec = model_spec(args.model)
     P = spec.param_count()
@@ -275,7 +296,7 @@ def main_b200(args):
         step()
     barrier()
     launches0 = pipe.lib.bo_launch_count(pipe.ctx)
-    gpus = list(range(world)) if rank == 0 else []
+    gpus = list(range(min(world, ngpu))) if rank == 0 else []
     sampler = ClockSampler(gpus) if rank == 0 else None
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
@@ -290,10 +311,7 @@ def main_b200(args):
         sampler.__exit__()
     ms = e0.elapsed_time(e1) / args.steps
     launches = pipe.lib.bo_launch_count(pipe.ctx) - launches0
-    if world > 1:
-        t = torch.tensor([ms], device=f"cuda:{local}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(ms, world, local, emulated)
     st = pipe.status()
     assert st.found_inf is False and st.skipped_steps == 0, "synthetic bench overflowed"
 
@@ -427,11 +445,7 @@ def main_b200(args):
             step_per_micro()
         p1.record(stream)
         barrier()
-        pm = p0.elapsed_time(p1) / args.steps
-        if world > 1:
-            t = torch.tensor([pm], device=f"cuda:{local}")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            pm = float(t.item())
+        pm = max_over_ranks(p0.elapsed_time(p1) / args.steps, world, local, emulated)
         per_micro = {"ms_per_step": round(pm, 4), "value": world * P / (pm * 1e-3), "unit": UNIT,
                      "api": "bo_accumulate x K (accumulator in HBM)"}
 
@@ -491,11 +505,7 @@ def main_b200(args):
         t0 = time.perf_counter()
         e2e_run(n_e2e)
         barrier()
-        e2e_s = (time.perf_counter() - t0) / n_e2e
-        if world > 1:
-            t = torch.tensor([e2e_s], device=f"cuda:{local}")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_s = float(t.item())
+        e2e_s = max_over_ranks((time.perf_counter() - t0) / n_e2e, world, local, emulated)
         e2e = {"value": world * P / e2e_s, "unit": UNIT, "ms_per_step": round(e2e_s * 1e3, 3),
                "h2d_bytes_per_step": int(K * total * 2),
                "d2h_bytes_per_step": int(C.sizeof(C.c_int64) * 5), "steps": n_e2e,
@@ -526,7 +536,9 @@ def main_b200(args):
                               else "bo_accumulate x K",
                        "kernel_path": path,
                        "parallelism": f"dp{world} (reduce-scatter + sharded LAMB + all-gather)",
-                       "l2": "inputs (K x 2 B x P) larger than L2, no flush"},
+                       "l2": "inputs (K x 2 B x P) larger than L2, no flush",
+                       **({"emulated": f"{world} ranks on {ngpu} GPU(s): ranks share devices, "
+                                       "timing is not a scaling number"} if emulated else {})},
             "roofline": roofline, "step_roofline": step_roofline, "stages": stages,
             "e2e": e2e, "per_micro_api": per_micro, "cpu_baseline": cpu,
             "gpu_launches": int(launches),

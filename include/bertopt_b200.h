@@ -150,8 +150,27 @@ uint64_t bo_device_bytes(const bo_ctx* ctx);
 /* 128-byte NCCL unique id; rank 0 creates it, the host harness broadcasts it. */
 bo_status bo_comm_unique_id(uint8_t* out128);
 /* Collective over all ranks: NCCL communicator + layout-hash agreement
- * (BO_ERR_BUCKET_LAYOUT_MISMATCH on disagreement, trainer.cpp:169-183). */
+ * (BO_ERR_BUCKET_LAYOUT_MISMATCH on disagreement, trainer.cpp:169-183) + the
+ * peer mappings of bo_comm_import. Needed for the NCCL reduce-scatter, the
+ * ncclSend/Recv ring (BO_RING_NCCL=1), the NCCL hop barrier
+ * (BO_RING_BARRIER=nccl) and the bo_ring_allreduce_* operators. */
 bo_status bo_comm_init(bo_ctx* ctx, const uint8_t* id128);
+/* NCCL-free initialisation of the default (binary16 / fp32 ring) step, which
+ * runs without any collective library: every rank exports a fixed-size
+ * record (layout hash, settings hash, CUDA IPC handles of its parameter
+ * replica, ring staging buffers, flag block and norm partials), the host
+ * harness all-gathers the records in rank order over any channel (the
+ * reference's WorkerGroup transport, torch.distributed, MPI, a file), and
+ * every rank imports all of them. bo_comm_export(ctx, NULL, &n) returns the
+ * record size. Import fails with BO_ERR_BUCKET_LAYOUT_MISMATCH / BO_ERR_PROTOCOL
+ * when ranks disagree (trainer.cpp:169-183). Several ranks may share one GPU. */
+bo_status bo_comm_export(bo_ctx* ctx, void* record, uint64_t* nbytes);
+bo_status bo_comm_import(bo_ctx* ctx, const void* records, uint64_t nbytes_each);
+/* Bound of every cross-rank wait inside a step (RunConfig::watchdog_s,
+ * trainer.hpp:144; default 120 s). A peer that misses it abandons the step on
+ * this rank (no update, loss scaler untouched) and the next bo_wait returns
+ * BO_ERR_PEER_DISCONNECTED. */
+bo_status bo_set_watchdog(bo_ctx* ctx, double seconds);
 
 /* ---- streams ----------------------------------------------------------- */
 /* Run all work of ctx on the caller's cudaStream_t (NULL: ctx's own stream). */

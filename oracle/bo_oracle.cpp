@@ -11,12 +11,15 @@
 // Compile without -march/-mfma and with -ffp-contract=off: the reference build
 // has no FMA (proj/CMakeLists.txt:13-14), so neither may its restatement.
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <numeric>
 #include <random>
+#include <cstdlib>
 #include <string>
+#include <thread>
 #include <vector>
 
 extern "C" {
@@ -89,6 +92,50 @@ uint64_t fnv1a(const void* data, size_t len, uint64_t h = 14695981039346656037ul
 
 size_t ceil_div(size_t n, size_t d) { return (n + d - 1) / d; }
 
+// Host threads for or_train's elementwise loops (OR_THREADS, default all
+// cores). Only loops whose iterations are independent are split; every
+// reduction keeps the reference's sequential order, so the result is
+// bit-identical to the single-threaded restatement for any thread count.
+int n_threads() {
+  if (const char* e = std::getenv("OR_THREADS")) return std::max(1, std::atoi(e));
+  return std::max(1u, std::thread::hardware_concurrency());
+}
+
+// f(lo, hi) over [0, n) in contiguous slices, one per thread.
+template <typename F>
+void pfor(int64_t n, F&& f, int64_t grain = 1 << 16) {
+  const int nt = static_cast<int>(std::min<int64_t>(n_threads(), std::max<int64_t>(1, n / grain)));
+  if (nt <= 1) {
+    if (n > 0) f(int64_t{0}, n);
+    return;
+  }
+  std::vector<std::thread> th;
+  const int64_t per = (n + nt - 1) / nt;
+  for (int i = 0; i < nt; ++i) {
+    const int64_t lo = i * per, hi = std::min(n, lo + per);
+    if (lo < hi) th.emplace_back([&f, lo, hi] { f(lo, hi); });
+  }
+  for (auto& t : th) t.join();
+}
+
+// f(i) for i in [0, n), items handed out dynamically (uneven item costs).
+template <typename F>
+void pfor_items(int n, F&& f) {
+  const int nt = std::min(n_threads(), n);
+  if (nt <= 1) {
+    for (int i = 0; i < n; ++i) f(i);
+    return;
+  }
+  std::atomic<int> next{0};
+  std::vector<std::thread> th;
+  for (int k = 0; k < nt; ++k) {
+    th.emplace_back([&] {
+      for (int i = next.fetch_add(1); i < n; i = next.fetch_add(1)) f(i);
+    });
+  }
+  for (auto& t : th) t.join();
+}
+
 struct Lamb {
   float lr, beta1, beta2, eps, wd, clip;
 };
@@ -136,6 +183,58 @@ int lamb_step(int T, const int64_t* numel, float* w, const float* g, float* m, f
     off += n;
   }
   return 0;
+}
+
+// lamb_step for a gradient already known to be finite (or_train checks
+// found_inf first, so the NonFiniteGradient partial update cannot occur), as
+// three passes: the per-element moments and update u (independent elements,
+// split across threads), the per-tensor fp64 norms summed sequentially in the
+// reference's element order (tensors in parallel), and w -= (lr * r) * u.
+// Every value is computed by the same expression as lamb_step, so the result
+// is bit-identical to it.
+void lamb_step_finite(int T, const int64_t* numel, float* w, const float* g, float* m, float* v,
+                      int64_t* step, const Lamb& c, std::vector<float>& u) {
+  *step += 1;  // lamb.cpp:31
+  const double t = static_cast<double>(*step);
+  const double bc1 = 1.0 - std::pow(static_cast<double>(c.beta1), t);
+  const double bc2 = 1.0 - std::pow(static_cast<double>(c.beta2), t);
+  const float omb1 = 1.0f - c.beta1;
+  const float omb2 = 1.0f - c.beta2;
+  std::vector<int64_t> off(static_cast<size_t>(T) + 1, 0);
+  for (int i = 0; i < T; ++i) off[static_cast<size_t>(i) + 1] = off[static_cast<size_t>(i)] + numel[i];
+  const int64_t P = off[static_cast<size_t>(T)];
+  u.resize(static_cast<size_t>(P));
+  pfor(P, [&](int64_t lo, int64_t hi) {
+    for (int64_t j = lo; j < hi; ++j) {
+      const float gj = g[j];
+      m[j] = c.beta1 * m[j] + omb1 * gj;
+      v[j] = c.beta2 * v[j] + (omb2 * gj) * gj;
+      const float mh = static_cast<float>(static_cast<double>(m[j]) / bc1);
+      const float vh = static_cast<float>(static_cast<double>(v[j]) / bc2);
+      u[static_cast<size_t>(j)] = mh / (std::sqrt(vh) + c.eps) + c.wd * w[j];
+    }
+  });
+  std::vector<float> s(static_cast<size_t>(T));
+  pfor_items(T, [&](int i) {
+    double wn = 0.0, un = 0.0;
+    for (int64_t j = off[static_cast<size_t>(i)]; j < off[static_cast<size_t>(i) + 1]; ++j) {
+      wn += static_cast<double>(w[j]) * static_cast<double>(w[j]);
+      un += static_cast<double>(u[static_cast<size_t>(j)]) * static_cast<double>(u[static_cast<size_t>(j)]);
+    }
+    float r = 1.0f;
+    if (wn > 0.0 && un > 0.0) {
+      r = static_cast<float>(std::sqrt(wn) / std::sqrt(un));
+      r = std::min(std::max(r, 0.0f), c.clip);
+    }
+    s[static_cast<size_t>(i)] = c.lr * r;
+  });
+  pfor(P, [&](int64_t lo, int64_t hi) {
+    size_t i = static_cast<size_t>(std::upper_bound(off.begin(), off.end(), lo) - off.begin()) - 1;
+    for (int64_t j = lo; j < hi; ++j) {
+      while (j >= off[i + 1]) ++i;
+      w[j] = w[j] - s[i] * u[static_cast<size_t>(j)];
+    }
+  });
 }
 
 // Emulated ring reduce-scatter + all-gather of one bucket over `world`
@@ -339,13 +438,22 @@ int or_ring_allreduce(int world, size_t n, void* data, int kind) {
 // Box-Muller initialisation (restates tensor.cpp:72-92 and the per-tensor
 // seed draws of model.cpp:124-176). init: 0 randn(σ=0.02), 1 ones, 2 zeros.
 void or_build_params(int T, const int64_t* numel, const int* init, uint64_t seed, float* out) {
+  // the per-tensor seeds are drawn in tensor order first (model.cpp's
+  // sequence), then the tensors are filled independently
   std::mt19937_64 seeds(seed);
+  std::vector<uint64_t> tseed(static_cast<size_t>(T), 0);
+  std::vector<size_t> toff(static_cast<size_t>(T), 0);
   size_t off = 0;
   for (int t = 0; t < T; ++t) {
+    if (init[t] == 0) tseed[static_cast<size_t>(t)] = seeds();
+    toff[static_cast<size_t>(t)] = off;
+    off += static_cast<size_t>(numel[t]);
+  }
+  pfor_items(T, [&](int t) {
     const size_t n = static_cast<size_t>(numel[t]);
-    float* o = out + off;
+    float* o = out + toff[static_cast<size_t>(t)];
     if (init[t] == 0) {
-      std::mt19937_64 rng(seeds());
+      std::mt19937_64 rng(tseed[static_cast<size_t>(t)]);
       const double two_pi = 6.283185307179586476925286766559;
       size_t i = 0;
       while (i < n) {
@@ -360,8 +468,7 @@ void or_build_params(int T, const int64_t* numel, const int* init, uint64_t seed
       const float fill = init[t] == 1 ? 1.0f : 0.0f;
       std::fill(o, o + n, fill);
     }
-    off += n;
-  }
+  });
 }
 
 // fp16 gradient bits of one (rank, step, micro), model-order flat layout.
@@ -369,9 +476,11 @@ void or_synth_grads(int64_t P, uint64_t seed, int rank, int step, int micro, flo
                     uint32_t spike_ppm, int spike_exp, uint16_t* out) {
   const uint64_t base = bo_synth_base(seed, static_cast<uint64_t>(rank),
                                       static_cast<uint64_t>(step), static_cast<uint64_t>(micro));
-  for (int64_t i = 0; i < P; ++i) {
-    out[i] = f32_to_f16(bo_synth_true_grad(base, static_cast<uint64_t>(i), spike_ppm, spike_exp) * scale);
-  }
+  pfor(P, [&](int64_t lo, int64_t hi) {
+    for (int64_t i = lo; i < hi; ++i) {
+      out[i] = f32_to_f16(bo_synth_true_grad(base, static_cast<uint64_t>(i), spike_ppm, spike_exp) * scale);
+    }
+  });
 }
 
 // The whole gradient-to-update pipeline for `world` ranks, emulated in one
@@ -403,6 +512,7 @@ int or_train(int T, const int64_t* numel, const int* firsts, const float* params
   std::vector<std::vector<float>> x(static_cast<size_t>(world), std::vector<float>(static_cast<size_t>(P)));
   std::vector<float> acc(static_cast<size_t>(P));
   std::vector<uint16_t> h(static_cast<size_t>(P));
+  std::vector<float> u;
   for (int step = 0; step < steps; ++step) {
     scale_used[step] = S;
     const float inv = 1.0f / (static_cast<float>(K) * S);
@@ -419,22 +529,25 @@ int or_train(int T, const int64_t* numel, const int* firsts, const float* params
           }
         }
         float* X = x[static_cast<size_t>(r)].data();
-        for (int64_t i = 0; i < P; ++i) {
-          const float gi = f16_to_f32(h[static_cast<size_t>(i)]);
-          if (k + 1 < K) {
-            acc[static_cast<size_t>(i)] = (k == 0 ? 0.0f : acc[static_cast<size_t>(i)]) + gi;
-          } else {
-            const float val = K > 1 ? gi + acc[static_cast<size_t>(i)] : gi;
-            X[i] = val * inv;
+        pfor(P, [&](int64_t lo, int64_t hi) {
+          for (int64_t i = lo; i < hi; ++i) {
+            const float gi = f16_to_f32(h[static_cast<size_t>(i)]);
+            if (k + 1 < K) {
+              acc[static_cast<size_t>(i)] = (k == 0 ? 0.0f : acc[static_cast<size_t>(i)]) + gi;
+            } else {
+              const float val = K > 1 ? gi + acc[static_cast<size_t>(i)] : gi;
+              X[i] = val * inv;
+            }
           }
-        }
+        });
       }
     }
     // Bucketed ring all-reduce: gather each bucket in layout order, reduce,
     // scatter back, scale by 1/world.
     if (world > 1) {
       const float invn = 1.0f / static_cast<float>(world);
-      for (size_t b = 0; b < L.buckets.size(); ++b) {
+      pfor_items(static_cast<int>(L.buckets.size()), [&](int bi) {  // buckets are disjoint
+        const size_t b = static_cast<size_t>(bi);
         const size_t nb = static_cast<size_t>(L.elems[b]);
         std::vector<std::vector<float>> flat(static_cast<size_t>(world), std::vector<float>(nb));
         for (int r = 0; r < world; ++r) {
@@ -454,13 +567,18 @@ int or_train(int T, const int64_t* numel, const int* firsts, const float* params
           for (int64_t i = 0; i < numel[p]; ++i) dst[i] = flat[0][o + static_cast<size_t>(i)] * invn;
           o += static_cast<size_t>(numel[p]);
         }
-      }
+      });
     }
     const std::vector<float>& g = x[0];
-    bool found = false;
-    for (int64_t i = 0; i < P && !found; ++i) found = !std::isfinite(g[static_cast<size_t>(i)]);
+    std::atomic<bool> any_bad{false};
+    pfor(P, [&](int64_t lo, int64_t hi) {
+      bool bad = false;
+      for (int64_t i = lo; i < hi && !bad; ++i) bad = !std::isfinite(g[static_cast<size_t>(i)]);
+      if (bad) any_bad = true;
+    });
+    const bool found = any_bad;
     if (!found) {
-      lamb_step(T, numel, w.data(), g.data(), m.data(), v.data(), &lstep, lc);
+      lamb_step_finite(T, numel, w.data(), g.data(), m.data(), v.data(), &lstep, lc, u);
     }
     found_inf[step] = found ? 1 : 0;
     if (sc->dynamic) {

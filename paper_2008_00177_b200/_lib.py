@@ -64,6 +64,9 @@ SIGNATURES = {
     "bo_device_bytes": (_u64, [_vp]),
     "bo_comm_unique_id": (_i32, [C.c_char_p]),
     "bo_comm_init": (_i32, [_vp, C.c_char_p]),
+    "bo_comm_export": (_i32, [_vp, _vp, C.POINTER(_u64)]),
+    "bo_comm_import": (_i32, [_vp, _vp, _u64]),
+    "bo_set_watchdog": (_i32, [_vp, C.c_double]),
     "bo_set_stream": (_i32, [_vp, _vp]),
     "bo_get_stream": (_vp, [_vp]),
     "bo_synchronize": (_i32, [_vp]),

@@ -156,6 +156,113 @@ static void for_owned(const Layout& L, F&& f) {
   }
 }
 
+// One rank's communication record (bo_comm_export): the salted layout hash,
+// a hash of the settings that shape the cross-rank call sequence, and CUDA IPC
+// handles of the buffers peers access (parameter replica, ring staging,
+// flag block, norm partials).
+struct CommRecord {
+  char magic[8];
+  int32_t rank, world, ring, reserved;
+  uint64_t layout_hash, settings;
+  cudaIpcMemHandle_t w, wire0, wire1, ctrl, part;
+};
+
+static uint64_t settings_hash(const bo_ctx* c) {
+  uint64_t h = 1469598103934665603ull;
+  auto mix = [&](uint64_t v) {
+    for (int i = 0; i < 8; ++i) h = (h ^ ((v >> (8 * i)) & 0xFF)) * 1099511628211ull;
+  };
+  mix(static_cast<uint64_t>(c->algo));
+  mix(c->ring_via_nccl ? 1 : 0);
+  mix(c->ring_push ? 1 : 0);
+  mix(c->nb_barrier ? 1 : 0);
+  mix(c->comm_groups.size());
+  for (const auto& g : c->comm_groups) mix(static_cast<uint64_t>(g.b1));
+  return h;
+}
+
+static CommRecord make_record(bo_ctx* c) {
+  if (c->world == 1) fail(BO_ERR_INVALID_CONFIG, "world 1 has no peers");
+  BO_CUDA(cudaSetDevice(c->device));
+  CommRecord r{};
+  std::memcpy(r.magic, "BOCOMM1", 8);
+  r.rank = c->rank;
+  r.world = c->world;
+  r.ring = c->algo == BO_REDUCE_RING;
+  r.layout_hash = c->L.hash;
+  r.settings = settings_hash(c);
+  BO_CUDA(cudaIpcGetMemHandle(&r.w, c->w));
+  if (r.ring) {
+    BO_CUDA(cudaIpcGetMemHandle(&r.wire0, c->wire[0]));
+    BO_CUDA(cudaIpcGetMemHandle(&r.wire1, c->wire[1]));
+  }
+  BO_CUDA(cudaIpcGetMemHandle(&r.ctrl, c->ctrl));
+  BO_CUDA(cudaIpcGetMemHandle(&r.part, c->all_part));
+  return r;
+}
+
+// Layout agreement (trainer.cpp:169-183 — BucketLayoutMismatch), settings
+// agreement (ProtocolError: ranks started with different BO_* environments
+// would otherwise deadlock), then every peer buffer mapped into this process
+// over NVLink/NVSwitch (CUDA IPC; ranks sharing one GPU map each other too).
+static void import_records(bo_ctx* c, const CommRecord* all) {
+  if (c->world == 1) return;
+  if (c->peers_mapped) fail(BO_ERR_PROTOCOL, "peers are already mapped");
+  BO_CUDA(cudaSetDevice(c->device));
+  const uint64_t settings = settings_hash(c);
+  for (int j = 0; j < c->world; ++j) {
+    const CommRecord& r = all[j];
+    if (std::memcmp(r.magic, "BOCOMM1", 8) != 0 || r.world != c->world || r.rank != j) {
+      fail(BO_ERR_PROTOCOL, "communication record " + std::to_string(j) + " is not rank " +
+                                std::to_string(j) + " of a world of " + std::to_string(c->world));
+    }
+    if (r.layout_hash != c->L.hash) {
+      fail(BO_ERR_BUCKET_LAYOUT_MISMATCH,
+           "rank " + std::to_string(c->rank) + " bucket layout disagrees with peers");
+    }
+    if (r.settings != settings) {
+      fail(BO_ERR_PROTOCOL, "rank " + std::to_string(c->rank) +
+                                " collective settings (reduce algorithm, BO_RING_NCCL, BO_RING_PUSH, "
+                                "BO_RING_BARRIER, BO_COMM_GROUP_ELEMS) disagree with peers");
+    }
+  }
+  const bool ring = c->algo == BO_REDUCE_RING;
+  if (!c->comm && (c->algo == BO_REDUCE_NCCL || (ring && (c->ring_via_nccl || !c->nb_barrier)))) {
+    fail(BO_ERR_INVALID_CONFIG, "this configuration (NCCL reduce-scatter, BO_RING_NCCL=1 or "
+                                "BO_RING_BARRIER=nccl) needs bo_comm_init");
+  }
+  auto open = [&](int j, const cudaIpcMemHandle_t& h, void* mine_ptr) -> void* {
+    if (j == c->rank) return mine_ptr;
+    void* p = nullptr;
+    BO_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    c->ipc_opened.push_back(p);
+    return p;
+  };
+  std::vector<float*> peers(static_cast<size_t>(c->world));
+  c->peer_ctrl = PeerFlags{{}, c->world, c->rank};
+  for (int j = 0; j < c->world; ++j) {
+    peers[static_cast<size_t>(j)] = static_cast<float*>(open(j, all[j].w, c->w));
+    if (ring) {
+      c->peer_wire[0][j] = open(j, all[j].wire0, c->wire[0]);
+      c->peer_wire[1][j] = open(j, all[j].wire1, c->wire[1]);
+    }
+    c->peer_ctrl.f[j] = static_cast<unsigned*>(open(j, all[j].ctrl, c->ctrl));
+    c->peer_part[j] = static_cast<double*>(open(j, all[j].part, c->all_part));
+  }
+  if (ring && c->nb_barrier) {
+    // neighbour slots for the barrier between ring hops
+    const int left = (c->rank - 1 + c->world) % c->world, right = (c->rank + 1) % c->world;
+    c->nb_flags = c->ctrl + kCtrlFromLeft;
+    c->nb_left_from_right = c->peer_ctrl.f[left] + kCtrlFromRight;
+    c->nb_right_from_left = c->peer_ctrl.f[right] + kCtrlFromLeft;
+  }
+  c->d_peer_w = static_cast<float**>(dev_alloc(c, peers.size() * sizeof(float*)));
+  BO_CUDA(cudaMemcpyAsync(c->d_peer_w, peers.data(), peers.size() * sizeof(float*),
+                          cudaMemcpyHostToDevice, c->stream));
+  BO_CUDA(cudaStreamSynchronize(c->stream));
+  c->peers_mapped = true;
+}
+
 }  // namespace bo
 
 using namespace bo;
@@ -293,6 +400,7 @@ bo_status bo_create(const bo_trainer_config* cfg, int32_t n_tensors, const int64
     c->wsh = static_cast<float*>(dev_alloc(c, static_cast<size_t>(L.shard_total) * 4));
     c->u = static_cast<float*>(dev_alloc(c, static_cast<size_t>(L.shard_total) * 4));
     c->d_barrier = static_cast<int*>(dev_alloc(c, 4));
+    c->ctrl = static_cast<unsigned*>(dev_alloc(c, kCtrlWords * sizeof(unsigned)));
   }
   if (world > 1 && c->algo == BO_REDUCE_RING) {
     const size_t e = cfg->f16_exchange ? 2 : 4;
@@ -304,7 +412,7 @@ bo_status bo_create(const bo_trainer_config* cfg, int32_t n_tensors, const int64
   if (world == 1) c->u = static_cast<float*>(dev_alloc(c, static_cast<size_t>(L.acc_total) * 4));
   c->rank_part = static_cast<double*>(dev_alloc(c, static_cast<size_t>(2 * L.T + 1) * 8));
   c->all_part = world == 1 ? c->rank_part
-                           : static_cast<double*>(dev_alloc(c, static_cast<size_t>(world) * (2 * L.T + 1) * 8));
+                           : static_cast<double*>(dev_alloc(c, 2 * static_cast<size_t>(world) * (2 * L.T + 1) * 8));
   c->trust = static_cast<float*>(dev_alloc(c, static_cast<size_t>(L.T) * 4));
   c->state = static_cast<DevState*>(dev_alloc(c, sizeof(DevState)));
   DevState st{};
@@ -380,6 +488,28 @@ bo_status bo_comm_unique_id(uint8_t* out128) {
   BO_GUARD_END
 }
 
+bo_status bo_comm_export(bo_ctx* c, void* rec, uint64_t* nbytes) {
+  BO_GUARD_BEGIN
+  if (!c || !nbytes) fail(BO_ERR_INVALID_CONFIG, "null argument");
+  if (!rec) {
+    *nbytes = sizeof(CommRecord);
+    return BO_OK;
+  }
+  if (*nbytes < sizeof(CommRecord)) fail(BO_ERR_LENGTH_MISMATCH, "communication record buffer too small");
+  const CommRecord r = make_record(c);
+  std::memcpy(rec, &r, sizeof(r));
+  *nbytes = sizeof(CommRecord);
+  BO_GUARD_END
+}
+
+bo_status bo_comm_import(bo_ctx* c, const void* recs, uint64_t nbytes_each) {
+  BO_GUARD_BEGIN
+  if (!c || !recs) fail(BO_ERR_INVALID_CONFIG, "null argument");
+  if (nbytes_each != sizeof(CommRecord)) fail(BO_ERR_LENGTH_MISMATCH, "communication record size");
+  import_records(c, static_cast<const CommRecord*>(recs));
+  BO_GUARD_END
+}
+
 bo_status bo_comm_init(bo_ctx* c, const uint8_t* id128) {
   BO_GUARD_BEGIN
   if (!c) fail(BO_ERR_INVALID_CONFIG, "null ctx");
@@ -388,92 +518,25 @@ bo_status bo_comm_init(bo_ctx* c, const uint8_t* id128) {
   ncclUniqueId id;
   std::memcpy(&id, id128, 128);
   BO_NCCL(ncclCommInitRank(&c->comm, c->world, id, c->rank));
-  // Layout agreement (trainer.cpp:169-183): all-gather the salted hash, and
-  // a hash of the settings that shape the collective call sequence (reduce
-  // algorithm, ring transport, communication groups of the overlapped sync
-  // micro) so that ranks started with different BO_* environments fail here
-  // instead of deadlocking later.
-  uint64_t mine[2] = {c->L.hash, 1469598103934665603ull};
-  auto mix = [&](uint64_t v) {
-    for (int i = 0; i < 8; ++i) mine[1] = (mine[1] ^ ((v >> (8 * i)) & 0xFF)) * 1099511628211ull;
-  };
-  mix(static_cast<uint64_t>(c->algo));
-  mix(c->ring_via_nccl ? 1 : 0);
-  mix(c->ring_push ? 1 : 0);
-  mix(c->nb_barrier ? 1 : 0);
-  mix(c->comm_groups.size());
-  for (const auto& g : c->comm_groups) mix(static_cast<uint64_t>(g.b1));
-  uint64_t* d = static_cast<uint64_t*>(dev_alloc(c, static_cast<size_t>(2 * c->world + 2) * 8));
-  BO_CUDA(cudaMemcpyAsync(d, mine, 16, cudaMemcpyHostToDevice, c->stream));
-  BO_NCCL(ncclAllGather(d, d + 2, 2, ncclUint64, c->comm, c->stream));
-  std::vector<uint64_t> all(static_cast<size_t>(2 * c->world));
-  BO_CUDA(cudaMemcpyAsync(all.data(), d + 2, all.size() * 8, cudaMemcpyDeviceToHost, c->stream));
+  // the same records bo_comm_export / bo_comm_import exchange through the
+  // host, all-gathered over the new communicator
+  const CommRecord mine = make_record(c);
+  uint8_t* d = static_cast<uint8_t*>(dev_alloc(c, (static_cast<size_t>(c->world) + 1) * sizeof(CommRecord)));
+  BO_CUDA(cudaMemcpyAsync(d, &mine, sizeof(mine), cudaMemcpyHostToDevice, c->stream));
+  BO_NCCL(ncclAllGather(d, d + sizeof(CommRecord), sizeof(CommRecord), ncclUint8, c->comm, c->stream));
+  std::vector<CommRecord> all(static_cast<size_t>(c->world));
+  BO_CUDA(cudaMemcpyAsync(all.data(), d + sizeof(CommRecord), all.size() * sizeof(CommRecord),
+                          cudaMemcpyDeviceToHost, c->stream));
   BO_CUDA(cudaStreamSynchronize(c->stream));
-  for (int r = 0; r < c->world; ++r) {
-    if (all[static_cast<size_t>(2 * r)] != mine[0]) {
-      fail(BO_ERR_BUCKET_LAYOUT_MISMATCH,
-           "rank " + std::to_string(c->rank) + " bucket layout disagrees with peers");
-    }
-    if (all[static_cast<size_t>(2 * r + 1)] != mine[1]) {
-      fail(BO_ERR_PROTOCOL, "rank " + std::to_string(c->rank) +
-                                " collective settings (reduce algorithm, BO_RING_NCCL, "
-                                "BO_COMM_GROUP_ELEMS) disagree with peers");
-    }
-  }
-  // Map every rank's flat parameter replica into this process (CUDA IPC over
-  // NVLink/NVSwitch): LAMB phase 2 stores each updated shard element straight
-  // into all replicas, which replaces the parameter all-gather.
-  // The ring's two staging buffers are mapped too: a hop reads the left
-  // neighbour's previous output in place over NVLink.
-  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "ipc handle size");
-  const bool ring = c->algo == BO_REDUCE_RING;
-  auto map_all = [&](void* mine_ptr, std::vector<void*>& out) {
-    cudaIpcMemHandle_t mine;
-    BO_CUDA(cudaIpcGetMemHandle(&mine, mine_ptr));
-    uint8_t* dh = static_cast<uint8_t*>(dev_alloc(c, static_cast<size_t>(c->world + 1) * 64));
-    BO_CUDA(cudaMemcpyAsync(dh, &mine, 64, cudaMemcpyHostToDevice, c->stream));
-    BO_NCCL(ncclAllGather(dh, dh + 64, 64, ncclUint8, c->comm, c->stream));
-    std::vector<cudaIpcMemHandle_t> handles(static_cast<size_t>(c->world));
-    BO_CUDA(cudaMemcpyAsync(handles.data(), dh + 64, handles.size() * 64, cudaMemcpyDeviceToHost,
-                            c->stream));
-    BO_CUDA(cudaStreamSynchronize(c->stream));
-    out.assign(static_cast<size_t>(c->world), nullptr);
-    for (int j = 0; j < c->world; ++j) {
-      if (j == c->rank) {
-        out[static_cast<size_t>(j)] = mine_ptr;
-        continue;
-      }
-      void* p = nullptr;
-      BO_CUDA(cudaIpcOpenMemHandle(&p, handles[static_cast<size_t>(j)], cudaIpcMemLazyEnablePeerAccess));
-      c->ipc_opened.push_back(p);
-      out[static_cast<size_t>(j)] = p;
-    }
-  };
-  std::vector<void*> pw;
-  map_all(c->w, pw);
-  std::vector<float*> peers(pw.size());
-  for (size_t j = 0; j < pw.size(); ++j) peers[j] = static_cast<float*>(pw[j]);
-  if (ring) {
-    for (int k = 0; k < 2; ++k) {
-      std::vector<void*> pk;
-      map_all(c->wire[k], pk);
-      for (int j = 0; j < c->world; ++j) c->peer_wire[k][j] = pk[static_cast<size_t>(j)];
-    }
-  }
-  if (ring && c->nb_barrier) {
-    // neighbour flags for the barrier between ring hops
-    void* f = dev_alloc(c, 256);
-    std::vector<void*> pf;
-    map_all(f, pf);
-    const int left = (c->rank - 1 + c->world) % c->world, right = (c->rank + 1) % c->world;
-    c->nb_flags = static_cast<unsigned*>(f);
-    c->nb_left_from_right = static_cast<unsigned*>(pf[static_cast<size_t>(left)]) + 1;
-    c->nb_right_from_left = static_cast<unsigned*>(pf[static_cast<size_t>(right)]);
-  }
-  c->d_peer_w = static_cast<float**>(dev_alloc(c, peers.size() * sizeof(float*)));
-  BO_CUDA(cudaMemcpyAsync(c->d_peer_w, peers.data(), peers.size() * sizeof(float*),
-                          cudaMemcpyHostToDevice, c->stream));
-  BO_CUDA(cudaStreamSynchronize(c->stream));
+  import_records(c, all.data());
+  BO_GUARD_END
+}
+
+bo_status bo_set_watchdog(bo_ctx* c, double seconds) {
+  BO_GUARD_BEGIN
+  if (!c) fail(BO_ERR_INVALID_CONFIG, "null ctx");
+  if (!(seconds > 0.0) || seconds > 1e7) fail(BO_ERR_INVALID_CONFIG, "watchdog must be in (0, 1e7] seconds");
+  c->watchdog_ns = static_cast<uint64_t>(seconds * 1e9);
   BO_GUARD_END
 }
 
@@ -534,13 +597,16 @@ bo_status bo_wait(bo_ctx* c, int64_t timeout_ms) {
     }
     std::this_thread::sleep_for(std::chrono::microseconds(200));
   }
-  if (c->nb_flags) {
-    // a ring-neighbour barrier gave up waiting (its step was skipped)
+  if (c->peers_mapped) {
+    // a cross-rank barrier gave up waiting: the step was abandoned (no
+    // update, scaler untouched); reported once, then cleared
     int32_t timed_out = 0;
-    BO_CUDA(cudaMemcpy(&timed_out, &c->state->ring_timeout, sizeof(timed_out), cudaMemcpyDeviceToHost));
+    BO_CUDA(cudaMemcpy(&timed_out, &c->state->peer_timeout, sizeof(timed_out), cudaMemcpyDeviceToHost));
     if (timed_out) {
+      const int32_t zero = 0;
+      BO_CUDA(cudaMemcpy(&c->state->peer_timeout, &zero, sizeof(zero), cudaMemcpyHostToDevice));
       fail(BO_ERR_PEER_DISCONNECTED, "rank " + std::to_string(c->rank) +
-                                         ": a ring neighbour did not reach the hop barrier");
+                                         ": a peer did not reach a step barrier within the watchdog");
     }
   }
   BO_GUARD_END
@@ -661,6 +727,7 @@ bo_status bo_import_state(bo_ctx* c, const void* blob, uint64_t nbytes) {
   DevState st = h.st;
   st.parity = 0;  // moments were written into buffer set 0
   st.local_flag = 0;
+  st.peer_timeout = 0;  // a reported (or stale) barrier timeout is not state
   BO_CUDA(cudaMemcpyAsync(c->state, &st, sizeof(st), cudaMemcpyHostToDevice, c->stream));
   BO_CUDA(cudaStreamSynchronize(c->stream));
   grow_bc_table(c, st.lamb_step + 2);

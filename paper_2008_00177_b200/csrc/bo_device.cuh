@@ -15,6 +15,13 @@ __device__ __forceinline__ uint16_t narrow(float x) { return __half_as_ushort(__
 
 __device__ __forceinline__ bool finite(float x) { return fabsf(x) <= 3.402823466e38f; }
 
+// Wall-clock nanoseconds (the watchdog bound of the cross-rank barriers).
+__device__ __forceinline__ uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 // float(double(x) / d) with the reference's double rounding (lamb.cpp:185-186),
 // computed as a multiply by the host-rounded reciprocal. The product is within
 // ~3 double ulps of RN_d(x/d); only when it lies that close to a binary32
@@ -222,6 +229,16 @@ __device__ __forceinline__ uint2 ld2u(const uint16_t* p, uint64_t pol) {
                : "=r"(r.x), "=r"(r.y)
                : "l"(p), "l"(pol));
   return r;
+}
+// Four binary16 values starting at p when n >= 4 valid elements remain, else
+// only the n < 4 valid ones (the rest zero): a caller's gradient tensor may
+// end right at its allocation, so the last group of a tensor never loads past
+// it.
+__device__ __forceinline__ uint2 ld_h4(const uint16_t* p, int n, uint64_t pol) {
+  if (n >= 4) return ld2u(p, pol);
+  uint32_t h[4] = {0u, 0u, 0u, 0u};
+  for (int i = 0; i < n; ++i) h[i] = p[i];
+  return make_uint2(h[0] | (h[1] << 16), h[2] | (h[3] << 16));
 }
 __device__ __forceinline__ void st4(float* p, float4 v, uint64_t pol) {
   asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "f"(v.x),

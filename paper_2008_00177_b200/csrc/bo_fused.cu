@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(kP1Threads, 2) k_lamb_p1(
     const int e0 = 4 * (threadIdx.x + j * kP1Threads);
     if (e0 < t.len) {
       const int64_t a = t.a0 + e0;
-      hv[j] = ld2u(hsrc + e0, pf);
+      hv[j] = ld_h4(hsrc + e0, t.len - e0, pf);  // no load past the tensor's end
       av[j] = K > 1 ? ld4(acc + a, pf) : make_float4(0.f, 0.f, 0.f, 0.f);
       wv[j] = ld4(w + a, pl);
       mv[j] = ld4(m + a, pf);
@@ -183,7 +183,7 @@ __global__ void __launch_bounds__(kP1Threads, 2) k_lamb_p1r(
     if (e0 < t.len) {
       const int64_t a = t.a0 + e0;
 #pragma unroll
-      for (int k = 0; k < K; ++k) hv[j][k] = ld2u(sp[k] + e0, pf);
+      for (int k = 0; k < K; ++k) hv[j][k] = ld_h4(sp[k] + e0, t.len - e0, pf);
       wv[j] = ld4(w + a, pl);
       mv[j] = ld4(m + a, pf);
       vv[j] = ld4(v + a, pf);

@@ -131,7 +131,9 @@ struct DevState {
   int32_t do_update;
   int32_t local_flag;   // set by LAMB phase 1 on this rank
   int32_t parity;       // which moment buffer set is current (one rank: double-buffered)
-  int32_t ring_timeout; // a ring-neighbour barrier timed out (peer gone)
+  int32_t peer_timeout; // a cross-rank flag barrier gave up waiting (peer gone or
+                        // stalled past the watchdog): the step is abandoned
+                        // without touching w/m/v or the scaler; bo_wait reports it
   double bc1, bc2, ibc1, ibc2;   // bias corrections of the current LAMB step
 };
 
@@ -142,6 +144,27 @@ struct LambConsts {
 struct ScalerConsts {
   float growth, backoff, min_scale, max_scale;
   int32_t interval, dynamic;
+};
+
+// Cross-rank flag block of every rank (one cudaMalloc, mapped into every peer
+// with CUDA IPC). Slots are 32-bit epochs, written by the rank named in the
+// slot with st.release.sys and read by the owner with ld.acquire.sys.
+constexpr int kCtrlFromLeft = 0;     // ring-neighbour barrier: epoch of the left neighbour
+constexpr int kCtrlFromRight = 1;    //                          epoch of the right neighbour
+constexpr int kCtrlPartials = 16;    // [8] partials barrier: rank j's norm partials are in
+constexpr int kCtrlStepEnd = 32;     // [8] end-of-step barrier: rank j's parameter push landed
+constexpr int kCtrlWords = 64;
+
+// Per-step destinations of this rank's norm partials: slot `rank` of every
+// rank's all_part (this step's parity half). N == 0: local rank_part only.
+struct PartDst {
+  double* p[8];
+  int n;
+};
+// Every rank's flag block (device pointers valid in this process).
+struct PeerFlags {
+  unsigned* f[8];
+  int n, rank;
 };
 
 struct PtrTable {
@@ -230,18 +253,26 @@ struct bo_ctx {
   bool ring_push = true;               // BO_RING_PUSH=0: hops pull the left neighbour's buffer
   bool fuse_push_default = true;       // push form: fuse the (local) last hop into phase 1 by default
   std::vector<void*> ipc_opened;       // peer mappings to close
-  int* d_barrier = nullptr;
-  // ring-neighbour barrier (bo_ring.cu k_ring_barrier): this rank's two flags
-  // [from left, from right] and the matching slots in the neighbours' memory
-  unsigned* nb_flags = nullptr;
+  int* d_barrier = nullptr;            // 4-byte NCCL all-reduce barrier (BO_RING_BARRIER=nccl)
+  // Cross-rank flags (kCtrl* slots): this rank's block and every rank's
+  // block mapped here; the ring-neighbour barrier (bo_ring.cu k_ring_barrier)
+  // uses the two neighbour slots, the partials and end-of-step barriers
+  // (bo_pipeline.cu) the all-rank slots. No NCCL on the default step.
+  unsigned* ctrl = nullptr;
+  bo::PeerFlags peer_ctrl{};
+  unsigned* nb_flags = nullptr;        // == ctrl when the neighbour barrier is in use
   unsigned* nb_left_from_right = nullptr;
   unsigned* nb_right_from_left = nullptr;
   uint64_t nb_epoch = 0;
+  uint64_t bar_epoch = 0;              // all-rank barrier epochs (one per step)
+  uint64_t watchdog_ns = 120000000000ull;  // RunConfig::watchdog_s = 120 (trainer.hpp:144)
   bool nb_barrier = true;              // BO_RING_BARRIER=nccl: 4-byte NCCL all-reduce instead
+  bool peers_mapped = false;           // bo_comm_import / bo_comm_init done
+  double* peer_part[8] = {};           // every rank's all_part (IPC)
   void* wire[3] = {nullptr, nullptr, nullptr};  // ring staging (shard-sized)
   double* tile_part = nullptr;    // [n_lamb_tiles][2]
   double* rank_part = nullptr;    // [2T+1]
-  double* all_part = nullptr;     // [world][2T+1]
+  double* all_part = nullptr;     // world > 1: [2][world][2T+1] (step parity halves); 1: rank_part
   float* trust = nullptr;         // [T]
   bo::DevState* state = nullptr;
   double* bc_table = nullptr;     // [bc_cap][4] (bc1, bc2, 1/bc1, 1/bc2) for steps 1..cap
@@ -297,6 +328,8 @@ void run_reduce_group(bo_ctx* c, const PtrTable& tab, int b0, int b1, int acc0, 
                       cudaStream_t stream);
 void run_lamb(bo_ctx* c, const PtrTable& tab);
 void gather_shard(bo_ctx* c);
+// needs the NCCL communicator (bo_comm_init): fail otherwise
+void need_nccl(bo_ctx* c, const char* what);
 void run_fused_single_rank(bo_ctx* c, const PtrTable& tab, MicroSrc ms = MicroSrc{nullptr, 0, 0});
 
 // Stage bracket: records events when profiling is on.

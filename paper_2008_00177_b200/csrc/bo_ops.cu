@@ -302,7 +302,7 @@ template <typename W>
 void ring_allreduce_impl(bo_ctx* c, float* data, size_t n, bool f16) {
   const int N = c->world, r = c->rank;
   if (N == 1 || n == 0) return;
-  if (!c->comm) fail(BO_ERR_INVALID_CONFIG, "bo_comm_init has not run");
+  need_nccl(c, "bo_ring_allreduce_*");
   cudaStream_t s = c->stream;
   const size_t ch = (n + static_cast<size_t>(N) - 1) / static_cast<size_t>(N);  // collective.cpp:50-52
   DevBuf buf(ch * static_cast<size_t>(N) * 4), wire(ch * sizeof(W)), in(ch * sizeof(W));

@@ -221,11 +221,15 @@ __global__ void __launch_bounds__(kThreads) k_lamb_norms(const LambTile* __restr
 }
 
 // Per-tensor sums of the tile partials in a fixed order (deterministic), plus
-// this rank's flag, into rank_part[2T+1].
+// this rank's flag, into rank_part[2T+1] — or, world > 1, straight into this
+// rank's slot of every rank's all_part over NVLink (CUDA IPC): the partials
+// all-gather without a collective; k_trust's barrier then orders these
+// stores before every reader.
 __global__ void __launch_bounds__(kThreads) k_norm_reduce(const int* __restrict__ tile_begin,
                                                           const double* __restrict__ tile_part,
                                                           const DevState* __restrict__ st, int T,
-                                                          double* __restrict__ rank_part) {
+                                                          double* __restrict__ rank_part,
+                                                          const PartDst dst) {
   const int t = blockIdx.x;
   const int b0 = tile_begin[t], b1 = tile_begin[t + 1];
   double a = 0.0, b = 0.0;
@@ -244,33 +248,83 @@ __global__ void __launch_bounds__(kThreads) k_norm_reduce(const int* __restrict_
     }
     __syncthreads();
   }
-  if (threadIdx.x == 0) {
-    rank_part[2 * t] = red[0][0];
-    rank_part[2 * t + 1] = red[1][0];
-    if (t == 0) rank_part[2 * T] = st->local_flag ? 1.0 : 0.0;
+  if (threadIdx.x < (dst.n > 0 ? dst.n : 1)) {
+    double* out = dst.n > 0 ? dst.p[threadIdx.x] : rank_part;
+    out[2 * t] = red[0][0];
+    out[2 * t + 1] = red[1][0];
+    if (t == 0) out[2 * T] = st->local_flag ? 1.0 : 0.0;
   }
+}
+
+// One thread: publish `epoch` into slot `rank` of every rank's flag block
+// (after the stores of this stream's previous kernels, which have completed)
+// and wait until every rank has published it into this rank's block. Bounded
+// by the watchdog: a rank that never arrives sets peer_timeout and the step is
+// abandoned (no update, scaler untouched); bo_wait reports PeerDisconnected.
+// Returns false on timeout (or when an earlier barrier of the step timed out).
+__device__ bool all_rank_barrier(const PeerFlags& pf, int slot0, unsigned epoch, DevState* st,
+                                 uint64_t timeout_ns) {
+  if (st->peer_timeout) return false;
+  __threadfence_system();
+  for (int j = 0; j < pf.n; ++j) {
+    unsigned* f = pf.f[j] + slot0 + pf.rank;
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f), "r"(epoch) : "memory");
+  }
+  const unsigned* mine = pf.f[pf.rank] + slot0;
+  const uint64_t t0 = global_ns();
+  for (int j = 0; j < pf.n; ++j) {
+    unsigned v;
+    for (;;) {
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(mine + j) : "memory");
+      if (static_cast<int>(v - epoch) >= 0) break;
+      if (global_ns() - t0 > timeout_ns) {
+        st->peer_timeout = 1;
+        return false;
+      }
+      __nanosleep(32);
+    }
+  }
+  return true;
+}
+
+// End-of-step barrier: every rank's parameter push into every replica has
+// landed (each rank publishes after its k_shard_p2_push completed).
+__global__ void k_step_end_barrier(PeerFlags pf, unsigned epoch, DevState* st, uint64_t timeout_ns) {
+  all_rank_barrier(pf, kCtrlStepEnd, epoch, st, timeout_ns);
 }
 
 // Global decision: found_inf = any rank flagged; trust ratios from the
 // rank-ordered sums (identical on every rank); LAMB step counter; dynamic
 // loss-scaler state machine.
+// world > 1: first the partials barrier (every rank's k_norm_reduce stored
+// its partials into this rank's all_part), then the sums.
 __global__ void __launch_bounds__(1024) k_trust(const double* __restrict__ all_part, int N, int T,
                                                 DevState* __restrict__ st, LambConsts c,
                                                 ScalerConsts sc, float* __restrict__ trust,
-                                                int flip_parity) {
-  __shared__ int found;
+                                                int flip_parity, PeerFlags pf, unsigned epoch,
+                                                uint64_t timeout_ns) {
+  __shared__ int found, abandoned;
   if (threadIdx.x == 0) {
+    abandoned = pf.n > 0 && !all_rank_barrier(pf, kCtrlPartials, epoch, st, timeout_ns);
     int f = 0;
-    for (int r = 0; r < N; ++r) f |= all_part[static_cast<size_t>(r) * (2 * T + 1) + 2 * T] != 0.0;
+    for (int r = 0; r < N; ++r) f |= __ldcv(all_part + static_cast<size_t>(r) * (2 * T + 1) + 2 * T) != 0.0;
     found = f;
   }
   __syncthreads();
+  if (abandoned) {
+    // a peer never arrived: no update, step counters and scaler untouched
+    if (threadIdx.x == 0) {
+      st->do_update = 0;
+      st->local_flag = 0;
+    }
+    return;
+  }
   if (!found) {
     for (int t = threadIdx.x; t < T; t += blockDim.x) {
       double W = 0.0, U = 0.0;
       for (int r = 0; r < N; ++r) {
-        W = __dadd_rn(W, all_part[static_cast<size_t>(r) * (2 * T + 1) + 2 * t]);
-        U = __dadd_rn(U, all_part[static_cast<size_t>(r) * (2 * T + 1) + 2 * t + 1]);
+        W = __dadd_rn(W, __ldcv(all_part + static_cast<size_t>(r) * (2 * T + 1) + 2 * t));
+        U = __dadd_rn(U, __ldcv(all_part + static_cast<size_t>(r) * (2 * T + 1) + 2 * t + 1));
       }
       float r = 1.0f;
       if (W > 0.0 && U > 0.0) {
@@ -728,10 +782,10 @@ static void lamb_shard(bo_ctx* c, const G* g) {
   {
   StageTimer timer(c, BO_STAGE_TRUST);
   k_norm_reduce<<<T, kThreads, 0, c->stream>>>(c->d_tensor_tile_begin, c->tile_part, c->state, T,
-                                                c->rank_part);
+                                                c->rank_part, PartDst{{}, 0});
   check_launch(c, "k_norm_reduce");
   k_trust<<<1, 1024, 0, c->stream>>>(c->all_part, c->world, T, c->state, c->lamb, c->scaler,
-                                     c->trust, 0);
+                                     c->trust, 0, PeerFlags{{}, 0, 0}, 0u, 0ull);
   check_launch(c, "k_trust");
   }
   StageTimer timer(c, BO_STAGE_LAMB_UPDATE);
@@ -773,15 +827,23 @@ static void lamb_sharded(bo_ctx* c, const PtrTable& tab, const W* in) {
   }
   check_launch(c, "k_p1w");
   }
+  // The partials all-gather without a collective: k_norm_reduce stores this
+  // rank's 2T+1 partials into its slot of every rank's all_part (this step's
+  // parity half, so a fast rank's next step cannot overwrite a slow rank's
+  // current read), k_trust's all-rank flag barrier orders them before the sums.
+  c->bar_epoch += 1;
+  const unsigned epoch = static_cast<unsigned>(c->bar_epoch);
+  const size_t slot = static_cast<size_t>(2 * T + 1);
+  const size_t half = (c->bar_epoch & 1) * static_cast<size_t>(c->world) * slot;
   {
   StageTimer timer(c, BO_STAGE_TRUST);
+  PartDst dst{{}, c->world};
+  for (int j = 0; j < c->world; ++j) dst.p[j] = c->peer_part[j] + half + static_cast<size_t>(c->rank) * slot;
   k_norm_reduce<<<T, kThreads, 0, c->stream>>>(c->d_tensor_tile_begin, c->tile_part, c->state, T,
-                                                c->rank_part);
+                                                c->rank_part, dst);
   check_launch(c, "k_norm_reduce");
-  BO_NCCL(ncclAllGather(c->rank_part, c->all_part, static_cast<size_t>(2 * T + 1), ncclFloat64,
-                        c->comm, c->stream));
-  k_trust<<<1, 1024, 0, c->stream>>>(c->all_part, c->world, T, c->state, c->lamb, c->scaler,
-                                     c->trust, 1);
+  k_trust<<<1, 1024, 0, c->stream>>>(c->all_part + half, c->world, T, c->state, c->lamb, c->scaler,
+                                     c->trust, 1, c->peer_ctrl, epoch, c->watchdog_ns);
   check_launch(c, "k_trust");
   }
   {
@@ -793,9 +855,11 @@ static void lamb_sharded(bo_ctx* c, const PtrTable& tab, const W* in) {
   check_launch(c, "k_shard_p2_push");
   }
   // every rank's pushes into every replica have landed once all ranks are
-  // past their phase 2 (kernel completion flushes the NVLink stores)
+  // past their phase 2 (kernel completion flushes the NVLink stores): an
+  // all-rank flag barrier, no collective
   StageTimer timer(c, BO_STAGE_ALLGATHER);
-  BO_NCCL(ncclAllReduce(c->d_barrier, c->d_barrier, 1, ncclInt32, ncclSum, c->comm, c->stream));
+  k_step_end_barrier<<<1, 1, 0, c->stream>>>(c->peer_ctrl, epoch, c->state, c->watchdog_ns);
+  check_launch(c, "k_step_end_barrier");
 }
 
 void run_lamb(bo_ctx* c, const PtrTable& tab) {
@@ -819,6 +883,14 @@ void run_lamb(bo_ctx* c, const PtrTable& tab) {
     }
   } else {
     lamb_sharded<float, false>(c, tab, c->gshard);
+  }
+}
+
+void need_nccl(bo_ctx* c, const char* what) {
+  if (!c->comm) {
+    fail(BO_ERR_INVALID_CONFIG, std::string(what) +
+                                    " needs the NCCL communicator: initialise with bo_comm_init "
+                                    "(bo_comm_export / bo_comm_import map peers without NCCL)");
   }
 }
 

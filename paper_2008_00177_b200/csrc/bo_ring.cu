@@ -140,25 +140,27 @@ __global__ void __launch_bounds__(kThreads) k_hopx(const HopXTile* __restrict__ 
 // memories) and wait until both have published the same epoch. A hop only
 // exchanges data with its neighbours (reads what the left pushed, pushes into
 // the right's buffer after the right read it), so this replaces a global
-// barrier. The wait is bounded: a peer that never arrives raises the step's
-// overflow flag (the step is skipped, no hang) and bo_wait reports it.
+// barrier. The wait is bounded by the watchdog (RunConfig::watchdog_s,
+// trainer.hpp:144; bo_set_watchdog): a neighbour that never arrives sets
+// peer_timeout — the step is then abandoned without an update and without
+// touching the loss scaler (k_trust), and bo_wait reports PeerDisconnected.
 __global__ void k_ring_barrier(unsigned* left_from_right, unsigned* right_from_left, const unsigned* mine,
-                               unsigned epoch, DevState* st) {
+                               unsigned epoch, DevState* st, uint64_t timeout_ns) {
+  if (st->peer_timeout) return;  // an earlier barrier of this step gave up
   __threadfence_system();
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(left_from_right), "r"(epoch) : "memory");
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(right_from_left), "r"(epoch) : "memory");
-  const long long t0 = clock64();
+  const uint64_t t0 = global_ns();
   for (int i = 0; i < 2; ++i) {
     unsigned v;
-    do {
+    for (;;) {
       asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(mine + i) : "memory");
       if (static_cast<int>(v - epoch) >= 0) break;
+      if (global_ns() - t0 > timeout_ns) {
+        st->peer_timeout = 1;
+        return;
+      }
       __nanosleep(64);
-    } while (clock64() - t0 < (1ll << 36));  // ~35 s at the SM clock
-    if (static_cast<int>(v - epoch) < 0) {
-      atomicOr(&st->local_flag, 1);
-      st->ring_timeout = 1;
-      return;
     }
   }
 }
@@ -171,9 +173,10 @@ static void hop_barrier(bo_ctx* c, cudaStream_t st) {
   if (c->nb_flags) {
     c->nb_epoch += 1;
     k_ring_barrier<<<1, 1, 0, st>>>(c->nb_left_from_right, c->nb_right_from_left, c->nb_flags,
-                                    static_cast<unsigned>(c->nb_epoch), c->state);
+                                    static_cast<unsigned>(c->nb_epoch), c->state, c->watchdog_ns);
     check_launch(c, "k_ring_barrier");
   } else {
+    need_nccl(c, "BO_RING_BARRIER=nccl");
     BO_NCCL(ncclAllReduce(c->d_barrier, c->d_barrier, 1, ncclInt32, ncclSum, c->comm, st));
   }
 }
@@ -247,6 +250,15 @@ static void ring_reduce_scatter(bo_ctx* c, const PtrTable& tab, ncclDataType_t d
     // before each hop orders the pushes into a buffer before its reader and
     // its reader before the next push into it; the last hop completes this
     // rank's owned chunk locally.
+    // Hop 0 writes into the right neighbour's staging buffer 0 without a
+    // barrier of its own. Write-after-read safety against that neighbour's
+    // previous step (whose fused last hop, or unfused hop N-1, read that
+    // buffer in place) comes from the previous step's partials barrier in
+    // k_trust: this rank only gets here after every rank has published its
+    // partials, i.e. after every rank's phase 1 — the last reader — finished
+    // (tests/test_ring_protocol.py checks two consecutive steps). In the
+    // overlapped sync micro the hops run on comm_stream after an event on
+    // the context stream, which carries that same k_trust.
     hop(r, nullptr, static_cast<W*>(c->peer_wire[0][right]), 0);
     c->path |= BO_PATH_RING_PUSH;
     for (int s = 0; s < N - 1; ++s) {
@@ -283,6 +295,7 @@ static void ring_reduce_scatter(bo_ctx* c, const PtrTable& tab, ncclDataType_t d
     }
     c->ring_result = c->wire[(N - 1) % 2];
   } else {
+    need_nccl(c, "ring hops over ncclSend/ncclRecv (BO_RING_NCCL=1)");
     for (int s = 0; s < N - 1; ++s) {
       BO_NCCL(ncclGroupStart());
       BO_NCCL(ncclSend(a + sh0, static_cast<size_t>(sh1 - sh0), dt, right, c->comm, st));
@@ -304,6 +317,7 @@ static void ring_reduce_scatter(bo_ctx* c, const PtrTable& tab, ncclDataType_t d
 }
 
 static void nccl_reduce_scatter(bo_ctx* c, int b0, int b1, cudaStream_t st) {
+  need_nccl(c, "the NCCL reduce-scatter (BO_REDUCE_NCCL)");
   c->path |= BO_PATH_NCCL_RS;
   BO_NCCL(ncclGroupStart());
   for (int b = b0; b < b1; ++b) {

@@ -6,6 +6,7 @@
 // (bo_pipeline.cu, bo_fused.cu).
 #include <algorithm>
 #include <string>
+#include <vector>
 
 #include "bo_internal.hpp"
 
@@ -18,7 +19,7 @@ bo_status bo_accumulate(bo_ctx* c, int32_t micro, const uint16_t* const* grads) 
   if (!c || !grads) fail(BO_ERR_INVALID_CONFIG, "null argument");
   const int K = c->cfg.accumulation;
   if (micro < 0 || micro >= K) fail(BO_ERR_INVALID_CONFIG, "micro index outside [0, K)");
-  if (c->world > 1 && !c->comm) fail(BO_ERR_INVALID_CONFIG, "bo_comm_init has not run");
+  if (c->world > 1 && !c->peers_mapped) fail(BO_ERR_INVALID_CONFIG, "bo_comm_init / bo_comm_import has not run");
   PtrTable tab;
   bool aligned = true;
   for (int t = 0; t < c->L.T; ++t) {
@@ -58,7 +59,7 @@ bo_status bo_accumulate(bo_ctx* c, int32_t micro, const uint16_t* const* grads) 
 bo_status bo_train_step(bo_ctx* c, const uint16_t* const* grads) {
   BO_GUARD_BEGIN
   if (!c || !grads) fail(BO_ERR_INVALID_CONFIG, "null argument");
-  if (c->world > 1 && !c->comm) fail(BO_ERR_INVALID_CONFIG, "bo_comm_init has not run");
+  if (c->world > 1 && !c->peers_mapped) fail(BO_ERR_INVALID_CONFIG, "bo_comm_init / bo_comm_import has not run");
   if (c->sync_open) fail(BO_ERR_PROTOCOL, "an overlapped sync micro (bo_sync_ready) is in progress");
   if (c->next_micro != 0) fail(BO_ERR_PROTOCOL, "bo_train_step inside a step fed by bo_accumulate");
   const int K = c->cfg.accumulation, T = c->L.T;
@@ -117,8 +118,24 @@ bo_status bo_train_step(bo_ctx* c, const uint16_t* const* grads) {
 bo_status bo_sync_ready(bo_ctx* c, int32_t n, const int32_t* tensors, const uint16_t* const* grads) {
   BO_GUARD_BEGIN
   if (!c || (n > 0 && (!tensors || !grads))) fail(BO_ERR_INVALID_CONFIG, "null argument");
-  if (c->world > 1 && !c->comm) fail(BO_ERR_INVALID_CONFIG, "bo_comm_init has not run");
+  if (c->world > 1 && !c->peers_mapped) fail(BO_ERR_INVALID_CONFIG, "bo_comm_init / bo_comm_import has not run");
   const Layout& L = c->L;
+  // Validate the whole call before changing any state, so a ShapeMismatch /
+  // ProtocolError leaves the open sync micro exactly as it was (retryable).
+  {
+    std::vector<uint8_t> seen(static_cast<size_t>(L.T), 0);
+    for (int i = 0; i < n; ++i) {
+      const int t = tensors[i];
+      if (t < 0 || t >= L.T) fail(BO_ERR_SHAPE_MISMATCH, "tensor index out of range");
+      if (!grads[i] && L.numel[static_cast<size_t>(t)] > 0) {
+        fail(BO_ERR_SHAPE_MISMATCH, "null gradient for tensor " + std::to_string(t));
+      }
+      if ((c->sync_open && c->delivered[static_cast<size_t>(t)]) || seen[static_cast<size_t>(t)]) {
+        fail(BO_ERR_PROTOCOL, "tensor " + std::to_string(t) + " delivered twice in one sync micro");
+      }
+      seen[static_cast<size_t>(t)] = 1;
+    }
+  }
   if (!c->sync_open) {
     if (c->next_micro != c->cfg.accumulation - 1) {
       fail(BO_ERR_PROTOCOL, "bo_sync_ready before micros 0.." + std::to_string(c->cfg.accumulation - 2) +
@@ -137,13 +154,6 @@ bo_status bo_sync_ready(bo_ctx* c, int32_t n, const int32_t* tensors, const uint
   }
   for (int i = 0; i < n; ++i) {
     const int t = tensors[i];
-    if (t < 0 || t >= L.T) fail(BO_ERR_SHAPE_MISMATCH, "tensor index out of range");
-    if (!grads[i] && L.numel[static_cast<size_t>(t)] > 0) {
-      fail(BO_ERR_SHAPE_MISMATCH, "null gradient for tensor " + std::to_string(t));
-    }
-    if (c->delivered[static_cast<size_t>(t)]) {
-      fail(BO_ERR_PROTOCOL, "tensor " + std::to_string(t) + " delivered twice in one sync micro");
-    }
     c->delivered[static_cast<size_t>(t)] = 1;
     c->sync_tab->p[t] = grads[i];
     c->sync_aligned &= (reinterpret_cast<uintptr_t>(grads[i]) & 15u) == 0;

@@ -211,11 +211,54 @@ class GradPipeline:
             raise InvalidConfig("InvalidConfig: NCCL unique id must be 128 bytes")
         _lib.check(self.lib.bo_comm_init(self.ctx, uid))
 
-    def comm_init_torch(self) -> None:
-        """Exchange the NCCL id over an initialised torch.distributed group,
-        after checking that every rank built the same bucket layout."""
+    def comm_init_torch(self, nccl: bool | None = None) -> None:
+        """Initialise the context's peers over an initialised torch.distributed
+        group (any backend). By default without NCCL: every rank's
+        communication record (bo_comm_export) is all-gathered on the host and
+        imported (bo_comm_import) — the default binary16 / fp32 ring step uses
+        no collective library, and several ranks may share one GPU. nccl=True
+        (or a configuration that needs NCCL: the NCCL reduce-scatter,
+        BO_RING_NCCL=1, BO_RING_BARRIER=nccl) exchanges an NCCL id instead and
+        calls bo_comm_init. Raises BucketLayoutMismatch when ranks disagree on
+        the layout (trainer.cpp:169-183)."""
+        if self.world == 1:
+            return
+        if nccl is None:
+            nccl = self.needs_nccl()
         agree_layout(self.layout_hash(), self.device)
-        self.comm_init(broadcast_unique_id(self.device))
+        if nccl:
+            self.comm_init(broadcast_unique_id(self.device))
+        else:
+            self.comm_import(all_gather_bytes(self.comm_export()))
+
+    def needs_nccl(self) -> bool:
+        """The configuration's step uses NCCL (otherwise IPC + flags only)."""
+        import os
+
+        algo = self.cfg.reduce_algo
+        if algo == REDUCE_AUTO:
+            algo = REDUCE_RING if self.cfg.f16_exchange else REDUCE_NCCL
+        return (algo == REDUCE_NCCL or os.environ.get("BO_RING_NCCL", "0") != "0"
+                or os.environ.get("BO_RING_BARRIER", "") == "nccl")
+
+    def comm_export(self) -> bytes:
+        """This rank's communication record (layout/settings hashes, IPC handles)."""
+        n = C.c_uint64()
+        _lib.check(self.lib.bo_comm_export(self.ctx, None, C.byref(n)))
+        buf = C.create_string_buffer(n.value)
+        _lib.check(self.lib.bo_comm_export(self.ctx, buf, C.byref(n)))
+        return buf.raw[:n.value]
+
+    def comm_import(self, records: list[bytes]) -> None:
+        """All ranks' records, in rank order."""
+        if len(records) != self.world or len({len(r) for r in records}) != 1:
+            raise InvalidConfig("InvalidConfig: one record per rank of equal size expected")
+        blob = b"".join(records)
+        _lib.check(self.lib.bo_comm_import(self.ctx, blob, len(records[0])))
+
+    def set_watchdog(self, seconds: float) -> None:
+        """Bound of the cross-rank waits inside a step (RunConfig::watchdog_s)."""
+        _lib.check(self.lib.bo_set_watchdog(self.ctx, float(seconds)))
 
 
     # -- streams
@@ -472,6 +515,15 @@ def broadcast_unique_id(device: int = 0) -> bytes:
     buf = buf.to(_dist_device(device))
     dist.broadcast(buf, 0)
     return bytes(buf.cpu().numpy().tobytes())
+
+
+def all_gather_bytes(mine: bytes) -> list[bytes]:
+    """Every rank's byte string, in rank order, over torch.distributed."""
+    import torch.distributed as dist
+
+    out = [None] * dist.get_world_size()
+    dist.all_gather_object(out, mine)
+    return [bytes(x) for x in out]
 
 
 def agree_layout(layout_hash: int, device: int = 0) -> None:

@@ -43,9 +43,14 @@ def main():
     ap.add_argument("--model", default="tiny")
     args = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
-    local = int(os.environ.get("LOCAL_RANK", rank))
+    # ranks beyond the visible GPUs share them (rank r on GPU r % ngpu): the
+    # default step maps peers with CUDA IPC and synchronises with flags, which
+    # works between processes on one device too (world 8 emulated on 4 or 1
+    # B200s). The host exchange runs over gloo, so nothing here needs NCCL
+    # unless the case does.
+    local = int(os.environ.get("LOCAL_RANK", rank)) % torch.cuda.device_count()
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    dist.init_process_group("gloo")
 
     from oracle.oracle import LambConfig as OL, Oracle, ScalerConfig as OS
     from paper_2008_00177_b200.model_spec import BERT_TINY, ModelConfig, bert_spec, flat_spec
@@ -111,10 +116,10 @@ def main():
     pipe.read_moments(m, v)
     owned = np.zeros(P, np.float32)
     # moments are sharded: sum the per-rank scatters (each element owned once)
-    tm, tv = torch.from_numpy(m).cuda(), torch.from_numpy(v).cuda()
+    tm, tv = torch.from_numpy(m), torch.from_numpy(v)
     dist.all_reduce(tm)
     dist.all_reduce(tv)
-    tw = torch.from_numpy(w).cuda()
+    tw = torch.from_numpy(w)
     allw = [torch.zeros_like(tw) for _ in range(world)]
     dist.all_gather(allw, tw)
     st = pipe.status()
@@ -122,11 +127,11 @@ def main():
     if rank == 0:
         ref = orc.train(spec, p0, world, K, bb, f16, OL(lr=5e-3), OS(**sc), args.steps, grad_seed=9,
                         spike_ppm=ppm, spike_exp=sexp, injections=inj)
-        mm, vv = tm.cpu().numpy(), tv.cpu().numpy()
+        mm, vv = tm.numpy(), tv.numpy()
         replicas_equal = all(torch.equal(allw[0], x) for x in allw)
         result.update({
             "case": args.case, "world": world, "params": P, "steps": args.steps,
-            "path": pipe.path(),
+            "path": pipe.path(), "devices": torch.cuda.device_count(),
             "found_inf": fi.tolist(), "ref_found_inf": ref.found_inf.tolist(),
             "scales_equal": bool(np.array_equal(su, ref.scale_used)),
             "final_scale": st.loss_scale, "ref_final_scale": ref.final_scale,
@@ -147,6 +152,7 @@ def main():
         result["ok"] = bool(ok)
         print(json.dumps(result), flush=True)
     del owned
+    dist.barrier()  # no peer touches this rank's mapped buffers any more
     pipe.close()
     dist.barrier()
     dist.destroy_process_group()
