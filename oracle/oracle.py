@@ -284,13 +284,14 @@ class Reference:
         L.ref_train.argtypes = [C.POINTER(_Spec), C.c_uint64, C.c_int, C.c_int, C.c_uint64, C.c_int,
                                 C.c_int, _f32p, C.POINTER(_Scaler), C.c_uint64, C.c_uint32, C.c_int,
                                 _i64p, C.c_int, C.c_int, _f32p, _f32p, _f32p, _i64p, _f32p, _i32p,
-                                _f32p, _i32p, C.c_char_p, C.c_int]
+                                _f32p, _i32p, C.c_char_p, C.c_int, C.POINTER(C.c_double)]
         L.ref_stage_bench.argtypes = [C.c_int, _i64p, _i32p, C.c_int, C.c_int, C.c_uint64, C.c_int,
                                       C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double),
-                                      C.POINTER(C.c_double), C.c_char_p, C.c_int]
+                                      C.POINTER(C.c_double), C.c_char_p, C.c_int, C.c_int]
         self._keep = []
 
-    def stage_bench(self, numels, firsts, world, K, bucket_bytes, f16, groups, warmup, steps):
+    def stage_bench(self, numels, firsts, world, K, bucket_bytes, f16, groups, warmup, steps,
+                    shared_micros=False):
         """Wall seconds per timed step (max over all threads) and rank-0 stage seconds."""
         nm = np.asarray(numels, np.int64)
         fs = np.asarray(firsts, np.int32)
@@ -299,7 +300,7 @@ class Reference:
         err = C.create_string_buffer(1024)
         rc = self.lib.ref_stage_bench(len(nm), _ptr(nm, _i64p), _ptr(fs, _i32p), world, K,
                                       bucket_bytes, int(f16), groups, warmup, steps, secs, stages,
-                                      err, 1024)
+                                      err, 1024, int(shared_micros))
         self._check(rc, err)
         return list(secs), list(stages)
 
@@ -389,7 +390,9 @@ class Reference:
 
     def train(self, spec, init_seed, world, K, bucket_bytes, f16_wire, lamb: LambConfig,
               scaler: ScalerConfig, steps, grad_seed=1, spike_ppm=0, spike_exp=1,
-              injections=(), overlap=True) -> TrainResult:
+              injections=(), overlap=True, step_seconds=None) -> TrainResult:
+        """step_seconds: optional list, filled with rank 0's wall seconds of
+        every real train_step call."""
         s = self._spec(spec)
         P = spec.param_count()
         inj = _inj_array(injections)
@@ -401,12 +404,16 @@ class Reference:
         fg = np.empty(1, np.int32)
         sc = _scaler(scaler)
         err = C.create_string_buffer(1024)
+        secs = (C.c_double * steps)()
         rc = self.lib.ref_train(C.byref(s), init_seed, world, K, bucket_bytes, int(f16_wire),
                                 int(overlap), lamb.arr(), C.byref(sc), grad_seed, spike_ppm,
                                 spike_exp, _ptr(inj, _i64p), len(injections), steps, _ptr(po, _f32p),
                                 _ptr(mo, _f32p), _ptr(vo, _f32p), _ptr(ls, _i64p), _ptr(su, _f32p),
-                                _ptr(fi, _i32p), _ptr(fsc, _f32p), _ptr(fg, _i32p), err, 1024)
+                                _ptr(fi, _i32p), _ptr(fsc, _f32p), _ptr(fg, _i32p), err, 1024,
+                                secs)
         self._check(rc, err)
+        if step_seconds is not None:
+            step_seconds[:] = list(secs)
         return TrainResult(po, mo, vo, int(ls[0]), su, fi, float(fsc[0]), int(fg[0]))
 
 

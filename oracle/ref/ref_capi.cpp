@@ -271,12 +271,33 @@ int ref_bucket_layout(const bo_spec_c* spec, const int* firsts, uint64_t bucket_
 // that all host cores are used. seconds[s] is the wall time of timed step s
 // between all-thread barriers; stage_seconds[4] sums rank 0 of group 0's
 // accumulate / flatten / reduce / lamb time over the timed steps.
+// shared_micros: the K fp32 micro-batch gradient sets are generated once and
+// read by every rank thread (rank 0's values) instead of one copy per rank —
+// the same bytes streamed per rank, K x 4 x P bytes less host memory per rank
+// (the full BERT-large workload at world 8 would otherwise need ~110 GB).
 int ref_stage_bench(int T, const int64_t* numels, const int* firsts, int world, int K,
                     uint64_t bucket_bytes, int f16, int groups, int warmup, int steps,
-                    double* seconds, double* stage_seconds, char* err, int errlen) {
+                    double* seconds, double* stage_seconds, char* err, int errlen,
+                    int shared_micros) {
   try {
     if (world < 1 || K < 1 || groups < 1) throw InvalidConfig("bad bench config");
     const int nthreads = groups * world;
+    auto make_micros = [&](int r) {
+      std::vector<std::vector<Tensor>> micro(static_cast<size_t>(K));
+      for (int t = 0; t < T; ++t) {
+        for (int k = 0; k < K; ++k) {
+          std::vector<float> g(static_cast<size_t>(numels[t]));
+          const uint64_t base = bo_synth_base(1, static_cast<uint64_t>(r), 0, static_cast<uint64_t>(k));
+          for (int64_t i = 0; i < numels[t]; ++i) {
+            g[static_cast<size_t>(i)] = bo_synth_true_grad(base, static_cast<uint64_t>(i), 0, 1);
+          }
+          micro[static_cast<size_t>(k)].push_back(Tensor::from({numels[t]}, std::move(g)));
+        }
+      }
+      return micro;
+    };
+    std::vector<std::vector<Tensor>> shared;
+    if (shared_micros) shared = make_micros(0);
     std::vector<std::shared_ptr<InProcHub>> hubs;
     for (int g = 0; g < groups; ++g) hubs.push_back(std::make_shared<InProcHub>(world));
     std::barrier<> bar(nthreads);
@@ -297,19 +318,13 @@ int ref_stage_bench(int T, const int64_t* numels, const int* firsts, int world, 
             wg.transport = tr.get();
           }
           Model m;
-          std::vector<std::vector<Tensor>> micro(static_cast<size_t>(K));
           for (int t = 0; t < T; ++t) {
             m.names.push_back("t" + std::to_string(t));
             m.params.push_back(Tensor::randn({numels[t]}, 1000 + static_cast<uint64_t>(t), 0.02f));
-            for (int k = 0; k < K; ++k) {
-              std::vector<float> g(static_cast<size_t>(numels[t]));
-              const uint64_t base = bo_synth_base(1, static_cast<uint64_t>(r), 0, static_cast<uint64_t>(k));
-              for (int64_t i = 0; i < numels[t]; ++i) {
-                g[static_cast<size_t>(i)] = bo_synth_true_grad(base, static_cast<uint64_t>(i), 0, 1);
-              }
-              micro[static_cast<size_t>(k)].push_back(Tensor::from({numels[t]}, std::move(g)));
-            }
           }
+          std::vector<std::vector<Tensor>> own;
+          if (!shared_micros) own = make_micros(r);
+          const std::vector<std::vector<Tensor>>& micro = shared_micros ? shared : own;
           std::vector<int> fs(firsts, firsts + T);
           const BucketLayout L = BucketLayout::build(m, fs, static_cast<size_t>(bucket_bytes));
           LambState st;
@@ -424,7 +439,8 @@ int ref_train(const bo_spec_c* spec, uint64_t init_seed, int world, int K,
               const bo_scaler_c* sc, uint64_t grad_seed, uint32_t spike_ppm, int spike_exp,
               const int64_t* inj, int n_inj, int steps, float* params_out, float* m_out,
               float* v_out, int64_t* lamb_step_out, float* scale_used, int* found_inf,
-              float* final_scale, int* final_good, char* err, int errlen) {
+              float* final_scale, int* final_good, char* err, int errlen,
+              double* step_seconds) {
   try {
     const refshim::ModelSpec ms = to_spec(spec);
     const int T = spec->n_tensors;
@@ -507,7 +523,14 @@ int ref_train(const bo_spec_c* spec, uint64_t init_seed, int world, int K,
               DistributedTrainer trainer(g, m, tc);
               trainer.state() = saved;
               try {
+                const auto ts0 = std::chrono::steady_clock::now();
                 (void)trainer.train_step(batches);
+                if (r == 0 && step_seconds) {
+                  // rank 0's wall time of the real DistributedTrainer::train_step
+                  // (synthetic forward/backward + accumulate, flatten, ring, lamb_step)
+                  step_seconds[step] =
+                      std::chrono::duration<double>(std::chrono::steady_clock::now() - ts0).count();
+                }
                 saved = trainer.state();
               } catch (const NonFiniteGradient&) {
                 found = true;
