@@ -16,12 +16,12 @@
  *   bo_accumulate (micro=K-1)    flatten_param + reduce_bucket trainer.cpp:186-215
  *                                + unpack + lamb_step          trainer.cpp:356-366
  *                                (the sync micro of train_step trainer.cpp:217-373)
- *   bo_lamb_step                 lamb_step                     lamb.hpp:182-183, lamb.cpp:140-201
+ *   bo_lamb_step                 lamb_step                     lamb.hpp:47-48, lamb.cpp:23-84
  *   bo_ring_allreduce_f32        ring_allreduce<float>         collective.hpp:104-107
  *   bo_ring_allreduce_f16_wire   ring_allreduce_f16_wire       collective.hpp:113-114
- *   bo_unscale_gradients         unscale_gradients             half.hpp:131, half.cpp:105-115
+ *   bo_unscale_gradients         unscale_gradients             half.hpp:77, half.cpp:105-115
  *   bo_narrow_f16 / bo_widen_f16 narrow/widen_f16_block        graph.hpp:160-163
- *   bo_scale_loss                scale_loss                    half.hpp:127
+ *   bo_scale_loss                scale_loss                    half.hpp:73
  *
  * Error convention: every call returns a bo_status whose values map 1:1 onto
  * the bertopt::Error subclasses (errors.hpp:35-48), plus CUDA/NCCL failures.
@@ -59,13 +59,13 @@ typedef enum {
   BO_ERR_NO_DEVICE = 22
 } bo_status;
 
-/* bertopt::LambConfig (lamb.hpp:165-172); defaults via bo_default_config. */
+/* bertopt::LambConfig (lamb.hpp:30-37); defaults via bo_default_config. */
 typedef struct {
   float lr, beta1, beta2, eps, weight_decay, trust_clip;
 } bo_lamb_config;
 
 /* Dynamic loss scaler (builder-defined extension; the reference scaler is
- * static, half.hpp:106-124). Scales stay powers of two. dynamic = 0 keeps
+ * static, half.hpp:52-70). Scales stay powers of two. dynamic = 0 keeps
  * init_scale for the whole run (the reference behaviour). */
 typedef struct {
   float init_scale, growth_factor, backoff_factor, min_scale, max_scale;
@@ -93,7 +93,7 @@ typedef struct {
 typedef struct {
   float loss_scale;       /* scale the NEXT step will use */
   int32_t good_steps;     /* consecutive finite steps since last change */
-  int64_t lamb_step;      /* LambState::step (lamb.hpp:174-178) */
+  int64_t lamb_step;      /* LambState::step (lamb.hpp:39-43) */
   int64_t steps;          /* optimizer steps attempted (incl. skipped) */
   int64_t skipped_steps;  /* steps skipped on overflow */
   int32_t found_inf;      /* last step's global overflow flag */
@@ -173,6 +173,13 @@ bo_status bo_comm_import(bo_ctx* ctx, const void* records, uint64_t nbytes_each)
 bo_status bo_set_watchdog(bo_ctx* ctx, double seconds);
 
 /* ---- streams ----------------------------------------------------------- */
+/* Stream contract: every hot-path call is asynchronous on the context stream
+ * and reads the caller's gradient buffers there; the library does not
+ * synchronise with any other stream. The caller must produce the gradients on
+ * the context stream (bo_set_stream to the producer's stream — the simplest),
+ * or order the context stream after the producer (an event), and keep the
+ * buffers alive and unmodified until the step's work has run (bo_synchronize,
+ * bo_wait, or an event recorded on the context stream). */
 /* Run all work of ctx on the caller's cudaStream_t (NULL: ctx's own stream). */
 bo_status bo_set_stream(bo_ctx* ctx, void* cuda_stream);
 void* bo_get_stream(const bo_ctx* ctx);
@@ -269,7 +276,7 @@ int64_t bo_launch_count(const bo_ctx* ctx);
 int32_t bo_path_flags(const bo_ctx* ctx);
 
 /* ---- operator-level drop-ins -------------------------------------------- */
-/* lamb_step (lamb.cpp:140-201) over device tensors; exact reference numerics
+/* lamb_step (lamb.cpp:23-84) over device tensors; exact reference numerics
  * and error behaviour (step incremented first; on a non-finite gradient the
  * tensors before it are updated and BO_ERR_NON_FINITE_GRADIENT returned). */
 bo_status bo_lamb_step(int32_t n_tensors, const int64_t* numels, float* const* params,
@@ -297,7 +304,7 @@ bo_status bo_fused_optimizer_step(int32_t n_tensors, const int64_t* numels, floa
                                   float lr, float beta1, float beta2, float eps,
                                   float weight_decay, int32_t step, void* stream);
 /* The AMP cast (Tape::cast to f16, ops.cpp:655-668 -> quantize_inplace):
- * x = binary16_RNE(x) in place (f16_round, half.cpp:59-62). */
+ * x = binary16_RNE(x) in place (f16_round, half.cpp:79). */
 bo_status bo_f16_round(float* x, size_t n, void* stream);
 float bo_scale_loss(float loss, float scale, int32_t enabled);
 

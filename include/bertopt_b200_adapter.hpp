@@ -4,13 +4,16 @@
 // tree; nothing in the reference changes. Every bo_status becomes the typed
 // bertopt::Error subclass it mirrors (errors.hpp:35-48).
 //
-//   bertopt::b200::lamb_step          == bertopt::lamb_step      (lamb.hpp:182-183)
-//   bertopt::b200::unscale_gradients  == unscale_gradients       (half.hpp:131)
+//   bertopt::b200::lamb_step          == bertopt::lamb_step      (lamb.hpp:47-48)
+//   bertopt::b200::unscale_gradients  == unscale_gradients       (half.hpp:77)
 //   bertopt::b200::ring_allreduce_f32 / _f16_wire over a device communicator
 //                                     == ring_allreduce / ring_allreduce_f16_wire
 //                                        (collective.hpp:104-114) on host data
 //   bertopt::b200::GradPipeline       the DistributedTrainer gradient-to-update
-//                                     seam (trainer.cpp:186-215, 356-366)
+//                                     seam (trainer.cpp:186-215, 356-366);
+//                                     train_step == DistributedTrainer::train_step
+//                                     (trainer.cpp:217-373) from the K micros'
+//                                     binary16 gradients (the backward's output)
 #ifndef BERTOPT_B200_ADAPTER_HPP_
 #define BERTOPT_B200_ADAPTER_HPP_
 
@@ -71,7 +74,7 @@ inline bo_lamb_config to_c(const LambConfig& c) {
 }
 
 // lamb_step with the reference's argument meaning and error behaviour
-// (lamb.cpp:140-201): lazy zero moments, step incremented first, tensors
+// (lamb.cpp:23-84): lazy zero moments, step incremented first, tensors
 // before a failing one updated, then ShapeMismatch / NonFiniteGradient.
 inline void lamb_step(std::vector<Tensor>& params, const std::vector<Tensor>& grads,
                       LambState& state, const LambConfig& cfg, int device = 0) {
@@ -116,7 +119,7 @@ inline void lamb_step(std::vector<Tensor>& params, const std::vector<Tensor>& gr
     bufs[4 * i].download(params[i].data.data(), bytes);
     bufs[4 * i + 2].download(state.m[i].data.data(), bytes);
     bufs[4 * i + 3].download(state.v[i].data.data(), bytes);
-    quantize_inplace(params[i]);  // lamb.cpp:199
+    quantize_inplace(params[i]);  // lamb.cpp:82
   }
   if (s != BO_OK) raise(s);
   if (ok < params.size()) {
@@ -174,6 +177,8 @@ class GradPipeline {
     std::vector<int32_t> firsts(first_consumers.begin(), first_consumers.end());
     check(bo_create(&cfg, static_cast<int32_t>(numels.size()), numels.data(), firsts.data(),
                     names.data(), ndims.data(), dims.data(), device, rank, world, &ctx_));
+    k_ = tc.accumulation;
+    n_params_ = numels.size();
     std::vector<float> flat;
     for (const Tensor& t : model.params) flat.insert(flat.end(), t.data.begin(), t.data.end());
     check(bo_load_params(ctx_, flat.data(), 1));
@@ -182,9 +187,45 @@ class GradPipeline {
   GradPipeline(const GradPipeline&) = delete;
   GradPipeline& operator=(const GradPipeline&) = delete;
 
+  // NCCL communicator + peer mappings (bo_comm_init), or the NCCL-free pair:
+  // comm_record() from every rank, all-gathered by the caller's transport,
+  // then comm_import(records in rank order).
   void comm_init(const uint8_t* id128) { check(bo_comm_init(ctx_, id128)); }
+  std::vector<uint8_t> comm_record() {
+    uint64_t n = 0;
+    check(bo_comm_export(ctx_, nullptr, &n));
+    std::vector<uint8_t> r(n);
+    check(bo_comm_export(ctx_, r.data(), &n));
+    return r;
+  }
+  void comm_import(const std::vector<std::vector<uint8_t>>& records) {
+    std::vector<uint8_t> all;
+    for (const auto& r : records) {
+      if (r.size() != records[0].size()) throw LengthMismatch("comm_import: record sizes differ");
+      all.insert(all.end(), r.begin(), r.end());
+    }
+    check(bo_comm_import(ctx_, all.data(), records.empty() ? 0 : records[0].size()));
+  }
+  void set_watchdog(double seconds) { check(bo_set_watchdog(ctx_, seconds)); }
   void accumulate(int micro, const std::vector<const uint16_t*>& device_grads) {
     check(bo_accumulate(ctx_, micro, device_grads.data()));
+  }
+  // DistributedTrainer::train_step (trainer.cpp:217-373) from the K micros'
+  // gradients: micros[k][p] is a device pointer to micro k's binary16
+  // gradient of parameter p (loss-scaled by status().loss_scale), all resident
+  // until the step has run. Throws InvalidConfig unless exactly K micros are
+  // given (trainer.cpp:219-221). A non-finite reduced gradient does not throw
+  // here: the step is skipped and the dynamic loss scaler backs off.
+  void train_step(const std::vector<std::vector<const uint16_t*>>& micros) {
+    if (static_cast<int>(micros.size()) != k_) {
+      throw InvalidConfig("train_step expects exactly K micro batches");
+    }
+    std::vector<const uint16_t*> flat;
+    for (const auto& m : micros) {
+      if (m.size() != n_params_) throw ShapeMismatch("train_step: gradient count differs from the model");
+      flat.insert(flat.end(), m.begin(), m.end());
+    }
+    check(bo_train_step(ctx_, flat.data()));
   }
   // TrainerConfig::overlap: the sync micro's gradients as they become final
   // (call from Tape::backward's progress hook, in ready order).
@@ -193,13 +234,30 @@ class GradPipeline {
     check(bo_sync_ready(ctx_, static_cast<int32_t>(params.size()), params.data(), device_grads.data()));
   }
   void read_params(Model& model) {
-    std::vector<float> flat(static_cast<size_t>(model.param_count()));
+    std::vector<float> flat(count(model));
     check(bo_read_params(ctx_, flat.data(), 1));
     size_t off = 0;
     for (Tensor& t : model.params) {
       std::copy_n(flat.data() + off, t.data.size(), t.data.data());
       off += t.data.size();
     }
+  }
+  // LambState m, v of the elements this rank owns (world 1: all), model order.
+  void read_moments(LambState& state, const Model& model) {
+    const size_t P = count(model);
+    std::vector<float> m(P, 0.0f), v(P, 0.0f);
+    check(bo_read_moments(ctx_, m.data(), v.data(), 1));
+    state.m.clear();
+    state.v.clear();
+    size_t off = 0;
+    for (const Tensor& t : model.params) {
+      state.m.push_back(Tensor::zeros(t.shape));
+      state.v.push_back(Tensor::zeros(t.shape));
+      std::copy_n(m.data() + off, t.data.size(), state.m.back().data.data());
+      std::copy_n(v.data() + off, t.data.size(), state.v.back().data.data());
+      off += t.data.size();
+    }
+    state.step = status().lamb_step;
   }
   bo_step_status status() {
     bo_step_status s;
@@ -209,7 +267,14 @@ class GradPipeline {
   bo_ctx* handle() const { return ctx_; }
 
  private:
+  static size_t count(const Model& model) {
+    size_t n = 0;
+    for (const Tensor& t : model.params) n += t.data.size();
+    return n;
+  }
   bo_ctx* ctx_ = nullptr;
+  int k_ = 1;
+  size_t n_params_ = 0;
 };
 
 }  // namespace bertopt::b200

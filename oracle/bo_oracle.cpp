@@ -143,10 +143,10 @@ struct Lamb {
 Lamb lamb_from(const float* c) { return Lamb{c[0], c[1], c[2], c[3], c[4], c[5]}; }
 
 // Returns 0, or 2 (NonFiniteGradient) with the reference's partial-update
-// side effects (restates lamb.cpp:140-201 operation by operation).
+// side effects (restates lamb.cpp:23-84 operation by operation).
 int lamb_step(int T, const int64_t* numel, float* w, const float* g, float* m, float* v,
               int64_t* step, const Lamb& c) {
-  *step += 1;  // lamb.cpp:157 — incremented before any tensor is checked
+  *step += 1;  // lamb.cpp:40 — incremented before any tensor is checked
   const double t = static_cast<double>(*step);
   const double bc1 = 1.0 - std::pow(static_cast<double>(c.beta1), t);
   const double bc2 = 1.0 - std::pow(static_cast<double>(c.beta2), t);
@@ -194,7 +194,7 @@ int lamb_step(int T, const int64_t* numel, float* w, const float* g, float* m, f
 // is bit-identical to it.
 void lamb_step_finite(int T, const int64_t* numel, float* w, const float* g, float* m, float* v,
                       int64_t* step, const Lamb& c, std::vector<float>& u) {
-  *step += 1;  // lamb.cpp:31
+  *step += 1;  // lamb.cpp:40
   const double t = static_cast<double>(*step);
   const double bc1 = 1.0 - std::pow(static_cast<double>(c.beta1), t);
   const double bc2 = 1.0 - std::pow(static_cast<double>(c.beta2), t);
@@ -240,7 +240,7 @@ void lamb_step_finite(int T, const int64_t* numel, float* w, const float* g, flo
 // Emulated ring reduce-scatter + all-gather of one bucket over `world`
 // ranks, all in this thread. xs[r] is rank r's length-n vector; on return
 // every xs[r] holds the identical reduced result (collective.hpp:53-99 for
-// fp32, collective.cpp:163-212 for the binary16 wire).
+// fp32, collective.cpp:37-86 for the binary16 wire).
 void ring_allreduce_emulated(std::vector<float*>& xs, size_t n, bool f16_wire) {
   const int N = static_cast<int>(xs.size());
   if (N == 1 || n == 0) return;
@@ -256,7 +256,7 @@ void ring_allreduce_emulated(std::vector<float*>& xs, size_t n, bool f16_wire) {
         const float incoming = f16_wire ? f16_round(p) : p;  // hop narrows the partial
         p = incoming + local;
       }
-      out[idx] = f16_wire ? f16_round(p) : p;  // owner re-round (collective.cpp:205-209)
+      out[idx] = f16_wire ? f16_round(p) : p;  // owner re-round (collective.cpp:79-83)
     }
   }
   for (int r = 0; r < N; ++r) std::memcpy(xs[static_cast<size_t>(r)], out.data(), n * 4);
@@ -321,7 +321,7 @@ uint64_t or_fnv1a(const void* data, size_t len, uint64_t seed) { return fnv1a(da
 
 size_t or_ring_chunk_elems(size_t n, int world) { return ceil_div(n, static_cast<size_t>(world)); }
 
-// Per-rank payload bytes of one ring all-reduce (collective.cpp:157-161).
+// Per-rank payload bytes of one ring all-reduce (collective.cpp:31-35).
 uint64_t or_ring_allreduce_bytes(size_t n, int world, size_t e) {
   if (world <= 1 || n == 0) return 0;
   return 2ull * static_cast<uint64_t>(world - 1) * or_ring_chunk_elems(n, world) * e;
@@ -488,7 +488,7 @@ void or_synth_grads(int64_t P, uint64_t seed, int rank, int step, int micro, flo
 //   acc   = ((0 + g0) + g1) + ... + g_{K-2}          (trainer.cpp:240-244)
 //   x     = (g_{K-1} [+ acc]) * (1/(K*S))             (trainer.cpp:186-203)
 //   bucket ring all-reduce, then * (1/world)          (trainer.cpp:205-215)
-//   lamb_step on the reduced gradient                 (lamb.cpp:140-201)
+//   lamb_step on the reduced gradient                 (lamb.cpp:23-84)
 // plus the dynamic loss-scaler extension (found_inf := the reduced gradient
 // holds a non-finite -> skip the LAMB step entirely).
 // grads_in: optional caller-supplied fp16 inputs [steps][world][K][P]; when

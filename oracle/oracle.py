@@ -42,7 +42,7 @@ def build(force: bool = False) -> None:
 
 @dataclass
 class LambConfig:
-    """Mirror of ``bertopt::LambConfig`` (lamb.hpp:165-172)."""
+    """Mirror of ``bertopt::LambConfig`` (lamb.hpp:30-37)."""
 
     lr: float = 1e-3
     beta1: float = 0.9

@@ -10,8 +10,15 @@
 
 #include "bertopt/half.hpp"
 #include "bertopt/lamb.hpp"
+#include "bertopt/model.hpp"
 #include "bertopt/tensor.hpp"
+#include "bertopt/trainer.hpp"
 #include "bertopt_b200_adapter.hpp"
+#include "ref_shim.hpp"
+
+extern "C" {
+#include "../synth_grad.h"
+}
 
 using namespace bertopt;
 
@@ -100,6 +107,111 @@ int main() {
     bool thrown = false;
     try { b200::unscale_gradients(bad, LossScaler(4096.0f)); } catch (const OverflowDetected&) { thrown = true; }
     EXPECT(thrown && bad[0] == 1.0f);
+  }
+  // --- GradPipeline::train_step against the REAL DistributedTrainer::train_step
+  // (trainer.cpp:217-373, world 1, static loss scale, the synthetic-forward
+  // shim making each micro's gradient exactly widen(h) / S): K = 3 micros,
+  // ragged tensors, 4 KiB buckets, 3 steps. Moments bit-exact, parameters
+  // within 1e-6 relative (fp64 norms summed in another order).
+  {
+    refshim::ModelSpec spec;
+    const std::vector<std::vector<int64_t>> shapes = {{64, 65}, {1}, {300}, {4096}, {7}, {33, 17}};
+    for (size_t i = 0; i < shapes.size(); ++i) {
+      spec.names.push_back("p" + std::to_string(i));
+      spec.shapes.push_back(shapes[i]);
+      spec.init.push_back(i == 1 ? 2 : (i == 2 ? 1 : 0));
+    }
+    const std::vector<int> first_use = {2, 0, 5, 1, 4, 3};
+    const int K = 3, steps = 3;
+    const float S = 1024.0f;
+    Model mr = refshim::build_model_from_spec(spec, 5);
+    Model md = refshim::build_model_from_spec(spec, 5);
+    TrainerConfig tc;
+    tc.accumulation = K;
+    tc.bucket_bytes = 4096;
+    tc.loss_scale = S;
+    tc.overlap = false;
+    tc.lamb.lr = 1e-2f;
+    WorkerGroup g;
+    g.rank = 0;
+    g.world = 1;
+    DistributedTrainer trainer(g, mr, tc);
+    const size_t T = shapes.size();
+    std::vector<refshim::SynthMicro> micros(static_cast<size_t>(K));
+    std::vector<std::vector<std::vector<uint16_t>>> h(static_cast<size_t>(K), std::vector<std::vector<uint16_t>>(T));
+    auto fill = [&](int step) {
+      int64_t flat = 0;
+      for (size_t t = 0; t < T; ++t) {
+        const int64_t n = mr.params[t].numel();
+        for (int k = 0; k < K; ++k) {
+          refshim::SynthMicro& sm = micros[static_cast<size_t>(k)];
+          sm.first_use_order = first_use;
+          sm.G.resize(T);
+          sm.G[t].resize(static_cast<size_t>(n));
+          h[static_cast<size_t>(k)][t].resize(static_cast<size_t>(n));
+          const uint64_t base = bo_synth_base(3, 0, static_cast<uint64_t>(step), static_cast<uint64_t>(k));
+          for (int64_t i = 0; i < n; ++i) {
+            const float gt = bo_synth_true_grad(base, static_cast<uint64_t>(flat + i), 0, 1);
+            const Binary16 b = f32_to_f16(gt * S);
+            h[static_cast<size_t>(k)][t][static_cast<size_t>(i)] = b.bits;
+            sm.G[t][static_cast<size_t>(i)] = f16_to_f32(b) / S;
+          }
+        }
+        flat += n;
+      }
+    };
+    // first consumers exactly as ensure_layout derives them (trainer.cpp:161-168)
+    fill(0);
+    refshim::register_micro(1, &micros[0]);
+    std::vector<int> firsts(T);
+    {
+      Model probe = refshim::build_model_from_spec(spec, 5);
+      Tape tape;
+      Batch b;
+      b.ids = {1};
+      (void)forward(probe, tape, b, ForwardOptions{});
+      const std::vector<int> all = tape.first_consumers();
+      for (size_t p = 0; p < T; ++p) firsts[p] = all[static_cast<size_t>(probe.params[p].node)];
+    }
+    refshim::unregister_micro(1);
+    const bo_scaler_config sc{S, 2.0f, 0.5f, 1.0f, 16777216.0f, 1 << 30, 0};  // static S
+    b200::GradPipeline pipe(md, firsts, tc, sc, 0, 0, 1);
+    std::vector<b200::DeviceBuffer> dev;
+    for (int step = 0; step < steps; ++step) {
+      fill(step);
+      std::vector<Batch> batches(static_cast<size_t>(K));
+      std::vector<std::vector<const uint16_t*>> ptrs(static_cast<size_t>(K));
+      dev.clear();
+      for (int k = 0; k < K; ++k) {
+        refshim::register_micro(100 + k, &micros[static_cast<size_t>(k)]);
+        batches[static_cast<size_t>(k)].ids = {100 + k};
+        for (size_t t = 0; t < T; ++t) {
+          const std::vector<uint16_t>& src = h[static_cast<size_t>(k)][t];
+          dev.emplace_back(src.size() * 2);
+          dev.back().upload(src.data(), src.size() * 2);
+          ptrs[static_cast<size_t>(k)].push_back(dev.back().as<uint16_t>());
+        }
+      }
+      (void)trainer.train_step(batches);
+      pipe.train_step(ptrs);
+      (void)pipe.status();  // stream sync before the inputs are freed
+      for (int k = 0; k < K; ++k) refshim::unregister_micro(100 + k);
+    }
+    Model out = refshim::build_model_from_spec(spec, 5);
+    pipe.read_params(out);
+    LambState sd;
+    pipe.read_moments(sd, out);
+    const LambState& sr = trainer.state();
+    EXPECT(sr.step == steps && sd.step == steps);
+    for (size_t t = 0; t < T; ++t) {
+      EXPECT(bits_equal(sr.m[t], sd.m[t]));
+      EXPECT(bits_equal(sr.v[t], sd.v[t]));
+      EXPECT(max_rel(out.params[t], mr.params[t]) <= 1e-6);
+    }
+    // the step API's own error: exactly K micros (trainer.cpp:219-221)
+    bool thrown = false;
+    try { pipe.train_step({}); } catch (const InvalidConfig&) { thrown = true; }
+    EXPECT(thrown);
   }
   std::printf(failures ? "ADAPTER FAILED %d\n" : "ADAPTER OK\n", failures);
   return failures ? 1 : 0;

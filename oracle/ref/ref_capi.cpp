@@ -8,8 +8,8 @@
 // Every entry point calls the reference function it is named after:
 //   ref_f32_to_f16 / ref_f16_to_f32      half.cpp:23-77
 //   ref_unscale_gradients                half.cpp:105-115
-//   ref_lamb_step                        lamb.cpp:140-201
-//   ref_ring_allreduce                   collective.hpp:53-99 / collective.cpp:163-212
+//   ref_lamb_step                        lamb.cpp:23-84
+//   ref_ring_allreduce                   collective.hpp:53-99 / collective.cpp:37-86
 //   ref_bucket_layout                    trainer.cpp:73-134
 //   ref_train                            trainer.cpp:217-373 (DistributedTrainer::train_step)
 //                                        + the dynamic loss-scaler extension
@@ -266,7 +266,7 @@ int ref_bucket_layout(const bo_spec_c* spec, const int* firsts, uint64_t bucket_
 //   flatten into the fusion buckets trainer.cpp:186-203
 //   ring_allreduce[_f16_wire] per bucket + x 1/world (real, InProcHub)
 //                                  trainer.cpp:205-215, collective.hpp:53-99
-//   unpack + the real lamb_step    trainer.cpp:356-366, lamb.cpp:140-201
+//   unpack + the real lamb_step    trainer.cpp:356-366, lamb.cpp:23-84
 // `groups` independent replicas (groups * world threads) run concurrently so
 // that all host cores are used. seconds[s] is the wall time of timed step s
 // between all-thread barriers; stage_seconds[4] sums rank 0 of group 0's
@@ -427,7 +427,7 @@ int ref_build_params(const bo_spec_c* spec, uint64_t seed, float* out) {
 //     from the synthetic spec (synth_grad.h), overridden by injections;
 //   * the synthetic forward makes the trainer's live gradient exactly
 //     widen(h) (the loss is multiplied by S_t through tape.scalar_mul);
-//   * found_inf := train_step threw NonFiniteGradient (lamb.cpp:179-182: the
+//   * found_inf := train_step threw NonFiniteGradient (lamb.cpp:61-65: the
 //     reduced gradient lamb_step consumes held a non-finite). The step is then
 //     skipped: params / m / v / step are restored to their pre-step values;
 //   * scaler: found_inf -> S = max(S*backoff, min), good = 0;

@@ -294,7 +294,7 @@ const char* bo_last_error(void) { return g_last_error.c_str(); }
 
 void bo_default_config(bo_trainer_config* cfg) {
   std::memset(cfg, 0, sizeof(*cfg));
-  cfg->lamb = bo_lamb_config{1e-3f, 0.9f, 0.999f, 1e-6f, 0.01f, 10.0f};  // lamb.hpp:165-172
+  cfg->lamb = bo_lamb_config{1e-3f, 0.9f, 0.999f, 1e-6f, 0.01f, 10.0f};  // lamb.hpp:30-37
   cfg->accumulation = 1;
   cfg->bucket_bytes = 4ull << 20;  // trainer.hpp:78
   cfg->f16_exchange = 0;
@@ -328,7 +328,7 @@ bo_status bo_shard_ranges(int32_t n_buckets, const int64_t* bucket_elems, int32_
   BO_GUARD_BEGIN
   if (world < 1 || rank < 0 || rank >= world) fail(BO_ERR_INVALID_CONFIG, "bad rank/world");
   for (int b = 0; b < n_buckets; ++b) {
-    const int64_t c = (bucket_elems[b] + world - 1) / world;  // collective.cpp:50-52
+    const int64_t c = (bucket_elems[b] + world - 1) / world;  // collective.cpp:27-29
     lo[b] = std::min<int64_t>(rank * c, bucket_elems[b]);
     hi[b] = std::min<int64_t>((rank + 1) * c, bucket_elems[b]);
   }

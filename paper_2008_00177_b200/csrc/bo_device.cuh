@@ -22,7 +22,7 @@ __device__ __forceinline__ uint64_t global_ns() {
   return t;
 }
 
-// float(double(x) / d) with the reference's double rounding (lamb.cpp:185-186),
+// float(double(x) / d) with the reference's double rounding (lamb.cpp:68-69),
 // computed as a multiply by the host-rounded reciprocal. The product is within
 // ~3 double ulps of RN_d(x/d); only when it lies that close to a binary32
 // rounding midpoint (or in the binary32 subnormal range) can the two round to
@@ -48,7 +48,7 @@ __device__ __forceinline__ float div_to_float_fast(float x, double inv_d, bool& 
   return __double2float_rn(q);
 }
 
-// Four LAMB elements (lamb.cpp:183-187, operation order kept) with one rarely
+// Four LAMB elements (lamb.cpp:66-70, operation order kept) with one rarely
 // taken branch for the exact double divisions instead of one per value.
 struct Lamb4 {
   float m[4], v[4], u[4];
@@ -119,7 +119,7 @@ struct Moments {
   float m, v, u;
 };
 
-// One element of lamb_step's fused loop (lamb.cpp:183-187), operation order kept.
+// One element of lamb_step's fused loop (lamb.cpp:66-70), operation order kept.
 __device__ __forceinline__ Moments lamb_elem(float g, float w, float m, float v, const LambConsts& c,
                                              const double* bc) {
   Moments o;
@@ -149,7 +149,7 @@ __device__ __forceinline__ bool pair_nonfinite(uint32_t x) {
 // binary16 input makes the accumulated gradient non-finite (an fp32 sum of at
 // most K values <= 65504 cannot overflow on its own), so OR-ing the inputs'
 // flags equals checking the finalized gradient lamb_step would see
-// (lamb.cpp:179) on a single rank.
+// (lamb.cpp:61-65) on a single rank.
 __device__ __forceinline__ void raise_flag(bool bad, DevState* st) {
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&st->local_flag, 1);
 }

@@ -1,4 +1,4 @@
-// Single-rank sync micro: the whole LAMB step (lamb.cpp:140-201) with the
+// Single-rank sync micro: the whole LAMB step (lamb.cpp:23-84) with the
 // flatten_param unscale (trainer.cpp:186-203) fused in.
 //
 //   k_lamb_p1     g = (h + acc) * inv; m', v', u (one pass, vectorised);
@@ -8,7 +8,7 @@
 //                 end of this pass) and the update u; per-tile fp64 partials
 //                 of ||w||^2 and ||u||^2                                   30 B/elem
 //   k_lamb_trust  per-tensor fixed-order sums of the tile partials ->
-//                 trust ratios (lamb.cpp:192-196)
+//                 trust ratios (lamb.cpp:75-79)
 //   k_lamb_p2     w -= (lr * r) * u, tiles in reverse order so the update
 //                 and weights phase 1 wrote last are still in L2; the dead
 //                 u lines are then dropped from L2 (discard.global.L2)      12 B/elem
@@ -300,7 +300,7 @@ __global__ void __launch_bounds__(kThreads) k_lamb_trust(const int* __restrict__
   }
 }
 
-// Phase 2 (lamb.cpp:197-198): tiles in reverse order (block b takes tile
+// Phase 2 (lamb.cpp:80-81): tiles in reverse order (block b takes tile
 // n-1-b) so the most recently written w and u are L2 hits.
 __global__ void __launch_bounds__(kP2Threads) k_lamb_p2(const FusedTile* __restrict__ tiles,
                                                         int n_tiles, float* __restrict__ w,

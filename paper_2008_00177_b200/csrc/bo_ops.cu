@@ -2,15 +2,15 @@
 // the reference's argument meaning and error behaviour, plus the synthetic
 // gradient generator used by the bench and the tests.
 //
-//   bo_lamb_step               lamb_step              lamb.cpp:140-201
+//   bo_lamb_step               lamb_step              lamb.cpp:23-84
 //   bo_ring_allreduce_f32      ring_allreduce<float>  collective.hpp:53-99
-//   bo_ring_allreduce_f16_wire ring_allreduce_f16_wire collective.cpp:163-212
+//   bo_ring_allreduce_f16_wire ring_allreduce_f16_wire collective.cpp:37-86
 //   bo_unscale_gradients       unscale_gradients      half.cpp:105-115
 //   bo_narrow_f16/bo_widen_f16 narrow/widen_f16_block graph.cpp:176-199
 //   bo_fused_optimizer_step    fused_optimizer_step   graph.cpp:458-487 run by
 //                              run_fused_kernel (apply_block, graph.cpp:296-347)
 //   bo_f16_round               quantize_inplace of a binary16 tensor (Tape::cast,
-//                              ops.cpp:655-668; f16_round, half.cpp:59-62)
+//                              ops.cpp:655-668; f16_round, half.cpp:79)
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -144,7 +144,7 @@ __global__ void k_widen(const uint16_t* s, float* d, size_t n) {
   }
 }
 
-// mine = widen(in) + mine (f16) or in + mine (fp32): collective.cpp:184-187
+// mine = widen(in) + mine (f16) or in + mine (fp32): collective.cpp:58-61
 template <typename W>
 __global__ void k_ring_add(const W* in, float* mine, size_t n) {
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
@@ -304,7 +304,7 @@ void ring_allreduce_impl(bo_ctx* c, float* data, size_t n, bool f16) {
   if (N == 1 || n == 0) return;
   need_nccl(c, "bo_ring_allreduce_*");
   cudaStream_t s = c->stream;
-  const size_t ch = (n + static_cast<size_t>(N) - 1) / static_cast<size_t>(N);  // collective.cpp:50-52
+  const size_t ch = (n + static_cast<size_t>(N) - 1) / static_cast<size_t>(N);  // collective.cpp:27-29
   DevBuf buf(ch * static_cast<size_t>(N) * 4), wire(ch * sizeof(W)), in(ch * sizeof(W));
   float* B = buf.as<float>();
   BO_CUDA(cudaMemsetAsync(B, 0, ch * static_cast<size_t>(N) * 4, s));
@@ -341,7 +341,7 @@ void ring_allreduce_impl(bo_ctx* c, float* data, size_t n, bool f16) {
       BO_CUDA(cudaMemcpyAsync(B + recv_idx * ch, in.p, ch * 4, cudaMemcpyDeviceToDevice, s));
     }
   }
-  if (f16) {  // owner re-round (collective.cpp:205-209)
+  if (f16) {  // owner re-round (collective.cpp:79-83)
     k_round_f16<<<grid_for(ch), kThreads, 0, s>>>(B + static_cast<size_t>((r + 1) % N) * ch, ch);
     check("k_round_f16");
   }
@@ -373,7 +373,7 @@ bo_status bo_lamb_step(int32_t T, const int64_t* numels, float* const* params,
     fail(BO_ERR_SHAPE_MISMATCH, "lamb_step: null argument");
   }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  *step += 1;  // lamb.cpp:157, before any check
+  *step += 1;  // lamb.cpp:40, before any check
   const double t = static_cast<double>(*step);
   double bc[4];
   bc[0] = 1.0 - std::pow(static_cast<double>(cfg->beta1), t);
@@ -506,7 +506,7 @@ bo_status bo_ring_allreduce_f16_wire(bo_ctx* c, float* data, size_t n) {
 bo_status bo_unscale_gradients(float* g, size_t n, float scale, int32_t enabled, void* stream) {
   BO_OP_BEGIN
   if (!is_pow2(scale)) {
-    fail(BO_ERR_INVALID_CONFIG, "loss scale must be a positive power of two");  // half.cpp:93-98
+    fail(BO_ERR_INVALID_CONFIG, "loss scale must be a positive power of two");  // half.cpp:94-99
   }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (n == 0) return BO_OK;

@@ -6,10 +6,10 @@
 //   k_finalize       flatten_param: (live + accum) * inv trainer.cpp:186-203
 //   (ring hops: bo_ring.cu; one rank's fused LAMB: bo_fused.cu)
 //   k_p1w            lamb_step moments, u + fp64 norm partials on the shard
-//                                                        lamb.cpp:176-190
-//   k_norm_reduce / k_trust  trust ratio (lamb.cpp:192-196), found_inf and
+//                                                        lamb.cpp:59-73
+//   k_norm_reduce / k_trust  trust ratio (lamb.cpp:75-79), found_inf and
 //                    the loss scaler
-//   k_shard_p2_push  w -= (lr * r) * u (lamb.cpp:197-198) + the push into
+//   k_shard_p2_push  w -= (lr * r) * u (lamb.cpp:80-81) + the push into
 //                    every replica (the all-gather)
 //   k_lamb_norms / k_lamb_update  one rank with unaligned inputs
 //
@@ -162,8 +162,8 @@ __global__ void __launch_bounds__(kThreads) k_finalize(const AccTile* __restrict
 
 // ------------------------------------------------------------------- LAMB
 // Phase 1: per-tile fp64 partials of ||w||^2 and ||u||^2 and the non-finite
-// flag of the reduced gradient (lamb.cpp:176-190; the flag is the
-// NonFiniteGradient condition, lamb.cpp:179). Nothing is written to w/m/v.
+// flag of the reduced gradient (lamb.cpp:59-73; the flag is the
+// NonFiniteGradient condition, lamb.cpp:61-65). Nothing is written to w/m/v.
 template <typename G>
 __global__ void __launch_bounds__(kThreads) k_lamb_norms(const LambTile* __restrict__ tiles,
                                                          const G* __restrict__ g,
@@ -358,7 +358,7 @@ __global__ void __launch_bounds__(1024) k_trust(const double* __restrict__ all_p
 }
 
 // Phase 2: recompute the element (bit-identical to phase 1) and apply
-// w -= (lr * r) * u, storing w, m, v (lamb.cpp:197-198). Skipped steps exit.
+// w -= (lr * r) * u, storing w, m, v (lamb.cpp:80-81). Skipped steps exit.
 template <typename G>
 __global__ void __launch_bounds__(kThreads) k_lamb_update(const LambTile* __restrict__ tiles,
                                                           const G* __restrict__ g,
@@ -407,10 +407,10 @@ __device__ __forceinline__ Split split_tile(int64_t s0, int len) {
 }
 // ------------------------------------------------ phase 1 (world > 1)
 // Phase 1 on this rank's shard: the reduced gradient g (trainer.cpp:212
-// scaling), the NonFiniteGradient flag (lamb.cpp:179), m', v' into the other
+// scaling), the NonFiniteGradient flag (lamb.cpp:61-65), m', v' into the other
 // moment buffer set (double-buffered: found_inf is global, known only after
 // every rank's phase 1), the update u, and per-tile fp64 partials of
-// ||w||^2 and ||u||^2 (lamb.cpp:176-190).
+// ||w||^2 and ||u||^2 (lamb.cpp:59-73).
 struct P1Args {
   const TensorDev* td;
   const float* acc;
@@ -621,7 +621,7 @@ __global__ void __launch_bounds__(kWarpTileCTA, kMinBlocks) k_p1w(const LambTile
 }
 
 // Phase 2 fused with the parameter all-gather: w -= (lr * r) * u on the
-// master shard (lamb.cpp:197-198), and the new value written into every
+// master shard (lamb.cpp:80-81), and the new value written into every
 // rank's flat parameter replica over NVLink (CUDA IPC mappings) at the
 // element's fusion-buffer position. The replica writes are bulk asynchronous
 // copies (cp.async.bulk, the TMA engine) from a shared-memory copy of the

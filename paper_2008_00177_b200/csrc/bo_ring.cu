@@ -1,5 +1,5 @@
 // The reference ring's reduce-scatter on the device (collective.hpp:53-99,
-// binary16 wire collective.cpp:163-212), flatten_param fused into every hop:
+// binary16 wire collective.cpp:37-86), flatten_param fused into every hop:
 //   k_hopx       one hop over the chunk of every bucket this rank adds at hop s
 //   run_reduce   hop 0 (pack) + N-1 hops reading the left neighbour's staging
 //                buffer over NVLink (CUDA IPC), or grouped ncclSend/ncclRecv,
@@ -15,7 +15,7 @@ namespace {
 
 // --------------------------------------------------------------- ring hops
 // Ring hop with flatten_param fused in (trainer.cpp:186-203 + collective.hpp:65-80
-// / collective.cpp:170-190): x = (h + acc) * inv for the elements of chunk q,
+// / collective.cpp:47-62): x = (h + acc) * inv for the elements of chunk q,
 // out = wire(x) (combine == 0, the first send) or wire(from_wire(in) + x).
 // KR > 0 (bo_train_step): x from the KR resident micros instead of h + acc.
 template <typename W, int KR>
@@ -182,7 +182,7 @@ static void hop_barrier(bo_ctx* c, cudaStream_t st) {
 }
 
 // The reference ring's reduce-scatter phase (collective.hpp:65-80, binary16
-// wire collective.cpp:170-190) over buckets [b0, b1), with flatten_param fused
+// wire collective.cpp:47-62) over buckets [b0, b1), with flatten_param fused
 // into every hop: the local addend x of chunk q is computed from the sync
 // micro's binary16 input and the accumulator as the hop needs it.
 template <typename W>
@@ -275,7 +275,7 @@ static void ring_reduce_scatter(bo_ctx* c, const PtrTable& tab, ncclDataType_t d
     c->ring_result = c->wire[(N - 1) % 2];
     return;
   }
-  hop(r, nullptr, a, 0);  // hop 0 payload: this rank's own chunk r (collective.cpp:178)
+  hop(r, nullptr, a, 0);  // hop 0 payload: this rank's own chunk r (collective.cpp:52)
   if (p2p) {
     // Peer-to-peer hops: hop s reads the left neighbour's hop s-1 output in
     // place over NVLink (CUDA IPC mapping) and writes the other local buffer.
@@ -312,7 +312,7 @@ static void ring_reduce_scatter(bo_ctx* c, const PtrTable& tab, ncclDataType_t d
   }
   // Unfused: after N-1 hops the result buffer holds the finished chunk
   // (r+1) % N, already wire-rounded (the owner re-round of
-  // collective.cpp:205-209): the chunk this rank owns (Layout::own). LAMB
+  // collective.cpp:79-83): the chunk this rank owns (Layout::own). LAMB
   // reads it in place.
 }
 

@@ -152,7 +152,7 @@ void upload_tables(bo_ctx* c) {
 }
 
 // Bias corrections bc_t = 1 - pow(double(beta), double(t)) evaluated on the
-// host with the same libm the reference uses (lamb.cpp:158-161), with their
+// host with the same libm the reference uses (lamb.cpp:41-44), with their
 // reciprocals; the device indexes the table by its own step counter.
 void grow_bc_table(bo_ctx* c, int64_t need) {
   if (need <= c->bc_cap) return;

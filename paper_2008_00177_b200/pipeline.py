@@ -2,7 +2,7 @@
 
 Names and argument meaning follow the reference (proj/core/include/bertopt):
 
-* ``LambConfig``     — lamb.hpp:165-172
+* ``LambConfig``     — lamb.hpp:30-37
 * ``TrainerConfig``  — trainer.hpp:75-85 (hot-path fields) + the dynamic
   loss-scaler extension ``ScalerConfig``
 * ``GradPipeline``   — one rank's DistributedTrainer gradient-to-update path
@@ -338,11 +338,32 @@ class GradPipeline:
         return p.value
 
     # -- hot path
+    # Stream contract (include/bertopt_b200.h "streams"): the library runs on
+    # the context stream and does not synchronise with other streams. When the
+    # gradients are passed as torch tensors, the wrapper orders the context
+    # stream after torch's current stream (which produced them) and marks the
+    # tensors as used on the context stream, so the caching allocator cannot
+    # hand their memory out while the step still reads it. Raw pointers (ints,
+    # prebuilt pointer arrays) are the caller's responsibility.
+    def _order_after_producer(self, tensors) -> None:
+        ts = [t for t in tensors if not isinstance(t, int)]
+        if not ts:
+            return
+        import torch
+
+        ctx_stream = torch.cuda.ExternalStream(self.stream_handle(), device=ts[0].device)
+        producer = torch.cuda.current_stream(ts[0].device)
+        if producer.cuda_stream != ctx_stream.cuda_stream:
+            ctx_stream.wait_stream(producer)
+            for t in ts:
+                t.record_stream(ctx_stream)
+
     def accumulate(self, micro: int, grads) -> None:
         """grads: per-tensor device pointers (ints) or fp16/int16 CUDA tensors."""
         if len(grads) != self.spec.n_tensors:
             raise ShapeMismatch(f"ShapeMismatch: {len(grads)} gradients for "
                                 f"{self.spec.n_tensors} parameters")
+        self._order_after_producer(grads)
         ptrs = [g if isinstance(g, int) else g.data_ptr() for g in grads]
         _lib.check(self.lib.bo_accumulate(self.ctx, micro, _ptr_array(ptrs)))
 
@@ -362,6 +383,7 @@ class GradPipeline:
         tensors = [int(t) for t in tensors]
         if len(tensors) != len(grads):
             raise ShapeMismatch("ShapeMismatch: tensors and grads differ in length")
+        self._order_after_producer(grads)
         ptrs = [g if isinstance(g, int) else g.data_ptr() for g in grads]
         ids = (C.c_int32 * max(1, len(tensors)))(*tensors)
         _lib.check(self.lib.bo_sync_ready(self.ctx, len(tensors), ids, _ptr_array(ptrs)))
@@ -382,6 +404,7 @@ class GradPipeline:
             if len(g) != self.spec.n_tensors:
                 raise ShapeMismatch(f"ShapeMismatch: {len(g)} gradients for "
                                     f"{self.spec.n_tensors} parameters")
+            self._order_after_producer(g)
             ptrs += [x if isinstance(x, int) else x.data_ptr() for x in g]
         _lib.check(self.lib.bo_train_step(self.ctx, _ptr_array(ptrs)))
 
@@ -400,10 +423,10 @@ def _stream(stream) -> C.c_void_p:
 
 
 def lamb_step(params, grads, state: dict, cfg: LambConfig, stream=None) -> None:
-    """``lamb_step(params, grads, state, cfg)`` (lamb.hpp:182-183) on CUDA fp32 tensors.
+    """``lamb_step(params, grads, state, cfg)`` (lamb.hpp:47-48) on CUDA fp32 tensors.
 
     ``state`` mirrors LambState: {'m': [...], 'v': [...], 'step': int}; m/v are
-    created lazily as zeros (lamb.cpp:147-152). Raises ShapeMismatch /
+    created lazily as zeros (lamb.cpp:30-35). Raises ShapeMismatch /
     NonFiniteGradient like the reference (after the same partial update).
     """
     import torch

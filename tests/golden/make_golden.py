@@ -68,7 +68,7 @@ def main() -> None:
             lay[k + "_hash"] = np.array([h], np.uint64)
     np.savez_compressed(os.path.join(HERE, "layout.npz"), **lay)
 
-    # --- lamb_step (lamb.cpp:140-201), including the NonFiniteGradient partial update
+    # --- lamb_step (lamb.cpp:23-84), including the NonFiniteGradient partial update
     numels = np.array([4097, 1, 300, 2048, 7], np.int64)
     P = int(numels.sum())
     w0 = (rng.standard_normal(P) * 0.02).astype(np.float32)
@@ -84,7 +84,7 @@ def main() -> None:
         out[f"step{s + 1}"] = np.array([step])
     np.savez_compressed(os.path.join(HERE, "lamb.npz"), **out)
 
-    # --- ring all-reduce (collective.hpp:53-99, collective.cpp:163-212)
+    # --- ring all-reduce (collective.hpp:53-99, collective.cpp:37-86)
     ring = {}
     for world in (2, 3, 4, 8):
         for n in (1, 5, 64, 1537):

@@ -145,7 +145,7 @@ def test_lamb_step_nonfinite_partial_update(torch, oracle):
     got, ref, rcs = _lamb_case(oracle, numels, 2, 3, {}, inf_at=300 + 1234)
     rc_ref, err = rcs[-1]
     assert rc_ref == 2 and isinstance(err, NonFiniteGradient)
-    assert got[3] == ref[3] == 3  # step incremented before the throw (lamb.cpp:157)
+    assert got[3] == ref[3] == 3  # step incremented before the throw (lamb.cpp:40)
     assert np.array_equal(got[1].view(np.uint32), ref[1].view(np.uint32))
     assert np.array_equal(got[2].view(np.uint32), ref[2].view(np.uint32))
     rel = np.abs(got[0].astype(np.float64) - ref[0]) / np.maximum(np.abs(ref[0]), 1e-6)
