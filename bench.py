@@ -274,17 +274,15 @@ def main_b200(args):
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     ngpu = torch.cuda.device_count()
-    # one rank per GPU; more ranks than GPUs (world 8 on a 4-GPU lease) share
-    # them round-robin — the pipeline's default step needs no NCCL, so this
-    # runs end to end (emulation: the timing is then not a scaling number)
-    emulated = world > ngpu
-    local = local % ngpu
+    # one rank per GPU: ranks must never share a device (their flag-spinning
+    # kernels must run concurrently); worlds larger than the box run through
+    # tools/world_emu.py (all ranks in one process, lockstep on one stream)
+    if local >= ngpu:
+        raise SystemExit(f"rank {rank}: {world} ranks need {world} GPUs ({ngpu} visible)")
+    emulated = False
     torch.cuda.set_device(local)
     if world > 1:
-        if emulated:
-            dist.init_process_group("gloo")
-        else:
-            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     K = args.accumulation
     spec = model_spec(args.model)
     P = spec.param_count()
@@ -616,9 +614,7 @@ def main_b200(args):
                               else "bo_accumulate x K",
                        "kernel_path": path,
                        "parallelism": f"dp{world} (reduce-scatter + sharded LAMB + all-gather)",
-                       "l2": "inputs (K x 2 B x P) larger than L2, no flush",
-                       **({"emulated": f"{world} ranks on {ngpu} GPU(s): ranks share devices, "
-                                       "timing is not a scaling number"} if emulated else {})},
+                       "l2": "inputs (K x 2 B x P) larger than L2, no flush"},
             "roofline": roofline, "step_roofline": step_roofline, "stages": stages,
             "e2e": e2e, "per_micro_api": per_micro, "cpu_baseline": cpu,
             "gpu_launches": int(launches),

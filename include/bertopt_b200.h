@@ -245,6 +245,20 @@ bo_status bo_train_step(bo_ctx* ctx, const uint16_t* const* grads);
  * 0..K-2 still go through bo_accumulate. */
 bo_status bo_sync_ready(bo_ctx* ctx, int32_t n, const int32_t* tensors, const uint16_t* const* grads);
 
+/* The next step's forward overlapping this step's parameter all-gather:
+ * enqueue on `stream` (a cudaStream_t, typically the forward's) a wait until
+ * the parameters of `tensor`'s parameter group, as updated by the most
+ * recently enqueued step, are in this rank's replica (bo_param_ptr) — every
+ * rank pushes its updated shard into every replica group by group, in model
+ * (= forward first-use) order, and publishes each group as it lands. Kernels
+ * enqueued on `stream` afterwards read the new values; the rest of the push
+ * continues on the context stream. The parameters read must not be those of
+ * a later step still in flight. World 1: the stream waits for the whole
+ * step. Bounded by the watchdog (bo_set_watchdog). */
+bo_status bo_params_wait(bo_ctx* ctx, int32_t tensor, void* stream);
+/* Parameter group of a tensor (world 1: 0; -1 for a bad index). */
+int32_t bo_param_group(const bo_ctx* ctx, int32_t tensor);
+
 /* ---- measurement ---------------------------------------------------------- */
 /* Stage timing with CUDA events recorded on the context stream around every
  * stage of bo_accumulate (off by default). Stages: */

@@ -81,6 +81,8 @@ SIGNATURES = {
     "bo_accumulate": (_i32, [_vp, _i32, C.POINTER(_vp)]),
     "bo_sync_ready": (_i32, [_vp, _i32, C.POINTER(_i32), C.POINTER(_vp)]),
     "bo_train_step": (_i32, [_vp, C.POINTER(_vp)]),
+    "bo_params_wait": (_i32, [_vp, _i32, _vp]),
+    "bo_param_group": (_i32, [_vp, _i32]),
     "bo_profile_enable": (_i32, [_vp, _i32]),
     "bo_profile_read": (_i32, [_vp, C.POINTER(C.c_double), C.POINTER(_i64), _i32]),
     "bo_launch_count": (_i64, [_vp]),

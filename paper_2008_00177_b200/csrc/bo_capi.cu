@@ -443,6 +443,7 @@ void bo_destroy(bo_ctx* c) {
   if (c->comm_stream) cudaStreamSynchronize(c->comm_stream);
   if (c->comm_ready) cudaEventDestroy(c->comm_ready);
   if (c->comm_done) cudaEventDestroy(c->comm_done);
+  if (c->params_done) cudaEventDestroy(c->params_done);
   if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
   delete c->sync_tab;
   for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);

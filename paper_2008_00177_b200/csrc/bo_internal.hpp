@@ -153,7 +153,9 @@ constexpr int kCtrlFromLeft = 0;     // ring-neighbour barrier: epoch of the lef
 constexpr int kCtrlFromRight = 1;    //                          epoch of the right neighbour
 constexpr int kCtrlPartials = 16;    // [8] partials barrier: rank j's norm partials are in
 constexpr int kCtrlStepEnd = 32;     // [8] end-of-step barrier: rank j's parameter push landed
-constexpr int kCtrlWords = 64;
+constexpr int kCtrlReady = 64;       // [kMaxPushGroups][8] rank j's push of parameter group g landed
+constexpr int kMaxPushGroups = 112;
+constexpr int kCtrlWords = kCtrlReady + 8 * kMaxPushGroups;
 
 // Per-step destinations of this rank's norm partials: slot `rank` of every
 // rank's all_part (this step's parity half). N == 0: local rank_part only.
@@ -268,6 +270,19 @@ struct bo_ctx {
   uint64_t watchdog_ns = 120000000000ull;  // RunConfig::watchdog_s = 120 (trainer.hpp:144)
   bool nb_barrier = true;              // BO_RING_BARRIER=nccl: 4-byte NCCL all-reduce instead
   bool peers_mapped = false;           // bo_comm_import / bo_comm_init done
+  // Parameter groups of the push (world > 1): consecutive tensors in model
+  // (= forward first-use) order; the push tiles are the LAMB tiles plus one
+  // empty tile for every group this rank owns no element of, so that every
+  // group has a last CTA that publishes "group g of this step landed" into
+  // every rank's kCtrlReady slots (bo_params_wait).
+  bo::LambTile* d_push_tiles = nullptr;
+  int n_push_tiles = 0;
+  int n_push_groups = 0;
+  std::vector<int> push_group_of_tensor;
+  int* d_push_group_of_tensor = nullptr;
+  int* d_push_group_tiles = nullptr;   // [G] tiles of group g on this rank
+  unsigned* d_push_count = nullptr;    // [G] cumulative finished tiles
+  cudaEvent_t params_done = nullptr;   // world 1: the step's update, for bo_params_wait
   double* peer_part[8] = {};           // every rank's all_part (IPC)
   void* wire[3] = {nullptr, nullptr, nullptr};  // ring staging (shard-sized)
   double* tile_part = nullptr;    // [n_lamb_tiles][2]
@@ -328,6 +343,8 @@ void run_reduce_group(bo_ctx* c, const PtrTable& tab, int b0, int b1, int acc0, 
                       cudaStream_t stream);
 void run_lamb(bo_ctx* c, const PtrTable& tab);
 void gather_shard(bo_ctx* c);
+// the caller's stream waits for tensor's parameter group of the last step
+void params_wait(bo_ctx* c, int tensor, cudaStream_t stream);
 // needs the NCCL communicator (bo_comm_init): fail otherwise
 void need_nccl(bo_ctx* c, const char* what);
 void run_fused_single_rank(bo_ctx* c, const PtrTable& tab, MicroSrc ms = MicroSrc{nullptr, 0, 0});

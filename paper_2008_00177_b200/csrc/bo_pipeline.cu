@@ -634,6 +634,35 @@ __device__ __forceinline__ void bulk_s2g(float* gdst, const float* ssrc, uint32_
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(s), "r"(bytes)
                : "memory");
 }
+// Parameter groups (bo_params_wait): the tiles run in model order, grouped by
+// parameter group; the last CTA of group g to finish publishes "group g of
+// step `epoch` landed in every replica" into slot `rank` of every rank's
+// kCtrlReady[g] flags — after its own bulk copies completed and with a
+// system-scope fence behind every CTA's stores of the group.
+struct PushGroups {
+  const int* group_of_tensor;
+  const int* group_tiles;
+  unsigned* count;
+  PeerFlags pf;
+  unsigned epoch;
+};
+
+__device__ __forceinline__ void push_group_done(const PushGroups& G, int tensor) {
+  __threadfence_system();  // this thread's replica stores (edges) before the count
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int g = G.group_of_tensor[tensor];
+    const unsigned done = atomicAdd(G.count + g, 1u) + 1u;
+    if (done % static_cast<unsigned>(G.group_tiles[g]) == 0u) {
+      __threadfence_system();
+      for (int j = 0; j < G.pf.n; ++j) {
+        unsigned* f = G.pf.f[j] + kCtrlReady + 8 * g + G.pf.rank;
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f), "r"(G.epoch) : "memory");
+      }
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kThreads) k_shard_p2_push(const LambTile* __restrict__ tiles,
                                                             float* __restrict__ wsh,
                                                             const float* __restrict__ u,
@@ -641,12 +670,15 @@ __global__ void __launch_bounds__(kThreads) k_shard_p2_push(const LambTile* __re
                                                                  LambConsts c,
                                                                  const float* __restrict__ trust,
                                                                  float* const* __restrict__ peer_w,
-                                                                 int N) {
-  if (!st->do_update) return;
+                                                                 int N, const PushGroups G) {
+  const LambTile t = tiles[blockIdx.x];
+  if (!st->do_update || t.len == 0) {  // skipped step / a group's empty tile: publish only
+    push_group_done(G, t.t);
+    return;
+  }
   __shared__ __align__(128) float buf[kTileElems + 4];
   __shared__ float* dst[8];
   if (threadIdx.x < N) dst[threadIdx.x] = peer_w[threadIdx.x];
-  const LambTile t = tiles[blockIdx.x];
   const float step_scale = __fmul_rn(c.lr, trust[t.t]);
   const int off = static_cast<int>(t.w0 & 3);  // buf[off + e] <-> flat element w0 + e
   const Split sp = split_tile(t.s0, t.len);
@@ -703,9 +735,29 @@ __global__ void __launch_bounds__(kThreads) k_shard_p2_push(const LambTile* __re
     const int e = static_cast<int>(a1 - t.w0) + i % ntail, j = i / ntail;
     dst[j][t.w0 + e] = buf[off + e];
   }
-  // the shared-memory tile must outlive the copies; kernel completion then
-  // implies the replica writes are done
+  // the shared-memory tile must outlive the copies (wait for their writes,
+  // not only their smem reads, so the group flag below covers them)
   if (threadIdx.x == 0 && a1 > a0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  push_group_done(G, t.t);
+}
+
+// bo_params_wait: one thread on the caller's stream waits until every rank
+// published parameter group g of step `epoch` (bounded by the watchdog).
+__global__ void k_params_wait(const unsigned* __restrict__ slots, int N, unsigned epoch,
+                              DevState* st, uint64_t timeout_ns) {
+  const uint64_t t0 = global_ns();
+  for (int j = 0; j < N; ++j) {
+    unsigned v;
+    for (;;) {
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(slots + j) : "memory");
+      if (static_cast<int>(v - epoch) >= 0) break;
+      if (global_ns() - t0 > timeout_ns) {
+        st->peer_timeout = 1;
+        return;
+      }
+      __nanosleep(64);
+    }
+  }
 }
 
 // Owned chunk positions of the flat replica -> the master shard (load time).
@@ -848,10 +900,10 @@ static void lamb_sharded(bo_ctx* c, const PtrTable& tab, const W* in) {
   }
   {
   StageTimer timer(c, BO_STAGE_LAMB_UPDATE);
-  if (c->n_lamb_tiles > 0)
-  k_shard_p2_push<<<c->n_lamb_tiles, kThreads, 0, c->stream>>>(c->d_lamb_tiles, c->wsh, c->u,
+  const PushGroups G{c->d_push_group_of_tensor, c->d_push_group_tiles, c->d_push_count, c->peer_ctrl, epoch};
+  k_shard_p2_push<<<c->n_push_tiles, kThreads, 0, c->stream>>>(c->d_push_tiles, c->wsh, c->u,
                                                               c->state, c->lamb, c->trust,
-                                                              c->d_peer_w, c->world);
+                                                              c->d_peer_w, c->world, G);
   check_launch(c, "k_shard_p2_push");
   }
   // every rank's pushes into every replica have landed once all ranks are
@@ -884,6 +936,22 @@ void run_lamb(bo_ctx* c, const PtrTable& tab) {
   } else {
     lamb_sharded<float, false>(c, tab, c->gshard);
   }
+}
+
+void params_wait(bo_ctx* c, int tensor, cudaStream_t stream) {
+  if (c->world == 1) {
+    // one rank: the update runs on the context stream; order the caller's
+    // stream after the most recent step
+    if (!c->params_done) BO_CUDA(cudaEventCreateWithFlags(&c->params_done, cudaEventDisableTiming));
+    BO_CUDA(cudaEventRecord(c->params_done, c->stream));
+    BO_CUDA(cudaStreamWaitEvent(stream, c->params_done, 0));
+    return;
+  }
+  if (c->bar_epoch == 0) return;  // no step enqueued yet
+  const int g = c->push_group_of_tensor[static_cast<size_t>(tensor)];
+  k_params_wait<<<1, 1, 0, stream>>>(c->ctrl + kCtrlReady + 8 * g, c->world,
+                                     static_cast<unsigned>(c->bar_epoch), c->state, c->watchdog_ns);
+  check_launch(c, "k_params_wait");
 }
 
 void need_nccl(bo_ctx* c, const char* what) {

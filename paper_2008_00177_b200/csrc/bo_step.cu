@@ -201,4 +201,18 @@ bo_status bo_sync_ready(bo_ctx* c, int32_t n, const int32_t* tensors, const uint
   BO_GUARD_END
 }
 
+bo_status bo_params_wait(bo_ctx* c, int32_t tensor, void* stream) {
+  BO_GUARD_BEGIN
+  if (!c) fail(BO_ERR_INVALID_CONFIG, "null ctx");
+  if (tensor < 0 || tensor >= c->L.T) fail(BO_ERR_SHAPE_MISMATCH, "tensor index out of range");
+  if (c->world > 1 && !c->peers_mapped) fail(BO_ERR_INVALID_CONFIG, "bo_comm_init / bo_comm_import has not run");
+  params_wait(c, tensor, static_cast<cudaStream_t>(stream));
+  BO_GUARD_END
+}
+
+int32_t bo_param_group(const bo_ctx* c, int32_t tensor) {
+  if (!c || tensor < 0 || tensor >= c->L.T) return -1;
+  return c->world > 1 ? c->push_group_of_tensor[static_cast<size_t>(tensor)] : 0;
+}
+
 }  // extern "C"

@@ -142,6 +142,53 @@ void upload_tables(bo_ctx* c) {
       }
     }
     c->d_group_acc_tiles = upload(c, gacc);
+
+    // Parameter groups of the push, in model order (the forward's first-use
+    // order: embeddings, layer 0, ..., heads), >= BO_PUSH_GROUP_ELEMS elements
+    // each (default 8 Mi), at most kMaxPushGroups. Every rank derives the same
+    // groups from the layout.
+    int64_t push_elems = 8ll << 20;
+    if (const char* e = std::getenv("BO_PUSH_GROUP_ELEMS")) push_elems = std::max<int64_t>(1, std::atoll(e));
+    push_elems = std::max<int64_t>(push_elems, (L.P + kMaxPushGroups - 1) / kMaxPushGroups);
+    c->push_group_of_tensor.assign(static_cast<size_t>(L.T), 0);
+    int G = 0;
+    int64_t acc_n = 0;
+    for (int t = 0; t < L.T; ++t) {
+      c->push_group_of_tensor[static_cast<size_t>(t)] = G;
+      acc_n += L.numel[static_cast<size_t>(t)];
+      if (acc_n >= push_elems && t + 1 < L.T) {
+        G += 1;
+        acc_n = 0;
+      }
+    }
+    c->n_push_groups = G + 1;
+    std::vector<LambTile> push;
+    std::vector<int> gtiles(static_cast<size_t>(c->n_push_groups), 0);
+    int gcur = 0, first_t = 0;
+    auto close_group = [&](int g, int t_first) {
+      if (gtiles[static_cast<size_t>(g)] == 0) {  // nothing owned here: one empty tile publishes
+        push.push_back(LambTile{0, 0, 0, t_first});
+        gtiles[static_cast<size_t>(g)] = 1;
+      }
+    };
+    for (int t = 0; t < L.T; ++t) {
+      const int g = c->push_group_of_tensor[static_cast<size_t>(t)];
+      if (g != gcur) {
+        close_group(gcur, first_t);
+        gcur = g;
+        first_t = t;
+      }
+      for (int i = tile_begin[static_cast<size_t>(t)]; i < tile_begin[static_cast<size_t>(t) + 1]; ++i) {
+        push.push_back(lamb_tiles[static_cast<size_t>(i)]);
+        gtiles[static_cast<size_t>(g)] += 1;
+      }
+    }
+    close_group(gcur, first_t);
+    c->d_push_tiles = upload(c, push);
+    c->n_push_tiles = static_cast<int>(push.size());
+    c->d_push_group_of_tensor = upload(c, c->push_group_of_tensor);
+    c->d_push_group_tiles = upload(c, gtiles);
+    c->d_push_count = static_cast<unsigned*>(dev_alloc(c, static_cast<size_t>(c->n_push_groups) * sizeof(unsigned)));
   }
   c->d_tensors = upload(c, td);
   c->d_acc_tiles = upload(c, acc_tiles);

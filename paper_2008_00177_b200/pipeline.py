@@ -408,6 +408,18 @@ class GradPipeline:
             ptrs += [x if isinstance(x, int) else x.data_ptr() for x in g]
         _lib.check(self.lib.bo_train_step(self.ctx, _ptr_array(ptrs)))
 
+    def params_wait(self, tensor: int, stream=None) -> None:
+        """Order `stream` (torch stream; default: torch's current stream)
+        after the arrival of `tensor`'s parameter group from the most recent
+        step (the next forward overlapping the parameter all-gather)."""
+        import torch
+
+        s = stream if stream is not None else torch.cuda.current_stream()
+        _lib.check(self.lib.bo_params_wait(self.ctx, int(tensor), C.c_void_p(int(s.cuda_stream))))
+
+    def param_group(self, tensor: int) -> int:
+        return int(self.lib.bo_param_group(self.ctx, int(tensor)))
+
     def train_step_ptr_array(self, arr) -> None:
         """Fast path: a prebuilt ctypes array of the K x T pointers (make_ptr_array)."""
         _lib.check(self.lib.bo_train_step(self.ctx, arr))

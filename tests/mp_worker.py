@@ -43,12 +43,12 @@ def main():
     ap.add_argument("--model", default="tiny")
     args = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
-    # ranks beyond the visible GPUs share them (rank r on GPU r % ngpu): the
-    # default step maps peers with CUDA IPC and synchronises with flags, which
-    # works between processes on one device too (world 8 emulated on 4 or 1
-    # B200s). The host exchange runs over gloo, so nothing here needs NCCL
-    # unless the case does.
-    local = int(os.environ.get("LOCAL_RANK", rank)) % torch.cuda.device_count()
+    # one GPU per rank (never two ranks on one device: their flag-spinning
+    # kernels must run concurrently). The host exchange runs over gloo, so
+    # nothing here needs NCCL unless the case does.
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    if local >= torch.cuda.device_count():
+        raise SystemExit(f"rank {rank}: needs one GPU per rank")
     torch.cuda.set_device(local)
     dist.init_process_group("gloo")
 

@@ -1,12 +1,10 @@
 """Multi-rank parity (reduce-scatter -> sharded LAMB -> all-gather) against the
 oracle's emulation of the same world. Each case runs tests/mp_worker.py under
-torchrun, one process per rank. With at least as many GPUs as ranks every rank
-has its own B200 (NVLink between them); with fewer, ranks share GPUs
-round-robin (rank r on GPU r % ngpu): the default step maps its peers with
-CUDA IPC and synchronises with flags, no NCCL, which is legal between
-processes on one device — so world 2, 4 and 8 run even on a one-GPU box
-(bit-identical arithmetic; only the timing differs). Cases that use NCCL
-(the NCCL reduce-scatter, the NCCL hop barrier) need one GPU per rank."""
+torchrun, one process per rank, one GPU per rank (NVLink between them). Ranks
+never share a GPU here: kernels that spin on flags other ranks' kernels set
+must not run as separate launches on one device (B200_PROFILING.md: Xid 109).
+Worlds larger than the box are covered by tests/test_gpu_world_emu.py, which
+runs all ranks in ONE process in lockstep on one stream (no kernel waits)."""
 import json
 import os
 import socket
@@ -24,25 +22,12 @@ def _ngpu():
     return torch.cuda.device_count() if torch.cuda.is_available() else 0
 
 
-# cases run when ranks share GPUs (a bounded subset: every shared-GPU launch
-# time-slices the device between the ranks' contexts)
-SHARED = {"ring16", "ring32", "ring16_resident", "ring32_unfused_resident", "ring16_overlap",
-          "ring16_pull", "ring16_unfused", "ring32_resident"}
-
-
 def _placement(case, n):
-    """'own' (a GPU per rank), 'shared' (ranks share GPUs) or skip."""
+    """One GPU per rank, or skip."""
     g = _ngpu()
-    if g == 0:
-        pytest.skip("no CUDA device")
-    if g >= n:
-        return "own"
-    if "nccl" in case:
-        pytest.skip(f"{case} uses NCCL, which needs one GPU per rank ({n} > {g} GPUs)")
-    if case not in SHARED:
-        pytest.skip(f"{case}: run with one GPU per rank ({n} > {g} GPUs; the shared-GPU "
-                    "emulation runs the SHARED subset)")
-    return "shared"
+    if g < n:
+        pytest.skip(f"needs {n} GPUs (one per rank; {g} visible)")
+    return "own"
 
 
 def _port():
@@ -131,11 +116,10 @@ def test_two_gpus_bert_large_full_size():
 
 @pytest.mark.parametrize("n", [4, 8])
 def test_more_gpus(n):
-    """Worlds 4 and 8 (8 is the north star's target; with fewer GPUs the ranks
-    share them, which exercises the identical protocol and arithmetic)."""
+    """Worlds 4 and 8 (8 is the north star's target), one GPU per rank."""
     g = _ngpu()
-    if g == 0:
-        pytest.skip("no CUDA device")
+    if g < n:
+        pytest.skip(f"needs {n} GPUs (one per rank); world {n} on fewer GPUs: test_gpu_world_emu.py")
     expect = {
         "ring16": ["ring_p2p", "last_hop_fused", "ring_push"],
         "ring16_unfused": ["ring_p2p", "ring_push"],
@@ -146,11 +130,8 @@ def test_more_gpus(n):
         "ring16_pull_fused": ["ring_p2p", "last_hop_fused"],
     }
     for case, path in expect.items():
-        if g < n and case not in SHARED:
-            continue
         res = run_case(case, n)
         assert res["m_bit_exact"] and res["v_bit_exact"], case
         assert res["path"] == path, (case, res["path"])
         assert res["world"] == n and res["replicas_identical"]
-    if g >= n:
-        run_case("nccl32", n)
+    run_case("nccl32", n)
