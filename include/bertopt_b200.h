@@ -166,6 +166,15 @@ bo_status bo_comm_init(bo_ctx* ctx, const uint8_t* id128);
  * when ranks disagree (trainer.cpp:169-183). Several ranks may share one GPU. */
 bo_status bo_comm_export(bo_ctx* ctx, void* record, uint64_t* nbytes);
 bo_status bo_comm_import(bo_ctx* ctx, const void* records, uint64_t nbytes_each);
+/* A whole world in THIS process (the reference's run_data_parallel: one host
+ * thread per rank, trainer.cpp:397-470), all contexts on one device: peers
+ * are mapped directly, all contexts share one stream, and every cross-rank
+ * wait of the step becomes a rendezvous of the ranks' host threads between
+ * kernel launches (lockstep) — no kernel ever waits for another. Each rank's
+ * thread then calls the step entry points as usual, concurrently. Runs a
+ * world larger than the machine (world 8 on one B200) with the same kernels
+ * and bit-identical results; ring reduction only (no NCCL). */
+bo_status bo_world_init_local(bo_ctx* const* ctxs, int32_t n);
 /* Bound of every cross-rank wait inside a step (RunConfig::watchdog_s,
  * trainer.hpp:144; default 120 s). A peer that misses it abandons the step on
  * this rank (no update, loss scaler untouched) and the next bo_wait returns

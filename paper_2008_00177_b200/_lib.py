@@ -67,6 +67,7 @@ SIGNATURES = {
     "bo_comm_export": (_i32, [_vp, _vp, C.POINTER(_u64)]),
     "bo_comm_import": (_i32, [_vp, _vp, _u64]),
     "bo_set_watchdog": (_i32, [_vp, C.c_double]),
+    "bo_world_init_local": (_i32, [C.POINTER(_vp), _i32]),
     "bo_set_stream": (_i32, [_vp, _vp]),
     "bo_get_stream": (_vp, [_vp]),
     "bo_synchronize": (_i32, [_vp]),

@@ -444,7 +444,7 @@ void bo_destroy(bo_ctx* c) {
   if (c->comm_ready) cudaEventDestroy(c->comm_ready);
   if (c->comm_done) cudaEventDestroy(c->comm_done);
   if (c->params_done) cudaEventDestroy(c->params_done);
-  if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+  if (c->comm_stream && !c->shared_stream) cudaStreamDestroy(c->comm_stream);
   delete c->sync_tab;
   for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
   if (c->comm) ncclCommDestroy(c->comm);
@@ -533,6 +533,70 @@ bo_status bo_comm_init(bo_ctx* c, const uint8_t* id128) {
   BO_GUARD_END
 }
 
+bo_status bo_world_init_local(bo_ctx* const* ctxs, int32_t n) {
+  BO_GUARD_BEGIN
+  if (!ctxs || n < 2) fail(BO_ERR_INVALID_CONFIG, "a local world needs >= 2 contexts");
+  for (int i = 0; i < n; ++i) {
+    bo_ctx* c = ctxs[i];
+    if (!c) fail(BO_ERR_INVALID_CONFIG, "null ctx");
+    if (c->world != n || c->rank != i) {
+      fail(BO_ERR_PROTOCOL, "context " + std::to_string(i) + " is not rank " + std::to_string(i) +
+                                " of a world of " + std::to_string(n));
+    }
+    if (c->peers_mapped) fail(BO_ERR_PROTOCOL, "peers are already mapped");
+    if (c->device != ctxs[0]->device) fail(BO_ERR_INVALID_CONFIG, "a lockstep world shares one device");
+    if (c->L.hash != ctxs[0]->L.hash) {
+      fail(BO_ERR_BUCKET_LAYOUT_MISMATCH, "rank " + std::to_string(i) + " bucket layout disagrees with peers");
+    }
+    if (settings_hash(c) != settings_hash(ctxs[0])) {
+      fail(BO_ERR_PROTOCOL, "rank " + std::to_string(i) + " collective settings disagree with peers");
+    }
+    const bool ring = c->algo == BO_REDUCE_RING;
+    if (!ring || c->ring_via_nccl || !c->nb_barrier) {
+      fail(BO_ERR_INVALID_CONFIG, "a lockstep world runs the ring reduction without NCCL");
+    }
+  }
+  BO_CUDA(cudaSetDevice(ctxs[0]->device));
+  auto shared = std::make_shared<SharedStream>();
+  BO_CUDA(cudaStreamCreateWithFlags(&shared->s, cudaStreamNonBlocking));
+  auto bar = std::make_shared<HostBarrier>();
+  bar->n = n;
+  for (int i = 0; i < n; ++i) {
+    bo_ctx* c = ctxs[i];
+    BO_CUDA(cudaStreamSynchronize(c->stream));
+    if (c->own_stream) BO_CUDA(cudaStreamDestroy(c->stream));
+    if (c->comm_stream) {
+      BO_CUDA(cudaStreamSynchronize(c->comm_stream));
+      BO_CUDA(cudaStreamDestroy(c->comm_stream));
+    }
+    c->stream = shared->s;
+    c->comm_stream = shared->s;  // the overlapped sync micro's hops join the one stream too
+    c->own_stream = false;
+    c->shared_stream = shared;
+    c->lockstep = bar;
+    // peers are plain pointers in this process (no IPC)
+    std::vector<float*> peers(static_cast<size_t>(n));
+    c->peer_ctrl = PeerFlags{{}, n, i};
+    for (int j = 0; j < n; ++j) {
+      peers[static_cast<size_t>(j)] = ctxs[j]->w;
+      c->peer_wire[0][j] = ctxs[j]->wire[0];
+      c->peer_wire[1][j] = ctxs[j]->wire[1];
+      c->peer_ctrl.f[j] = ctxs[j]->ctrl;
+      c->peer_part[j] = ctxs[j]->all_part;
+    }
+    const int left = (i - 1 + n) % n, right = (i + 1) % n;
+    c->nb_flags = c->ctrl + kCtrlFromLeft;  // (the rendezvous replaces the flag waits)
+    c->nb_left_from_right = ctxs[left]->ctrl + kCtrlFromRight;
+    c->nb_right_from_left = ctxs[right]->ctrl + kCtrlFromLeft;
+    c->d_peer_w = static_cast<float**>(dev_alloc(c, peers.size() * sizeof(float*)));
+    BO_CUDA(cudaMemcpyAsync(c->d_peer_w, peers.data(), peers.size() * sizeof(float*),
+                            cudaMemcpyHostToDevice, c->stream));
+    c->peers_mapped = true;
+  }
+  BO_CUDA(cudaStreamSynchronize(shared->s));
+  BO_GUARD_END
+}
+
 bo_status bo_set_watchdog(bo_ctx* c, double seconds) {
   BO_GUARD_BEGIN
   if (!c) fail(BO_ERR_INVALID_CONFIG, "null ctx");
@@ -544,6 +608,7 @@ bo_status bo_set_watchdog(bo_ctx* c, double seconds) {
 bo_status bo_set_stream(bo_ctx* c, void* s) {
   BO_GUARD_BEGIN
   if (!c) fail(BO_ERR_INVALID_CONFIG, "null ctx");
+  if (c->lockstep) fail(BO_ERR_PROTOCOL, "the ranks of a lockstep world share one stream");
   BO_CUDA(cudaStreamSynchronize(c->stream));
   if (c->own_stream) BO_CUDA(cudaStreamDestroy(c->stream));
   if (s) {

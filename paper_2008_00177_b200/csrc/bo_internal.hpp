@@ -5,7 +5,10 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <condition_variable>
 #include <cstdint>
+#include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -173,6 +176,25 @@ struct PtrTable {
   const uint16_t* p[kMaxTensors];
 };
 
+// Lockstep world (bo_world_init_local): all ranks of a world live in one
+// process and share ONE stream; every cross-rank wait of the step (ring hop
+// barriers, the partials barrier, the end-of-step barrier) becomes a
+// rendezvous of the ranks' host threads between kernel launches, so the
+// stream holds every rank's phase-i kernels before any rank's phase-i+1
+// kernel — the device never has a kernel waiting for another one. Used to
+// run a world larger than the box (world 8 on one B200) bit for bit.
+struct HostBarrier {
+  std::mutex m;
+  std::condition_variable cv;
+  int n = 0, count = 0;
+  uint64_t gen = 0;
+  bool wait(uint64_t timeout_ns);
+};
+struct SharedStream {
+  cudaStream_t s = nullptr;
+  ~SharedStream();
+};
+
 // All K micro-batches of a step resident (bo_train_step): micro k's gradient
 // of tensor t is hk[k * T + t] (a device array). K == 0: not in use.
 struct MicroSrc {
@@ -269,7 +291,9 @@ struct bo_ctx {
   uint64_t bar_epoch = 0;              // all-rank barrier epochs (one per step)
   uint64_t watchdog_ns = 120000000000ull;  // RunConfig::watchdog_s = 120 (trainer.hpp:144)
   bool nb_barrier = true;              // BO_RING_BARRIER=nccl: 4-byte NCCL all-reduce instead
-  bool peers_mapped = false;           // bo_comm_import / bo_comm_init done
+  bool peers_mapped = false;           // bo_comm_import / bo_comm_init / bo_world_init_local done
+  std::shared_ptr<bo::HostBarrier> lockstep;      // bo_world_init_local
+  std::shared_ptr<bo::SharedStream> shared_stream;
   // Parameter groups of the push (world > 1): consecutive tensors in model
   // (= forward first-use) order; the push tiles are the LAMB tiles plus one
   // empty tile for every group this rank owns no element of, so that every
@@ -343,6 +367,8 @@ void run_reduce_group(bo_ctx* c, const PtrTable& tab, int b0, int b1, int acc0, 
                       cudaStream_t stream);
 void run_lamb(bo_ctx* c, const PtrTable& tab);
 void gather_shard(bo_ctx* c);
+// lockstep world: rendezvous of the ranks' host threads (no-op otherwise)
+void lockstep_sync(bo_ctx* c, const char* where);
 // the caller's stream waits for tensor's parameter group of the last step
 void params_wait(bo_ctx* c, int tensor, cudaStream_t stream);
 // needs the NCCL communicator (bo_comm_init): fail otherwise

@@ -18,6 +18,8 @@
 // --fmad=false, so nothing contracts into an FMA the reference does not have.
 #include <cuda_fp16.h>
 
+#include <chrono>
+
 #include "bo_device.cuh"
 #include "bo_internal.hpp"
 
@@ -894,8 +896,13 @@ static void lamb_sharded(bo_ctx* c, const PtrTable& tab, const W* in) {
   k_norm_reduce<<<T, kThreads, 0, c->stream>>>(c->d_tensor_tile_begin, c->tile_part, c->state, T,
                                                 c->rank_part, dst);
   check_launch(c, "k_norm_reduce");
+  PeerFlags pf = c->peer_ctrl;
+  if (c->lockstep) {  // every rank's k_norm_reduce is on the shared stream before any k_trust
+    lockstep_sync(c, "partials");
+    pf.n = 0;
+  }
   k_trust<<<1, 1024, 0, c->stream>>>(c->all_part + half, c->world, T, c->state, c->lamb, c->scaler,
-                                     c->trust, 1, c->peer_ctrl, epoch, c->watchdog_ns);
+                                     c->trust, 1, pf, epoch, c->watchdog_ns);
   check_launch(c, "k_trust");
   }
   {
@@ -910,6 +917,10 @@ static void lamb_sharded(bo_ctx* c, const PtrTable& tab, const W* in) {
   // past their phase 2 (kernel completion flushes the NVLink stores): an
   // all-rank flag barrier, no collective
   StageTimer timer(c, BO_STAGE_ALLGATHER);
+  if (c->lockstep) {
+    lockstep_sync(c, "end of step");
+    return;
+  }
   k_step_end_barrier<<<1, 1, 0, c->stream>>>(c->peer_ctrl, epoch, c->state, c->watchdog_ns);
   check_launch(c, "k_step_end_barrier");
 }
@@ -938,10 +949,37 @@ void run_lamb(bo_ctx* c, const PtrTable& tab) {
   }
 }
 
+bool HostBarrier::wait(uint64_t timeout_ns) {
+  std::unique_lock<std::mutex> lk(m);
+  const uint64_t g = gen;
+  if (++count == n) {
+    count = 0;
+    ++gen;
+    cv.notify_all();
+    return true;
+  }
+  return cv.wait_for(lk, std::chrono::nanoseconds(timeout_ns), [&] { return gen != g; });
+}
+
+SharedStream::~SharedStream() {
+  if (s) {
+    cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+  }
+}
+
+void lockstep_sync(bo_ctx* c, const char* where) {
+  if (!c->lockstep) return;
+  if (!c->lockstep->wait(c->watchdog_ns)) {
+    fail(BO_ERR_PEER_DISCONNECTED, "rank " + std::to_string(c->rank) + ": a rank thread of the lockstep "
+                                       "world did not reach the " + where + " rendezvous within the watchdog");
+  }
+}
+
 void params_wait(bo_ctx* c, int tensor, cudaStream_t stream) {
-  if (c->world == 1) {
-    // one rank: the update runs on the context stream; order the caller's
-    // stream after the most recent step
+  if (c->world == 1 || c->lockstep) {
+    // one rank (or a lockstep world on one stream): the update runs on the
+    // context stream; order the caller's stream after the most recent step
     if (!c->params_done) BO_CUDA(cudaEventCreateWithFlags(&c->params_done, cudaEventDisableTiming));
     BO_CUDA(cudaEventRecord(c->params_done, c->stream));
     BO_CUDA(cudaStreamWaitEvent(stream, c->params_done, 0));

@@ -170,6 +170,10 @@ __global__ void k_ring_barrier(unsigned* left_from_right, unsigned* right_from_l
 // Barrier before a ring hop: the neighbour flags when mapped, else a 4-byte
 // NCCL all-reduce.
 static void hop_barrier(bo_ctx* c, cudaStream_t st) {
+  if (c->lockstep) {
+    lockstep_sync(c, "ring hop");
+    return;
+  }
   if (c->nb_flags) {
     c->nb_epoch += 1;
     k_ring_barrier<<<1, 1, 0, st>>>(c->nb_left_from_right, c->nb_right_from_left, c->nb_flags,

@@ -256,6 +256,14 @@ class GradPipeline:
         blob = b"".join(records)
         _lib.check(self.lib.bo_comm_import(self.ctx, blob, len(records[0])))
 
+    @staticmethod
+    def world_init_local(pipes: list["GradPipeline"]) -> None:
+        """All ranks of a world in this process, one device, lockstep on one
+        stream (bo_world_init_local); then drive each rank from its own thread."""
+        lib = _lib.load()
+        arr = (C.c_void_p * len(pipes))(*[p.ctx.value for p in pipes])
+        _lib.check(lib.bo_world_init_local(arr, len(pipes)))
+
     def set_watchdog(self, seconds: float) -> None:
         """Bound of the cross-rank waits inside a step (RunConfig::watchdog_s)."""
         _lib.check(self.lib.bo_set_watchdog(self.ctx, float(seconds)))

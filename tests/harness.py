@@ -117,3 +117,37 @@ def max_rel_or_abs(a, b, floor=1e-6) -> float:
     a = a.astype(np.float64)
     b = b.astype(np.float64)
     return float(np.max(np.abs(a - b) / np.maximum(np.abs(b), floor))) if a.size else 0.0
+
+
+def run_world_lockstep(spec, cfg, params0, world, steps, device=0, grad_seed=1, spike_ppm=0,
+                       spike_exp=1, injections=(), resident=False, overlap=None):
+    """A whole world in this process on one GPU (bo_world_init_local): one
+    host thread per rank, as the reference's run_data_parallel, every rank's
+    kernels on one shared stream in lockstep. Returns (pipes, scale_used,
+    found_inf) with rank 0's sequences."""
+    import threading
+
+    pipes = [GradPipeline(spec, cfg, device=device, rank=r, world=world) for r in range(world)]
+    for p in pipes:
+        p.load_params(np.asarray(params0, np.float32))
+    GradPipeline.world_init_local(pipes)
+    out = [None] * world
+    errors = []
+
+    def rank_thread(r):
+        try:
+            torch.cuda.set_device(device)
+            out[r] = run_pipeline(spec, cfg, None, steps, grad_seed=grad_seed, spike_ppm=spike_ppm,
+                                  spike_exp=spike_exp, injections=injections, rank=r, world=world,
+                                  pipe=pipes[r], device=device, resident=resident, overlap=overlap)
+        except BaseException as e:  # noqa: BLE001
+            errors.append((r, e))
+
+    threads = [threading.Thread(target=rank_thread, args=(r,)) for r in range(world)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    if errors:
+        raise errors[0][1]
+    return pipes, out[0][1], out[0][2]
