@@ -237,6 +237,33 @@ class ClockSampler:
                 "reasons": names, "samples": len(self.samples)}
 
 
+def nvlink_counters(gpus):
+    """Cumulative NVLink data bytes (TX, RX) per GPU, summed over its links
+    (NVML field values NVLINK_THROUGHPUT_DATA_TX/RX, KiB), or None."""
+    try:
+        import pynvml as nv
+
+        nv.nvmlInit()
+        out = []
+        for i in gpus:
+            h = nv.nvmlDeviceGetHandleByIndex(i)
+            tx = rx = 0
+            for link in range(18):
+                try:
+                    vals = nv.nvmlDeviceGetFieldValues(h, [(nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX, link),
+                                                           (nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX, link)])
+                except Exception:  # noqa: BLE001
+                    break
+                if vals[0].nvmlReturn != 0 or vals[1].nvmlReturn != 0:
+                    continue
+                tx += vals[0].value.ullVal
+                rx += vals[1].value.ullVal
+            out.append((tx * 1024, rx * 1024))
+        return out
+    except Exception:  # noqa: BLE001
+        return None
+
+
 def traffic_from_profiles(kernel):
     path = os.path.join(ROOT, "profiles", "traffic.json")
     try:
@@ -345,6 +372,8 @@ def main_b200(args):
     sampler = ClockSampler(gpus) if rank == 0 else None
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
+    nvl0 = nvlink_counters(gpus) if rank == 0 and world > 1 else None
+    barrier()
     if sampler:
         sampler.__enter__()
     e0.record(stream)
@@ -354,6 +383,13 @@ def main_b200(args):
     barrier()
     if sampler:
         sampler.__exit__()
+    nvl1 = nvlink_counters(gpus) if rank == 0 and world > 1 else None
+    nvl_traffic = None
+    if nvl0 and nvl1:
+        per = [((b[0] - a[0]) / args.steps, (b[1] - a[1]) / args.steps) for a, b in zip(nvl0, nvl1)]
+        nvl_traffic = {"source": "NVML NVLINK_THROUGHPUT_DATA_TX/RX over the timed steps, per GPU per step",
+                       "tx_bytes_per_step": [int(t) for t, _ in per],
+                       "rx_bytes_per_step": [int(r) for _, r in per]}
     ms = e0.elapsed_time(e1) / args.steps
     launches = pipe.lib.bo_launch_count(pipe.ctx) - launches0
     ms = max_over_ranks(ms, world, local, emulated)
@@ -497,6 +533,12 @@ def main_b200(args):
     t_roof = hbm_a / (hbm * 1e9) + hbm_c / (hbm * 1e9) + nvl_b / (NVLINK_GBS * 1e9) + \
         nvl_d / (NVLINK_GBS * 1e9)
     t_pipe = max((hbm_a + hbm_c) / (hbm * 1e9), (nvl_b + nvl_d) / (NVLINK_GBS * 1e9))
+    if nvl_traffic:
+        # what the step must move per rank: the ring reduce-scatter and the
+        # parameter push into the N-1 other replicas (protocol bytes on top)
+        nvl_traffic["algorithmic_bytes_per_step"] = int(nvl_b + nvl_d)
+        nvl_traffic["measured_over_algorithmic"] = round(
+            max(nvl_traffic["tx_bytes_per_step"]) / max(nvl_b + nvl_d, 1), 4)
     step_roofline = {"t_roof_ms": round(t_roof * 1e3, 4), "frac": round(t_roof * 1e3 / ms, 4),
                      "t_pipelined_ms": round(t_pipe * 1e3, 4),
                      "pipelined_frac": round(t_pipe * 1e3 / ms, 4),
@@ -617,6 +659,7 @@ def main_b200(args):
                        "l2": "inputs (K x 2 B x P) larger than L2, no flush"},
             "roofline": roofline, "step_roofline": step_roofline, "stages": stages,
             "e2e": e2e, "per_micro_api": per_micro, "cpu_baseline": cpu,
+            "nvlink_traffic": nvl_traffic,
             "gpu_launches": int(launches),
             "clocks": sampler.summary() if sampler else None,
         }
@@ -625,6 +668,104 @@ def main_b200(args):
     pipe.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def main_lockstep(args):
+    """`python bench.py --gpus N` without torchrun: the N-rank world emulated
+    in this process on ONE GPU (bo_world_init_local: one host thread per rank,
+    every rank's kernels serialized on one stream, the cross-rank waits as
+    host rendezvous). Runs the world-N step end to end — same kernels, same
+    data flow — but its time is the sum of all ranks' work on one device, not
+    a scaling number (the JSON line says so)."""
+    json_fd = os.dup(1)
+    os.dup2(2, 1)
+    import threading
+
+    import numpy as np
+    import torch
+
+    from paper_2008_00177_b200.pipeline import (REDUCE_AUTO, REDUCE_NCCL, REDUCE_RING, GradPipeline,
+                                                LambConfig, ScalerConfig, TrainerConfig, synth_grads)
+
+    world, K = args.gpus, args.accumulation
+    torch.cuda.set_device(0)
+    spec = model_spec(args.model)
+    P = spec.param_count()
+    algo = {"auto": REDUCE_AUTO, "ring": REDUCE_RING, "nccl": REDUCE_NCCL}[args.algo]
+    cfg = TrainerConfig(LambConfig(lr=1e-4), K, int(args.bucket_mb * (1 << 20)), args.wire == "f16",
+                        REDUCE_RING if algo == REDUCE_AUTO else algo,
+                        ScalerConfig(init_scale=65536.0, growth_interval=1 << 30))
+    pipes = [GradPipeline(spec, cfg, device=0, rank=r, world=world) for r in range(world)]
+    w0 = torch.randn(P, device="cuda:0", generator=torch.Generator(device="cuda:0").manual_seed(1234)) * 0.02
+    for p in pipes:
+        p.load_params(w0)
+    del w0
+    GradPipeline.world_init_local(pipes)
+    numels = spec.numels()
+    slots, off = [], 0
+    for n in numels:
+        slots.append(off)
+        off += (n + 127) // 128 * 128
+    model_off = np.concatenate([[0], np.cumsum(numels)[:-1]])
+    arrays, keep = [], []
+    for r in range(world):
+        bufs = []
+        for k in range(K):
+            b = torch.empty(off, dtype=torch.int16, device="cuda:0")
+            for t, n in enumerate(numels):
+                synth_grads(b[slots[t]:slots[t] + n], int(model_off[t]), 1, r, 0, k, 65536.0)
+            bufs.append(b)
+        keep.append(bufs)
+        arrays.append(GradPipeline.make_ptr_array([b.data_ptr() + 2 * s for b in bufs for s in slots]))
+    torch.cuda.synchronize()
+    stream = torch.cuda.ExternalStream(pipes[0].stream_handle())
+    gate = threading.Barrier(world)
+    errors = []
+
+    def run(r, n):
+        try:
+            gate.wait()
+            for _ in range(n):
+                pipes[r].train_step_ptr_array(arrays[r])
+        except BaseException as e:  # noqa: BLE001
+            errors.append(e)
+
+    def steps(n):
+        th = [threading.Thread(target=run, args=(r, n)) for r in range(world)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        if errors:
+            raise errors[0]
+
+    steps(args.warmup)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    steps(args.steps)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    w = [p.read_params() for p in pipes]
+    same = all(np.array_equal(w[0].view(np.uint32), x.view(np.uint32)) for x in w[1:])
+    st = pipes[0].status()
+    line = {"metric": METRIC, "value": world * P / (ms * 1e-3), "unit": UNIT, "n_gpus": 1,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (counter-based fp16 gradients, random-init fp32 weights)",
+            "config": {"workload": f"{args.model} optimizer step, world {world} emulated on one GPU",
+                       "params": P, "accumulation": K, "wire": args.wire,
+                       "kernel_path": pipes[0].path(),
+                       "emulated": f"lockstep world of {world} ranks in one process on 1 GPU: every "
+                                   "rank's kernels serialized on one stream, cross-rank waits as "
+                                   "host-thread rendezvous; ms_per_step is ALL ranks' work on one "
+                                   "device, not a scaling number",
+                       "replicas_identical": bool(same), "lamb_step": st.lamb_step,
+                       "skipped_steps": st.skipped_steps}}
+    os.write(json_fd, (json.dumps(line) + "\n").encode())
+    for p in pipes:
+        p.close()
 
 
 def main_reference(args):
@@ -667,5 +808,7 @@ if __name__ == "__main__":
     a = parse()
     if a.impl == "reference":
         main_reference(a)
+    elif a.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        main_lockstep(a)
     else:
         main_b200(a)

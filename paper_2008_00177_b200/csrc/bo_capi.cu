@@ -361,6 +361,7 @@ bo_status bo_create(const bo_trainer_config* cfg, int32_t n_tensors, const int64
   if (const char* e = std::getenv("BO_RING_PUSH")) c->ring_push = std::strcmp(e, "0") != 0;
   if (const char* e = std::getenv("BO_RING_BARRIER")) c->nb_barrier = std::strcmp(e, "nccl") != 0;
   if (const char* e = std::getenv("BO_FUSE_LAST")) c->fuse_last_hop = std::strcmp(e, "0") != 0;
+  if (const char* e = std::getenv("BO_PUSH_CTAS")) c->push_ctas = std::max(0, std::atoi(e));
   c->algo = cfg->reduce_algo == BO_REDUCE_AUTO ? (cfg->f16_exchange ? BO_REDUCE_RING : BO_REDUCE_NCCL)
                                                : cfg->reduce_algo;
   BO_CUDA(cudaSetDevice(device));

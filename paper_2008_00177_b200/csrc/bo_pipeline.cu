@@ -649,98 +649,120 @@ struct PushGroups {
   unsigned epoch;
 };
 
-__device__ __forceinline__ void push_group_done(const PushGroups& G, int tensor) {
-  __threadfence_system();  // this thread's replica stores (edges) before the count
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const int g = G.group_of_tensor[tensor];
-    const unsigned done = atomicAdd(G.count + g, 1u) + 1u;
-    if (done % static_cast<unsigned>(G.group_tiles[g]) == 0u) {
-      __threadfence_system();
-      for (int j = 0; j < G.pf.n; ++j) {
-        unsigned* f = G.pf.f[j] + kCtrlReady + 8 * g + G.pf.rank;
-        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f), "r"(G.epoch) : "memory");
-      }
+// Thread 0, once every store of a finished tile has completed (bulk copies
+// waited for, the CTA's edge stores ordered by a barrier): count the tile;
+// the group's last tile publishes the group into every rank's flags.
+__device__ __forceinline__ void push_tile_done(const PushGroups& G, int tensor) {
+  __threadfence_system();
+  const int g = G.group_of_tensor[tensor];
+  const unsigned done = atomicAdd(G.count + g, 1u) + 1u;
+  if (done % static_cast<unsigned>(G.group_tiles[g]) == 0u) {
+    __threadfence_system();
+    for (int j = 0; j < G.pf.n; ++j) {
+      unsigned* f = G.pf.f[j] + kCtrlReady + 8 * g + G.pf.rank;
+      asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f), "r"(G.epoch) : "memory");
     }
   }
 }
 
+// Persistent: gridDim.x CTAs walk the push tiles (model order, so parameter
+// groups complete front to back) with two shared-memory tile buffers: the
+// bulk copies of tile i fly while tile i + grid is computed. A small grid
+// (BO_PUSH_CTAS) leaves the other SMs to a concurrent forward
+// (bo_params_wait); the default fills the GPU. Skipped steps only count.
+constexpr int kPushBufs = 2;
 __global__ void __launch_bounds__(kThreads) k_shard_p2_push(const LambTile* __restrict__ tiles,
-                                                            float* __restrict__ wsh,
+                                                            int n_tiles, float* __restrict__ wsh,
                                                             const float* __restrict__ u,
-                                                                 const DevState* __restrict__ st,
-                                                                 LambConsts c,
-                                                                 const float* __restrict__ trust,
-                                                                 float* const* __restrict__ peer_w,
-                                                                 int N, const PushGroups G) {
-  const LambTile t = tiles[blockIdx.x];
-  if (!st->do_update || t.len == 0) {  // skipped step / a group's empty tile: publish only
-    push_group_done(G, t.t);
-    return;
-  }
-  __shared__ __align__(128) float buf[kTileElems + 4];
+                                                            const DevState* __restrict__ st,
+                                                            LambConsts c,
+                                                            const float* __restrict__ trust,
+                                                            float* const* __restrict__ peer_w,
+                                                            int N, const PushGroups G) {
+  __shared__ __align__(128) float bufs[kPushBufs][kTileElems + 4];
   __shared__ float* dst[8];
   if (threadIdx.x < N) dst[threadIdx.x] = peer_w[threadIdx.x];
-  const float step_scale = __fmul_rn(c.lr, trust[t.t]);
-  const int off = static_cast<int>(t.w0 & 3);  // buf[off + e] <-> flat element w0 + e
-  const Split sp = split_tile(t.s0, t.len);
-  auto one = [&](int e) {
-    const int64_t s = t.s0 + e;
-    const float nw = __fsub_rn(wsh[s], __fmul_rn(step_scale, u[s]));
-    wsh[s] = nw;
-    buf[off + e] = nw;
-  };
-  if (static_cast<int>(threadIdx.x) < sp.head) one(threadIdx.x);
-  if (threadIdx.x >= 32 && static_cast<int>(threadIdx.x) - 32 < sp.tail) {
-    one(sp.head + 4 * sp.nv + static_cast<int>(threadIdx.x) - 32);
-  }
-  for (int q = threadIdx.x; q < sp.nv; q += kThreads) {
-    const int e = sp.head + 4 * q;
-    const int64_t s = t.s0 + e;
-    const float4 w4 = *reinterpret_cast<const float4*>(wsh + s);
-    const float4 u4 = __ldcs(reinterpret_cast<const float4*>(u + s));
-    const float4 n4 = make_float4(__fsub_rn(w4.x, __fmul_rn(step_scale, u4.x)),
-                                  __fsub_rn(w4.y, __fmul_rn(step_scale, u4.y)),
-                                  __fsub_rn(w4.z, __fmul_rn(step_scale, u4.z)),
-                                  __fsub_rn(w4.w, __fmul_rn(step_scale, u4.w)));
-    *reinterpret_cast<float4*>(wsh + s) = n4;
-    buf[off + e] = n4.x;
-    buf[off + e + 1] = n4.y;
-    buf[off + e + 2] = n4.z;
-    buf[off + e + 3] = n4.w;
-  }
-  // make the generic-proxy shared-memory writes visible to the bulk copies
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  __syncthreads();
-  // flat elements [w0, w0 + len): aligned middle [a0, a1) by bulk copy
-  const int64_t a0 = (t.w0 + 3) & ~static_cast<int64_t>(3);
-  const int64_t a1 = (t.w0 + t.len) & ~static_cast<int64_t>(3);
-  if (a1 > a0) {
-    if (threadIdx.x == 0) {
-      // destinations in a per-tile rotated order, so the CTAs of all ranks
-      // spread their pushes over every peer's NVLink ingress at any moment
-      for (int i = 0; i < N; ++i) {
-        const int j = (static_cast<int>(blockIdx.x) + i) % N;
-        bulk_s2g(dst[j] + a0, buf + off + (a0 - t.w0), static_cast<uint32_t>(a1 - a0) * 4u);
+  const bool update = st->do_update != 0;
+  int pending = -1;  // tensor of the previous tile (its stores in flight)
+  int it = 0;
+  for (int i = blockIdx.x; i < n_tiles; i += gridDim.x, ++it) {
+    const LambTile t = tiles[i];
+    float* __restrict__ buf = bufs[it & 1];
+    // this buffer's previous copies (two tiles ago) have finished reading it
+    if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+    __syncthreads();
+    int64_t a0 = 0, a1 = 0;
+    if (update && t.len > 0) {
+      const float step_scale = __fmul_rn(c.lr, trust[t.t]);
+      const int off = static_cast<int>(t.w0 & 3);  // buf[off + e] <-> flat element w0 + e
+      const Split sp = split_tile(t.s0, t.len);
+      auto one = [&](int e) {
+        const int64_t s = t.s0 + e;
+        const float nw = __fsub_rn(wsh[s], __fmul_rn(step_scale, u[s]));
+        wsh[s] = nw;
+        buf[off + e] = nw;
+      };
+      if (static_cast<int>(threadIdx.x) < sp.head) one(threadIdx.x);
+      if (threadIdx.x >= 32 && static_cast<int>(threadIdx.x) - 32 < sp.tail) {
+        one(sp.head + 4 * sp.nv + static_cast<int>(threadIdx.x) - 32);
       }
-      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      for (int q = threadIdx.x; q < sp.nv; q += kThreads) {
+        const int e = sp.head + 4 * q;
+        const int64_t s = t.s0 + e;
+        const float4 w4 = *reinterpret_cast<const float4*>(wsh + s);
+        const float4 u4 = __ldcs(reinterpret_cast<const float4*>(u + s));
+        const float4 n4 = make_float4(__fsub_rn(w4.x, __fmul_rn(step_scale, u4.x)),
+                                      __fsub_rn(w4.y, __fmul_rn(step_scale, u4.y)),
+                                      __fsub_rn(w4.z, __fmul_rn(step_scale, u4.z)),
+                                      __fsub_rn(w4.w, __fmul_rn(step_scale, u4.w)));
+        *reinterpret_cast<float4*>(wsh + s) = n4;
+        buf[off + e] = n4.x;
+        buf[off + e + 1] = n4.y;
+        buf[off + e + 2] = n4.z;
+        buf[off + e + 3] = n4.w;
+      }
+      // make the generic-proxy shared-memory writes visible to the bulk copies
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncthreads();
+      // flat elements [w0, w0 + len): aligned middle [a0, a1) by bulk copy
+      a0 = (t.w0 + 3) & ~static_cast<int64_t>(3);
+      a1 = (t.w0 + t.len) & ~static_cast<int64_t>(3);
+      if (a1 > a0 && threadIdx.x == 0) {
+        // destinations in a per-tile rotated order, so the CTAs of all ranks
+        // spread their pushes over every peer's NVLink ingress at any moment
+        for (int k = 0; k < N; ++k) {
+          const int j = (i + k) % N;
+          bulk_s2g(dst[j] + a0, buf + off + (a0 - t.w0), static_cast<uint32_t>(a1 - a0) * 4u);
+        }
+      }
+      // edges (and tiles shorter than one aligned 16-byte group)
+      const int nhead = static_cast<int>(a1 > a0 ? a0 - t.w0 : t.len);
+      const int ntail = static_cast<int>(a1 > a0 ? t.w0 + t.len - a1 : 0);
+      if (static_cast<int>(threadIdx.x) < nhead * N) {
+        const int e = threadIdx.x % nhead, j = threadIdx.x / nhead;
+        dst[j][t.w0 + e] = buf[off + e];
+      } else if (static_cast<int>(threadIdx.x) >= 128 && static_cast<int>(threadIdx.x) - 128 < ntail * N) {
+        const int k = static_cast<int>(threadIdx.x) - 128;
+        const int e = static_cast<int>(a1 - t.w0) + k % ntail, j = k / ntail;
+        dst[j][t.w0 + e] = buf[off + e];
+      }
     }
+    if (threadIdx.x == 0) {
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");  // (empty when nothing was issued)
+      if (pending >= 0) {
+        // the previous tile's copies are complete once only this tile's group is
+        // outstanding; its edge stores precede this iteration's barrier
+        asm volatile("cp.async.bulk.wait_group 1;" ::: "memory");
+        push_tile_done(G, pending);
+      }
+    }
+    pending = t.t;
   }
-  // edges (and tiles shorter than one aligned 16-byte group)
-  const int nhead = static_cast<int>(a1 > a0 ? a0 - t.w0 : t.len);
-  const int ntail = static_cast<int>(a1 > a0 ? t.w0 + t.len - a1 : 0);
-  if (static_cast<int>(threadIdx.x) < nhead * N) {
-    const int e = threadIdx.x % nhead, j = threadIdx.x / nhead;
-    dst[j][t.w0 + e] = buf[off + e];
-  } else if (static_cast<int>(threadIdx.x) >= 128 && static_cast<int>(threadIdx.x) - 128 < ntail * N) {
-    const int i = static_cast<int>(threadIdx.x) - 128;
-    const int e = static_cast<int>(a1 - t.w0) + i % ntail, j = i / ntail;
-    dst[j][t.w0 + e] = buf[off + e];
+  __syncthreads();  // the last tile's edge stores
+  if (threadIdx.x == 0 && pending >= 0) {
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    push_tile_done(G, pending);
   }
-  // the shared-memory tile must outlive the copies (wait for their writes,
-  // not only their smem reads, so the group flag below covers them)
-  if (threadIdx.x == 0 && a1 > a0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-  push_group_done(G, t.t);
 }
 
 // bo_params_wait: one thread on the caller's stream waits until every rank
@@ -908,9 +930,10 @@ static void lamb_sharded(bo_ctx* c, const PtrTable& tab, const W* in) {
   {
   StageTimer timer(c, BO_STAGE_LAMB_UPDATE);
   const PushGroups G{c->d_push_group_of_tensor, c->d_push_group_tiles, c->d_push_count, c->peer_ctrl, epoch};
-  k_shard_p2_push<<<c->n_push_tiles, kThreads, 0, c->stream>>>(c->d_push_tiles, c->wsh, c->u,
-                                                              c->state, c->lamb, c->trust,
-                                                              c->d_peer_w, c->world, G);
+  const int grid = std::min(c->n_push_tiles, c->push_ctas > 0 ? c->push_ctas : 6 * c->num_sms);
+  k_shard_p2_push<<<grid, kThreads, 0, c->stream>>>(c->d_push_tiles, c->n_push_tiles, c->wsh, c->u,
+                                                    c->state, c->lamb, c->trust, c->d_peer_w,
+                                                    c->world, G);
   check_launch(c, "k_shard_p2_push");
   }
   // every rank's pushes into every replica have landed once all ranks are

@@ -6,7 +6,8 @@ phase-1 (max_seq 128) and phase-2 (max_seq 512) parameter sets, bucket_bytes in
 {1, 4, 16, 64, 256, 1024} MiB (BucketLayout::build gives 295/294/122/25/6/2
 buckets for BERT-large) — and writes one summary JSON (stdout and --out).
 
-    python sweep.py --gpus 4 --steps 10 --warmup 3 --out profiles/sweep_r01_n4.json
+    python sweep.py --gpus 4 --steps 10 --warmup 3 --out profiles/r02_sweep_n4.json
+    (wires: the binary16 ring, the bit-exact fp32 ring, the NCCL fp32 reduce-scatter)
 """
 from __future__ import annotations
 
@@ -55,13 +56,15 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--out", default=None)
-    ap.add_argument("--wires", default="f16:ring,f32:nccl")
+    ap.add_argument("--wires", default="f16:ring,f32:ring,f32:nccl")
+    ap.add_argument("--models", default="bert-large-128,bert-large")
+    ap.add_argument("--buckets", default=",".join(str(b) for b in BUCKETS_MB))
     args = ap.parse_args()
     rows = []
-    for model in ("bert-large-128", "bert-large"):
+    for model in args.models.split(","):
         for wa in args.wires.split(","):
             wire, algo = wa.split(":")
-            for mb in BUCKETS_MB:
+            for mb in [float(b) for b in args.buckets.split(",")]:
                 res = run_one(args.gpus, model, wire, algo, mb, args.steps, args.warmup)
                 row = {"model": model, "wire": wire, "algo": algo, "bucket_mb": mb, **res}
                 rows.append(row)
