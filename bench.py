@@ -237,29 +237,37 @@ class ClockSampler:
                 "reasons": names, "samples": len(self.samples)}
 
 
+# NVML NVLink byte counters, per link: (tx field, rx field, bytes per unit)
+NVL_FIELDS = [(202, 204, 1),     # NVML_FI_DEV_NVLINK_COUNT_XMIT_BYTES / RCV_BYTES
+              (138, 139, 1024)]  # NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX / RX (KiB)
+
+
 def nvlink_counters(gpus):
-    """Cumulative NVLink data bytes (TX, RX) per GPU, summed over its links
-    (NVML field values NVLINK_THROUGHPUT_DATA_TX/RX, KiB), or None."""
+    """Cumulative NVLink bytes (TX, RX) per GPU summed over its 18 links, from
+    the first NVML counter pair the driver reports, or None."""
     try:
         import pynvml as nv
 
         nv.nvmlInit()
-        out = []
-        for i in gpus:
-            h = nv.nvmlDeviceGetHandleByIndex(i)
-            tx = rx = 0
-            for link in range(18):
-                try:
-                    vals = nv.nvmlDeviceGetFieldValues(h, [(nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX, link),
-                                                           (nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX, link)])
-                except Exception:  # noqa: BLE001
-                    break
-                if vals[0].nvmlReturn != 0 or vals[1].nvmlReturn != 0:
-                    continue
-                tx += vals[0].value.ullVal
-                rx += vals[1].value.ullVal
-            out.append((tx * 1024, rx * 1024))
-        return out
+        handles = [nv.nvmlDeviceGetHandleByIndex(i) for i in gpus]
+        for ftx, frx, unit in NVL_FIELDS:
+            out, seen = [], False
+            for h in handles:
+                tx = rx = 0
+                for link in range(18):
+                    try:
+                        vals = nv.nvmlDeviceGetFieldValues(h, [(ftx, link), (frx, link)])
+                    except Exception:  # noqa: BLE001
+                        break
+                    if vals[0].nvmlReturn != 0 or vals[1].nvmlReturn != 0:
+                        continue
+                    tx += vals[0].value.ullVal
+                    rx += vals[1].value.ullVal
+                seen |= tx > 0 or rx > 0
+                out.append((tx * unit, rx * unit))
+            if seen:
+                return out
+        return None
     except Exception:  # noqa: BLE001
         return None
 
@@ -387,7 +395,8 @@ def main_b200(args):
     nvl_traffic = None
     if nvl0 and nvl1:
         per = [((b[0] - a[0]) / args.steps, (b[1] - a[1]) / args.steps) for a, b in zip(nvl0, nvl1)]
-        nvl_traffic = {"source": "NVML NVLINK_THROUGHPUT_DATA_TX/RX over the timed steps, per GPU per step",
+        nvl_traffic = {"source": "NVML NVLink byte counters (per link, summed) over the timed steps, "
+                                 "per GPU per step",
                        "tx_bytes_per_step": [int(t) for t, _ in per],
                        "rx_bytes_per_step": [int(r) for _, r in per]}
     ms = e0.elapsed_time(e1) / args.steps

@@ -307,7 +307,7 @@ struct bo_ctx {
   int* d_push_group_tiles = nullptr;   // [G] tiles of group g on this rank
   unsigned* d_push_count = nullptr;    // [G] cumulative finished tiles
   cudaEvent_t params_done = nullptr;   // world 1: the step's update, for bo_params_wait
-  int push_ctas = 0;                   // BO_PUSH_CTAS: persistent push grid (0: 6 per SM)
+  int push_ctas = 0;                   // BO_PUSH_CTAS: persistent push grid (0: one CTA per tile)
   double* peer_part[8] = {};           // every rank's all_part (IPC)
   void* wire[3] = {nullptr, nullptr, nullptr};  // ring staging (shard-sized)
   double* tile_part = nullptr;    // [n_lamb_tiles][2]

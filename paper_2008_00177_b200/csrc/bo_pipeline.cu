@@ -665,12 +665,15 @@ __device__ __forceinline__ void push_tile_done(const PushGroups& G, int tensor) 
   }
 }
 
-// Persistent: gridDim.x CTAs walk the push tiles (model order, so parameter
-// groups complete front to back) with two shared-memory tile buffers: the
-// bulk copies of tile i fly while tile i + grid is computed. A small grid
-// (BO_PUSH_CTAS) leaves the other SMs to a concurrent forward
-// (bo_params_wait); the default fills the GPU. Skipped steps only count.
-constexpr int kPushBufs = 2;
+// gridDim.x CTAs walk the push tiles (model order, so parameter groups
+// complete front to back). NB = 1 (default): one tile per CTA, the hardware
+// keeps ~8 CTAs — 8 tiles' copies — in flight per SM (measured fastest:
+// 0.99 vs 1.28 ms at world 2 for a persistent grid of 6 CTAs per SM).
+// NB = 2 (BO_PUSH_CTAS > 0): a persistent grid with two shared-memory tile
+// buffers, the copies of tile i flying while tile i + grid is computed; a
+// small grid leaves SMs to a concurrent forward (bo_params_wait) at the cost
+// of push bandwidth. Skipped steps only count.
+template <int NB>
 __global__ void __launch_bounds__(kThreads) k_shard_p2_push(const LambTile* __restrict__ tiles,
                                                             int n_tiles, float* __restrict__ wsh,
                                                             const float* __restrict__ u,
@@ -679,7 +682,7 @@ __global__ void __launch_bounds__(kThreads) k_shard_p2_push(const LambTile* __re
                                                             const float* __restrict__ trust,
                                                             float* const* __restrict__ peer_w,
                                                             int N, const PushGroups G) {
-  __shared__ __align__(128) float bufs[kPushBufs][kTileElems + 4];
+  __shared__ __align__(128) float bufs[NB][kTileElems + 4];
   __shared__ float* dst[8];
   if (threadIdx.x < N) dst[threadIdx.x] = peer_w[threadIdx.x];
   const bool update = st->do_update != 0;
@@ -687,9 +690,9 @@ __global__ void __launch_bounds__(kThreads) k_shard_p2_push(const LambTile* __re
   int it = 0;
   for (int i = blockIdx.x; i < n_tiles; i += gridDim.x, ++it) {
     const LambTile t = tiles[i];
-    float* __restrict__ buf = bufs[it & 1];
-    // this buffer's previous copies (two tiles ago) have finished reading it
-    if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+    float* __restrict__ buf = bufs[it % NB];
+    // this buffer's previous copies (NB tiles ago) have finished reading it
+    if (NB > 1 && threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
     __syncthreads();
     int64_t a0 = 0, a1 = 0;
     if (update && t.len > 0) {
@@ -930,10 +933,15 @@ static void lamb_sharded(bo_ctx* c, const PtrTable& tab, const W* in) {
   {
   StageTimer timer(c, BO_STAGE_LAMB_UPDATE);
   const PushGroups G{c->d_push_group_of_tensor, c->d_push_group_tiles, c->d_push_count, c->peer_ctrl, epoch};
-  const int grid = std::min(c->n_push_tiles, c->push_ctas > 0 ? c->push_ctas : 6 * c->num_sms);
-  k_shard_p2_push<<<grid, kThreads, 0, c->stream>>>(c->d_push_tiles, c->n_push_tiles, c->wsh, c->u,
-                                                    c->state, c->lamb, c->trust, c->d_peer_w,
-                                                    c->world, G);
+  if (c->push_ctas > 0 && c->push_ctas < c->n_push_tiles) {
+    k_shard_p2_push<2><<<c->push_ctas, kThreads, 0, c->stream>>>(c->d_push_tiles, c->n_push_tiles, c->wsh,
+                                                                 c->u, c->state, c->lamb, c->trust,
+                                                                 c->d_peer_w, c->world, G);
+  } else {
+    k_shard_p2_push<1><<<c->n_push_tiles, kThreads, 0, c->stream>>>(c->d_push_tiles, c->n_push_tiles,
+                                                                    c->wsh, c->u, c->state, c->lamb,
+                                                                    c->trust, c->d_peer_w, c->world, G);
+  }
   check_launch(c, "k_shard_p2_push");
   }
   // every rank's pushes into every replica have landed once all ranks are

@@ -91,12 +91,15 @@ def run_pipeline_case(lib, arena, aligned, resident):
     for k in range(K):
         row = []
         for n in SIZES:
-            # aligned: the slot starts 16-byte aligned (vector paths); unaligned:
-            # 2 bytes off (scalar paths); either way it ends at the guard
-            nb = n * 2 + (0 if aligned else 2)
-            nb = (nb + 15) // 16 * 16 if aligned else nb
-            base = arena.alloc_tail(max(nb, 16))
-            row.append(base + (max(nb, 16) - n * 2))
+            if aligned:
+                # 16-byte aligned slot (the vector paths): the tensor ends at
+                # most 14 bytes before the guard (its last 16-byte group)
+                nb = max(16, (n * 2 + 15) // 16 * 16)
+                row.append(arena.alloc_tail(nb))
+            else:
+                # one binary16 into an allocation (the scalar paths): the
+                # tensor ends exactly at the guard
+                row.append(arena.alloc_tail(n * 2 + 2) + 2)
         ptrs.append(row)
     for step in range(2):
         S = pipe.status().loss_scale
@@ -153,7 +156,11 @@ def main():
     paths = []
     for aligned in (True, False):
         for resident in (False, True):
-            paths.append(run_pipeline_case(lib, arena, aligned, resident))
+            path = run_pipeline_case(lib, arena, aligned, resident)
+            # aligned slots take the fused vector kernels, unaligned the scalar ones
+            assert ("one_rank_fused" in path) == aligned, (aligned, path)
+            assert ("resident_micros" in path) == (aligned and resident), (aligned, resident, path)
+            paths.append(path)
     run_operator_cases(lib, arena)
     _lib.check(lib.bo_free(p))
     arena.close()
