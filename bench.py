@@ -237,41 +237,6 @@ class ClockSampler:
                 "reasons": names, "samples": len(self.samples)}
 
 
-# NVML NVLink byte counters, per link: (tx field, rx field, bytes per unit)
-NVL_FIELDS = [(202, 204, 1),     # NVML_FI_DEV_NVLINK_COUNT_XMIT_BYTES / RCV_BYTES
-              (138, 139, 1024)]  # NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX / RX (KiB)
-
-
-def nvlink_counters(gpus):
-    """Cumulative NVLink bytes (TX, RX) per GPU summed over its 18 links, from
-    the first NVML counter pair the driver reports, or None."""
-    try:
-        import pynvml as nv
-
-        nv.nvmlInit()
-        handles = [nv.nvmlDeviceGetHandleByIndex(i) for i in gpus]
-        for ftx, frx, unit in NVL_FIELDS:
-            out, seen = [], False
-            for h in handles:
-                tx = rx = 0
-                for link in range(18):
-                    try:
-                        vals = nv.nvmlDeviceGetFieldValues(h, [(ftx, link), (frx, link)])
-                    except Exception:  # noqa: BLE001
-                        break
-                    if vals[0].nvmlReturn != 0 or vals[1].nvmlReturn != 0:
-                        continue
-                    tx += vals[0].value.ullVal
-                    rx += vals[1].value.ullVal
-                seen |= tx > 0 or rx > 0
-                out.append((tx * unit, rx * unit))
-            if seen:
-                return out
-        return None
-    except Exception:  # noqa: BLE001
-        return None
-
-
 def traffic_from_profiles(kernel):
     path = os.path.join(ROOT, "profiles", "traffic.json")
     try:
@@ -380,8 +345,6 @@ def main_b200(args):
     sampler = ClockSampler(gpus) if rank == 0 else None
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
-    nvl0 = nvlink_counters(gpus) if rank == 0 and world > 1 else None
-    barrier()
     if sampler:
         sampler.__enter__()
     e0.record(stream)
@@ -391,14 +354,6 @@ def main_b200(args):
     barrier()
     if sampler:
         sampler.__exit__()
-    nvl1 = nvlink_counters(gpus) if rank == 0 and world > 1 else None
-    nvl_traffic = None
-    if nvl0 and nvl1:
-        per = [((b[0] - a[0]) / args.steps, (b[1] - a[1]) / args.steps) for a, b in zip(nvl0, nvl1)]
-        nvl_traffic = {"source": "NVML NVLink byte counters (per link, summed) over the timed steps, "
-                                 "per GPU per step",
-                       "tx_bytes_per_step": [int(t) for t, _ in per],
-                       "rx_bytes_per_step": [int(r) for _, r in per]}
     ms = e0.elapsed_time(e1) / args.steps
     launches = pipe.lib.bo_launch_count(pipe.ctx) - launches0
     ms = max_over_ranks(ms, world, local, emulated)
@@ -542,12 +497,6 @@ def main_b200(args):
     t_roof = hbm_a / (hbm * 1e9) + hbm_c / (hbm * 1e9) + nvl_b / (NVLINK_GBS * 1e9) + \
         nvl_d / (NVLINK_GBS * 1e9)
     t_pipe = max((hbm_a + hbm_c) / (hbm * 1e9), (nvl_b + nvl_d) / (NVLINK_GBS * 1e9))
-    if nvl_traffic:
-        # what the step must move per rank: the ring reduce-scatter and the
-        # parameter push into the N-1 other replicas (protocol bytes on top)
-        nvl_traffic["algorithmic_bytes_per_step"] = int(nvl_b + nvl_d)
-        nvl_traffic["measured_over_algorithmic"] = round(
-            max(nvl_traffic["tx_bytes_per_step"]) / max(nvl_b + nvl_d, 1), 4)
     step_roofline = {"t_roof_ms": round(t_roof * 1e3, 4), "frac": round(t_roof * 1e3 / ms, 4),
                      "t_pipelined_ms": round(t_pipe * 1e3, 4),
                      "pipelined_frac": round(t_pipe * 1e3 / ms, 4),
@@ -668,7 +617,6 @@ def main_b200(args):
                        "l2": "inputs (K x 2 B x P) larger than L2, no flush"},
             "roofline": roofline, "step_roofline": step_roofline, "stages": stages,
             "e2e": e2e, "per_micro_api": per_micro, "cpu_baseline": cpu,
-            "nvlink_traffic": nvl_traffic,
             "gpu_launches": int(launches),
             "clocks": sampler.summary() if sampler else None,
         }

@@ -362,7 +362,6 @@ bo_status bo_create(const bo_trainer_config* cfg, int32_t n_tensors, const int64
   if (const char* e = std::getenv("BO_RING_BARRIER")) c->nb_barrier = std::strcmp(e, "nccl") != 0;
   if (const char* e = std::getenv("BO_FUSE_LAST")) c->fuse_last_hop = std::strcmp(e, "0") != 0;
   if (const char* e = std::getenv("BO_PUSH_CTAS")) c->push_ctas = std::max(0, std::atoi(e));
-  if (const char* e = std::getenv("BO_PUSH_CE")) c->push_ce = std::strcmp(e, "0") != 0;
   c->algo = cfg->reduce_algo == BO_REDUCE_AUTO ? (cfg->f16_exchange ? BO_REDUCE_RING : BO_REDUCE_NCCL)
                                                : cfg->reduce_algo;
   BO_CUDA(cudaSetDevice(device));
@@ -447,11 +446,6 @@ void bo_destroy(bo_ctx* c) {
   if (c->comm_done) cudaEventDestroy(c->comm_done);
   if (c->params_done) cudaEventDestroy(c->params_done);
   if (c->comm_stream && !c->shared_stream) cudaStreamDestroy(c->comm_stream);
-  if (c->push_stream) cudaStreamSynchronize(c->push_stream);
-  if (c->push_graph) cudaGraphExecDestroy(c->push_graph);
-  if (c->push_stream) cudaStreamDestroy(c->push_stream);
-  if (c->ev_upd) cudaEventDestroy(c->ev_upd);
-  if (c->ev_push) cudaEventDestroy(c->ev_push);
   delete c->sync_tab;
   for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
   if (c->comm) ncclCommDestroy(c->comm);

@@ -309,13 +309,7 @@ struct bo_ctx {
   unsigned* d_push_count = nullptr;    // [G] cumulative finished tiles
   cudaEvent_t params_done = nullptr;   // world 1: the step's update, for bo_params_wait
   int push_ctas = 0;                   // BO_PUSH_CTAS: persistent push grid (0: one CTA per tile)
-  // BO_PUSH_CE=1: the parameter all-gather on the copy engines — a CUDA graph
-  // of one peer memcpy per (owned bucket chunk, destination rank), in lanes,
-  // with a publish kernel per parameter group; built once, launched per step
-  bool push_ce = false;
-  cudaGraphExec_t push_graph = nullptr;
-  cudaStream_t push_stream = nullptr;
-  cudaEvent_t ev_upd = nullptr, ev_push = nullptr;
+
   double* peer_part[8] = {};           // every rank's all_part (IPC)
   void* wire[3] = {nullptr, nullptr, nullptr};  // ring staging (shard-sized)
   double* tile_part = nullptr;    // [n_lamb_tiles][2]

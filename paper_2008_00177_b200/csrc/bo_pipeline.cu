@@ -769,58 +769,6 @@ __global__ void __launch_bounds__(kThreads) k_shard_p2_push(const LambTile* __re
   }
 }
 
-// Copy-engine push (BO_PUSH_CE): the SMs only update the shard and this
-// rank's own replica; the copies into the peers' replicas are memcpy nodes of
-// a CUDA graph (push_graph), off the SMs.
-__global__ void __launch_bounds__(kThreads) k_shard_p2_update(const LambTile* __restrict__ tiles,
-                                                              float* __restrict__ wsh,
-                                                              const float* __restrict__ u,
-                                                              const DevState* __restrict__ st,
-                                                              LambConsts c,
-                                                              const float* __restrict__ trust,
-                                                              float* __restrict__ w) {
-  if (!st->do_update) return;
-  const LambTile t = tiles[blockIdx.x];
-  const float step_scale = __fmul_rn(c.lr, trust[t.t]);
-  const Split sp = split_tile(t.s0, t.len);
-  auto one = [&](int e) {
-    const int64_t s = t.s0 + e;
-    const float nw = __fsub_rn(wsh[s], __fmul_rn(step_scale, u[s]));
-    wsh[s] = nw;
-    w[t.w0 + e] = nw;
-  };
-  if (static_cast<int>(threadIdx.x) < sp.head) one(threadIdx.x);
-  if (threadIdx.x >= 32 && static_cast<int>(threadIdx.x) - 32 < sp.tail) {
-    one(sp.head + 4 * sp.nv + static_cast<int>(threadIdx.x) - 32);
-  }
-  for (int q = threadIdx.x; q < sp.nv; q += kThreads) {
-    const int e = sp.head + 4 * q;
-    const int64_t s = t.s0 + e;
-    const float4 w4 = *reinterpret_cast<const float4*>(wsh + s);
-    const float4 u4 = __ldcs(reinterpret_cast<const float4*>(u + s));
-    const float4 n4 = make_float4(__fsub_rn(w4.x, __fmul_rn(step_scale, u4.x)),
-                                  __fsub_rn(w4.y, __fmul_rn(step_scale, u4.y)),
-                                  __fsub_rn(w4.z, __fmul_rn(step_scale, u4.z)),
-                                  __fsub_rn(w4.w, __fmul_rn(step_scale, u4.w)));
-    *reinterpret_cast<float4*>(wsh + s) = n4;
-    float* wo = w + t.w0 + e;  // the flat replica's phase may differ from the shard's
-    wo[0] = n4.x;
-    wo[1] = n4.y;
-    wo[2] = n4.z;
-    wo[3] = n4.w;
-  }
-}
-
-// Graph node after a parameter group's copies: publish it to every rank.
-__global__ void k_publish_group(PeerFlags pf, int g, const DevState* __restrict__ st) {
-  __threadfence_system();
-  const unsigned epoch = st->epoch;
-  for (int j = 0; j < pf.n; ++j) {
-    unsigned* f = pf.f[j] + kCtrlReady + 8 * g + pf.rank;
-    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f), "r"(epoch) : "memory");
-  }
-}
-
 // bo_params_wait: one thread on the caller's stream waits until every rank
 // published parameter group g of step `epoch` (bounded by the watchdog).
 __global__ void k_params_wait(const unsigned* __restrict__ slots, int N, unsigned epoch,
@@ -932,91 +880,6 @@ static void lamb_shard(bo_ctx* c, const G* g) {
 // the partials and flags (2T+1 doubles per rank, summed in rank order so all
 // ranks agree) -> trust ratios, found_inf, scaler -> phase 2 pushing the new
 // parameters into every rank's replica -> barrier.
-// The copy-engine push graph: for every parameter group in model order, the
-// owned chunk of every bucket the group touches (contiguous in the shard and
-// in the flat replica) copied into every other rank's replica, the copies
-// spread over kCeLanes independent chains (the driver runs independent
-// branches on several copy engines), then a publish node that depends on the
-// latest copy of every lane. Built once per context (all pointers fixed).
-constexpr int kCeLanes = 8;
-static void build_push_graph(bo_ctx* c) {
-  const Layout& L = c->L;
-  cudaGraph_t graph;
-  BO_CUDA(cudaGraphCreate(&graph, 0));
-  std::vector<float*> peers(static_cast<size_t>(c->world));
-  BO_CUDA(cudaMemcpy(peers.data(), c->d_peer_w, peers.size() * sizeof(float*), cudaMemcpyDeviceToHost));
-  std::vector<cudaGraphNode_t> lane(kCeLanes, nullptr);
-  std::vector<uint8_t> copied(static_cast<size_t>(L.B), 0);
-  int next_lane = 0;
-  int t = 0;
-  for (int g = 0; g < c->n_push_groups; ++g) {
-    for (; t < L.T && c->push_group_of_tensor[static_cast<size_t>(t)] == g; ++t) {
-      const int b = L.bucket_of[static_cast<size_t>(t)];
-      if (copied[static_cast<size_t>(b)]) continue;
-      copied[static_cast<size_t>(b)] = 1;
-      const int64_t cb = L.chunk[static_cast<size_t>(b)];
-      const int64_t lo = L.own * cb, hi = std::min<int64_t>((L.own + 1) * cb, L.elems[static_cast<size_t>(b)]);
-      if (hi <= lo) continue;
-      for (int k = 1; k < c->world; ++k) {
-        const int j = (c->rank + k) % c->world;
-        cudaGraphNode_t node;
-        cudaGraphNode_t* dep = lane[static_cast<size_t>(next_lane)] ? &lane[static_cast<size_t>(next_lane)] : nullptr;
-        BO_CUDA(cudaGraphAddMemcpyNode1D(&node, graph, dep, dep ? 1 : 0,
-                                         peers[static_cast<size_t>(j)] + L.base[static_cast<size_t>(b)] + lo,
-                                         c->wsh + L.shoff[static_cast<size_t>(b)],
-                                         static_cast<size_t>(hi - lo) * sizeof(float),
-                                         cudaMemcpyDeviceToDevice));
-        lane[static_cast<size_t>(next_lane)] = node;
-        next_lane = (next_lane + 1) % kCeLanes;
-      }
-    }
-    std::vector<cudaGraphNode_t> deps;
-    for (cudaGraphNode_t n : lane) {
-      if (n) deps.push_back(n);
-    }
-    PeerFlags pf = c->peer_ctrl;
-    int gg = g;
-    const DevState* st = c->state;
-    void* args[] = {&pf, &gg, &st};
-    cudaKernelNodeParams kp{};
-    kp.func = reinterpret_cast<void*>(k_publish_group);
-    kp.gridDim = dim3(1);
-    kp.blockDim = dim3(1);
-    kp.sharedMemBytes = 0;
-    kp.kernelParams = args;
-    kp.extra = nullptr;
-    cudaGraphNode_t pub;
-    BO_CUDA(cudaGraphAddKernelNode(&pub, graph, deps.data(), deps.size(), &kp));
-  }
-  BO_CUDA(cudaGraphInstantiate(&c->push_graph, graph, 0));
-  BO_CUDA(cudaGraphDestroy(graph));
-}
-
-static void push_copy_engines(bo_ctx* c) {
-  if (!c->push_graph) {
-    build_push_graph(c);
-    if (!c->lockstep) {
-      BO_CUDA(cudaStreamCreateWithFlags(&c->push_stream, cudaStreamNonBlocking));
-      BO_CUDA(cudaEventCreateWithFlags(&c->ev_upd, cudaEventDisableTiming));
-      BO_CUDA(cudaEventCreateWithFlags(&c->ev_push, cudaEventDisableTiming));
-    }
-  }
-  if (c->n_lamb_tiles > 0) {
-    k_shard_p2_update<<<c->n_lamb_tiles, kThreads, 0, c->stream>>>(c->d_lamb_tiles, c->wsh, c->u, c->state,
-                                                                  c->lamb, c->trust, c->w);
-    check_launch(c, "k_shard_p2_update");
-  }
-  if (c->lockstep) {  // one shared stream: the graph in stream order
-    BO_CUDA(cudaGraphLaunch(c->push_graph, c->stream));
-    return;
-  }
-  BO_CUDA(cudaEventRecord(c->ev_upd, c->stream));
-  BO_CUDA(cudaStreamWaitEvent(c->push_stream, c->ev_upd, 0));
-  BO_CUDA(cudaGraphLaunch(c->push_graph, c->push_stream));
-  BO_CUDA(cudaEventRecord(c->ev_push, c->push_stream));
-  BO_CUDA(cudaStreamWaitEvent(c->stream, c->ev_push, 0));
-}
-
 template <typename W, bool kHop>
 static void lamb_sharded(bo_ctx* c, const PtrTable& tab, const W* in) {
   const int T = c->L.T;
@@ -1068,10 +931,7 @@ static void lamb_sharded(bo_ctx* c, const PtrTable& tab, const W* in) {
                                      c->trust, 1, pf, epoch, c->watchdog_ns);
   check_launch(c, "k_trust");
   }
-  if (c->push_ce) {
-    StageTimer timer(c, BO_STAGE_LAMB_UPDATE);
-    push_copy_engines(c);
-  } else {
+  {
   StageTimer timer(c, BO_STAGE_LAMB_UPDATE);
   const PushGroups G{c->d_push_group_of_tensor, c->d_push_group_tiles, c->d_push_count, c->peer_ctrl, epoch};
   if (c->push_ctas > 0 && c->push_ctas < c->n_push_tiles) {
