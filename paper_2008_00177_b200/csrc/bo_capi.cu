@@ -178,6 +178,8 @@ static uint64_t settings_hash(const bo_ctx* c) {
   mix(c->nb_barrier ? 1 : 0);
   mix(c->comm_groups.size());
   for (const auto& g : c->comm_groups) mix(static_cast<uint64_t>(g.b1));
+  mix(c->lamb_groups.size());  // grouped LAMB: one partials barrier per group
+  for (const auto& g : c->lamb_groups) mix(static_cast<uint64_t>(g.t1));
   return h;
 }
 
@@ -400,6 +402,7 @@ bo_status bo_create(const bo_trainer_config* cfg, int32_t n_tensors, const int64
     BO_CUDA(cudaEventCreateWithFlags(&c->comm_done, cudaEventDisableTiming));
     c->wsh = static_cast<float*>(dev_alloc(c, static_cast<size_t>(L.shard_total) * 4));
     c->u = static_cast<float*>(dev_alloc(c, static_cast<size_t>(L.shard_total) * 4));
+    if (c->lamb_groups.size() > 1) c->wsh_alt = static_cast<float*>(dev_alloc(c, static_cast<size_t>(L.shard_total) * 4));
     c->d_barrier = static_cast<int*>(dev_alloc(c, 4));
     c->ctrl = static_cast<unsigned*>(dev_alloc(c, kCtrlWords * sizeof(unsigned)));
   }
@@ -446,6 +449,11 @@ void bo_destroy(bo_ctx* c) {
   if (c->comm_done) cudaEventDestroy(c->comm_done);
   if (c->params_done) cudaEventDestroy(c->params_done);
   if (c->comm_stream && !c->shared_stream) cudaStreamDestroy(c->comm_stream);
+  if (c->push_stream) {
+    cudaStreamSynchronize(c->push_stream);
+    cudaStreamDestroy(c->push_stream);
+  }
+  for (cudaEvent_t e : c->group_events) cudaEventDestroy(e);
   delete c->sync_tab;
   for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
   if (c->comm) ncclCommDestroy(c->comm);

@@ -309,6 +309,17 @@ struct bo_ctx {
   unsigned* d_push_count = nullptr;    // [G] cumulative finished tiles
   cudaEvent_t params_done = nullptr;   // world 1: the step's update, for bo_params_wait
   int push_ctas = 0;                   // BO_PUSH_CTAS: persistent push grid (0: one CTA per tile)
+  // Grouped LAMB (BO_LAMB_GROUP_ELEMS, world > 1): consecutive tensors (model
+  // order), the push of each group speculative on push_stream, the master
+  // shard double-buffered (wsh / wsh_alt by DevState::parity)
+  struct LambGroup {
+    int t0, t1;        // tensors [t0, t1)
+    int tile0, tile1;  // their LAMB tiles (contiguous: tiles are in model order)
+  };
+  std::vector<LambGroup> lamb_groups;
+  float* wsh_alt = nullptr;
+  cudaStream_t push_stream = nullptr;
+  std::vector<cudaEvent_t> group_events;
 
   double* peer_part[8] = {};           // every rank's all_part (IPC)
   void* wire[3] = {nullptr, nullptr, nullptr};  // ring staging (shard-sized)

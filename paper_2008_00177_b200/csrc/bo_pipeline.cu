@@ -231,8 +231,8 @@ __global__ void __launch_bounds__(kThreads) k_norm_reduce(const int* __restrict_
                                                           const double* __restrict__ tile_part,
                                                           const DevState* __restrict__ st, int T,
                                                           double* __restrict__ rank_part,
-                                                          const PartDst dst) {
-  const int t = blockIdx.x;
+                                                          const PartDst dst, int t_first = 0) {
+  const int t = t_first + static_cast<int>(blockIdx.x);  // grouped LAMB: tensors [t_first, ...)
   const int b0 = tile_begin[t], b1 = tile_begin[t + 1];
   double a = 0.0, b = 0.0;
   for (int i = b0 + threadIdx.x; i < b1; i += kThreads) {
@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(kThreads) k_norm_reduce(const int* __restrict_
     double* out = dst.n > 0 ? dst.p[threadIdx.x] : rank_part;
     out[2 * t] = red[0][0];
     out[2 * t + 1] = red[1][0];
-    if (t == 0) out[2 * T] = st->local_flag ? 1.0 : 0.0;
+    if (blockIdx.x == 0) out[2 * T] = st->local_flag ? 1.0 : 0.0;  // (cumulative over groups)
   }
 }
 
@@ -300,12 +300,35 @@ __global__ void k_step_end_barrier(PeerFlags pf, unsigned epoch, DevState* st, u
 // loss-scaler state machine.
 // world > 1: first the partials barrier (every rank's k_norm_reduce stored
 // its partials into this rank's all_part), then the sums.
+// Grouped LAMB (group_mode, tensors [t0, t1)): the barrier and that group's
+// trust ratios only, computed whatever the flags (the push of the group is
+// speculative); the step's decision and state update is k_step_final's.
 __global__ void __launch_bounds__(1024) k_trust(const double* __restrict__ all_part, int N, int T,
                                                 DevState* __restrict__ st, LambConsts c,
                                                 ScalerConsts sc, float* __restrict__ trust,
                                                 int flip_parity, PeerFlags pf, unsigned epoch,
-                                                uint64_t timeout_ns) {
+                                                uint64_t timeout_ns, int group_mode = 0, int t0 = 0,
+                                                int t1 = 0) {
   __shared__ int found, abandoned;
+  if (group_mode) {
+    if (threadIdx.x == 0) abandoned = pf.n > 0 && !all_rank_barrier(pf, kCtrlPartials, epoch, st, timeout_ns);
+    __syncthreads();
+    if (abandoned) return;
+    for (int t = t0 + static_cast<int>(threadIdx.x); t < t1; t += blockDim.x) {
+      double W = 0.0, U = 0.0;
+      for (int r = 0; r < N; ++r) {
+        W = __dadd_rn(W, __ldcv(all_part + static_cast<size_t>(r) * (2 * T + 1) + 2 * t));
+        U = __dadd_rn(U, __ldcv(all_part + static_cast<size_t>(r) * (2 * T + 1) + 2 * t + 1));
+      }
+      float r = 1.0f;
+      if (W > 0.0 && U > 0.0) {
+        r = __double2float_rn(__ddiv_rn(__dsqrt_rn(W), __dsqrt_rn(U)));
+        r = fminf(fmaxf(r, 0.0f), c.clip);
+      }
+      trust[t] = r;
+    }
+    return;
+  }
   if (threadIdx.x == 0) {
     st->epoch = epoch;
     abandoned = pf.n > 0 && !all_rank_barrier(pf, kCtrlPartials, epoch, st, timeout_ns);
@@ -421,6 +444,7 @@ struct P1Args {
   float invn;
   const float* wsh;
   float *m0, *v0, *m1, *v1, *u;
+  const float* wsh_alt;  // grouped LAMB: the master shard is double-buffered (parity)
   DevState* st;
   LambConsts c;
   const double* bc_table;
@@ -461,7 +485,7 @@ __global__ void __launch_bounds__(kWarpTileCTA, kMinBlocks) k_p1w(const LambTile
   const float* __restrict__ v = par ? A.v1 : A.v0;
   float* __restrict__ mn = par ? A.m0 : A.m1;
   float* __restrict__ vn = par ? A.v0 : A.v1;
-  const float* __restrict__ wsh = A.wsh + t.s0;
+  const float* __restrict__ wsh = (A.wsh_alt && par ? A.wsh_alt : A.wsh) + t.s0;
   float* __restrict__ u = A.u + t.s0;
   m += t.s0;
   v += t.s0;
@@ -674,19 +698,27 @@ __device__ __forceinline__ void push_tile_done(const PushGroups& G, int tensor) 
 // buffers, the copies of tile i flying while tile i + grid is computed; a
 // small grid leaves SMs to a concurrent forward (bo_params_wait) at the cost
 // of push bandwidth. Skipped steps only count.
+// Grouped LAMB (wsh_alt != null): speculative — runs before the step's
+// decision, reads the current master shard (parity) and writes the other one
+// (k_step_final flips, k_rollback undoes the replicas on a skipped step).
 template <int NB>
 __global__ void __launch_bounds__(kThreads) k_shard_p2_push(const LambTile* __restrict__ tiles,
-                                                            int n_tiles, float* __restrict__ wsh,
+                                                            int n_tiles, float* wsh_main,
                                                             const float* __restrict__ u,
                                                             const DevState* __restrict__ st,
                                                             LambConsts c,
                                                             const float* __restrict__ trust,
                                                             float* const* __restrict__ peer_w,
-                                                            int N, const PushGroups G) {
+                                                            int N, const PushGroups G,
+                                                            float* wsh_alt = nullptr) {
   __shared__ __align__(128) float bufs[NB][kTileElems + 4];
   __shared__ float* dst[8];
   if (threadIdx.x < N) dst[threadIdx.x] = peer_w[threadIdx.x];
-  const bool update = st->do_update != 0;
+  const bool speculative = wsh_alt != nullptr;
+  const bool update = speculative || st->do_update != 0;
+  const int par = speculative ? st->parity : 0;
+  const float* __restrict__ wsrc = par ? wsh_alt : wsh_main;
+  float* __restrict__ wdst = speculative ? (par ? wsh_main : wsh_alt) : wsh_main;
   int pending = -1;  // tensor of the previous tile (its stores in flight)
   int it = 0;
   for (int i = blockIdx.x; i < n_tiles; i += gridDim.x, ++it) {
@@ -702,8 +734,8 @@ __global__ void __launch_bounds__(kThreads) k_shard_p2_push(const LambTile* __re
       const Split sp = split_tile(t.s0, t.len);
       auto one = [&](int e) {
         const int64_t s = t.s0 + e;
-        const float nw = __fsub_rn(wsh[s], __fmul_rn(step_scale, u[s]));
-        wsh[s] = nw;
+        const float nw = __fsub_rn(wsrc[s], __fmul_rn(step_scale, u[s]));
+        wdst[s] = nw;
         buf[off + e] = nw;
       };
       if (static_cast<int>(threadIdx.x) < sp.head) one(threadIdx.x);
@@ -713,13 +745,13 @@ __global__ void __launch_bounds__(kThreads) k_shard_p2_push(const LambTile* __re
       for (int q = threadIdx.x; q < sp.nv; q += kThreads) {
         const int e = sp.head + 4 * q;
         const int64_t s = t.s0 + e;
-        const float4 w4 = *reinterpret_cast<const float4*>(wsh + s);
+        const float4 w4 = *reinterpret_cast<const float4*>(wsrc + s);
         const float4 u4 = __ldcs(reinterpret_cast<const float4*>(u + s));
         const float4 n4 = make_float4(__fsub_rn(w4.x, __fmul_rn(step_scale, u4.x)),
                                       __fsub_rn(w4.y, __fmul_rn(step_scale, u4.y)),
                                       __fsub_rn(w4.z, __fmul_rn(step_scale, u4.z)),
                                       __fsub_rn(w4.w, __fmul_rn(step_scale, u4.w)));
-        *reinterpret_cast<float4*>(wsh + s) = n4;
+        *reinterpret_cast<float4*>(wdst + s) = n4;
         buf[off + e] = n4.x;
         buf[off + e + 1] = n4.y;
         buf[off + e + 2] = n4.z;
@@ -789,10 +821,80 @@ __global__ void k_params_wait(const unsigned* __restrict__ slots, int N, unsigne
 }
 
 // Owned chunk positions of the flat replica -> the master shard (load time).
+// Grouped LAMB, after every group's speculative push: the step's decision
+// from the last group's exchange (each rank's cumulative flag), then the same
+// state transitions as k_trust — the parity flip now also makes the pushed
+// master shard current.
+__global__ void k_step_final(const double* __restrict__ all_part, int N, int T, DevState* st,
+                             ScalerConsts sc, unsigned epoch) {
+  st->epoch = epoch;
+  if (st->peer_timeout) {  // abandoned: no update, counters and scaler untouched
+    st->do_update = 0;
+    st->local_flag = 0;
+    return;
+  }
+  int found = 0;
+  for (int r = 0; r < N; ++r) found |= __ldcv(all_part + static_cast<size_t>(r) * (2 * T + 1) + 2 * T) != 0.0;
+  st->found_inf = found;
+  st->do_update = !found;
+  st->steps += 1;
+  st->local_flag = 0;
+  if (found) {
+    st->skipped += 1;
+  } else {
+    st->lamb_step += 1;
+    st->parity ^= 1;  // moments written by phase 1, master shard written by the push
+  }
+  if (sc.dynamic) {
+    if (found) {
+      st->scale = fmaxf(__fmul_rn(st->scale, sc.backoff), sc.min_scale);
+      st->good = 0;
+    } else if (++st->good == sc.interval) {
+      st->scale = fminf(__fmul_rn(st->scale, sc.growth), sc.max_scale);
+      st->good = 0;
+    }
+  }
+}
+
+// A skipped (or abandoned) grouped step: the speculative pushes are undone by
+// pushing the unchanged current master shard into every replica again. Exits
+// at once on a normal step.
+__global__ void __launch_bounds__(kThreads) k_rollback(const LambTile* __restrict__ tiles, int n_tiles,
+                                                       const float* __restrict__ wsh0,
+                                                       const float* __restrict__ wsh1,
+                                                       float* const* __restrict__ peer_w, int N,
+                                                       const DevState* __restrict__ st) {
+  if (st->do_update) return;
+  const float* __restrict__ wsh = st->parity ? wsh1 : wsh0;
+  for (int i = blockIdx.x; i < n_tiles; i += gridDim.x) {
+    const LambTile t = tiles[i];
+    for (int e = threadIdx.x; e < t.len; e += blockDim.x) {
+      const float v = wsh[t.s0 + e];
+      for (int j = 0; j < N; ++j) peer_w[j][t.w0 + e] = v;
+    }
+  }
+}
+
+// Grouped LAMB: every parameter group is published once the step's decision
+// (and any rollback) is final — the pushes themselves are speculative.
+__global__ void k_publish_all(PeerFlags pf, int n_groups, unsigned epoch) {
+  __threadfence_system();
+  for (int g = threadIdx.x; g < n_groups; g += blockDim.x) {
+    for (int j = 0; j < pf.n; ++j) {
+      unsigned* f = pf.f[j] + kCtrlReady + 8 * g + pf.rank;
+      asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f), "r"(epoch) : "memory");
+    }
+  }
+}
+
 __global__ void k_gather_shard(const LambTile* __restrict__ tiles, const float* __restrict__ w,
-                               float* __restrict__ wsh) {
+                               float* __restrict__ wsh, float* __restrict__ wsh_alt) {
   const LambTile t = tiles[blockIdx.x];
-  for (int e = threadIdx.x; e < t.len; e += blockDim.x) wsh[t.s0 + e] = w[t.w0 + e];
+  for (int e = threadIdx.x; e < t.len; e += blockDim.x) {
+    const float v = w[t.w0 + e];
+    wsh[t.s0 + e] = v;
+    if (wsh_alt) wsh_alt[t.s0 + e] = v;
+  }
 }
 
 }  // namespace
@@ -881,13 +983,127 @@ static void lamb_shard(bo_ctx* c, const G* g) {
 // ranks agree) -> trust ratios, found_inf, scaler -> phase 2 pushing the new
 // parameters into every rank's replica -> barrier.
 template <typename W, bool kHop>
+static void launch_p1w(bo_ctx* c, const PtrTable& tab, const W* in, const P1Args& A, int tile0, int n) {
+  if (n <= 0) return;
+  P1Args a = A;
+  a.tile_part = A.tile_part + 2 * static_cast<size_t>(tile0);  // partials at global tile indices
+  const LambTile* tiles = c->d_lamb_tiles + tile0;
+  const int grid = (n * 32 + kWarpTileCTA - 1) / kWarpTileCTA;
+  auto go = [&](auto kern) { kern<<<grid, kWarpTileCTA, 0, c->stream>>>(tiles, n, tab, in, a); };
+  if constexpr (!kHop) {
+    go(k_p1w<W, true, false, 1, 4>);
+  } else if (c->ms.K == 0) {
+    go(k_p1w<W, true, true, 1, 4>);
+  } else if (c->ms.K == 2) {
+    go(k_p1w<W, true, true, 1, 4, 2>);
+  } else if (c->ms.K == 4) {
+    go(k_p1w<W, true, true, 1, 4, 4>);
+  } else {
+    fail(BO_ERR_INVALID_CONFIG, "fused last hop with resident micros: K must be 2 or 4");
+  }
+  check_launch(c, "k_p1w");
+}
+
+// Grouped LAMB (BO_LAMB_GROUP_ELEMS): the shard's LAMB in groups of
+// consecutive tensors (model order), each group's parameter push speculative
+// and on its own stream, so the push of group g (NVLink) overlaps phase 1 of
+// group g + 1 (HBM):
+//   compute stream: p1w(g) -> norm partials(g) -> k_trust(g) [all-rank barrier,
+//                   trust ratios of g] -> event(g)            for g = 0..G-1
+//   push stream:    wait event(g) -> push(g) (reads the current master shard,
+//                   writes the other one + every replica)      for g = 0..G-1
+//   then:           k_step_final (found_inf from every rank's cumulative flag,
+//                   counters, scaler, parity flip), k_rollback (a skipped step
+//                   re-pushes the unchanged master shard), publish, barrier.
+// Same arithmetic per element as the serial path; only the order of the
+// independent tensor groups changes.
+template <typename W, bool kHop>
+static void lamb_grouped(bo_ctx* c, const PtrTable& tab, const W* in) {
+  const int T = c->L.T;
+  const float invn = 1.0f / static_cast<float>(c->world);  // trainer.cpp:212
+  const P1Args A{c->d_tensors, c->acc, c->cfg.accumulation, invn, c->wsh, c->m, c->v,
+                 c->m_alt, c->v_alt, c->u, c->wsh_alt, c->state, c->lamb, c->bc_table, c->tile_part, c->ms};
+  const size_t slot = static_cast<size_t>(2 * T + 1);
+  const int G = static_cast<int>(c->lamb_groups.size());
+  cudaStream_t ps = c->lockstep ? c->stream : c->push_stream;
+  if (!c->lockstep && !c->push_stream) {
+    BO_CUDA(cudaStreamCreateWithPriority(&c->push_stream, cudaStreamNonBlocking, -1));
+    ps = c->push_stream;
+    c->group_events.assign(static_cast<size_t>(G) + 1, nullptr);
+    for (auto& e : c->group_events) BO_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  PushGroups none{c->d_push_group_of_tensor, c->d_push_group_tiles, c->d_push_count, PeerFlags{{}, 0, c->rank}, 0u};
+  unsigned epoch = 0;
+  size_t half = 0;
+  {
+  StageTimer timer(c, BO_STAGE_LAMB_NORMS);
+  for (int g = 0; g < G; ++g) {
+    const bo_ctx::LambGroup& lg = c->lamb_groups[static_cast<size_t>(g)];
+    launch_p1w<W, kHop>(c, tab, in, A, lg.tile0, lg.tile1 - lg.tile0);
+    c->bar_epoch += 1;
+    epoch = static_cast<unsigned>(c->bar_epoch);
+    half = (c->bar_epoch & 1) * static_cast<size_t>(c->world) * slot;
+    PartDst dst{{}, c->world};
+    for (int j = 0; j < c->world; ++j) dst.p[j] = c->peer_part[j] + half + static_cast<size_t>(c->rank) * slot;
+    if (lg.t1 > lg.t0) {
+      k_norm_reduce<<<lg.t1 - lg.t0, kThreads, 0, c->stream>>>(c->d_tensor_tile_begin, c->tile_part, c->state, T,
+                                                               c->rank_part, dst, lg.t0);
+      check_launch(c, "k_norm_reduce");
+    }
+    PeerFlags pf = c->peer_ctrl;
+    if (c->lockstep) {
+      lockstep_sync(c, "partials");
+      pf.n = 0;
+    }
+    k_trust<<<1, 1024, 0, c->stream>>>(c->all_part + half, c->world, T, c->state, c->lamb, c->scaler,
+                                       c->trust, 0, pf, epoch, c->watchdog_ns, 1, lg.t0, lg.t1);
+    check_launch(c, "k_trust");
+    if (!c->lockstep) {
+      BO_CUDA(cudaEventRecord(c->group_events[static_cast<size_t>(g)], c->stream));
+      BO_CUDA(cudaStreamWaitEvent(ps, c->group_events[static_cast<size_t>(g)], 0));
+    }
+    if (lg.tile1 > lg.tile0) {
+      k_shard_p2_push<1><<<lg.tile1 - lg.tile0, kThreads, 0, ps>>>(
+          c->d_lamb_tiles + lg.tile0, lg.tile1 - lg.tile0, c->wsh, c->u, c->state, c->lamb, c->trust,
+          c->d_peer_w, c->world, none, c->wsh_alt);
+      check_launch(c, "k_shard_p2_push");
+    }
+  }
+  if (!c->lockstep) {
+    BO_CUDA(cudaEventRecord(c->group_events[static_cast<size_t>(G)], ps));
+    BO_CUDA(cudaStreamWaitEvent(c->stream, c->group_events[static_cast<size_t>(G)], 0));
+  }
+  }
+  StageTimer timer(c, BO_STAGE_ALLGATHER);
+  k_step_final<<<1, 1, 0, c->stream>>>(c->all_part + half, c->world, T, c->state, c->scaler, epoch);
+  check_launch(c, "k_step_final");
+  if (c->n_lamb_tiles > 0) {
+    k_rollback<<<std::min(c->n_lamb_tiles, 2 * c->num_sms), kThreads, 0, c->stream>>>(
+        c->d_lamb_tiles, c->n_lamb_tiles, c->wsh, c->wsh_alt, c->d_peer_w, c->world, c->state);
+    check_launch(c, "k_rollback");
+  }
+  k_publish_all<<<1, 128, 0, c->stream>>>(c->peer_ctrl, c->n_push_groups, epoch);
+  check_launch(c, "k_publish_all");
+  if (c->lockstep) {
+    lockstep_sync(c, "end of step");
+    return;
+  }
+  k_step_end_barrier<<<1, 1, 0, c->stream>>>(c->peer_ctrl, epoch, c->state, c->watchdog_ns);
+  check_launch(c, "k_step_end_barrier");
+}
+
+template <typename W, bool kHop>
 static void lamb_sharded(bo_ctx* c, const PtrTable& tab, const W* in) {
+  if (c->lamb_groups.size() > 1) {
+    lamb_grouped<W, kHop>(c, tab, in);
+    return;
+  }
   const int T = c->L.T;
   const float invn = 1.0f / static_cast<float>(c->world);  // trainer.cpp:212
   {
   StageTimer timer(c, BO_STAGE_LAMB_NORMS);
   const P1Args A{c->d_tensors, c->acc, c->cfg.accumulation, invn, c->wsh, c->m, c->v,
-                 c->m_alt, c->v_alt, c->u, c->state, c->lamb, c->bc_table, c->tile_part, c->ms};
+                 c->m_alt, c->v_alt, c->u, nullptr, c->state, c->lamb, c->bc_table, c->tile_part, c->ms};
   const int grid = (c->n_lamb_tiles * 32 + kWarpTileCTA - 1) / kWarpTileCTA;
   auto go = [&](auto kern) {
     kern<<<grid, kWarpTileCTA, 0, c->stream>>>(c->d_lamb_tiles, c->n_lamb_tiles, tab, in, A);
@@ -1035,7 +1251,7 @@ void need_nccl(bo_ctx* c, const char* what) {
 void gather_shard(bo_ctx* c) {
   if (c->world == 1) return;
   if (c->n_lamb_tiles == 0) return;
-  k_gather_shard<<<c->n_lamb_tiles, kThreads, 0, c->stream>>>(c->d_lamb_tiles, c->w, c->wsh);
+  k_gather_shard<<<c->n_lamb_tiles, kThreads, 0, c->stream>>>(c->d_lamb_tiles, c->w, c->wsh, c->wsh_alt);
   check_launch(c, "k_gather_shard");
 }
 

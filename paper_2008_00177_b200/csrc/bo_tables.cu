@@ -189,6 +189,26 @@ void upload_tables(bo_ctx* c) {
     c->d_push_group_of_tensor = upload(c, c->push_group_of_tensor);
     c->d_push_group_tiles = upload(c, gtiles);
     c->d_push_count = static_cast<unsigned*>(dev_alloc(c, static_cast<size_t>(c->n_push_groups) * sizeof(unsigned)));
+
+    // Grouped LAMB: consecutive tensors in model order, >= BO_LAMB_GROUP_ELEMS
+    // elements each (unset / 0: one group, the serial path)
+    int64_t lg_elems = 0;
+    if (const char* e = std::getenv("BO_LAMB_GROUP_ELEMS")) lg_elems = std::max<int64_t>(0, std::atoll(e));
+    c->lamb_groups.clear();
+    if (lg_elems > 0) {
+      int t0 = 0;
+      int64_t n = 0;
+      for (int t = 0; t < L.T; ++t) {
+        n += L.numel[static_cast<size_t>(t)];
+        if (n >= lg_elems || t == L.T - 1) {
+          c->lamb_groups.push_back(bo_ctx::LambGroup{t0, t + 1, tile_begin[static_cast<size_t>(t0)],
+                                                     tile_begin[static_cast<size_t>(t) + 1]});
+          t0 = t + 1;
+          n = 0;
+        }
+      }
+      if (c->lamb_groups.size() <= 1) c->lamb_groups.clear();
+    }
   }
   c->d_tensors = upload(c, td);
   c->d_acc_tiles = upload(c, acc_tiles);
