@@ -82,6 +82,10 @@ def main():
         elif case.endswith("_unfused"):
             os.environ["BO_UNFUSED"] = "1"
             case = case[: -len("_unfused")]
+        elif case.endswith("_grouped"):
+            # grouped speculative LAMB (BO_LAMB_GROUP_ELEMS)
+            os.environ["BO_LAMB_GROUP_ELEMS"] = "30000"
+            case = case[: -len("_grouped")]
         elif case.endswith("_fused"):
             os.environ["BO_FUSE_LAST"] = "1"
             case = case[: -len("_fused")]

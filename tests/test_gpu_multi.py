@@ -61,7 +61,8 @@ def run_case(case, nproc, model="tiny", steps=4):
                                   "ring16_overlap", "ring32_unfused_overlap", "nccl32_overlap",
                                   "ring16_resident", "ring32_unfused_resident", "nccl32_resident",
                                   "ring16_pull_resident", "ring32_unfused_pull", "ring32_resident",
-                                  "ring16_pull", "ring16_ncclbar_resident"])
+                                  "ring16_pull", "ring16_ncclbar_resident", "ring16_grouped",
+                                  "ring16_grouped_resident", "ring32_grouped", "nccl32_grouped"])
 def test_two_gpus(case):
     _placement(case, 2)
     res = run_case(case, 2)
@@ -72,7 +73,7 @@ def test_two_gpus(case):
         # sync micro is overlapped; push form (default): per-micro or K = 2 / 4
         # resident micros (ring16: K = 2, ring32: K = 3); pull form: world 2,
         # per-micro only
-        resident = case.endswith("_resident")
+        resident = "_resident" in case
         k_ok = (not resident) or case.startswith("ring16")
         fused = "_unfused" not in case and "_overlap" not in case and \
             (k_ok if "_pull" not in case else not resident)
@@ -81,7 +82,7 @@ def test_two_gpus(case):
         assert "nccl_reduce_scatter" in res["path"]
     assert ("overlap" in res["path"]) == case.endswith("_overlap")
     # bo_train_step reads the resident micros (ring hops, NCCL-wire finalize)
-    assert ("resident_micros" in res["path"]) == case.endswith("_resident")
+    assert ("resident_micros" in res["path"]) == ("_resident" in case)
     # hops push into the right neighbour's buffer unless BO_RING_PUSH=0
     assert ("ring_push" in res["path"]) == (case.startswith("ring") and "_pull" not in case)
 

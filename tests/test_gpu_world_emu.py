@@ -58,6 +58,10 @@ CASES = {
     "ring32_resident": (False, 3, 4096, dict(init_scale=1024.0), 0, True, None),
     "ring16_k4_resident": (True, 4, 1 << 20, dict(init_scale=4096.0), 0, True, None),
     "ring16_overlap": (True, 2, 8192, dict(init_scale=2.0 ** 13, growth_interval=3), 20, False, [1, 5, 2, 17]),
+    # grouped speculative LAMB (push of group g overlapping phase 1 of g+1),
+    # skipped steps included (the rollback path)
+    "ring16_grouped": (True, 2, 8192, dict(init_scale=2.0 ** 13, growth_interval=3), 20, False, None),
+    "ring16_grouped_resident": (True, 4, 8192, dict(init_scale=2.0 ** 13, growth_interval=3), 20, True, None),
 }
 
 
@@ -72,6 +76,8 @@ def test_world_lockstep_matches_oracle(torch_cuda, oracle, world, case, monkeypa
     f16, K, bb, sc, ppm, resident, overlap = CASES[case]
     if overlap:
         monkeypatch.setenv("BO_COMM_GROUP_ELEMS", "20000")  # several communication groups
+    if "grouped" in case:
+        monkeypatch.setenv("BO_LAMB_GROUP_ELEMS", "30000")  # ~6 LAMB groups of BERT_TINY
     spec = bert_spec(BERT_TINY)
     P = spec.param_count()
     p0 = oracle.build_params(spec, 21)
