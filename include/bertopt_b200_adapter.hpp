@@ -93,34 +93,52 @@ inline void lamb_step(std::vector<Tensor>& params, const std::vector<Tensor>& gr
   }
   size_t ok = 0;  // tensors before the first shape mismatch take the step
   while (ok < params.size() && grads[ok].shape == params[ok].shape) ++ok;
-  std::vector<DeviceBuffer> bufs;
+  // w, g, m, v of all tensors packed into four device arrays: four uploads
+  // and three downloads per call, not four of each per tensor
   std::vector<int64_t> numels;
+  std::vector<size_t> off;
+  size_t total = 0;
+  for (size_t i = 0; i < ok; ++i) {
+    numels.push_back(static_cast<int64_t>(params[i].data.size()));
+    off.push_back(total);
+    total += params[i].data.size();
+  }
+  std::vector<float> host(total);
+  DeviceBuffer dev[4] = {DeviceBuffer(total * sizeof(float) + 16, device), DeviceBuffer(total * sizeof(float) + 16, device),
+                         DeviceBuffer(total * sizeof(float) + 16, device), DeviceBuffer(total * sizeof(float) + 16, device)};
+  auto pack = [&](int a, auto&& get) {
+    for (size_t i = 0; i < ok; ++i) {
+      const std::vector<float>& src = get(i);
+      std::copy(src.begin(), src.end(), host.begin() + static_cast<std::ptrdiff_t>(off[i]));
+    }
+    dev[a].upload(host.data(), total * sizeof(float));
+  };
+  pack(0, [&](size_t i) -> const std::vector<float>& { return params[i].data; });
+  pack(1, [&](size_t i) -> const std::vector<float>& { return grads[i].data; });
+  pack(2, [&](size_t i) -> const std::vector<float>& { return state.m[i].data; });
+  pack(3, [&](size_t i) -> const std::vector<float>& { return state.v[i].data; });
   std::vector<float*> w, m, v;
   std::vector<const float*> g;
   for (size_t i = 0; i < ok; ++i) {
-    const size_t bytes = params[i].data.size() * sizeof(float);
-    numels.push_back(static_cast<int64_t>(params[i].data.size()));
-    const std::vector<float>* srcs[4] = {&params[i].data, &grads[i].data, &state.m[i].data,
-                                         &state.v[i].data};
-    for (const std::vector<float>* src : srcs) {
-      bufs.emplace_back(bytes, device);
-      bufs.back().upload(src->data(), bytes);
-    }
-    w.push_back(bufs[bufs.size() - 4].as<float>());
-    g.push_back(bufs[bufs.size() - 3].as<float>());
-    m.push_back(bufs[bufs.size() - 2].as<float>());
-    v.push_back(bufs[bufs.size() - 1].as<float>());
+    w.push_back(dev[0].as<float>() + off[i]);
+    g.push_back(dev[1].as<float>() + off[i]);
+    m.push_back(dev[2].as<float>() + off[i]);
+    v.push_back(dev[3].as<float>() + off[i]);
   }
   const bo_lamb_config c = to_c(cfg);
   const bo_status s = bo_lamb_step(static_cast<int32_t>(ok), numels.data(), w.data(), g.data(),
                                    m.data(), v.data(), &state.step, &c, nullptr);
-  for (size_t i = 0; i < ok; ++i) {
-    const size_t bytes = params[i].data.size() * sizeof(float);
-    bufs[4 * i].download(params[i].data.data(), bytes);
-    bufs[4 * i + 2].download(state.m[i].data.data(), bytes);
-    bufs[4 * i + 3].download(state.v[i].data.data(), bytes);
-    quantize_inplace(params[i]);  // lamb.cpp:82
-  }
+  auto unpack = [&](int a, auto&& get) {
+    dev[a].download(host.data(), total * sizeof(float));
+    for (size_t i = 0; i < ok; ++i) {
+      std::vector<float>& dst = get(i);
+      std::copy_n(host.begin() + static_cast<std::ptrdiff_t>(off[i]), dst.size(), dst.begin());
+    }
+  };
+  unpack(0, [&](size_t i) -> std::vector<float>& { return params[i].data; });
+  unpack(2, [&](size_t i) -> std::vector<float>& { return state.m[i].data; });
+  unpack(3, [&](size_t i) -> std::vector<float>& { return state.v[i].data; });
+  for (size_t i = 0; i < ok; ++i) quantize_inplace(params[i]);  // lamb.cpp:82
   if (s != BO_OK) raise(s);
   if (ok < params.size()) {
     throw ShapeMismatch("lamb_step: gradient shape mismatch at tensor " + std::to_string(ok));

@@ -364,6 +364,7 @@ bo_status bo_create(const bo_trainer_config* cfg, int32_t n_tensors, const int64
   if (const char* e = std::getenv("BO_RING_BARRIER")) c->nb_barrier = std::strcmp(e, "nccl") != 0;
   if (const char* e = std::getenv("BO_FUSE_LAST")) c->fuse_last_hop = std::strcmp(e, "0") != 0;
   if (const char* e = std::getenv("BO_PUSH_CTAS")) c->push_ctas = std::max(0, std::atoi(e));
+  if (const char* e = std::getenv("BO_PUSH_STORES")) c->push_stores = std::strcmp(e, "0") != 0;
   c->algo = cfg->reduce_algo == BO_REDUCE_AUTO ? (cfg->f16_exchange ? BO_REDUCE_RING : BO_REDUCE_NCCL)
                                                : cfg->reduce_algo;
   BO_CUDA(cudaSetDevice(device));
@@ -458,6 +459,7 @@ void bo_destroy(bo_ctx* c) {
   for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
   if (c->comm) ncclCommDestroy(c->comm);
   for (void* p : c->allocations) cudaFree(p);
+  if (c->op_ws) cudaFree(c->op_ws);
   if (c->bc_table) cudaFree(c->bc_table);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;

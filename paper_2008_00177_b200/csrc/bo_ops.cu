@@ -285,6 +285,12 @@ void check(const char* what) {
   if (e != cudaSuccess) fail(BO_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+// A view of part of a workspace.
+struct View {
+  void* p;
+  template <typename T> T* as() { return static_cast<T*>(p); }
+};
+
 struct DevBuf {
   void* p = nullptr;
   explicit DevBuf(size_t bytes) { BO_CUDA(cudaMalloc(&p, std::max<size_t>(bytes, 16))); }
@@ -305,7 +311,19 @@ void ring_allreduce_impl(bo_ctx* c, float* data, size_t n, bool f16) {
   need_nccl(c, "bo_ring_allreduce_*");
   cudaStream_t s = c->stream;
   const size_t ch = (n + static_cast<size_t>(N) - 1) / static_cast<size_t>(N);  // collective.cpp:27-29
-  DevBuf buf(ch * static_cast<size_t>(N) * 4), wire(ch * sizeof(W)), in(ch * sizeof(W));
+  // one grow-only workspace per context (the padded buffer, the outgoing
+  // and the incoming wire chunk) instead of three allocations per call
+  const size_t need = ch * static_cast<size_t>(N) * 4 + 2 * align_up(static_cast<int64_t>(ch * sizeof(W)), 256);
+  if (c->op_ws_bytes < need) {
+    if (c->op_ws) BO_CUDA(cudaFree(c->op_ws));
+    c->op_ws = nullptr;
+    BO_CUDA(cudaMalloc(&c->op_ws, need));
+    c->op_ws_bytes = need;
+  }
+  uint8_t* ws = static_cast<uint8_t*>(c->op_ws);
+  View buf{ws};
+  View wire{ws + ch * static_cast<size_t>(N) * 4};
+  View in{ws + ch * static_cast<size_t>(N) * 4 + align_up(static_cast<int64_t>(ch * sizeof(W)), 256)};
   float* B = buf.as<float>();
   BO_CUDA(cudaMemsetAsync(B, 0, ch * static_cast<size_t>(N) * 4, s));
   BO_CUDA(cudaMemcpyAsync(B, data, n * 4, cudaMemcpyDeviceToDevice, s));

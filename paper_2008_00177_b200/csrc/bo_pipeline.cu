@@ -667,6 +667,7 @@ __device__ __forceinline__ void bulk_s2g(float* gdst, const float* ssrc, uint32_
 // kCtrlReady[g] flags — after its own bulk copies completed and with a
 // system-scope fence behind every CTA's stores of the group.
 struct PushGroups {
+  int plain_stores;  // BO_PUSH_STORES
   const int* group_of_tensor;
   const int* group_tiles;
   unsigned* count;
@@ -763,7 +764,20 @@ __global__ void __launch_bounds__(kThreads) k_shard_p2_push(const LambTile* __re
       // flat elements [w0, w0 + len): aligned middle [a0, a1) by bulk copy
       a0 = (t.w0 + 3) & ~static_cast<int64_t>(3);
       a1 = (t.w0 + t.len) & ~static_cast<int64_t>(3);
-      if (a1 > a0 && threadIdx.x == 0) {
+      if (G.plain_stores) {
+        // BO_PUSH_STORES=1: 16-byte stores from shared memory straight to
+        // every replica (fire and forget: the CTA does not wait for the copies)
+        const float* src = buf + off + (a0 - t.w0);  // 16-byte aligned in shared memory
+        const int nq = static_cast<int>((a1 - a0) >> 2);
+        for (int q = threadIdx.x; q < nq; q += kThreads) {
+          const float4 v = *reinterpret_cast<const float4*>(src + 4 * q);
+          for (int k = 0; k < N; ++k) {
+            const int j = (i + k) % N;
+            *reinterpret_cast<float4*>(dst[j] + a0 + 4 * q) = v;
+          }
+        }
+        a1 = a0;  // nothing for the bulk-copy wait below
+      } else if (a1 > a0 && threadIdx.x == 0) {
         // destinations in a per-tile rotated order, so the CTAs of all ranks
         // spread their pushes over every peer's NVLink ingress at any moment
         for (int k = 0; k < N; ++k) {
@@ -1032,7 +1046,8 @@ static void lamb_grouped(bo_ctx* c, const PtrTable& tab, const W* in) {
     c->group_events.assign(static_cast<size_t>(G) + 1, nullptr);
     for (auto& e : c->group_events) BO_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
-  PushGroups none{c->d_push_group_of_tensor, c->d_push_group_tiles, c->d_push_count, PeerFlags{{}, 0, c->rank}, 0u};
+  PushGroups none{c->push_stores, c->d_push_group_of_tensor, c->d_push_group_tiles, c->d_push_count,
+                  PeerFlags{{}, 0, c->rank}, 0u};
   unsigned epoch = 0;
   size_t half = 0;
   {
@@ -1149,7 +1164,8 @@ static void lamb_sharded(bo_ctx* c, const PtrTable& tab, const W* in) {
   }
   {
   StageTimer timer(c, BO_STAGE_LAMB_UPDATE);
-  const PushGroups G{c->d_push_group_of_tensor, c->d_push_group_tiles, c->d_push_count, c->peer_ctrl, epoch};
+  const PushGroups G{c->push_stores, c->d_push_group_of_tensor, c->d_push_group_tiles, c->d_push_count,
+                     c->peer_ctrl, epoch};
   if (c->push_ctas > 0 && c->push_ctas < c->n_push_tiles) {
     k_shard_p2_push<2><<<c->push_ctas, kThreads, 0, c->stream>>>(c->d_push_tiles, c->n_push_tiles, c->wsh,
                                                                  c->u, c->state, c->lamb, c->trust,
