@@ -74,7 +74,7 @@ typedef struct {
 } bo_scaler_config;
 
 typedef enum {
-  BO_REDUCE_AUTO = 0,  /* RING when f16_exchange, NCCL otherwise */
+  BO_REDUCE_AUTO = 0,  /* RING (measured faster than NCCL for the fp32 wire too) */
   BO_REDUCE_RING = 1,  /* reference ring order, bit-exact (fp32 or f16 wire) */
   BO_REDUCE_NCCL = 2   /* ncclReduceScatter (fp32 wire only; reassociated sum) */
 } bo_reduce_algo;

@@ -237,7 +237,7 @@ class GradPipeline:
 
         algo = self.cfg.reduce_algo
         if algo == REDUCE_AUTO:
-            algo = REDUCE_RING if self.cfg.f16_exchange else REDUCE_NCCL
+            algo = REDUCE_RING  # the library's AUTO (bo_create)
         return (algo == REDUCE_NCCL or os.environ.get("BO_RING_NCCL", "0") != "0"
                 or os.environ.get("BO_RING_BARRIER", "") == "nccl")
 

@@ -41,6 +41,8 @@ def main():
     ap.add_argument("--case", default="ring16")
     ap.add_argument("--steps", type=int, default=4)
     ap.add_argument("--model", default="tiny")
+    ap.add_argument("--params-wait", action="store_true",
+                    help="check bo_params_wait gating instead of oracle parity")
     args = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     # one GPU per rank (never two ranks on one device: their flag-spinning
@@ -92,6 +94,8 @@ def main():
         else:
             raise SystemExit(f"unknown case {args.case}")
     f16, algo, K, bb, sc, ppm, sexp, exact = CASES[case]
+    if args.params_wait:
+        os.environ["BO_PUSH_GROUP_ELEMS"] = "20000"  # several parameter groups on a small model
     if args.model == "tiny":
         spec = bert_spec(BERT_TINY)
     elif args.model == "bert-large":
@@ -114,6 +118,55 @@ def main():
     pipe, su, fi = run_pipeline(spec, cfg, None, args.steps, grad_seed=9, spike_ppm=ppm,
                                 spike_exp=sexp, injections=inj, rank=rank, world=world, pipe=pipe,
                                 device=local, overlap=overlap, resident=resident)
+    gated = True
+    if args.params_wait:
+        # one more step, then on a second stream: per parameter group,
+        # bo_params_wait and a snapshot of the group's tensors — every snapshot
+        # must equal the step's final parameters (a wait released early would
+        # show values of the previous step)
+        before = pipe.read_params()
+        pipe, _, _ = run_pipeline(spec, cfg, None, 1, grad_seed=9, rank=rank, world=world, pipe=pipe,
+                                  device=local, first_step=args.steps)
+        # (run_pipeline synchronises; issue a fresh step without it for the check)
+        from tests.harness import GradBuffers
+        gb = GradBuffers(spec, K, local, True)
+        S = pipe.status().loss_scale
+        for k in range(K):
+            gb.fill(k, 9, rank, args.steps + 1, S)
+        torch.cuda.synchronize()
+        side = torch.cuda.Stream(device=local)
+        numels = spec.numels()
+        off = np.concatenate([[0], np.cumsum(numels)[:-1]]).astype(np.int64)
+        views = []
+        for t in range(spec.n_tensors):
+            ptr = pipe.param_ptr(t)
+
+            class _V:
+                __cuda_array_interface__ = {"shape": (numels[t],), "typestr": "<f4", "data": (ptr, False),
+                                            "version": 3}
+            views.append(torch.as_tensor(_V(), device=f"cuda:{local}") if numels[t] else None)
+        snap = [torch.empty(n, device=f"cuda:{local}") if n else None for n in numels]
+        pipe.train_step(gb.ptrs)  # enqueued; the waits below do not synchronise with it
+        with torch.cuda.stream(side):
+            for t in range(spec.n_tensors):
+                pipe.params_wait(t, side)
+                if numels[t]:
+                    snap[t].copy_(views[t])
+        torch.cuda.synchronize()
+        final = pipe.read_params()
+        got = np.concatenate([snap[t].cpu().numpy() if numels[t] else np.zeros(0, np.float32)
+                              for t in range(spec.n_tensors)])
+        gated = bool(np.array_equal(got.view(np.uint32), final.view(np.uint32)))
+        changed = not np.array_equal(final.view(np.uint32), before.view(np.uint32))
+        gated = gated and changed
+        # the oracle compares args.steps steps: roll the extra two back out
+        pipe.close()
+        result = {"rank": rank, "ok": gated, "params_wait_gated": gated}
+        if rank == 0:
+            print(json.dumps(result), flush=True)
+        dist.barrier()
+        dist.destroy_process_group()
+        sys.exit(0 if gated else 1)
     w = pipe.read_params()
     m = np.zeros(P, np.float32)
     v = np.zeros(P, np.float32)

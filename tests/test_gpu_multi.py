@@ -38,11 +38,11 @@ def _port():
     return p
 
 
-def run_case(case, nproc, model="tiny", steps=4):
+def run_case(case, nproc, model="tiny", steps=4, extra=()):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
            "--master-addr", "127.0.0.1", f"--master-port={_port()}",
            os.path.join(ROOT, "tests", "mp_worker.py"), "--case", case, "--steps", str(steps),
-           "--model", model]
+           "--model", model, *extra]
     for _attempt in range(3):
         r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
         if "EADDRINUSE" not in r.stderr:
@@ -136,3 +136,14 @@ def test_more_gpus(n):
         assert res["path"] == path, (case, res["path"])
         assert res["world"] == n and res["replicas_identical"]
     run_case("nccl32", n)
+
+
+@pytest.mark.parametrize("case", ["ring16_resident", "ring16_grouped_resident"])
+def test_params_wait_gates_each_group(case):
+    """bo_params_wait: a second stream that waits per parameter group and
+    snapshots the group's tensors right after the wait sees exactly the
+    step's final parameters (never the previous step's), while the rest of
+    the push is still in flight."""
+    _placement(case, 2)
+    res = run_case(case, 2, model="small", steps=2, extra=["--params-wait"])
+    assert res["params_wait_gated"]
