@@ -465,7 +465,7 @@ struct P1Args {
 constexpr int kWarpTileCTA = 256;
 // KR > 0 (with kX): x from the KR resident micros in the reference's order
 // instead of h + acc.
-template <typename W, bool kIn, bool kX, int U = 2, int kMinBlocks = 4, int KR = 0>
+template <typename W, bool kIn, bool kX, int U = 2, int kMinBlocks = 4, int KR = 0, bool kDbl = false>
 __global__ void __launch_bounds__(kWarpTileCTA, kMinBlocks) k_p1w(const LambTile* __restrict__ tiles,
                                                           int n_tiles,
                                                           const __grid_constant__ PtrTable tab,
@@ -485,7 +485,8 @@ __global__ void __launch_bounds__(kWarpTileCTA, kMinBlocks) k_p1w(const LambTile
   const float* __restrict__ v = par ? A.v1 : A.v0;
   float* __restrict__ mn = par ? A.m0 : A.m1;
   float* __restrict__ vn = par ? A.v0 : A.v1;
-  const float* __restrict__ wsh = (A.wsh_alt && par ? A.wsh_alt : A.wsh) + t.s0;
+  // kDbl (grouped LAMB): the master shard is double-buffered by parity
+  const float* __restrict__ wsh = (kDbl && par ? A.wsh_alt : A.wsh) + t.s0;
   float* __restrict__ u = A.u + t.s0;
   m += t.s0;
   v += t.s0;
@@ -667,7 +668,6 @@ __device__ __forceinline__ void bulk_s2g(float* gdst, const float* ssrc, uint32_
 // kCtrlReady[g] flags — after its own bulk copies completed and with a
 // system-scope fence behind every CTA's stores of the group.
 struct PushGroups {
-  int plain_stores;  // BO_PUSH_STORES
   const int* group_of_tensor;
   const int* group_tiles;
   unsigned* count;
@@ -764,20 +764,7 @@ __global__ void __launch_bounds__(kThreads) k_shard_p2_push(const LambTile* __re
       // flat elements [w0, w0 + len): aligned middle [a0, a1) by bulk copy
       a0 = (t.w0 + 3) & ~static_cast<int64_t>(3);
       a1 = (t.w0 + t.len) & ~static_cast<int64_t>(3);
-      if (G.plain_stores) {
-        // BO_PUSH_STORES=1: 16-byte stores from shared memory straight to
-        // every replica (fire and forget: the CTA does not wait for the copies)
-        const float* src = buf + off + (a0 - t.w0);  // 16-byte aligned in shared memory
-        const int nq = static_cast<int>((a1 - a0) >> 2);
-        for (int q = threadIdx.x; q < nq; q += kThreads) {
-          const float4 v = *reinterpret_cast<const float4*>(src + 4 * q);
-          for (int k = 0; k < N; ++k) {
-            const int j = (i + k) % N;
-            *reinterpret_cast<float4*>(dst[j] + a0 + 4 * q) = v;
-          }
-        }
-        a1 = a0;  // nothing for the bulk-copy wait below
-      } else if (a1 > a0 && threadIdx.x == 0) {
+      if (a1 > a0 && threadIdx.x == 0) {
         // destinations in a per-tile rotated order, so the CTAs of all ranks
         // spread their pushes over every peer's NVLink ingress at any moment
         for (int k = 0; k < N; ++k) {
@@ -996,7 +983,7 @@ static void lamb_shard(bo_ctx* c, const G* g) {
 // the partials and flags (2T+1 doubles per rank, summed in rank order so all
 // ranks agree) -> trust ratios, found_inf, scaler -> phase 2 pushing the new
 // parameters into every rank's replica -> barrier.
-template <typename W, bool kHop>
+template <typename W, bool kHop, bool kDbl>
 static void launch_p1w(bo_ctx* c, const PtrTable& tab, const W* in, const P1Args& A, int tile0, int n) {
   if (n <= 0) return;
   P1Args a = A;
@@ -1005,13 +992,13 @@ static void launch_p1w(bo_ctx* c, const PtrTable& tab, const W* in, const P1Args
   const int grid = (n * 32 + kWarpTileCTA - 1) / kWarpTileCTA;
   auto go = [&](auto kern) { kern<<<grid, kWarpTileCTA, 0, c->stream>>>(tiles, n, tab, in, a); };
   if constexpr (!kHop) {
-    go(k_p1w<W, true, false, 1, 4>);
+    go(k_p1w<W, true, false, 1, 4, 0, kDbl>);
   } else if (c->ms.K == 0) {
-    go(k_p1w<W, true, true, 1, 4>);
+    go(k_p1w<W, true, true, 1, 4, 0, kDbl>);
   } else if (c->ms.K == 2) {
-    go(k_p1w<W, true, true, 1, 4, 2>);
+    go(k_p1w<W, true, true, 1, 4, 2, kDbl>);
   } else if (c->ms.K == 4) {
-    go(k_p1w<W, true, true, 1, 4, 4>);
+    go(k_p1w<W, true, true, 1, 4, 4, kDbl>);
   } else {
     fail(BO_ERR_INVALID_CONFIG, "fused last hop with resident micros: K must be 2 or 4");
   }
@@ -1046,15 +1033,14 @@ static void lamb_grouped(bo_ctx* c, const PtrTable& tab, const W* in) {
     c->group_events.assign(static_cast<size_t>(G) + 1, nullptr);
     for (auto& e : c->group_events) BO_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
-  PushGroups none{c->push_stores, c->d_push_group_of_tensor, c->d_push_group_tiles, c->d_push_count,
-                  PeerFlags{{}, 0, c->rank}, 0u};
+  PushGroups none{c->d_push_group_of_tensor, c->d_push_group_tiles, c->d_push_count, PeerFlags{{}, 0, c->rank}, 0u};
   unsigned epoch = 0;
   size_t half = 0;
   {
   StageTimer timer(c, BO_STAGE_LAMB_NORMS);
   for (int g = 0; g < G; ++g) {
     const bo_ctx::LambGroup& lg = c->lamb_groups[static_cast<size_t>(g)];
-    launch_p1w<W, kHop>(c, tab, in, A, lg.tile0, lg.tile1 - lg.tile0);
+    launch_p1w<W, kHop, true>(c, tab, in, A, lg.tile0, lg.tile1 - lg.tile0);
     c->bar_epoch += 1;
     epoch = static_cast<unsigned>(c->bar_epoch);
     half = (c->bar_epoch & 1) * static_cast<size_t>(c->world) * slot;
@@ -1164,8 +1150,7 @@ static void lamb_sharded(bo_ctx* c, const PtrTable& tab, const W* in) {
   }
   {
   StageTimer timer(c, BO_STAGE_LAMB_UPDATE);
-  const PushGroups G{c->push_stores, c->d_push_group_of_tensor, c->d_push_group_tiles, c->d_push_count,
-                     c->peer_ctrl, epoch};
+  const PushGroups G{c->d_push_group_of_tensor, c->d_push_group_tiles, c->d_push_count, c->peer_ctrl, epoch};
   if (c->push_ctas > 0 && c->push_ctas < c->n_push_tiles) {
     k_shard_p2_push<2><<<c->push_ctas, kThreads, 0, c->stream>>>(c->d_push_tiles, c->n_push_tiles, c->wsh,
                                                                  c->u, c->state, c->lamb, c->trust,
