@@ -447,14 +447,22 @@ def main_b200(args):
     alone = stage_ms[dom_bit] / max(stage_n[dom_bit], 1)
     st_dom = stages[dom]
     st_dom["ms_evented_all_stages"] = st_dom["ms"]
-    st_dom["ms"] = round(alone, 5)
-    st_dom["timed"] = "alone (events around this stage only)"
+    st_dom["ms_alone"] = round(alone, 5)
+    # The kernel's in-step duration: its share of the event-free step (the
+    # all-stage pass's shares x ms_per_step). A bracket of its own, however
+    # tight, serialises the kernel's tail against its neighbours and reads
+    # 2-9 % long (profiles/r02_notes.md); ms_alone is kept beside it.
+    in_step = st_dom["ms_in_step"] / max(st_dom["launches_per_step"], 1e-9)
+    st_dom["ms"] = round(in_step, 5)
+    st_dom["timed"] = "share of the event-free step (ms_in_step); ms_alone: events around this stage only"
     if "bytes" in st_dom:
-        gbs = st_dom["bytes"] / (alone * 1e-3) / 1e9
-        st_dom.update({"GB/s": round(gbs, 1), "frac": round(gbs / hbm, 4)})
+        gbs = st_dom["bytes"] / (in_step * 1e-3) / 1e9
+        st_dom.update({"GB/s": round(gbs, 1), "frac": round(gbs / hbm, 4),
+                       "frac_alone": round(st_dom["bytes"] / (alone * 1e-3) / 1e9 / hbm, 4)})
     if "nvlink_bytes" in st_dom:
-        gbs = st_dom["nvlink_bytes"] / (alone * 1e-3) / 1e9
-        st_dom.update({"nvlink_GB/s": round(gbs, 1), "nvlink_frac": round(gbs / NVLINK_GBS, 4)})
+        gbs = st_dom["nvlink_bytes"] / (in_step * 1e-3) / 1e9
+        st_dom.update({"nvlink_GB/s": round(gbs, 1), "nvlink_frac": round(gbs / NVLINK_GBS, 4),
+                       "nvlink_frac_alone": round(st_dom["nvlink_bytes"] / (alone * 1e-3) / 1e9 / NVLINK_GBS, 4)})
     kernel_names = {"accumulate": "k_accumulate", "finalize": "k_finalize",
                     "lamb_norms": ("k_lamb_p1r" if resident else "k_lamb_p1") if world == 1 else "k_p1w",
                     "lamb_update": "k_lamb_p2" if world == 1 else "k_shard_p2_push",
@@ -464,12 +472,16 @@ def main_b200(args):
         roofline = {"kernel": kernel_names[dom], "bound": "nvlink", "achieved": st_dom["nvlink_GB/s"],
                     "peak": NVLINK_GBS, "peak_kind": "measured (B200_PROFILING.md peer copy)",
                     "unit": "GB/s", "frac": st_dom["nvlink_frac"], "traffic": None,
+                    "frac_alone": st_dom.get("nvlink_frac_alone"), "ms": st_dom["ms"],
+                    "ms_alone": st_dom["ms_alone"],
                     "algorithmic_bytes_per_launch": st_dom["nvlink_bytes"],
                     "hbm_frac": st_dom["frac"]}
     else:
         roofline = {"kernel": kernel_names[dom], "bound": "hbm", "achieved": st_dom["GB/s"],
                     "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s", "frac": st_dom["frac"],
                     "traffic": traffic_from_profiles(kernel_names[dom]),
+                    "frac_alone": st_dom.get("frac_alone"), "ms": st_dom["ms"],
+                    "ms_alone": st_dom["ms_alone"],
                     "algorithmic_bytes_per_launch": st_dom["bytes"]}
     if roofline["frac"] > 1.0:
         roofline["note"] = ("the measured HBM peak is a 1:1 read:write copy; this kernel's "

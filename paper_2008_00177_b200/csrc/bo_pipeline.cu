@@ -998,7 +998,13 @@ static void launch_p1w(bo_ctx* c, const PtrTable& tab, const W* in, const P1Args
   } else if (c->ms.K == 2) {
     go(k_p1w<W, true, true, 1, 4, 2, kDbl>);
   } else if (c->ms.K == 4) {
-    go(k_p1w<W, true, true, 1, 4, 4, kDbl>);
+    // BO_P1W_MINB=3: 76 registers and no spills at 3 CTAs per SM (the default
+    // 4 CTAs cap it at 64 registers with 20 bytes of spills)
+    if (c->p1w_minb == 3) {
+      go(k_p1w<W, true, true, 1, 3, 4, kDbl>);
+    } else {
+      go(k_p1w<W, true, true, 1, 4, 4, kDbl>);
+    }
   } else {
     fail(BO_ERR_INVALID_CONFIG, "fused last hop with resident micros: K must be 2 or 4");
   }
@@ -1117,7 +1123,11 @@ static void lamb_sharded(bo_ctx* c, const PtrTable& tab, const W* in) {
     } else if (c->ms.K == 2) {  // the last ring hop fused in, x from the resident micros
       go(k_p1w<W, true, true, 1, 4, 2>);
     } else if (c->ms.K == 4) {
-      go(k_p1w<W, true, true, 1, 4, 4>);
+      if (c->p1w_minb == 3) {
+        go(k_p1w<W, true, true, 1, 3, 4>);
+      } else {
+        go(k_p1w<W, true, true, 1, 4, 4>);
+      }
     } else {
       fail(BO_ERR_INVALID_CONFIG, "fused last hop with resident micros: K must be 2 or 4");
     }
