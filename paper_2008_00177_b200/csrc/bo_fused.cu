@@ -156,8 +156,8 @@ __global__ void __launch_bounds__(kP1Threads, 2) k_lamb_p1(
 // template parameter so the K loads of both float4 groups of a thread are
 // issued up front like k_lamb_p1's; the tile's K gradient pointers sit in
 // shared memory. 2K + 24 B/elem.
-template <int K, int kMinBlocks = 2>
-__global__ void __launch_bounds__(kP1Threads, kMinBlocks) k_lamb_p1r(
+template <int K>
+__global__ void __launch_bounds__(kP1Threads, 2) k_lamb_p1r(
     const FusedTile* __restrict__ tiles, MicroSrc ms, const float* __restrict__ w, float* m0,
     float* v0, float* m1, float* v1, float* __restrict__ u, DevState* __restrict__ st, LambConsts c,
     const double* __restrict__ bc_table, double* __restrict__ tile_part) {
@@ -386,11 +386,7 @@ void run_fused_single_rank(bo_ctx* c, const PtrTable& tab, MicroSrc ms) {
       switch (ms.K) {
         case 2: launch(k_lamb_p1r<2>); break;
         case 3: launch(k_lamb_p1r<3>); break;
-        case 4:
-          // BO_P1R_MINB=1: one 512-thread CTA per SM guaranteed, up to 128
-          // registers (no spills) — the register / occupancy trade-off probe
-          if (c->p1r_minb == 1) launch(k_lamb_p1r<4, 1>); else launch(k_lamb_p1r<4>);
-          break;
+        case 4: launch(k_lamb_p1r<4>); break;
         case 5: launch(k_lamb_p1r<5>); break;
         case 6: launch(k_lamb_p1r<6>); break;
         case 7: launch(k_lamb_p1r<7>); break;

@@ -802,6 +802,108 @@ __global__ void __launch_bounds__(kThreads) k_shard_p2_push(const LambTile* __re
   }
 }
 
+// Persistent push with an NB-stage shared-memory ring (BO_PUSH_CTAS > 0):
+// the copies of up to NB - 1 tiles are in flight per CTA while the next tile
+// is computed — a buffer is reused once its copies have READ it
+// (wait_group.read), and a tile is counted towards its parameter group once
+// its copies have COMPLETED, NB - 1 tiles later (wait_group NB - 1). A small
+// grid keeps the push at NVLink speed on few SMs (the rest stay free for a
+// concurrent forward or phase 1). Same arithmetic and destinations as
+// k_shard_p2_push.
+template <int NB>
+__global__ void __launch_bounds__(kThreads) k_shard_p2_push_pipe(const LambTile* __restrict__ tiles,
+                                                                 int n_tiles, float* wsh_main,
+                                                                 const float* __restrict__ u,
+                                                                 const DevState* __restrict__ st,
+                                                                 LambConsts c,
+                                                                 const float* __restrict__ trust,
+                                                                 float* const* __restrict__ peer_w,
+                                                                 int N, const PushGroups G,
+                                                                 float* wsh_alt) {
+  extern __shared__ __align__(128) float ring[];  // [NB][kTileElems + 4]
+  __shared__ float* dst[8];
+  __shared__ int pend[NB];                        // tensor of the tile in ring slot k (thread 0)
+  if (threadIdx.x < N) dst[threadIdx.x] = peer_w[threadIdx.x];
+  const bool speculative = wsh_alt != nullptr;
+  const bool update = speculative || st->do_update != 0;
+  const int par = speculative ? st->parity : 0;
+  const float* __restrict__ wsrc = par ? wsh_alt : wsh_main;
+  float* __restrict__ wdst = speculative ? (par ? wsh_main : wsh_alt) : wsh_main;
+  int it = 0;
+  for (int i = blockIdx.x; i < n_tiles; i += gridDim.x, ++it) {
+    const LambTile t = tiles[i];
+    float* __restrict__ buf = ring + (it % NB) * (kTileElems + 4);
+    // the copies issued from this slot NB tiles ago have finished reading it
+    if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(NB - 1) : "memory");
+    __syncthreads();
+    if (update && t.len > 0) {
+      const float step_scale = __fmul_rn(c.lr, trust[t.t]);
+      const int off = static_cast<int>(t.w0 & 3);
+      const Split sp = split_tile(t.s0, t.len);
+      auto one = [&](int e) {
+        const int64_t s = t.s0 + e;
+        const float nw = __fsub_rn(wsrc[s], __fmul_rn(step_scale, u[s]));
+        wdst[s] = nw;
+        buf[off + e] = nw;
+      };
+      if (static_cast<int>(threadIdx.x) < sp.head) one(threadIdx.x);
+      if (threadIdx.x >= 32 && static_cast<int>(threadIdx.x) - 32 < sp.tail) {
+        one(sp.head + 4 * sp.nv + static_cast<int>(threadIdx.x) - 32);
+      }
+      for (int q = threadIdx.x; q < sp.nv; q += kThreads) {
+        const int e = sp.head + 4 * q;
+        const int64_t s = t.s0 + e;
+        const float4 w4 = *reinterpret_cast<const float4*>(wsrc + s);
+        const float4 u4 = __ldcs(reinterpret_cast<const float4*>(u + s));
+        const float4 n4 = make_float4(__fsub_rn(w4.x, __fmul_rn(step_scale, u4.x)),
+                                      __fsub_rn(w4.y, __fmul_rn(step_scale, u4.y)),
+                                      __fsub_rn(w4.z, __fmul_rn(step_scale, u4.z)),
+                                      __fsub_rn(w4.w, __fmul_rn(step_scale, u4.w)));
+        *reinterpret_cast<float4*>(wdst + s) = n4;
+        buf[off + e] = n4.x;
+        buf[off + e + 1] = n4.y;
+        buf[off + e + 2] = n4.z;
+        buf[off + e + 3] = n4.w;
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncthreads();
+      const int64_t a0 = (t.w0 + 3) & ~static_cast<int64_t>(3);
+      const int64_t a1 = (t.w0 + t.len) & ~static_cast<int64_t>(3);
+      if (a1 > a0 && threadIdx.x == 0) {
+        for (int k = 0; k < N; ++k) {
+          const int j = (i + k) % N;
+          bulk_s2g(dst[j] + a0, buf + off + (a0 - t.w0), static_cast<uint32_t>(a1 - a0) * 4u);
+        }
+      }
+      const int nhead = static_cast<int>(a1 > a0 ? a0 - t.w0 : t.len);
+      const int ntail = static_cast<int>(a1 > a0 ? t.w0 + t.len - a1 : 0);
+      if (static_cast<int>(threadIdx.x) < nhead * N) {
+        const int e = threadIdx.x % nhead, j = threadIdx.x / nhead;
+        dst[j][t.w0 + e] = buf[off + e];
+      } else if (static_cast<int>(threadIdx.x) >= 128 && static_cast<int>(threadIdx.x) - 128 < ntail * N) {
+        const int k = static_cast<int>(threadIdx.x) - 128;
+        const int e = static_cast<int>(a1 - t.w0) + k % ntail, j = k / ntail;
+        dst[j][t.w0 + e] = buf[off + e];
+      }
+    }
+    if (threadIdx.x == 0) {
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      pend[it % NB] = t.t;
+      if (it >= NB - 1) {
+        // the tile NB - 1 iterations back has completed its copies; its edge
+        // stores precede this iteration's barriers
+        asm volatile("cp.async.bulk.wait_group %0;" ::"n"(NB - 1) : "memory");
+        push_tile_done(G, pend[(it - (NB - 1)) % NB]);
+      }
+    }
+  }
+  __syncthreads();  // the last tiles' edge stores
+  if (threadIdx.x == 0 && it > 0) {
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    for (int k = (it >= NB - 1 ? it - (NB - 1) + 1 : 0); k < it; ++k) push_tile_done(G, pend[k % NB]);
+  }
+}
+
 // bo_params_wait: one thread on the caller's stream waits until every rank
 // published parameter group g of step `epoch` (bounded by the watchdog).
 __global__ void k_params_wait(const unsigned* __restrict__ slots, int N, unsigned epoch,
@@ -983,6 +1085,31 @@ static void lamb_shard(bo_ctx* c, const G* g) {
 // the partials and flags (2T+1 doubles per rank, summed in rank order so all
 // ranks agree) -> trust ratios, found_inf, scaler -> phase 2 pushing the new
 // parameters into every rank's replica -> barrier.
+template <int NB>
+static void launch_push_pipe_nb(bo_ctx* c, const LambTile* tiles, int n, cudaStream_t st, const PushGroups& G,
+                                float* wsh_alt) {
+  const size_t smem = static_cast<size_t>(NB) * (kTileElems + 4) * sizeof(float);
+  static bool configured = false;  // per process: the attribute is per kernel
+  if (!configured) {
+    BO_CUDA(cudaFuncSetAttribute(k_shard_p2_push_pipe<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)));
+    configured = true;
+  }
+  const int grid = std::min(n, c->push_ctas);
+  k_shard_p2_push_pipe<NB><<<grid, kThreads, smem, st>>>(tiles, n, c->wsh, c->u, c->state, c->lamb, c->trust,
+                                                         c->d_peer_w, c->world, G, wsh_alt);
+}
+
+static void launch_push_pipe(bo_ctx* c, const LambTile* tiles, int n, cudaStream_t st, const PushGroups& G,
+                             float* wsh_alt) {
+  if (n <= 0) return;
+  if (c->push_stages >= 8) {
+    launch_push_pipe_nb<8>(c, tiles, n, st, G, wsh_alt);
+  } else {
+    launch_push_pipe_nb<4>(c, tiles, n, st, G, wsh_alt);
+  }
+}
+
 template <typename W, bool kHop, bool kDbl>
 static void launch_p1w(bo_ctx* c, const PtrTable& tab, const W* in, const P1Args& A, int tile0, int n) {
   if (n <= 0) return;
@@ -998,13 +1125,7 @@ static void launch_p1w(bo_ctx* c, const PtrTable& tab, const W* in, const P1Args
   } else if (c->ms.K == 2) {
     go(k_p1w<W, true, true, 1, 4, 2, kDbl>);
   } else if (c->ms.K == 4) {
-    // BO_P1W_MINB=3: 76 registers and no spills at 3 CTAs per SM (the default
-    // 4 CTAs cap it at 64 registers with 20 bytes of spills)
-    if (c->p1w_minb == 3) {
-      go(k_p1w<W, true, true, 1, 3, 4, kDbl>);
-    } else {
-      go(k_p1w<W, true, true, 1, 4, 4, kDbl>);
-    }
+    go(k_p1w<W, true, true, 1, 4, 4, kDbl>);
   } else {
     fail(BO_ERR_INVALID_CONFIG, "fused last hop with resident micros: K must be 2 or 4");
   }
@@ -1070,9 +1191,13 @@ static void lamb_grouped(bo_ctx* c, const PtrTable& tab, const W* in) {
       BO_CUDA(cudaStreamWaitEvent(ps, c->group_events[static_cast<size_t>(g)], 0));
     }
     if (lg.tile1 > lg.tile0) {
-      k_shard_p2_push<1><<<lg.tile1 - lg.tile0, kThreads, 0, ps>>>(
-          c->d_lamb_tiles + lg.tile0, lg.tile1 - lg.tile0, c->wsh, c->u, c->state, c->lamb, c->trust,
-          c->d_peer_w, c->world, none, c->wsh_alt);
+      if (c->push_ctas > 0) {
+        launch_push_pipe(c, c->d_lamb_tiles + lg.tile0, lg.tile1 - lg.tile0, ps, none, c->wsh_alt);
+      } else {
+        k_shard_p2_push<1><<<lg.tile1 - lg.tile0, kThreads, 0, ps>>>(
+            c->d_lamb_tiles + lg.tile0, lg.tile1 - lg.tile0, c->wsh, c->u, c->state, c->lamb, c->trust,
+            c->d_peer_w, c->world, none, c->wsh_alt);
+      }
       check_launch(c, "k_shard_p2_push");
     }
   }
@@ -1123,11 +1248,7 @@ static void lamb_sharded(bo_ctx* c, const PtrTable& tab, const W* in) {
     } else if (c->ms.K == 2) {  // the last ring hop fused in, x from the resident micros
       go(k_p1w<W, true, true, 1, 4, 2>);
     } else if (c->ms.K == 4) {
-      if (c->p1w_minb == 3) {
-        go(k_p1w<W, true, true, 1, 3, 4>);
-      } else {
-        go(k_p1w<W, true, true, 1, 4, 4>);
-      }
+      go(k_p1w<W, true, true, 1, 4, 4>);
     } else {
       fail(BO_ERR_INVALID_CONFIG, "fused last hop with resident micros: K must be 2 or 4");
     }
@@ -1162,9 +1283,7 @@ static void lamb_sharded(bo_ctx* c, const PtrTable& tab, const W* in) {
   StageTimer timer(c, BO_STAGE_LAMB_UPDATE);
   const PushGroups G{c->d_push_group_of_tensor, c->d_push_group_tiles, c->d_push_count, c->peer_ctrl, epoch};
   if (c->push_ctas > 0 && c->push_ctas < c->n_push_tiles) {
-    k_shard_p2_push<2><<<c->push_ctas, kThreads, 0, c->stream>>>(c->d_push_tiles, c->n_push_tiles, c->wsh,
-                                                                 c->u, c->state, c->lamb, c->trust,
-                                                                 c->d_peer_w, c->world, G);
+    launch_push_pipe(c, c->d_push_tiles, c->n_push_tiles, c->stream, G, nullptr);
   } else {
     k_shard_p2_push<1><<<c->n_push_tiles, kThreads, 0, c->stream>>>(c->d_push_tiles, c->n_push_tiles,
                                                                     c->wsh, c->u, c->state, c->lamb,
