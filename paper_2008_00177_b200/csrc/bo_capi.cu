@@ -364,8 +364,6 @@ bo_status bo_create(const bo_trainer_config* cfg, int32_t n_tensors, const int64
   if (const char* e = std::getenv("BO_RING_PUSH")) c->ring_push = std::strcmp(e, "0") != 0;
   if (const char* e = std::getenv("BO_RING_BARRIER")) c->nb_barrier = std::strcmp(e, "nccl") != 0;
   if (const char* e = std::getenv("BO_FUSE_LAST")) c->fuse_last_hop = std::strcmp(e, "0") != 0;
-  if (const char* e = std::getenv("BO_PUSH_CTAS")) c->push_ctas = std::max(0, std::atoi(e));
-  if (const char* e = std::getenv("BO_PUSH_STAGES")) c->push_stages = std::atoi(e);
   // AUTO: the device ring for both wires — bit-exact (the reference fold) and,
   // for fp32, faster than ncclReduceScatter at every bucket size measured
   // (BERT-large, 4 GPUs: 3.60 vs 4.33 ms per step at 4 MiB; profiles/r02_sweep_n4.json)

@@ -308,8 +308,6 @@ struct bo_ctx {
   int* d_push_group_tiles = nullptr;   // [G] tiles of group g on this rank
   unsigned* d_push_count = nullptr;    // [G] cumulative finished tiles
   cudaEvent_t params_done = nullptr;   // world 1: the step's update, for bo_params_wait
-  int push_ctas = 0;                   // BO_PUSH_CTAS: persistent push grid (0: one CTA per tile)
-  int push_stages = 4;                 // BO_PUSH_STAGES: its shared-memory ring depth (4 or 8)
   void* op_ws = nullptr;               // bo_ring_allreduce_* workspace (grow-only)
   size_t op_ws_bytes = 0;
   // Grouped LAMB (BO_LAMB_GROUP_ELEMS, world > 1): consecutive tensors (model

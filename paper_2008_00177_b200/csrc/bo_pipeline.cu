@@ -691,18 +691,14 @@ __device__ __forceinline__ void push_tile_done(const PushGroups& G, int tensor) 
   }
 }
 
-// gridDim.x CTAs walk the push tiles (model order, so parameter groups
-// complete front to back). NB = 1 (default): one tile per CTA, the hardware
-// keeps ~8 CTAs — 8 tiles' copies — in flight per SM (measured fastest:
-// 0.99 vs 1.28 ms at world 2 for a persistent grid of 6 CTAs per SM).
-// NB = 2 (BO_PUSH_CTAS > 0): a persistent grid with two shared-memory tile
-// buffers, the copies of tile i flying while tile i + grid is computed; a
-// small grid leaves SMs to a concurrent forward (bo_params_wait) at the cost
-// of push bandwidth. Skipped steps only count.
+// One CTA per tile (model order, so parameter groups complete front to back):
+// the hardware keeps ~8 CTAs — 8 tiles' bulk copies — in flight per SM and
+// launches the next CTA the moment one retires. Measured faster than every
+// persistent form tried (two or four shared-memory tile buffers, TMA-fed
+// input ring, 24-1184 CTAs: 20 % to 10x slower; profiles/r02_notes.md).
 // Grouped LAMB (wsh_alt != null): speculative — runs before the step's
 // decision, reads the current master shard (parity) and writes the other one
 // (k_step_final flips, k_rollback undoes the replicas on a skipped step).
-template <int NB>
 __global__ void __launch_bounds__(kThreads) k_shard_p2_push(const LambTile* __restrict__ tiles,
                                                             int n_tiles, float* wsh_main,
                                                             const float* __restrict__ u,
@@ -712,7 +708,7 @@ __global__ void __launch_bounds__(kThreads) k_shard_p2_push(const LambTile* __re
                                                             float* const* __restrict__ peer_w,
                                                             int N, const PushGroups G,
                                                             float* wsh_alt = nullptr) {
-  __shared__ __align__(128) float bufs[NB][kTileElems + 4];
+  __shared__ __align__(128) float buf[kTileElems + 4];
   __shared__ float* dst[8];
   if (threadIdx.x < N) dst[threadIdx.x] = peer_w[threadIdx.x];
   const bool speculative = wsh_alt != nullptr;
@@ -720,248 +716,72 @@ __global__ void __launch_bounds__(kThreads) k_shard_p2_push(const LambTile* __re
   const int par = speculative ? st->parity : 0;
   const float* __restrict__ wsrc = par ? wsh_alt : wsh_main;
   float* __restrict__ wdst = speculative ? (par ? wsh_main : wsh_alt) : wsh_main;
-  int pending = -1;  // tensor of the previous tile (its stores in flight)
-  int it = 0;
-  for (int i = blockIdx.x; i < n_tiles; i += gridDim.x, ++it) {
-    const LambTile t = tiles[i];
-    float* __restrict__ buf = bufs[it % NB];
-    // this buffer's previous copies (NB tiles ago) have finished reading it
-    if (NB > 1 && threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-    __syncthreads();
-    int64_t a0 = 0, a1 = 0;
-    if (update && t.len > 0) {
-      const float step_scale = __fmul_rn(c.lr, trust[t.t]);
-      const int off = static_cast<int>(t.w0 & 3);  // buf[off + e] <-> flat element w0 + e
-      const Split sp = split_tile(t.s0, t.len);
-      auto one = [&](int e) {
-        const int64_t s = t.s0 + e;
-        const float nw = __fsub_rn(wsrc[s], __fmul_rn(step_scale, u[s]));
-        wdst[s] = nw;
-        buf[off + e] = nw;
-      };
-      if (static_cast<int>(threadIdx.x) < sp.head) one(threadIdx.x);
-      if (threadIdx.x >= 32 && static_cast<int>(threadIdx.x) - 32 < sp.tail) {
-        one(sp.head + 4 * sp.nv + static_cast<int>(threadIdx.x) - 32);
-      }
-      for (int q = threadIdx.x; q < sp.nv; q += kThreads) {
-        const int e = sp.head + 4 * q;
-        const int64_t s = t.s0 + e;
-        const float4 w4 = *reinterpret_cast<const float4*>(wsrc + s);
-        const float4 u4 = __ldcs(reinterpret_cast<const float4*>(u + s));
-        const float4 n4 = make_float4(__fsub_rn(w4.x, __fmul_rn(step_scale, u4.x)),
-                                      __fsub_rn(w4.y, __fmul_rn(step_scale, u4.y)),
-                                      __fsub_rn(w4.z, __fmul_rn(step_scale, u4.z)),
-                                      __fsub_rn(w4.w, __fmul_rn(step_scale, u4.w)));
-        *reinterpret_cast<float4*>(wdst + s) = n4;
-        buf[off + e] = n4.x;
-        buf[off + e + 1] = n4.y;
-        buf[off + e + 2] = n4.z;
-        buf[off + e + 3] = n4.w;
-      }
-      // make the generic-proxy shared-memory writes visible to the bulk copies
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      __syncthreads();
-      // flat elements [w0, w0 + len): aligned middle [a0, a1) by bulk copy
-      a0 = (t.w0 + 3) & ~static_cast<int64_t>(3);
-      a1 = (t.w0 + t.len) & ~static_cast<int64_t>(3);
-      if (a1 > a0 && threadIdx.x == 0) {
-        // destinations in a per-tile rotated order, so the CTAs of all ranks
-        // spread their pushes over every peer's NVLink ingress at any moment
-        for (int k = 0; k < N; ++k) {
-          const int j = (i + k) % N;
-          bulk_s2g(dst[j] + a0, buf + off + (a0 - t.w0), static_cast<uint32_t>(a1 - a0) * 4u);
-        }
-      }
-      // edges (and tiles shorter than one aligned 16-byte group)
-      const int nhead = static_cast<int>(a1 > a0 ? a0 - t.w0 : t.len);
-      const int ntail = static_cast<int>(a1 > a0 ? t.w0 + t.len - a1 : 0);
-      if (static_cast<int>(threadIdx.x) < nhead * N) {
-        const int e = threadIdx.x % nhead, j = threadIdx.x / nhead;
-        dst[j][t.w0 + e] = buf[off + e];
-      } else if (static_cast<int>(threadIdx.x) >= 128 && static_cast<int>(threadIdx.x) - 128 < ntail * N) {
-        const int k = static_cast<int>(threadIdx.x) - 128;
-        const int e = static_cast<int>(a1 - t.w0) + k % ntail, j = k / ntail;
-        dst[j][t.w0 + e] = buf[off + e];
-      }
-    }
-    if (threadIdx.x == 0) {
-      asm volatile("cp.async.bulk.commit_group;" ::: "memory");  // (empty when nothing was issued)
-      if (pending >= 0) {
-        // the previous tile's copies are complete once only this tile's group is
-        // outstanding; its edge stores precede this iteration's barrier
-        asm volatile("cp.async.bulk.wait_group 1;" ::: "memory");
-        push_tile_done(G, pending);
-      }
-    }
-    pending = t.t;
-  }
-  __syncthreads();  // the last tile's edge stores
-  if (threadIdx.x == 0 && pending >= 0) {
-    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-    push_tile_done(G, pending);
-  }
-}
-
-// Persistent push on few SMs (BO_PUSH_CTAS > 0): every CTA walks its tiles
-// with an NB-stage shared-memory ring fed by TMA — the master-shard and
-// update tiles of the next NB - 1 tiles are loaded by bulk copies
-// (cp.async.bulk global->shared, mbarrier completion) while the current tile
-// is computed from shared memory, and the new tile leaves by bulk copies
-// (shared->global) into every replica; a buffer is reused once its copies
-// have read it. Nothing waits on a remote write until the end (unless
-// parameter groups are published, then a tile is counted NB - 1 tiles after
-// its copies were issued). Latency is hidden by the ring instead of by many
-// resident CTAs, so a small grid still streams — leaving SMs to a concurrent
-// forward (bo_params_wait) or to phase 1 (grouped LAMB). Same arithmetic
-// and destinations as k_shard_p2_push.
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(bar))),
-               "r"(count)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
-                   static_cast<unsigned>(__cvta_generic_to_shared(bar))),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
-  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
-  unsigned done = 0;
-  while (!done) {
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(done)
-        : "r"(a), "r"(parity)
-        : "memory");
-  }
-}
-__device__ __forceinline__ void bulk_g2s(float* sdst, const float* gsrc, unsigned bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          static_cast<unsigned>(__cvta_generic_to_shared(sdst))),
-      "l"(gsrc), "r"(bytes), "r"(static_cast<unsigned>(__cvta_generic_to_shared(bar)))
-      : "memory");
-}
-
-constexpr int kStageIn = kTileElems + 8;   // an aligned superset of a shard tile
-constexpr int kStageOut = kTileElems + 4;  // the new tile at its flat-replica phase
-
-template <int NB>
-__global__ void __launch_bounds__(kThreads) k_shard_p2_push_pipe(const LambTile* __restrict__ tiles,
-                                                                 int n_tiles, float* wsh_main,
-                                                                 const float* __restrict__ u,
-                                                                 const DevState* __restrict__ st,
-                                                                 LambConsts c,
-                                                                 const float* __restrict__ trust,
-                                                                 float* const* __restrict__ peer_w,
-                                                                 int N, const PushGroups G,
-                                                                 float* wsh_alt) {
-  extern __shared__ __align__(128) float smem[];  // [NB][w in | u in | out]
-  __shared__ __align__(8) uint64_t full[NB];
-  __shared__ float* dst[8];
-  __shared__ int pend[NB];
-  if (threadIdx.x < N) dst[threadIdx.x] = peer_w[threadIdx.x];
-  const bool speculative = wsh_alt != nullptr;
-  const bool update = speculative || st->do_update != 0;
-  const int par = speculative ? st->parity : 0;
-  const float* __restrict__ wsrc = par ? wsh_alt : wsh_main;
-  float* __restrict__ wdst = speculative ? (par ? wsh_main : wsh_alt) : wsh_main;
-  const bool publish = G.pf.n > 0;
-  auto stage_w = [&](int k) { return smem + k * (2 * kStageIn + kStageOut); };
-  auto stage_u = [&](int k) { return stage_w(k) + kStageIn; };
-  auto stage_o = [&](int k) { return stage_w(k) + 2 * kStageIn; };
-  const int n_mine = n_tiles > static_cast<int>(blockIdx.x)
-                         ? (n_tiles - 1 - static_cast<int>(blockIdx.x)) / static_cast<int>(gridDim.x) + 1
-                         : 0;
-  auto tile_of = [&](int it) { return static_cast<int>(blockIdx.x) + it * static_cast<int>(gridDim.x); };
-  // TMA load of tile `it`'s master-shard and update superset into its stage
-  auto load = [&](int it) {
-    const LambTile t = tiles[tile_of(it)];
-    const int k = it % NB;
-    const int64_t as = t.s0 & ~static_cast<int64_t>(3);
-    const int64_t ae = (t.s0 + t.len + 3) & ~static_cast<int64_t>(3);
-    const unsigned bytes = static_cast<unsigned>(ae - as) * 4u;
-    if (bytes == 0) {
-      mbar_expect_tx(&full[k], 0);
-      return;
-    }
-    mbar_expect_tx(&full[k], 2 * bytes);
-    bulk_g2s(stage_w(k), wsrc + as, bytes, &full[k]);
-    bulk_g2s(stage_u(k), u + as, bytes, &full[k]);
-  };
-  if (threadIdx.x == 0) {
-    for (int k = 0; k < NB; ++k) mbar_init(&full[k], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
+  const int i = blockIdx.x;
+  const LambTile t = tiles[i];
   __syncthreads();
-  if (threadIdx.x == 0 && update) {
-    for (int it = 0; it < NB - 1 && it < n_mine; ++it) load(it);
-  }
-  for (int it = 0; it < n_mine; ++it) {
-    const int i = tile_of(it);
-    const LambTile t = tiles[i];
-    const int k = it % NB;
-    if (threadIdx.x == 0) {
-      // the out buffer of this stage: its copies (NB tiles ago) have read it
-      asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(NB - 1) : "memory");
-      // refill the stage the previous tile used (its inputs are consumed: the
-      // generic reads are ordered before the async-proxy writes by the fence)
-      if (update && it + NB - 1 < n_mine) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        load(it + NB - 1);
-      }
+  int64_t a0 = 0, a1 = 0;
+  if (update && t.len > 0) {
+    const float step_scale = __fmul_rn(c.lr, trust[t.t]);
+    const int off = static_cast<int>(t.w0 & 3);  // buf[off + e] <-> flat element w0 + e
+    const Split sp = split_tile(t.s0, t.len);
+    auto one = [&](int e) {
+      const int64_t s = t.s0 + e;
+      const float nw = __fsub_rn(wsrc[s], __fmul_rn(step_scale, u[s]));
+      wdst[s] = nw;
+      buf[off + e] = nw;
+    };
+    if (static_cast<int>(threadIdx.x) < sp.head) one(threadIdx.x);
+    if (threadIdx.x >= 32 && static_cast<int>(threadIdx.x) - 32 < sp.tail) {
+      one(sp.head + 4 * sp.nv + static_cast<int>(threadIdx.x) - 32);
     }
+    for (int q = threadIdx.x; q < sp.nv; q += kThreads) {
+      const int e = sp.head + 4 * q;
+      const int64_t s = t.s0 + e;
+      const float4 w4 = *reinterpret_cast<const float4*>(wsrc + s);
+      const float4 u4 = __ldcs(reinterpret_cast<const float4*>(u + s));
+      const float4 n4 = make_float4(__fsub_rn(w4.x, __fmul_rn(step_scale, u4.x)),
+                                    __fsub_rn(w4.y, __fmul_rn(step_scale, u4.y)),
+                                    __fsub_rn(w4.z, __fmul_rn(step_scale, u4.z)),
+                                    __fsub_rn(w4.w, __fmul_rn(step_scale, u4.w)));
+      *reinterpret_cast<float4*>(wdst + s) = n4;
+      buf[off + e] = n4.x;
+      buf[off + e + 1] = n4.y;
+      buf[off + e + 2] = n4.z;
+      buf[off + e + 3] = n4.w;
+    }
+    // make the generic-proxy shared-memory writes visible to the bulk copies
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
-    if (update) {
-      mbar_wait(&full[k], static_cast<unsigned>((it / NB) & 1));
-      if (t.len > 0) {
-        const float step_scale = __fmul_rn(c.lr, trust[t.t]);
-        const float* __restrict__ ws = stage_w(k) + (t.s0 & 3);
-        const float* __restrict__ us = stage_u(k) + (t.s0 & 3);
-        float* __restrict__ ob = stage_o(k);
-        const int off = static_cast<int>(t.w0 & 3);
-        for (int e = threadIdx.x; e < t.len; e += kThreads) {
-          const float nw = __fsub_rn(ws[e], __fmul_rn(step_scale, us[e]));
-          wdst[t.s0 + e] = nw;
-          ob[off + e] = nw;
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncthreads();
-        const int64_t a0 = (t.w0 + 3) & ~static_cast<int64_t>(3);
-        const int64_t a1 = (t.w0 + t.len) & ~static_cast<int64_t>(3);
-        if (a1 > a0 && threadIdx.x == 0) {
-          for (int q = 0; q < N; ++q) {
-            const int j = (i + q) % N;
-            bulk_s2g(dst[j] + a0, ob + off + (a0 - t.w0), static_cast<uint32_t>(a1 - a0) * 4u);
-          }
-        }
-        const int nhead = static_cast<int>(a1 > a0 ? a0 - t.w0 : t.len);
-        const int ntail = static_cast<int>(a1 > a0 ? t.w0 + t.len - a1 : 0);
-        if (static_cast<int>(threadIdx.x) < nhead * N) {
-          const int e = threadIdx.x % nhead, j = threadIdx.x / nhead;
-          dst[j][t.w0 + e] = ob[off + e];
-        } else if (static_cast<int>(threadIdx.x) >= 128 && static_cast<int>(threadIdx.x) - 128 < ntail * N) {
-          const int q = static_cast<int>(threadIdx.x) - 128;
-          const int e = static_cast<int>(a1 - t.w0) + q % ntail, j = q / ntail;
-          dst[j][t.w0 + e] = ob[off + e];
-        }
+    // flat elements [w0, w0 + len): aligned middle [a0, a1) by bulk copy
+    a0 = (t.w0 + 3) & ~static_cast<int64_t>(3);
+    a1 = (t.w0 + t.len) & ~static_cast<int64_t>(3);
+    if (a1 > a0 && threadIdx.x == 0) {
+      // destinations in a per-tile rotated order, so the CTAs of all ranks
+      // spread their pushes over every peer's NVLink ingress at any moment
+      for (int k = 0; k < N; ++k) {
+        const int j = (i + k) % N;
+        bulk_s2g(dst[j] + a0, buf + off + (a0 - t.w0), static_cast<uint32_t>(a1 - a0) * 4u);
       }
-    }
-    if (threadIdx.x == 0) {
       asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-      pend[k] = t.t;
-      if (publish && it >= NB - 1) {
-        asm volatile("cp.async.bulk.wait_group %0;" ::"n"(NB - 1) : "memory");
-        push_tile_done(G, pend[(it - (NB - 1)) % NB]);
-      }
+    }
+    // edges (and tiles shorter than one aligned 16-byte group)
+    const int nhead = static_cast<int>(a1 > a0 ? a0 - t.w0 : t.len);
+    const int ntail = static_cast<int>(a1 > a0 ? t.w0 + t.len - a1 : 0);
+    if (static_cast<int>(threadIdx.x) < nhead * N) {
+      const int e = threadIdx.x % nhead, j = threadIdx.x / nhead;
+      dst[j][t.w0 + e] = buf[off + e];
+    } else if (static_cast<int>(threadIdx.x) >= 128 && static_cast<int>(threadIdx.x) - 128 < ntail * N) {
+      const int k = static_cast<int>(threadIdx.x) - 128;
+      const int e = static_cast<int>(a1 - t.w0) + k % ntail, j = k / ntail;
+      dst[j][t.w0 + e] = buf[off + e];
     }
   }
-  __syncthreads();  // the last tiles' edge stores
-  if (threadIdx.x == 0 && n_mine > 0) {
-    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-    const int first = publish ? (n_mine >= NB - 1 ? n_mine - (NB - 1) : 0) : 0;
-    for (int it = first; it < n_mine; ++it) push_tile_done(G, tiles[tile_of(it)].t);
+  // the shared-memory tile must outlive the copies (wait for their writes,
+  // not only their smem reads, so the group count below covers them)
+  __syncthreads();  // the edge stores
+  if (threadIdx.x == 0) {
+    if (a1 > a0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    push_tile_done(G, t.t);
   }
 }
 
@@ -1146,31 +966,6 @@ static void lamb_shard(bo_ctx* c, const G* g) {
 // the partials and flags (2T+1 doubles per rank, summed in rank order so all
 // ranks agree) -> trust ratios, found_inf, scaler -> phase 2 pushing the new
 // parameters into every rank's replica -> barrier.
-template <int NB>
-static void launch_push_pipe_nb(bo_ctx* c, const LambTile* tiles, int n, cudaStream_t st, const PushGroups& G,
-                                float* wsh_alt) {
-  const size_t smem = static_cast<size_t>(NB) * (2 * kStageIn + kStageOut) * sizeof(float);
-  static bool configured = false;  // per process: the attribute is per kernel
-  if (!configured) {
-    BO_CUDA(cudaFuncSetAttribute(k_shard_p2_push_pipe<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(smem)));
-    configured = true;
-  }
-  const int grid = std::min(n, c->push_ctas);
-  k_shard_p2_push_pipe<NB><<<grid, kThreads, smem, st>>>(tiles, n, c->wsh, c->u, c->state, c->lamb, c->trust,
-                                                         c->d_peer_w, c->world, G, wsh_alt);
-}
-
-static void launch_push_pipe(bo_ctx* c, const LambTile* tiles, int n, cudaStream_t st, const PushGroups& G,
-                             float* wsh_alt) {
-  if (n <= 0) return;
-  if (c->push_stages <= 2) {
-    launch_push_pipe_nb<2>(c, tiles, n, st, G, wsh_alt);
-  } else {
-    launch_push_pipe_nb<4>(c, tiles, n, st, G, wsh_alt);
-  }
-}
-
 template <typename W, bool kHop, bool kDbl>
 static void launch_p1w(bo_ctx* c, const PtrTable& tab, const W* in, const P1Args& A, int tile0, int n) {
   if (n <= 0) return;
@@ -1252,13 +1047,9 @@ static void lamb_grouped(bo_ctx* c, const PtrTable& tab, const W* in) {
       BO_CUDA(cudaStreamWaitEvent(ps, c->group_events[static_cast<size_t>(g)], 0));
     }
     if (lg.tile1 > lg.tile0) {
-      if (c->push_ctas > 0) {
-        launch_push_pipe(c, c->d_lamb_tiles + lg.tile0, lg.tile1 - lg.tile0, ps, none, c->wsh_alt);
-      } else {
-        k_shard_p2_push<1><<<lg.tile1 - lg.tile0, kThreads, 0, ps>>>(
-            c->d_lamb_tiles + lg.tile0, lg.tile1 - lg.tile0, c->wsh, c->u, c->state, c->lamb, c->trust,
-            c->d_peer_w, c->world, none, c->wsh_alt);
-      }
+      k_shard_p2_push<<<lg.tile1 - lg.tile0, kThreads, 0, ps>>>(
+          c->d_lamb_tiles + lg.tile0, lg.tile1 - lg.tile0, c->wsh, c->u, c->state, c->lamb, c->trust,
+          c->d_peer_w, c->world, none, c->wsh_alt);
       check_launch(c, "k_shard_p2_push");
     }
   }
@@ -1343,13 +1134,9 @@ static void lamb_sharded(bo_ctx* c, const PtrTable& tab, const W* in) {
   {
   StageTimer timer(c, BO_STAGE_LAMB_UPDATE);
   const PushGroups G{c->d_push_group_of_tensor, c->d_push_group_tiles, c->d_push_count, c->peer_ctrl, epoch};
-  if (c->push_ctas > 0 && c->push_ctas < c->n_push_tiles) {
-    launch_push_pipe(c, c->d_push_tiles, c->n_push_tiles, c->stream, G, nullptr);
-  } else {
-    k_shard_p2_push<1><<<c->n_push_tiles, kThreads, 0, c->stream>>>(c->d_push_tiles, c->n_push_tiles,
-                                                                    c->wsh, c->u, c->state, c->lamb,
-                                                                    c->trust, c->d_peer_w, c->world, G);
-  }
+  k_shard_p2_push<<<c->n_push_tiles, kThreads, 0, c->stream>>>(c->d_push_tiles, c->n_push_tiles, c->wsh, c->u,
+                                                                c->state, c->lamb, c->trust, c->d_peer_w,
+                                                                c->world, G);
   check_launch(c, "k_shard_p2_push");
   }
   // every rank's pushes into every replica have landed once all ranks are
