@@ -54,6 +54,7 @@ typedef enum {
   BO_ERR_PEER_DISCONNECTED = 7,      /* bertopt::PeerDisconnected */
   BO_ERR_WATCHDOG_TIMEOUT = 8,       /* bertopt::WatchdogTimeout */
   BO_ERR_PROTOCOL = 9,               /* bertopt::ProtocolError */
+  BO_ERR_IO_FAILURE = 10,            /* bertopt::IoFailure */
   BO_ERR_CUDA = 20,
   BO_ERR_NCCL = 21,
   BO_ERR_NO_DEVICE = 22
@@ -297,6 +298,20 @@ int64_t bo_launch_count(const bo_ctx* ctx);
 #define BO_PATH_RESIDENT 128         /* bo_train_step: the K micros read in the sync pass */
 #define BO_PATH_RING_PUSH 256        /* ring hops push their output into the right neighbour's buffer over NVLink */
 int32_t bo_path_flags(const bo_ctx* ctx);
+
+/* Event timeline in the reference's EventLog schema (trainer.cpp:43-71,
+ * events trainer.hpp:30-35): one JSON line per event,
+ *   {"ts":<seconds since bo_trace_enable>,"rank":<r>,"event":"<name>","bytes":<n>}
+ * with device timestamps (CUDA events on the stream that carries the work):
+ * micro_ready (a micro-batch's gradients entered the step; bytes: binary16
+ * gradient bytes), bucket_ready (bo_sync_ready: a communication group's
+ * gradients are final), comm_start / comm_end (the reduce-scatter, or one
+ * group of it; bytes: what this rank sends over NVLink), lamb_start,
+ * step_end. NVTX ranges name the stages for a timeline profiler while
+ * tracing is on. bo_trace_write syncs and writes the lines, oldest first
+ * (BO_ERR_IO_FAILURE if the file cannot be written). */
+bo_status bo_trace_enable(bo_ctx* ctx, int32_t enable);
+bo_status bo_trace_write(bo_ctx* ctx, const char* path);
 
 /* ---- operator-level drop-ins -------------------------------------------- */
 /* lamb_step (lamb.cpp:23-84) over device tensors; exact reference numerics

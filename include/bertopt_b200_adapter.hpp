@@ -44,6 +44,7 @@ namespace bertopt::b200 {
     case BO_ERR_PEER_DISCONNECTED: throw PeerDisconnected(msg);
     case BO_ERR_WATCHDOG_TIMEOUT: throw WatchdogTimeout(msg);
     case BO_ERR_PROTOCOL: throw ProtocolError(msg);
+    case BO_ERR_IO_FAILURE: throw IoFailure(msg);
     default: throw Error(std::string(bo_status_name(s)) + ": " + msg);
   }
 }

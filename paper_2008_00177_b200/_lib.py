@@ -88,6 +88,8 @@ SIGNATURES = {
     "bo_profile_read": (_i32, [_vp, C.POINTER(C.c_double), C.POINTER(_i64), _i32]),
     "bo_launch_count": (_i64, [_vp]),
     "bo_path_flags": (_i32, [_vp]),
+    "bo_trace_enable": (_i32, [_vp, _i32]),
+    "bo_trace_write": (_i32, [_vp, C.c_char_p]),
     "bo_lamb_step": (_i32, [_i32, C.POINTER(_i64), C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp),
                             C.POINTER(_vp), C.POINTER(_i64), C.POINTER(LambConfigC), _vp]),
     "bo_ring_allreduce_f32": (_i32, [_vp, _vp, _sz]),

@@ -9,6 +9,8 @@
 #include <cstdlib>
 #include <cstring>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "bo_internal.hpp"
 
 namespace bo {
@@ -41,18 +43,31 @@ static cudaEvent_t take_event(bo_ctx* c) {
   return e;
 }
 
+static const char* const kStageNames[BO_NUM_STAGES] = {"accumulate", "finalize", "reduce", "lamb_norms",
+                                                       "trust", "lamb_update", "allgather", "hop_kernels",
+                                                       "reserved"};
+
 StageTimer::StageTimer(bo_ctx* ctx, int s) : StageTimer(ctx, s, ctx->stream) {}
 
 StageTimer::StageTimer(bo_ctx* ctx, int s, cudaStream_t on) : c(ctx), stage(s), stream(on) {
+  if (c->tracing) nvtxRangePushA(kStageNames[s]);  // host-side issue range for a timeline profiler
   if (!c->profiling || !((c->profile_mask >> s) & 1)) return;
   b = take_event(c);
   BO_CUDA(cudaEventRecord(b, stream));
 }
 
 StageTimer::~StageTimer() {
+  if (c->tracing) nvtxRangePop();
   if (!c->profiling || !b) return;
   cudaEvent_t e = take_event(c);
   if (cudaEventRecord(e, stream) == cudaSuccess) c->marks.push_back({stage, b, e});
+}
+
+void trace(bo_ctx* c, const char* event, uint64_t bytes, cudaStream_t s) {
+  if (!c->tracing) return;
+  cudaEvent_t e = take_event(c);
+  BO_CUDA(cudaEventRecord(e, s));
+  c->trace_marks.push_back(bo_ctx::TraceMark{event, bytes, e});
 }
 
 static void drain_marks(bo_ctx* c) {
@@ -286,6 +301,7 @@ const char* bo_status_name(int32_t s) {
     case BO_ERR_PEER_DISCONNECTED: return "PeerDisconnected";
     case BO_ERR_WATCHDOG_TIMEOUT: return "WatchdogTimeout";
     case BO_ERR_PROTOCOL: return "ProtocolError";
+    case BO_ERR_IO_FAILURE: return "IoFailure";
     case BO_ERR_CUDA: return "CudaError";
     case BO_ERR_NCCL: return "NcclError";
     case BO_ERR_NO_DEVICE: return "NoDevice";
@@ -446,6 +462,8 @@ void bo_destroy(bo_ctx* c) {
     cudaEventDestroy(mk.b);
   }
   for (cudaEvent_t e : c->event_pool) cudaEventDestroy(e);
+  for (const auto& m : c->trace_marks) cudaEventDestroy(m.e);
+  if (c->trace_base) cudaEventDestroy(c->trace_base);
   if (c->comm_stream) cudaStreamSynchronize(c->comm_stream);
   if (c->comm_ready) cudaEventDestroy(c->comm_ready);
   if (c->comm_done) cudaEventDestroy(c->comm_done);
@@ -833,6 +851,50 @@ bo_status bo_param_ptr(bo_ctx* c, int32_t t, float** out) {
   BO_GUARD_BEGIN
   if (t < 0 || t >= c->L.T) fail(BO_ERR_SHAPE_MISMATCH, "tensor index out of range");
   *out = c->w + c->L.flat_off[static_cast<size_t>(t)];
+  BO_GUARD_END
+}
+
+bo_status bo_trace_enable(bo_ctx* c, int32_t enable) {
+  BO_GUARD_BEGIN
+  if (!c) fail(BO_ERR_INVALID_CONFIG, "null ctx");
+  BO_CUDA(cudaStreamSynchronize(c->stream));
+  for (const auto& m : c->trace_marks) c->event_pool.push_back(m.e);
+  c->trace_marks.clear();
+  c->tracing = enable != 0;
+  if (c->tracing) {
+    if (!c->trace_base) BO_CUDA(cudaEventCreate(&c->trace_base));
+    BO_CUDA(cudaEventRecord(c->trace_base, c->stream));
+  }
+  BO_GUARD_END
+}
+
+bo_status bo_trace_write(bo_ctx* c, const char* path) {
+  BO_GUARD_BEGIN
+  if (!c || !path) fail(BO_ERR_INVALID_CONFIG, "null argument");
+  if (!c->trace_base) fail(BO_ERR_PROTOCOL, "bo_trace_enable has not run");
+  BO_CUDA(cudaDeviceSynchronize());
+  struct Line {
+    double ts;
+    const char* ev;
+    uint64_t bytes;
+  };
+  std::vector<Line> lines;
+  for (const auto& m : c->trace_marks) {
+    float ms = 0.0f;
+    BO_CUDA(cudaEventElapsedTime(&ms, c->trace_base, m.e));
+    lines.push_back(Line{ms * 1e-3, m.event, m.bytes});
+  }
+  std::stable_sort(lines.begin(), lines.end(), [](const Line& a, const Line& b) { return a.ts < b.ts; });
+  FILE* f = std::fopen(path, "w");
+  if (!f) fail(BO_ERR_IO_FAILURE, std::string("cannot open ") + path);
+  bool ok = true;
+  for (const Line& l : lines) {
+    // the reference's line format (trainer.cpp:58-71)
+    ok &= std::fprintf(f, "{\"ts\":%.9f,\"rank\":%d,\"event\":\"%s\",\"bytes\":%llu}\n", l.ts, c->rank,
+                       l.ev, static_cast<unsigned long long>(l.bytes)) > 0;
+  }
+  ok &= std::fclose(f) == 0;
+  if (!ok) fail(BO_ERR_IO_FAILURE, std::string("write failed for ") + path);
   BO_GUARD_END
 }
 

@@ -375,6 +375,7 @@ void check(bo_ctx* c, const char* what) {
 }  // namespace
 
 void run_fused_single_rank(bo_ctx* c, const PtrTable& tab, MicroSrc ms) {
+  trace(c, "lamb_start", 0, c->stream);
   {
     StageTimer timer(c, BO_STAGE_LAMB_NORMS);
     if (ms.K > 0) {

@@ -348,6 +348,15 @@ struct bo_ctx {
   double stage_ms[BO_NUM_STAGES] = {};
   int64_t stage_count[BO_NUM_STAGES] = {};
   std::vector<bool> ptr_aligned_cache;
+  // tracing (bo_trace_enable): the reference's EventLog schema, device-timed
+  bool tracing = false;
+  cudaEvent_t trace_base = nullptr;
+  struct TraceMark {
+    const char* event;
+    uint64_t bytes;
+    cudaEvent_t e;
+  };
+  std::vector<TraceMark> trace_marks;
 };
 
 // Every C entry point: library failures become a bo_status plus the thread's
@@ -382,6 +391,9 @@ void run_reduce_group(bo_ctx* c, const PtrTable& tab, int b0, int b1, int acc0, 
                       cudaStream_t stream);
 void run_lamb(bo_ctx* c, const PtrTable& tab);
 void gather_shard(bo_ctx* c);
+// tracing: a device timestamp (an event on `s`) named like the reference's
+// EventLog events (trainer.hpp:30-35), no-op unless bo_trace_enable
+void trace(bo_ctx* c, const char* event, uint64_t bytes, cudaStream_t s);
 // lockstep world: rendezvous of the ranks' host threads (no-op otherwise)
 void lockstep_sync(bo_ctx* c, const char* where);
 // the caller's stream waits for tensor's parameter group of the last step

@@ -1152,6 +1152,7 @@ static void lamb_sharded(bo_ctx* c, const PtrTable& tab, const W* in) {
 }
 
 void run_lamb(bo_ctx* c, const PtrTable& tab) {
+  trace(c, "lamb_start", 0, c->stream);
   if (c->world == 1) {
     lamb_shard<float>(c, c->gshard);
   } else if (c->algo == BO_REDUCE_RING) {

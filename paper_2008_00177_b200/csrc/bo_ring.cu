@@ -333,9 +333,29 @@ static void nccl_reduce_scatter(bo_ctx* c, int b0, int b1, cudaStream_t st) {
   BO_NCCL(ncclGroupEnd());
 }
 
+// NVLink bytes this rank sends for buckets [b0, b1): (N-1) hops of one chunk each
+static uint64_t comm_bytes(const bo_ctx* c, int b0, int b1) {
+  const size_t e = c->algo == BO_REDUCE_RING && c->cfg.f16_exchange ? 2 : 4;
+  uint64_t n = 0;
+  for (int b = b0; b < b1; ++b) n += static_cast<uint64_t>(c->L.chunk[static_cast<size_t>(b)]);
+  return n * static_cast<uint64_t>(c->world - 1) * e;
+}
+
 void run_reduce(bo_ctx* c, const PtrTable& tab) {
   if (c->world == 1) return;
   StageTimer timer(c, BO_STAGE_REDUCE);
+  const uint64_t bytes = comm_bytes(c, 0, c->L.B);
+  trace(c, "comm_start", bytes, c->stream);
+  struct End {
+    bo_ctx* c;
+    uint64_t bytes;
+    ~End() {
+      try {
+        trace(c, "comm_end", bytes, c->stream);
+      } catch (...) {  // a failing event record must not escape a destructor
+      }
+    }
+  } end{c, bytes};
   c->ring_last_in = nullptr;
   c->ring_result = nullptr;
   if (c->algo == BO_REDUCE_NCCL) {
@@ -350,6 +370,19 @@ void run_reduce(bo_ctx* c, const PtrTable& tab) {
 void run_reduce_group(bo_ctx* c, const PtrTable& tab, int b0, int b1, int acc0, int acc1,
                       cudaStream_t stream) {
   StageTimer timer(c, BO_STAGE_REDUCE, stream);
+  const uint64_t bytes = comm_bytes(c, b0, b1);
+  trace(c, "comm_start", bytes, stream);
+  struct End {
+    bo_ctx* c;
+    uint64_t bytes;
+    cudaStream_t s;
+    ~End() {
+      try {
+        trace(c, "comm_end", bytes, s);
+      } catch (...) {
+      }
+    }
+  } end{c, bytes, stream};
   if (c->algo == BO_REDUCE_NCCL) {
     launch_finalize_tiles(c, c->d_group_acc_tiles + acc0, acc1 - acc0, tab, stream);
     nccl_reduce_scatter(c, b0, b1, stream);

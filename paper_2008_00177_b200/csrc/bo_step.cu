@@ -34,6 +34,7 @@ bo_status bo_accumulate(bo_ctx* c, int32_t micro, const uint16_t* const* grads) 
     fail(BO_ERR_PROTOCOL, "micro " + std::to_string(micro) + " out of order (expected " +
                               std::to_string(c->next_micro) + ")");
   }
+  trace(c, "micro_ready", static_cast<uint64_t>(c->L.P) * 2, c->stream);
   if (micro + 1 < K) {
     launch_accumulate(c, micro, tab, aligned);
     c->next_micro = micro + 1;
@@ -52,6 +53,7 @@ bo_status bo_accumulate(bo_ctx* c, int32_t micro, const uint16_t* const* grads) 
     run_reduce(c, tab);
     run_lamb(c, tab);  // world > 1: includes the fused parameter all-gather (IPC push)
   }
+  trace(c, "step_end", 0, c->stream);
   c->calls += 1;
   BO_GUARD_END
 }
@@ -97,6 +99,7 @@ bo_status bo_train_step(bo_ctx* c, const uint16_t* const* grads) {
   grow_bc_table(c, c->calls + 2);
   c->ms = MicroSrc{c->d_micro_tab, K, T};
   c->path = BO_PATH_RESIDENT;
+  for (int k = 0; k < K; ++k) trace(c, "micro_ready", static_cast<uint64_t>(c->L.P) * 2, c->stream);
   try {
     if (c->world == 1) {
       c->path |= BO_PATH_ONE_RANK_FUSED;
@@ -111,6 +114,7 @@ bo_status bo_train_step(bo_ctx* c, const uint16_t* const* grads) {
     throw;
   }
   c->ms = MicroSrc{nullptr, 0, 0};
+  trace(c, "step_end", 0, c->stream);
   c->calls += 1;
   BO_GUARD_END
 }
@@ -173,6 +177,11 @@ bo_status bo_sync_ready(bo_ctx* c, int32_t n, const int32_t* tensors, const uint
     }
     while (c->next_group < G && c->group_pending[static_cast<size_t>(c->next_group)] == 0) {
       const auto& g = c->comm_groups[static_cast<size_t>(c->next_group)];
+      if (c->tracing) {
+        int64_t n = 0;
+        for (int b = g.b0; b < g.b1; ++b) n += L.elems[static_cast<size_t>(b)];
+        trace(c, "bucket_ready", static_cast<uint64_t>(n) * 2, c->stream);
+      }
       run_reduce_group(c, *c->sync_tab, g.b0, g.b1, g.acc0, g.acc1, c->comm_stream);
       c->next_group += 1;
     }
@@ -197,6 +206,7 @@ bo_status bo_sync_ready(bo_ctx* c, int32_t n, const int32_t* tensors, const uint
     BO_CUDA(cudaStreamWaitEvent(c->stream, c->comm_done, 0));
     run_lamb(c, *c->sync_tab);
   }
+  trace(c, "step_end", 0, c->stream);
   c->calls += 1;
   BO_GUARD_END
 }

@@ -45,6 +45,10 @@ class ProtocolError(BertoptError):
     status = 9
 
 
+class IoFailure(BertoptError):
+    status = 10
+
+
 class CudaError(BertoptError):
     status = 20
 
@@ -59,8 +63,8 @@ class NoDevice(BertoptError):
 
 _BY_STATUS = {c.status: c for c in (ShapeMismatch, NonFiniteGradient, OverflowDetected,
                                      LengthMismatch, InvalidConfig, BucketLayoutMismatch,
-                                     PeerDisconnected, WatchdogTimeout, ProtocolError, CudaError,
-                                     NcclError, NoDevice)}
+                                     PeerDisconnected, WatchdogTimeout, ProtocolError, IoFailure,
+                                     CudaError, NcclError, NoDevice)}
 
 
 def from_status(status: int, msg: str) -> BertoptError:

@@ -296,6 +296,14 @@ class GradPipeline:
         f = int(self.lib.bo_path_flags(self.ctx))
         return [n for b, n in self.PATH_NAMES.items() if f & b]
 
+    def trace_enable(self, enable: bool = True) -> None:
+        """Record the step's event timeline (the reference's EventLog events,
+        device-timed) from now on; trace_write() dumps it as JSON lines."""
+        _lib.check(self.lib.bo_trace_enable(self.ctx, int(enable)))
+
+    def trace_write(self, path: str) -> None:
+        _lib.check(self.lib.bo_trace_write(self.ctx, path.encode()))
+
     def launch_count(self) -> int:
         return int(self.lib.bo_launch_count(self.ctx))
 
