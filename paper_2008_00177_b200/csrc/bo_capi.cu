@@ -379,6 +379,7 @@ bo_status bo_create(const bo_trainer_config* cfg, int32_t n_tensors, const int64
   // streamed one-rank LAMB (k_lamb_stream): 12 % less DRAM traffic than the
   // two passes but a slower step; an option (profiles/r02_notes.md)
   if (const char* e = std::getenv("BO_STREAM")) c->stream_lamb = std::strcmp(e, "0") != 0;
+
   if (const char* e = std::getenv("BO_RING_NCCL")) c->ring_via_nccl = std::strcmp(e, "0") != 0;
   if (const char* e = std::getenv("BO_RING_PUSH")) c->ring_push = std::strcmp(e, "0") != 0;
   if (const char* e = std::getenv("BO_RING_BARRIER")) c->nb_barrier = std::strcmp(e, "nccl") != 0;
@@ -389,6 +390,8 @@ bo_status bo_create(const bo_trainer_config* cfg, int32_t n_tensors, const int64
   c->algo = cfg->reduce_algo == BO_REDUCE_AUTO ? BO_REDUCE_RING : cfg->reduce_algo;
   BO_CUDA(cudaSetDevice(device));
   BO_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
+  c->p1r_prefetch = 4 * c->num_sms / 3;
+  if (const char* e = std::getenv("BO_P1R_PREFETCH")) c->p1r_prefetch = std::max(0, std::atoi(e));
   BO_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   c->own_stream = true;
   c->L = Layout::build(n_tensors, numels, first_consumers, cfg->bucket_bytes, world, rank);

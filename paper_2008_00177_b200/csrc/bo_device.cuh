@@ -240,6 +240,16 @@ __device__ __forceinline__ uint2 ld_h4(const uint16_t* p, int n, uint64_t pol) {
   for (int i = 0; i < n; ++i) h[i] = p[i];
   return make_uint2(h[0] | (h[1] << 16), h[2] | (h[3] << 16));
 }
+// Bulk L2 prefetch of the 16-byte aligned part of [p, p + bytes) (a hint:
+// no data moves into the SM; never touches memory outside the range).
+__device__ __forceinline__ void prefetch_l2(const void* p, uint64_t bytes) {
+  const uintptr_t lo = (reinterpret_cast<uintptr_t>(p) + 15) & ~static_cast<uintptr_t>(15);
+  const uintptr_t hi = (reinterpret_cast<uintptr_t>(p) + bytes) & ~static_cast<uintptr_t>(15);
+  if (hi > lo) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lo), "r"(static_cast<uint32_t>(hi - lo))
+                 : "memory");
+  }
+}
 __device__ __forceinline__ void st4(float* p, float4 v, uint64_t pol) {
   asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "f"(v.x),
                "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol));

@@ -56,7 +56,7 @@ __global__ void __launch_bounds__(kP1Threads, 2) k_lamb_p1(
     const FusedTile* __restrict__ tiles, const __grid_constant__ PtrTable tab,
     const float* __restrict__ acc, const float* __restrict__ w, float* m0, float* v0, float* m1,
     float* v1, float* __restrict__ u, DevState* __restrict__ st, LambConsts c,
-    const double* __restrict__ bc_table, int K, double* __restrict__ tile_part) {
+    const double* __restrict__ bc_table, int K, double* __restrict__ tile_part, int pref) {
   if (st->local_flag) return;  // an earlier micro overflowed: the step is skipped
   // double-buffered moments: read the current set, write the other one; the
   // epilogue makes it current only if the step's overflow flag stays clear
@@ -84,6 +84,18 @@ __global__ void __launch_bounds__(kP1Threads, 2) k_lamb_p1(
       wv[j] = ld4(w + a, pl);
       mv[j] = ld4(m + a, pf);
       vv[j] = ld4(v + a, pf);
+    }
+  }
+  // bulk L2 prefetch of the tile `pref` CTAs ahead (as k_lamb_p1r)
+  if (pref > 0 && threadIdx.x < 5 && blockIdx.x + pref < gridDim.x) {
+    const FusedTile nt = tiles[blockIdx.x + pref];
+    if (threadIdx.x == 0) {
+      prefetch_l2(tab.p[nt.t] + nt.e0, 2ull * nt.len);
+    } else if (threadIdx.x == 1) {
+      if (K > 1) prefetch_l2(acc + nt.a0, 4ull * nt.len);
+    } else {
+      const int which = threadIdx.x - 2;
+      prefetch_l2((which == 0 ? w : which == 1 ? m : v) + nt.a0, 4ull * nt.len);
     }
   }
   double wn = 0.0, un = 0.0;
@@ -280,7 +292,7 @@ template <int K>
 __global__ void __launch_bounds__(kP1Threads, 2) k_lamb_p1r(
     const FusedTile* __restrict__ tiles, MicroSrc ms, const float* __restrict__ w, float* m0,
     float* v0, float* m1, float* v1, float* __restrict__ u, DevState* __restrict__ st, LambConsts c,
-    const double* __restrict__ bc_table, double* __restrict__ tile_part) {
+    const double* __restrict__ bc_table, double* __restrict__ tile_part, int pref) {
   const FusedTile t = tiles[blockIdx.x];
   __shared__ const uint16_t* sp[K];
   __shared__ double red[2][kP1Threads / 32];
@@ -307,6 +319,20 @@ __global__ void __launch_bounds__(kP1Threads, 2) k_lamb_p1r(
       wv[j] = ld4(w + a, pl);
       mv[j] = ld4(m + a, pf);
       vv[j] = ld4(v + a, pf);
+    }
+  }
+  // Bulk L2 prefetch of the inputs of the tile `pref` CTAs ahead (one bulk
+  // request per array, issued by K + 3 threads): with two 512-thread CTAs
+  // per SM holding their loads in registers, the DRAM otherwise idles while
+  // both compute; the prefetched tile's loads then hit L2. BERT-large K = 4:
+  // 1.79 -> 1.65 ms at a distance of 4/3 x the SM count (profiles/r02_notes.md).
+  if (pref > 0 && threadIdx.x < K + 3 && blockIdx.x + pref < gridDim.x) {
+    const FusedTile nt = tiles[blockIdx.x + pref];
+    if (static_cast<int>(threadIdx.x) < K) {
+      prefetch_l2(ms.hk[threadIdx.x * ms.T + nt.t] + nt.e0, 2ull * nt.len);
+    } else {
+      const int which = threadIdx.x - K;
+      prefetch_l2((which == 0 ? w : which == 1 ? m : v) + nt.a0, 4ull * nt.len);
     }
   }
   double wn = 0.0, un = 0.0;
@@ -710,7 +736,7 @@ void run_fused_single_rank(bo_ctx* c, const PtrTable& tab, MicroSrc ms) {
       auto launch = [&](auto kern) {
         kern<<<c->n_fused_tiles, kP1Threads, 0, c->stream>>>(c->d_fused_tiles, ms, c->w, c->m, c->v, c->m_alt,
                                                              c->v_alt, c->u, c->state, c->lamb, c->bc_table,
-                                                             c->tile_part);
+                                                             c->tile_part, c->p1r_prefetch);
       };
       switch (ms.K) {
         case 2: launch(k_lamb_p1r<2>); break;
@@ -725,7 +751,7 @@ void run_fused_single_rank(bo_ctx* c, const PtrTable& tab, MicroSrc ms) {
     } else {
       k_lamb_p1<<<c->n_fused_tiles, kP1Threads, 0, c->stream>>>(
           c->d_fused_tiles, tab, c->acc, c->w, c->m, c->v, c->m_alt, c->v_alt, c->u, c->state, c->lamb,
-          c->bc_table, c->cfg.accumulation, c->tile_part);
+          c->bc_table, c->cfg.accumulation, c->tile_part, c->p1r_prefetch);
       check(c, "k_lamb_p1");
     }
   }

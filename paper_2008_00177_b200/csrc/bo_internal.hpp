@@ -272,6 +272,10 @@ struct bo_ctx {
   // tensor runs in the same launch as phase 1, a lag behind it, reading w and
   // u back from L2; the pre-update weights go to `undo` so a step whose
   // overflow flag is raised later in the pass can be rolled back
+  // k_lamb_p1r / k_lamb_p1: bulk L2 prefetch of the tile this many CTAs
+  // ahead (BO_P1R_PREFETCH, 0 = off; default 4/3 x the SM count, measured
+  // best: profiles/r02_notes.md)
+  int p1r_prefetch = 0;
   bool stream_lamb = false;             // BO_STREAM=1 (measured slower, profiles/r02_notes.md)
   int4* d_stream_items = nullptr;
   int n_stream_items = 0;
