@@ -46,7 +46,7 @@ BYTES_LAMB_FUSED = (2 + 4 + 3 * 4 + 3 * 4) + (2 * 4 + 4)
 
 # index = BO_STAGE_* in include/bertopt_b200.h
 STAGES = ["accumulate", "finalize", "reduce", "lamb_norms", "trust", "lamb_update", "allgather",
-          "hop_kernels", "lamb_stream"]
+          "hop_kernels", "reserved"]
 
 MODELS = {"bert-large": "BERT_LARGE", "bert-large-128": "BERT_LARGE_PHASE1", "bert-base": "BERT_BASE",
           "bert-tiny": "BERT_TINY"}
@@ -392,11 +392,6 @@ def main_b200(args):
         # read; w written)
         "lamb_norms": ((xb + 24) if world == 1 else ((xb if fused_last else E) + 24)) * S_shard,
         "lamb_update": 12 * S_shard,
-        # one rank, bo_train_step, streamed LAMB (k_lamb_stream): phase 1,
-        # trust ratios and phase 2 in one launch; algorithmic bytes = the
-        # resident step's floor, the K micros, w, m, v read and w, m, v
-        # written (its DRAM traffic adds the undo copy of w: 4 B/param)
-        "lamb_stream": (xb + 24) * S_shard,
         # one ring hop kernel (nested in "reduce"): the gradient source of one
         # chunk of every bucket, wire in and out
         "hop_kernels": (xb + 2 * E) * S_shard,
@@ -471,7 +466,7 @@ def main_b200(args):
     kernel_names = {"accumulate": "k_accumulate", "finalize": "k_finalize",
                     "lamb_norms": ("k_lamb_p1r" if resident else "k_lamb_p1") if world == 1 else "k_p1w",
                     "lamb_update": "k_lamb_p2" if world == 1 else "k_shard_p2_push",
-                    "hop_kernels": "k_hopx", "lamb_stream": "k_lamb_stream"}
+                    "hop_kernels": "k_hopx"}
     if st_dom.get("nvlink_frac", 0.0) > st_dom["frac"]:
         # the parameter push / ring hops at world > 1: NVLink is the bound
         roofline = {"kernel": kernel_names[dom], "bound": "nvlink", "achieved": st_dom["nvlink_GB/s"],

@@ -280,7 +280,7 @@ int32_t bo_param_group(const bo_ctx* ctx, int32_t tensor);
 #define BO_STAGE_LAMB_UPDATE 5  /* LAMB phase 2 (world > 1: + parameter push to all replicas) */
 #define BO_STAGE_ALLGATHER 6    /* world > 1: replica-completion barrier */
 #define BO_STAGE_FLAG 7         /* ring hop kernels alone (nested inside REDUCE) */
-#define BO_STAGE_LAMB_STREAM 8  /* one rank: k_lamb_stream (phase 1 + trust + phase 2 in one launch) */
+#define BO_STAGE_LAMB_FUSED 8   /* reserved */
 #define BO_NUM_STAGES 9
 bo_status bo_profile_enable(bo_ctx* ctx, int32_t enable);
 /* Total milliseconds and event count per stage since the last reset; syncs. */
@@ -297,7 +297,6 @@ int64_t bo_launch_count(const bo_ctx* ctx);
 #define BO_PATH_OVERLAP 64           /* sync micro delivered through bo_sync_ready */
 #define BO_PATH_RESIDENT 128         /* bo_train_step: the K micros read in the sync pass */
 #define BO_PATH_RING_PUSH 256        /* ring hops push their output into the right neighbour's buffer over NVLink */
-#define BO_PATH_ONE_RANK_STREAM 512  /* one rank, resident micros: phase 1 and 2 in one streamed launch (k_lamb_stream) */
 int32_t bo_path_flags(const bo_ctx* ctx);
 
 /* Event timeline in the reference's EventLog schema (trainer.cpp:43-71,

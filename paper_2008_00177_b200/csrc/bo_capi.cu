@@ -45,7 +45,7 @@ static cudaEvent_t take_event(bo_ctx* c) {
 
 static const char* const kStageNames[BO_NUM_STAGES] = {"accumulate", "finalize", "reduce", "lamb_norms",
                                                        "trust", "lamb_update", "allgather", "hop_kernels",
-                                                       "lamb_stream"};
+                                                       "reserved"};
 
 StageTimer::StageTimer(bo_ctx* ctx, int s) : StageTimer(ctx, s, ctx->stream) {}
 
@@ -376,9 +376,6 @@ bo_status bo_create(const bo_trainer_config* cfg, int32_t n_tensors, const int64
   c->rank = rank;
   c->world = world;
   if (const char* e = std::getenv("BO_UNFUSED")) c->force_unfused = std::strcmp(e, "0") != 0;
-  // streamed one-rank LAMB (k_lamb_stream): 12 % less DRAM traffic than the
-  // two passes but a slower step; an option (profiles/r02_notes.md)
-  if (const char* e = std::getenv("BO_STREAM")) c->stream_lamb = std::strcmp(e, "0") != 0;
 
   if (const char* e = std::getenv("BO_RING_NCCL")) c->ring_via_nccl = std::strcmp(e, "0") != 0;
   if (const char* e = std::getenv("BO_RING_PUSH")) c->ring_push = std::strcmp(e, "0") != 0;

@@ -16,10 +16,6 @@
 //                 g = micro sum * inv, no accumulator               2K + 24 B/elem
 //   k_fused_epilogue  step counters, the moment-buffer flip and the
 //                 loss-scaler state machine
-//   k_lamb_stream (option BO_STREAM=1) phase 1, trust ratios and phase 2 of
-//                 the resident-micro step in one launch, phase 2 re-reading
-//                 w and u from L2: 12 % less DRAM traffic, slower step
-//                 (profiles/r02_notes.md)
 //
 // Every per-tensor array (acc, w, m, v, u) uses the aligned tensor layout, so
 // a tile index a0 serves all of them and every access is a 16-byte vector.
@@ -28,9 +24,6 @@
 // grid-wide rendezvous and streamed at 2.2-3.3 TB/s; two plain passes with no
 // inter-CTA waiting stream faster.
 #include <cuda_fp16.h>
-
-#include <algorithm>
-#include <cstdlib>
 
 #include "bo_device.cuh"
 #include "bo_internal.hpp"
@@ -167,119 +160,6 @@ __global__ void __launch_bounds__(kP1Threads, 2) k_lamb_p1(
     }
     tile_part[2 * blockIdx.x] = A;
     tile_part[2 * blockIdx.x + 1] = B;
-  }
-}
-
-// Phase 1 of one tile of the streamed form (k_lamb_stream): the arithmetic
-// of k_lamb_p1r below (kept as its own kernel: the two-pass kernel's measured
-// code generation), with w loaded and u stored under the L2 policies pw / pu.
-// The tile's fp64 partials of ||w||^2, ||u||^2 go to tile_part[2*ti]. Ends
-// with a __syncthreads (inside raise_flag) before the partials' reduction;
-// thread 0 stores the partials. 2K + 24 B/elem.
-template <int K>
-__device__ __forceinline__ void p1r_tile(const FusedTile& t, int ti, const MicroSrc& ms,
-                                         const float* __restrict__ w, float* m0, float* v0, float* m1,
-                                         float* v1, float* __restrict__ u, DevState* __restrict__ st,
-                                         const LambConsts& c, const double* __restrict__ bc_table,
-                                         double* __restrict__ tile_part, uint64_t pw, uint64_t pu,
-                                         const uint16_t** sp, double (*red)[kP1Threads / 32]) {
-  if (threadIdx.x < K) sp[threadIdx.x] = ms.hk[threadIdx.x * ms.T + t.t] + t.e0;
-  const int par = st->parity;
-  const float* __restrict__ m = par ? m1 : m0;
-  const float* __restrict__ v = par ? v1 : v0;
-  float* __restrict__ mn = par ? m0 : m1;
-  float* __restrict__ vn = par ? v0 : v1;
-  const double* bcp = bc_table + 4 * st->lamb_step;
-  const double ibc1 = bcp[2], ibc2 = bcp[3];
-  const float inv = __fdiv_rn(1.0f, __fmul_rn(static_cast<float>(K), st->scale));
-  const uint64_t pf = policy_evict_first();
-  __syncthreads();
-  float4 wv[2], mv[2], vv[2];
-  uint2 hv[2][K];
-#pragma unroll
-  for (int j = 0; j < 2; ++j) {
-    const int e0 = 4 * (threadIdx.x + j * kP1Threads);
-    if (e0 < t.len) {
-      const int64_t a = t.a0 + e0;
-#pragma unroll
-      for (int k = 0; k < K; ++k) hv[j][k] = ld_h4(sp[k] + e0, t.len - e0, pf);
-      wv[j] = ld4(w + a, pw);
-      mv[j] = ld4(m + a, pf);
-      vv[j] = ld4(v + a, pf);
-    }
-  }
-  double wn = 0.0, un = 0.0;
-  bool bad = false;
-#pragma unroll
-  for (int j = 0; j < 2; ++j) {
-    const int e0 = 4 * (threadIdx.x + j * kP1Threads);
-    if (e0 >= t.len) continue;
-    const int n = min(4, t.len - e0);  // < 4 only in a tensor's last float4
-    // live + (((0 + g0) + g1) + ... + g_{K-2}) (trainer.cpp:240-244, 196-201)
-    float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f}, xs[4];
-#pragma unroll
-    for (int k = 0; k + 1 < K; ++k) {
-      float f[4];
-      widen4(hv[j][k], f);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) acc[i] = __fadd_rn(acc[i], f[i]);
-    }
-    widen4(hv[j][K - 1], xs);
-    float ga[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      xs[i] = __fadd_rn(xs[i], acc[i]);
-      ga[i] = __fmul_rn(xs[i], inv);
-      // a non-finite input makes the fp32 sum non-finite (K finite binary16
-      // values cannot overflow fp32): the step's overflow check
-      if (i < n) bad |= !finite(xs[i]);
-    }
-    const float wa[4] = {wv[j].x, wv[j].y, wv[j].z, wv[j].w};
-    const float ma[4] = {mv[j].x, mv[j].y, mv[j].z, mv[j].w};
-    const float va[4] = {vv[j].x, vv[j].y, vv[j].z, vv[j].w};
-    const Lamb4 o = lamb_elem4(ga, wa, ma, va, c, bcp, ibc1, ibc2);
-    float4 mo = make_float4(o.m[0], o.m[1], o.m[2], o.m[3]);
-    float4 vo = make_float4(o.v[0], o.v[1], o.v[2], o.v[3]);
-    float4 uo = make_float4(o.u[0], o.u[1], o.u[2], o.u[3]);
-    if (n == 4) {
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        wn = __dadd_rn(wn, __dmul_rn(static_cast<double>(wa[i]), static_cast<double>(wa[i])));
-        un = __dadd_rn(un, __dmul_rn(static_cast<double>(o.u[i]), static_cast<double>(o.u[i])));
-      }
-    } else {
-      for (int i = n; i < 4; ++i) {  // padding lanes keep their old m/v bits
-        put(mo, i, ma[i]);
-        put(vo, i, va[i]);
-        put(uo, i, 0.0f);
-      }
-      for (int i = 0; i < n; ++i) {
-        wn = __dadd_rn(wn, __dmul_rn(static_cast<double>(wa[i]), static_cast<double>(wa[i])));
-        un = __dadd_rn(un, __dmul_rn(static_cast<double>(o.u[i]), static_cast<double>(o.u[i])));
-      }
-    }
-    const int64_t a = t.a0 + e0;
-    st4(mn + a, mo, pf);
-    st4(vn + a, vo, pf);
-    st4(u + a, uo, pu);
-  }
-  raise_flag(bad, st);
-  wn = warp_sum(wn);
-  un = warp_sum(un);
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  if (lane == 0) {
-    red[0][wid] = wn;
-    red[1][wid] = un;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double A = 0.0, B = 0.0;
-    for (int i = 0; i < kP1Threads / 32; ++i) {
-      A += red[0][i];
-      B += red[1][i];
-    }
-    tile_part[2 * ti] = A;
-    tile_part[2 * ti + 1] = B;
   }
 }
 
@@ -526,160 +406,6 @@ __device__ __forceinline__ void step_epilogue(DevState* st, const ScalerConsts& 
 
 __global__ void k_fused_epilogue(DevState* st, ScalerConsts sc) { step_epilogue(st, sc); }
 
-// Streamed single-rank LAMB with the K micro-batches resident (bo_train_step):
-// phase 1, the trust ratios and phase 2 in ONE launch, so the w and u that
-// phase 2 re-reads come from L2 instead of HBM.
-//
-// CTA b runs work item items[b] = (phase-1 tile, up to three phase-2 tiles),
-// any may be absent (-1):
-//   phase 1 (p1r_tile); the CTA that finishes a tensor's last phase-1 tile
-//     (per-tensor counter) computes its trust ratio in the same fixed order as
-//     k_lamb_trust and publishes it (release, launch epoch);
-//   phase 2 of an EARLIER tile: waits (acquire) for its tensor's trust ratio,
-//     saves the pre-update weights to `undo`, w -= (lr*r)*u, drops u's L2
-//     lines (never written back).
-// The host schedule (bo_tables.cu) hands a tensor's phase-2 tiles to the items
-// that start a lag of phase-1 tiles after its last phase-1 tile: by then that
-// tile has finished (the wait is rare and short), and the tensor's w and u —
-// loaded / stored evict_last — are still in L2. Pairing one phase-2 tile with
-// each phase-1 tile halves the CTAs (each CTA's prologue and flag traffic is
-// latency the slot does not stream through). A phase-2 part only ever waits
-// for phase-1 parts of lower-numbered CTAs, which the hardware dispatches
-// first; the wait is bounded anyway (abandon the step rather than hang).
-// Tensors too large for the L2 window stream (evict_first) with their phase
-// 2 at the end.
-//
-// Phase 2 runs before the step's overflow flag is final (a later tile may
-// raise it), so it writes the pre-update weights to `undo` (4 B/elem);
-// k_stream_restore copies them back on a skipped step, before the epilogue.
-// The moments are double-buffered as in the two-pass form. DRAM bytes per
-// element: 2K + 12 (micros, w, m, v read) + 8 (m', v') + 8 (w, undo) = 2K + 28
-// (36 at K = 4; the two-pass form moves 2K + 36), algorithmic 2K + 24.
-template <int K>
-__global__ void __launch_bounds__(kP1Threads, 2) k_lamb_stream(
-    const int4* __restrict__ items, const FusedTile* __restrict__ tiles,
-    const int* __restrict__ tensor_tiles, MicroSrc ms, float* __restrict__ w, float* m0, float* v0,
-    float* m1, float* v1, float* __restrict__ u, float* __restrict__ undo, DevState* __restrict__ st,
-    LambConsts c, const double* __restrict__ bc_table, double* __restrict__ tile_part,
-    float* __restrict__ trust, StreamSync* __restrict__ sy) {
-  __shared__ const uint16_t* sp[K];
-  __shared__ double red[2][kP1Threads / 32];
-  __shared__ int s_last;
-  const int4 item = items[blockIdx.x];
-  const unsigned epoch = __ldcg(&sy->epoch) + 1u;
-  if (item.x >= 0) {
-    const int ti = item.x & 0x3FFFFFFF;
-    const FusedTile t = tiles[ti];
-    const uint64_t pw = (item.x >> 30) == kStreamP1Window ? policy_evict_last() : policy_evict_first();
-    p1r_tile<K>(t, ti, ms, w, m0, v0, m1, v1, u, st, c, bc_table, tile_part, pw, pw, sp, red);
-    // the CTA that completes tensor t's phase 1 publishes its trust ratio
-    if (threadIdx.x == 0) {
-      __threadfence();
-      const unsigned nt = static_cast<unsigned>(tensor_tiles[t.t + 1] - tensor_tiles[t.t]);
-      const unsigned o = atomicAdd(&sy->tensor_done[t.t], 1u);
-      s_last = o == nt - 1;
-      if (s_last) sy->tensor_done[t.t] = 0;
-    }
-    __syncthreads();
-    if (s_last) {
-      __threadfence();
-      const float r = trust_ratio(tensor_tiles, tile_part, t.t, c.clip, red[0], red[1]);
-      if (threadIdx.x == 0) {
-        trust[t.t] = r;
-        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&sy->ready[t.t]), "r"(epoch) : "memory");
-      }
-    }
-  }
-  // phase 2 of up to three earlier tiles (the schedule gives an item more
-  // than one while the phase-2 queue is long, so phase 2 catches up with
-  // phase 1 and the distance in L2 traffic between a tile's two visits
-  // shrinks)
-  const int q[3] = {item.y, item.z, item.w};
-  if (q[0] >= 0) {
-    __shared__ float s_r[3];
-    if (threadIdx.x == 0) {
-      for (int k = 0; k < 3 && q[k] >= 0; ++k) {
-        const int tt = tiles[q[k]].t;
-        unsigned v;
-        uint64_t t0 = 0;
-        for (;;) {
-          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(&sy->ready[tt]) : "memory");
-          if (v == epoch) break;
-          const uint64_t now = global_ns();
-          if (t0 == 0) {
-            t0 = now;
-          } else if (now - t0 > 2000000000ull || *reinterpret_cast<volatile int32_t*>(&st->peer_timeout)) {
-            atomicOr(&st->local_flag, 1);  // skipped and reported, never a hang
-            st->peer_timeout = 1;
-            break;
-          }
-          __nanosleep(32);
-        }
-        s_r[k] = __ldcg(trust + tt);
-      }
-    }
-    __syncthreads();
-    const uint64_t pf = policy_evict_first();
-#pragma unroll 1
-    for (int k = 0; k < 3 && q[k] >= 0; ++k) {
-      const FusedTile t = tiles[q[k]];
-      const float step_scale = __fmul_rn(c.lr, s_r[k]);
-      float4 wv[2], uv[2];
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const int e0 = 4 * (threadIdx.x + j * kP1Threads);
-        if (e0 < t.len) {
-          wv[j] = ld4(w + t.a0 + e0, pf);
-          uv[j] = ld4(u + t.a0 + e0, pf);
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const int e0 = 4 * (threadIdx.x + j * kP1Threads);
-        if (e0 >= t.len) continue;
-        const int n = min(4, t.len - e0);
-        float4 o = wv[j];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          if (i < n) put(o, i, __fsub_rn(at(wv[j], i), __fmul_rn(step_scale, at(uv[j], i))));
-        }
-        st4(undo + t.a0 + e0, wv[j], pf);
-        st4(w + t.a0 + e0, o, pf);
-      }
-    }
-    // the u scratch of these tiles is dead: drop its L2 lines without write-back
-    __syncthreads();
-    for (int k = 0; k < 3 && q[k] >= 0; ++k) {
-      const FusedTile t = tiles[q[k]];
-      const int nlines = (t.len * 4 + 127) / 128;
-      if (threadIdx.x < nlines) {
-        asm volatile("discard.global.L2 [%0], 128;" ::"l"(u + t.a0 + 32 * threadIdx.x) : "memory");
-      }
-    }
-  }
-}
-
-// After k_lamb_stream. A skipped step (the overflow flag raised anywhere in
-// the pass): put the pre-update weights back (grid-stride over the tiles).
-__global__ void __launch_bounds__(kThreads) k_stream_restore(const FusedTile* __restrict__ tiles, int n_tiles,
-                                                             float* __restrict__ w,
-                                                             const float* __restrict__ undo,
-                                                             const DevState* __restrict__ st) {
-  if (!st->local_flag) return;
-  for (int i = blockIdx.x; i < n_tiles; i += gridDim.x) {
-    const FusedTile t = tiles[i];
-    for (int e0 = 4 * threadIdx.x; e0 < t.len; e0 += 4 * kThreads) {
-      *reinterpret_cast<float4*>(w + t.a0 + e0) = *reinterpret_cast<const float4*>(undo + t.a0 + e0);
-    }
-  }
-}
-
-// Step bookkeeping after k_stream_restore, and the launch epoch.
-__global__ void k_stream_epilogue(DevState* st, ScalerConsts sc, StreamSync* sy) {
-  step_epilogue(st, sc);
-  sy->epoch += 1u;
-}
-
 void check(bo_ctx* c, const char* what) {
   c->launches += 1;
   const cudaError_t e = cudaGetLastError();
@@ -690,46 +416,6 @@ void check(bo_ctx* c, const char* what) {
 
 void run_fused_single_rank(bo_ctx* c, const PtrTable& tab, MicroSrc ms) {
   trace(c, "lamb_start", 0, c->stream);
-  if (ms.K > 0 && c->stream_lamb && c->n_stream_items > 0) {
-    if (!c->undo) {
-      c->undo = static_cast<float*>(dev_alloc(c, static_cast<size_t>(c->L.acc_total) * 4));
-      c->d_stream_sync = static_cast<StreamSync*>(dev_alloc(c, sizeof(StreamSync)));
-      BO_CUDA(cudaMemsetAsync(c->d_stream_sync, 0, sizeof(StreamSync), c->stream));
-      if (const char* e = std::getenv("BO_STREAM_PERSIST")) {
-        // experiment: an L2 set-aside for evict_last lines (device-wide limit)
-        int mx = 0;
-        BO_CUDA(cudaDeviceGetAttribute(&mx, cudaDevAttrMaxPersistingL2CacheSize, c->device));
-        const size_t want = std::min<size_t>(static_cast<size_t>(mx), static_cast<size_t>(std::atoll(e)) << 20);
-        BO_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want));
-      }
-    }
-    c->path |= BO_PATH_ONE_RANK_STREAM;
-    {
-      StageTimer timer(c, BO_STAGE_LAMB_STREAM);
-      auto launch = [&](auto kern) {
-        kern<<<c->n_stream_items, kP1Threads, 0, c->stream>>>(
-            c->d_stream_items, c->d_fused_tiles, c->d_fused_tensor_tiles, ms, c->w, c->m, c->v, c->m_alt,
-            c->v_alt, c->u, c->undo, c->state, c->lamb, c->bc_table, c->tile_part, c->trust, c->d_stream_sync);
-      };
-      switch (ms.K) {
-        case 2: launch(k_lamb_stream<2>); break;
-        case 3: launch(k_lamb_stream<3>); break;
-        case 4: launch(k_lamb_stream<4>); break;
-        case 5: launch(k_lamb_stream<5>); break;
-        case 6: launch(k_lamb_stream<6>); break;
-        case 7: launch(k_lamb_stream<7>); break;
-        default: launch(k_lamb_stream<8>); break;
-      }
-      check(c, "k_lamb_stream");
-    }
-    StageTimer timer(c, BO_STAGE_TRUST);
-    k_stream_restore<<<4 * c->num_sms, kThreads, 0, c->stream>>>(c->d_fused_tiles, c->n_fused_tiles, c->w, c->undo,
-                                                                 c->state);
-    check(c, "k_stream_restore");
-    k_stream_epilogue<<<1, 1, 0, c->stream>>>(c->state, c->scaler, c->d_stream_sync);
-    check(c, "k_stream_epilogue");
-    return;
-  }
   {
     StageTimer timer(c, BO_STAGE_LAMB_NORMS);
     if (ms.K > 0) {

@@ -117,23 +117,6 @@ struct FusedTile {
   int32_t t;
 };
 
-// Single-rank streamed LAMB (bo_fused.cu k_lamb_stream): CTA b runs the work
-// item (phase-1 tile, up to 3 phase-2 tiles) of a host-built schedule; -1 =
-// none. The
-// phase-1 entry carries its kind in bits 30-31.
-constexpr int kStreamP1Window = 0;   // phase 1, w and u kept in L2 for phase 2
-constexpr int kStreamP1Stream = 1;   // phase 1 of a tensor too large for the L2 window
-// Cross-CTA state of k_lamb_stream (device memory, zeroed once): per-tensor
-// phase-1 counters, returned to zero by the CTA that completes the tensor,
-// and the epoch at which each tensor's trust ratio was published (the epoch
-// counts launches, so no per-step reset is needed).
-struct StreamSync {
-  unsigned epoch;
-  unsigned pad[3];
-  unsigned tensor_done[kMaxTensors];
-  unsigned ready[kMaxTensors];
-};
-
 // Per-tensor constants used by the accumulate / finalize kernels.
 struct TensorDev {
   int64_t acc_off;
@@ -268,19 +251,10 @@ struct bo_ctx {
   int n_fused_tiles = 0;
   int* d_fused_tensor_tiles = nullptr;  // [T+1] fused-tile ranges per tensor
   float* u = nullptr;                   // LAMB update scratch
-  // streamed single-rank LAMB (bo_train_step, world 1): phase 2 of each
-  // tensor runs in the same launch as phase 1, a lag behind it, reading w and
-  // u back from L2; the pre-update weights go to `undo` so a step whose
-  // overflow flag is raised later in the pass can be rolled back
   // k_lamb_p1r / k_lamb_p1: bulk L2 prefetch of the tile this many CTAs
   // ahead (BO_P1R_PREFETCH, 0 = off; default 4/3 x the SM count, measured
   // best: profiles/r02_notes.md)
   int p1r_prefetch = 0;
-  bool stream_lamb = false;             // BO_STREAM=1 (measured slower, profiles/r02_notes.md)
-  int4* d_stream_items = nullptr;
-  int n_stream_items = 0;
-  bo::StreamSync* d_stream_sync = nullptr;
-  float* undo = nullptr;
   bool force_unfused = false;           // BO_UNFUSED=1: unfused kernels (one rank: multi-kernel LAMB; ring: staged last hop)
 
   // device buffers

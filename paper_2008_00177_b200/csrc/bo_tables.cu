@@ -72,80 +72,6 @@ void upload_tables(bo_ctx* c) {
       }
     }
     ttiles[static_cast<size_t>(L.T)] = static_cast<int>(ft.size());
-    if (c->stream_lamb) {
-      // Work items of k_lamb_stream (bo_fused.cu), one per CTA in launch
-      // order: (phase-1 tile, phase-2 tile). Phase 1 runs over the tensors in
-      // model order — first those larger than `window` elements (BERT's word
-      // embedding: 250 MB of w + u, streamed evict_first), then the rest
-      // (w, u evict_last). A window tensor's phase-2 tiles become available
-      // `lag` phase-1 tiles after its last one and are given, oldest first,
-      // up to `per_item` to each following item, so phase 2 catches up with
-      // phase 1 and at most ~(largest tensor + lag) x 8 B of w and u wait in
-      // L2; the large tensors' phase-2 tiles fill items whose window queue is
-      // empty; what is left after the last phase-1 tile gets items of its own.
-      int64_t window = 8ll << 20, lag = 256, per_item = 3;
-      if (const char* e = std::getenv("BO_STREAM_WINDOW")) window = std::max<int64_t>(0, std::atoll(e));
-      if (const char* e = std::getenv("BO_STREAM_LAG")) lag = std::max<int64_t>(0, std::atoll(e));
-      if (const char* e = std::getenv("BO_STREAM_P2")) per_item = std::min<int64_t>(3, std::max<int64_t>(1, std::atoll(e)));
-      std::vector<int32_t> p1;
-      std::vector<int> big, small;
-      for (int t = 0; t < L.T; ++t) {
-        (L.numel[static_cast<size_t>(t)] > window ? big : small).push_back(t);
-      }
-      for (int t : big) {
-        for (int i = ttiles[static_cast<size_t>(t)]; i < ttiles[static_cast<size_t>(t) + 1]; ++i) {
-          p1.push_back(i | (kStreamP1Stream << 30));
-        }
-      }
-      const int64_t n_big = static_cast<int64_t>(p1.size());
-      std::vector<std::pair<int64_t, int>> release;  // (phase-1 tiles issued, tensor)
-      for (int t : small) {
-        for (int i = ttiles[static_cast<size_t>(t)]; i < ttiles[static_cast<size_t>(t) + 1]; ++i) {
-          p1.push_back(i | (kStreamP1Window << 30));
-        }
-        release.emplace_back(static_cast<int64_t>(p1.size()) + lag, t);
-      }
-      std::vector<int4> items;
-      std::vector<int> q_small, q_big;  // phase-2 tiles ready to be paired
-      size_t qs = 0, qb = 0, next = 0;
-      bool big_released = false;
-      for (int64_t k = 0; k < static_cast<int64_t>(p1.size()); ++k) {
-        while (next < release.size() && release[next].first <= k) {
-          const int t = release[next++].second;
-          for (int i = ttiles[static_cast<size_t>(t)]; i < ttiles[static_cast<size_t>(t) + 1]; ++i) q_small.push_back(i);
-        }
-        if (!big_released && k >= n_big + lag) {
-          big_released = true;
-          for (int t : big) {
-            for (int i = ttiles[static_cast<size_t>(t)]; i < ttiles[static_cast<size_t>(t) + 1]; ++i) q_big.push_back(i);
-          }
-        }
-        int y[3] = {-1, -1, -1};
-        if (qs < q_small.size()) {
-          for (int j = 0; j < per_item && qs < q_small.size(); ++j) y[j] = q_small[qs++];
-        } else if (qb < q_big.size()) {
-          y[0] = q_big[qb++];
-        }
-        items.push_back(make_int4(p1[static_cast<size_t>(k)], y[0], y[1], y[2]));
-      }
-      while (next < release.size()) {
-        const int t = release[next++].second;
-        for (int i = ttiles[static_cast<size_t>(t)]; i < ttiles[static_cast<size_t>(t) + 1]; ++i) q_small.push_back(i);
-      }
-      if (!big_released) {
-        for (int t : big) {
-          for (int i = ttiles[static_cast<size_t>(t)]; i < ttiles[static_cast<size_t>(t) + 1]; ++i) q_big.push_back(i);
-        }
-      }
-      std::vector<int> rest(q_small.begin() + static_cast<int64_t>(qs), q_small.end());
-      rest.insert(rest.end(), q_big.begin() + static_cast<int64_t>(qb), q_big.end());
-      for (size_t i = 0; i < rest.size(); i += 3) {
-        items.push_back(make_int4(-1, rest[i], i + 1 < rest.size() ? rest[i + 1] : -1,
-                                  i + 2 < rest.size() ? rest[i + 2] : -1));
-      }
-      c->d_stream_items = upload(c, items);
-      c->n_stream_items = static_cast<int>(items.size());
-    }
     c->d_fused_tiles = upload(c, ft);
     c->n_fused_tiles = static_cast<int>(ft.size());
     c->d_fused_tensor_tiles = upload(c, ttiles);

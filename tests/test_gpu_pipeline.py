@@ -324,42 +324,6 @@ def test_train_step_resident_micros_bit_identical(torch_cuda, oracle, K, aligned
     assert np.array_equal(v0.view(np.uint32), v1.view(np.uint32))
 
 
-@pytest.mark.parametrize("window,lag", [(8 << 20, 512), (0, 0), (1 << 30, 0), (4096, 3), (1 << 30, 1 << 20)])
-def test_streamed_lamb_bit_identical(torch_cuda, oracle, monkeypatch, window, lag):
-    """The streamed one-rank LAMB (k_lamb_stream: phase 1, trust ratios and
-    phase 2 in one launch, phase 2 a lag behind) gives the two-pass kernels'
-    bits for every schedule: all tensors streaming (window 0), phase 2 right
-    behind phase 1 (lag 0: its CTAs wait for the trust ratio), phase 2 at the
-    end (huge lag); overflow steps roll the weights back from the undo copy."""
-    from paper_2008_00177_b200.model_spec import BERT_TINY, bert_spec
-    from paper_2008_00177_b200.pipeline import LambConfig, ScalerConfig, TrainerConfig
-    from tests.harness import run_pipeline
-
-    spec = bert_spec(BERT_TINY)
-    P = spec.param_count()
-    p0 = oracle.build_params(spec, 9)
-    cfg = TrainerConfig(LambConfig(lr=1e-2), 4, 4096, False, 0,
-                        ScalerConfig(init_scale=2.0 ** 14, growth_interval=3))
-    inj = [(1, 0, 3, P - 1, 0x7C00), (3, 0, 0, P // 2, 0x7E00)]
-    kw = dict(steps=6, spike_ppm=3, spike_exp=3, injections=inj, resident=True)
-    monkeypatch.setenv("BO_STREAM", "0")
-    base, su0, fi0 = run_pipeline(spec, cfg, p0, **kw)
-    assert "one_rank_stream" not in base.path()
-    monkeypatch.setenv("BO_STREAM", "1")
-    monkeypatch.setenv("BO_STREAM_WINDOW", str(window))
-    monkeypatch.setenv("BO_STREAM_LAG", str(lag))
-    res, su1, fi1 = run_pipeline(spec, cfg, p0, **kw)
-    assert "one_rank_stream" in res.path()
-    assert np.array_equal(su0, su1) and np.array_equal(fi0, fi1) and fi0.sum() >= 2
-    assert np.array_equal(base.read_params().view(np.uint32), res.read_params().view(np.uint32))
-    m0, v0, m1, v1 = (np.zeros(P, np.float32) for _ in range(4))
-    base.read_moments(m0, v0)
-    res.read_moments(m1, v1)
-    assert np.array_equal(m0.view(np.uint32), m1.view(np.uint32))
-    assert np.array_equal(v0.view(np.uint32), v1.view(np.uint32))
-    assert res.status().skipped_steps == base.status().skipped_steps
-
-
 def test_micro_order_protocol(torch_cuda, oracle):
     """Micros must arrive 0..K-1; bo_train_step cannot start inside a step fed
     by bo_accumulate (ProtocolError, the reference's protocol-violation class)."""

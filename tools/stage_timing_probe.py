@@ -19,7 +19,7 @@ from paper_2008_00177_b200.pipeline import (GradPipeline, LambConfig, ScalerConf
                                             TrainerConfig, synth_grads)
 
 STAGES = ["accumulate", "finalize", "reduce", "lamb_norms", "trust", "lamb_update", "allgather",
-          "hop_kernels", "lamb_stream"]
+          "hop_kernels", "reserved"]
 
 
 def main():
