@@ -463,6 +463,21 @@ def main_b200(args):
         gbs = st_dom["nvlink_bytes"] / (in_step * 1e-3) / 1e9
         st_dom.update({"nvlink_GB/s": round(gbs, 1), "nvlink_frac": round(gbs / NVLINK_GBS, 4),
                        "nvlink_frac_alone": round(st_dom["nvlink_bytes"] / (alone * 1e-3) / 1e9 / NVLINK_GBS, 4)})
+    # The other stages on the same footing: "ms" (and the rates derived from
+    # it) is the stage's share of the event-free step per launch, so the stage
+    # times add up to ms_per_step; the bracketed time stays as ms_evented.
+    for n, entry in stages.items():
+        if n == dom:
+            continue
+        per = entry["ms_in_step"] / max(entry["launches_per_step"], 1e-9)
+        entry["ms_evented"] = entry["ms"]
+        entry["ms"] = round(per, 5)
+        if "bytes" in entry:
+            gbs = entry["bytes"] / (per * 1e-3) / 1e9
+            entry.update({"GB/s": round(gbs, 1), "frac": round(gbs / hbm, 4)})
+        if "nvlink_bytes" in entry:
+            gbs = entry["nvlink_bytes"] / (per * 1e-3) / 1e9
+            entry.update({"nvlink_GB/s": round(gbs, 1), "nvlink_frac": round(gbs / NVLINK_GBS, 4)})
     kernel_names = {"accumulate": "k_accumulate", "finalize": "k_finalize",
                     "lamb_norms": ("k_lamb_p1r" if resident else "k_lamb_p1") if world == 1 else "k_p1w",
                     "lamb_update": "k_lamb_p2" if world == 1 else "k_shard_p2_push",
