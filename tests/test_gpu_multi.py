@@ -115,9 +115,10 @@ def test_two_gpus_bert_large_full_size():
     assert res["m_bit_exact"] and res["v_bit_exact"] and res["replicas_identical"]
 
 
-@pytest.mark.parametrize("n", [4, 8])
+@pytest.mark.parametrize("n", [3, 4, 8])
 def test_more_gpus(n):
-    """Worlds 4 and 8 (8 is the north star's target), one GPU per rank."""
+    """Worlds 3 (non-power-of-two: inexact 1/N, padded chunks), 4 and 8 (the
+    north star's target), one GPU per rank."""
     g = _ngpu()
     if g < n:
         pytest.skip(f"needs {n} GPUs (one per rank); world {n} on fewer GPUs: test_gpu_world_emu.py")

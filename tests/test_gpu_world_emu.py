@@ -1,4 +1,4 @@
-"""Worlds 2, 4 and 8 on ONE GPU, bit for bit: all ranks in this process
+"""Worlds 2, 3, 4, 6 and 8 on ONE GPU, bit for bit: all ranks in this process
 (bo_world_init_local), one host thread per rank, every rank's kernels on one
 shared stream in lockstep — the step's cross-rank waits become rendezvous of
 the host threads between launches, so no kernel ever waits for another
@@ -65,7 +65,11 @@ CASES = {
 }
 
 
-@pytest.mark.parametrize("world", [2, 4, 8])
+# 3 and 6: non-power-of-two worlds, where the reference's 1/world scaling
+# (trainer.cpp:212-213) is inexact and chunks are zero-padded to c * N
+# (collective.hpp:44-60); the reference's own ring tests run N in {2,3,4,8}
+# (test_collective.cpp:403-436)
+@pytest.mark.parametrize("world", [2, 3, 4, 6, 8])
 @pytest.mark.parametrize("case", sorted(CASES))
 def test_world_lockstep_matches_oracle(torch_cuda, oracle, world, case, monkeypatch):
     from oracle.oracle import LambConfig as OL, ScalerConfig as OS
