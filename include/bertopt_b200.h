@@ -154,7 +154,8 @@ bo_status bo_comm_unique_id(uint8_t* out128);
  * (BO_ERR_BUCKET_LAYOUT_MISMATCH on disagreement, trainer.cpp:169-183) + the
  * peer mappings of bo_comm_import. Needed for the NCCL reduce-scatter, the
  * ncclSend/Recv ring (BO_RING_NCCL=1), the NCCL hop barrier
- * (BO_RING_BARRIER=nccl) and the bo_ring_allreduce_* operators. */
+ * (BO_RING_BARRIER=nccl) and the bo_ring_allreduce_* operators of a context
+ * without mapped ring buffers. */
 bo_status bo_comm_init(bo_ctx* ctx, const uint8_t* id128);
 /* NCCL-free initialisation of the default (binary16 / fp32 ring) step, which
  * runs without any collective library: every rank exports a fixed-size
@@ -320,8 +321,16 @@ bo_status bo_trace_write(bo_ctx* ctx, const char* path);
 bo_status bo_lamb_step(int32_t n_tensors, const int64_t* numels, float* const* params,
                        const float* const* grads, float* const* m, float* const* v,
                        int64_t* step, const bo_lamb_config* cfg, void* stream);
-/* In-place elementwise sum over all ranks of ctx's communicator, reference
- * fold order, identical bits on every rank. data is a device pointer. */
+/* In-place elementwise sum over all ranks of ctx's world, reference fold
+ * order (chunk k folded over ranks k, k+1, ..., k-1; binary16 wire rounding
+ * per hop and the owner re-round for the f16 variant), identical bits on
+ * every rank. data is a device pointer; every rank calls with the same n.
+ * Runs over the context's own NVLink ring staging buffers (push form, a
+ * neighbour barrier per hop, chunks larger than the buffers in slices) once
+ * the peers are mapped (bo_comm_import / bo_comm_init / bo_world_init_local
+ * with the ring reduce algorithm), else over ncclSend/ncclRecv (bo_comm_init).
+ * Returns with the data reduced (the context stream is synchronised);
+ * BO_ERR_PROTOCOL while a bo_sync_ready micro is open. */
 bo_status bo_ring_allreduce_f32(bo_ctx* ctx, float* data, size_t n);
 bo_status bo_ring_allreduce_f16_wire(bo_ctx* ctx, float* data, size_t n);
 /* unscale_gradients: BO_ERR_OVERFLOW_DETECTED (and no change) if any entry is

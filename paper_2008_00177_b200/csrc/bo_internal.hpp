@@ -404,6 +404,9 @@ void lockstep_sync(bo_ctx* c, const char* where);
 void params_wait(bo_ctx* c, int tensor, cudaStream_t stream);
 // needs the NCCL communicator (bo_comm_init): fail otherwise
 void need_nccl(bo_ctx* c, const char* what);
+// bo_ring_allreduce_* over the mapped ring staging buffers (bo_ring.cu)
+bool ring_op_available(const bo_ctx* c);
+void ring_allreduce_op(bo_ctx* c, float* data, size_t n, bool f16);
 void run_fused_single_rank(bo_ctx* c, const PtrTable& tab, MicroSrc ms = MicroSrc{nullptr, 0, 0});
 
 // Stage bracket: records events when profiling is on.

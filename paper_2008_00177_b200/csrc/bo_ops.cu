@@ -308,7 +308,13 @@ template <typename W>
 void ring_allreduce_impl(bo_ctx* c, float* data, size_t n, bool f16) {
   const int N = c->world, r = c->rank;
   if (N == 1 || n == 0) return;
-  need_nccl(c, "bo_ring_allreduce_*");
+  if (ring_op_available(c)) {
+    // the library's own ring over NVLink (push form, neighbour barriers)
+    ring_allreduce_op(c, data, n, f16);
+    BO_CUDA(cudaStreamSynchronize(c->stream));  // returns with the data reduced, as the reference
+    return;
+  }
+  need_nccl(c, "bo_ring_allreduce_* without mapped ring buffers");
   cudaStream_t s = c->stream;
   const size_t ch = (n + static_cast<size_t>(N) - 1) / static_cast<size_t>(N);  // collective.cpp:27-29
   // one grow-only workspace per context (the padded buffer, the outgoing

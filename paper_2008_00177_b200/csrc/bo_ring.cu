@@ -7,6 +7,8 @@
 // Bit-level contract as in bo_pipeline.cu (--fmad=false, explicit _rn).
 #include <cuda_fp16.h>
 
+#include <algorithm>
+
 #include "bo_device.cuh"
 #include "bo_internal.hpp"
 
@@ -390,6 +392,112 @@ void run_reduce_group(bo_ctx* c, const PtrTable& tab, int b0, int b1, int acc0, 
     ring_reduce_scatter<uint16_t>(c, tab, ncclFloat16, b0, b1, stream);
   } else {
     ring_reduce_scatter<float>(c, tab, ncclFloat32, b0, b1, stream);
+  }
+}
+
+// ------------------------------------------------- operator drop-ins
+// ring_allreduce<float> / ring_allreduce_f16_wire (collective.hpp:53-99,
+// collective.cpp:37-86) on caller device data, over the context's mapped ring
+// staging buffers (CUDA IPC / NVLink) in push form: every hop writes its
+// output straight into the right neighbour's staging buffer and a neighbour
+// barrier orders it before the reader. Chunk k = ceil(n/N) elements, zero
+// padded (collective.hpp:44-60), folded over ranks k, k+1, ..., k-1 with the
+// wire rounding per hop; the owner's chunk is re-rounded (collective.cpp:79-83)
+// and the all-gather forwards the owner's wire bits, so every rank ends with
+// the same bits. Chunks larger than the staging buffers run in slices of the
+// chunk (the fold order per element is unchanged).
+namespace {
+template <typename W>
+__global__ void k_op_rs(const float* __restrict__ data, int64_t n, int64_t base, int64_t len,
+                        const W* __restrict__ in, W* __restrict__ out) {
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < len;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t i = base + e;
+    const float x = i < n ? data[i] : 0.0f;  // zero padding past n
+    out[e] = to_wire<W>(in ? __fadd_rn(from_wire(in[e]), x) : x);
+  }
+}
+// The owner: the chunk's last addition, its wire rounding (the owner
+// re-round), and the first all-gather push.
+template <typename W>
+__global__ void k_op_own(float* __restrict__ data, int64_t n, int64_t base, int64_t len,
+                         const W* __restrict__ in, W* __restrict__ out) {
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < len;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t i = base + e;
+    const W w = to_wire<W>(__fadd_rn(from_wire(in[e]), i < n ? data[i] : 0.0f));
+    out[e] = w;
+    if (i < n) data[i] = from_wire(w);
+  }
+}
+// All-gather: store the chunk received from the left and forward its bits
+// (out == nullptr: the last hop, store only).
+template <typename W>
+__global__ void k_op_fwd(float* __restrict__ data, int64_t n, int64_t base, int64_t len,
+                         const W* __restrict__ in, W* __restrict__ out) {
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < len;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const W w = in[e];
+    if (out) out[e] = w;
+    if (base + e < n) data[base + e] = from_wire(w);
+  }
+}
+int op_grid(int64_t len) {
+  return static_cast<int>(std::min<int64_t>(std::max<int64_t>((len + kThreads - 1) / kThreads, 1), 148 * 8));
+}
+}  // namespace
+
+bool ring_op_available(const bo_ctx* c) {
+  return c->world > 1 && c->peers_mapped && c->wire[0] && c->peer_wire[0][(c->rank + 1) % c->world] &&
+         !c->ring_via_nccl;
+}
+
+template <typename W>
+static void ring_allreduce_op_t(bo_ctx* c, float* data, size_t n) {
+  const int N = c->world, r = c->rank, right = (r + 1) % N;
+  if (c->sync_open) fail(BO_ERR_PROTOCOL, "bo_ring_allreduce_* while a sync micro (bo_sync_ready) is open");
+  cudaStream_t st = c->stream;
+  const int64_t ch = static_cast<int64_t>((n + static_cast<size_t>(N) - 1) / static_cast<size_t>(N));
+  const size_t wire_bytes = static_cast<size_t>(c->L.shard_total) * (c->cfg.f16_exchange ? 2 : 4);
+  const int64_t cap = static_cast<int64_t>(wire_bytes / sizeof(W));
+  if (cap <= 0) fail(BO_ERR_INVALID_CONFIG, "ring staging buffers are empty");
+  W* mine[2] = {static_cast<W*>(c->wire[0]), static_cast<W*>(c->wire[1])};
+  W* theirs[2] = {static_cast<W*>(c->peer_wire[0][right]), static_cast<W*>(c->peer_wire[1][right])};
+  auto chunk = [&](int k) { return static_cast<int64_t>(((k % N) + N) % N) * ch; };
+  for (int64_t o = 0; o < ch; o += cap) {
+    const int64_t len = std::min(cap, ch - o);
+    const int g = op_grid(len);
+    // every neighbour is done with its staging buffers (previous slice,
+    // operator call or step) before this rank pushes into them
+    hop_barrier(c, st);
+    int h = 0;  // hop counter: hop h pushes into the right's staging[h % 2]
+    for (int s = 0; s < N - 1; ++s, ++h) {  // reduce-scatter (collective.hpp:65-80)
+      if (s > 0) hop_barrier(c, st);
+      k_op_rs<W><<<g, kThreads, 0, st>>>(data, static_cast<int64_t>(n), chunk(r - s) + o, len,
+                                         s == 0 ? nullptr : mine[(h - 1) % 2], theirs[h % 2]);
+      check_launch(c, "k_op_rs");
+    }
+    hop_barrier(c, st);
+    k_op_own<W><<<g, kThreads, 0, st>>>(data, static_cast<int64_t>(n), chunk(r + 1) + o, len,
+                                        mine[(h - 1) % 2], theirs[h % 2]);
+    check_launch(c, "k_op_own");
+    ++h;
+    for (int t = 1; t < N; ++t, ++h) {  // all-gather (collective.hpp:83-96)
+      hop_barrier(c, st);
+      k_op_fwd<W><<<g, kThreads, 0, st>>>(data, static_cast<int64_t>(n), chunk(r - t + 1) + o, len,
+                                          mine[(h - 1) % 2], t < N - 1 ? theirs[h % 2] : nullptr);
+      check_launch(c, "k_op_fwd");
+    }
+  }
+  // the neighbours' last reads are done before anything else pushes here
+  hop_barrier(c, st);
+}
+
+void ring_allreduce_op(bo_ctx* c, float* data, size_t n, bool f16) {
+  if (f16) {
+    ring_allreduce_op_t<uint16_t>(c, data, n);
+  } else {
+    ring_allreduce_op_t<float>(c, data, n);
   }
 }
 
