@@ -7,12 +7,16 @@
 #include <cstring>
 #include <limits>
 #include <random>
+#include <thread>
+#include <memory>
 
 #include "bertopt/half.hpp"
 #include "bertopt/lamb.hpp"
 #include "bertopt/model.hpp"
 #include "bertopt/tensor.hpp"
 #include "bertopt/trainer.hpp"
+#include "bertopt/transport.hpp"
+#include "bertopt/collective.hpp"
 #include "bertopt_b200_adapter.hpp"
 #include "ref_shim.hpp"
 
@@ -212,6 +216,70 @@ int main() {
     bool thrown = false;
     try { pipe.train_step({}); } catch (const InvalidConfig&) { thrown = true; }
     EXPECT(thrown);
+  }
+  // --- ring_allreduce<float> / ring_allreduce_f16_wire through the adapter
+  // (b200::ring_allreduce_f32 / _f16_wire: host data in, the library's NVLink
+  // ring on the device) against the REAL reference collectives over InProcHub
+  // (collective.hpp:53-99, collective.cpp:37-86) on the same inputs: N
+  // contexts on this GPU in lockstep (bo_world_init_local), one host thread
+  // per rank, as run_data_parallel (trainer.cpp:397-470). Bits equal on every
+  // rank; sizes of test_collective.cpp:403-436 plus a ragged large one.
+  {
+    refshim::ModelSpec spec;
+    spec.names = {"a", "b"};
+    spec.shapes = {{4096}, {777}};
+    spec.init = {0, 0};
+    TrainerConfig tc;
+    tc.accumulation = 1;
+    tc.bucket_bytes = 4096;
+    tc.f16_exchange = true;
+    bo_trainer_config dc;
+    bo_default_config(&dc);
+    const bo_scaler_config sc = dc.scaler;
+    for (int world : {2, 3, 4}) {
+      std::vector<std::unique_ptr<b200::GradPipeline>> pipes;
+      std::vector<bo_ctx*> ctxs;
+      for (int r = 0; r < world; ++r) {
+        Model m = refshim::build_model_from_spec(spec, 1);
+        pipes.push_back(std::make_unique<b200::GradPipeline>(m, std::vector<int>{1, 0}, tc, sc, 0, r, world));
+        ctxs.push_back(pipes.back()->handle());
+      }
+      b200::check(bo_world_init_local(ctxs.data(), world));
+      for (size_t n : {size_t{1}, size_t{5}, size_t{64}, size_t{1537}, size_t{100003}}) {
+        for (int f16 = 0; f16 < 2; ++f16) {
+          std::vector<std::vector<float>> ref(static_cast<size_t>(world)), dev;
+          std::mt19937 gen(static_cast<unsigned>(world * 1000 + n + f16));
+          std::normal_distribution<float> nd(0.0f, f16 ? 0.25f : 1.0f);
+          for (auto& x : ref) {
+            x.resize(n);
+            for (float& y : x) y = nd(gen);
+          }
+          dev = ref;
+          auto hub = std::make_shared<InProcHub>(world);
+          std::vector<std::thread> th;
+          std::vector<int> errs(static_cast<size_t>(world), 0);
+          for (int r = 0; r < world; ++r) {
+            th.emplace_back([&, r] {
+              try {
+                InProcTransport tr(hub, r);
+                WorkerGroup g{r, world, 0, r, &tr};
+                if (f16) ring_allreduce_f16_wire(g, ref[static_cast<size_t>(r)].data(), n, 7);
+                else ring_allreduce<float>(g, ref[static_cast<size_t>(r)].data(), n, 7);
+                if (f16) b200::ring_allreduce_f16_wire(ctxs[static_cast<size_t>(r)], dev[static_cast<size_t>(r)].data(), n);
+                else b200::ring_allreduce_f32(ctxs[static_cast<size_t>(r)], dev[static_cast<size_t>(r)].data(), n);
+              } catch (...) {
+                errs[static_cast<size_t>(r)] = 1;
+              }
+            });
+          }
+          for (auto& t : th) t.join();
+          for (int r = 0; r < world; ++r) {
+            EXPECT(errs[static_cast<size_t>(r)] == 0);
+            EXPECT(std::memcmp(ref[static_cast<size_t>(r)].data(), dev[static_cast<size_t>(r)].data(), n * 4) == 0);
+          }
+        }
+      }
+    }
   }
   std::printf(failures ? "ADAPTER FAILED %d\n" : "ADAPTER OK\n", failures);
   return failures ? 1 : 0;

@@ -1,6 +1,9 @@
 """The C++ adapter over the C ABI, compiled against the reference's headers and
 objects (oracle/_ref/adapter_test), run next to the reference's own
-lamb_step / unscale_gradients on the same inputs."""
+lamb_step / unscale_gradients / DistributedTrainer::train_step and — for
+worlds 2, 3 and 4 in lockstep on one GPU — the reference's own
+ring_allreduce<float> / ring_allreduce_f16_wire over InProcHub, on the same
+inputs (bits equal on every rank)."""
 import os
 import subprocess
 
