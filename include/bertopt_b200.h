@@ -214,6 +214,16 @@ bo_status bo_read_params(bo_ctx* ctx, float* dst, int32_t dst_on_host);
 /* LAMB moments of the elements this rank owns, scattered into model-order
  * flat arrays (elements owned by other ranks are left untouched). */
 bo_status bo_read_moments(bo_ctx* ctx, float* m, float* v, int32_t dst_on_host);
+/* Replica hash, the device counterpart of the reference's per-step replica
+ * divergence check (DistributedTrainer::param_hash, trainer.cpp:136-142,
+ * 375-377, checked across ranks at trainer.cpp:442-453): sum mod 2^64 of
+ * mix64(mix64(t << 40 | i) ^ bits(param[t][i])) over this rank's parameter
+ * replica (splitmix64 finaliser), one pass over the replica on the device,
+ * after the context stream's work so far; synchronous. Equal on every rank
+ * whose replica is bit-identical. (The reference's own FNV-1a value is
+ * sequential by construction: the C++ adapter's GradPipeline::param_hash()
+ * computes it from a host copy.) */
+bo_status bo_replica_hash(bo_ctx* ctx, uint64_t* out);
 bo_status bo_get_status(bo_ctx* ctx, bo_step_status* out);
 /* Checkpoint / resume of the device state (the reference
  * BCKP checkpoint, model.cpp:360-425, keeps only parameters). The blob holds

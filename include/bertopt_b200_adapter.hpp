@@ -278,6 +278,22 @@ class GradPipeline {
     }
     state.step = status().lamb_step;
   }
+  // DistributedTrainer::param_hash (trainer.cpp:375-377): the reference's
+  // FNV-1a over the parameters in model order, from a host copy into
+  // `scratch` (a model of the same shapes) — the value trainer.param_hash()
+  // gives for the same parameters.
+  uint64_t param_hash(Model& scratch) {
+    read_params(scratch);
+    return model_param_hash(scratch);
+  }
+  // The device-side replica hash (bo_replica_hash): one pass over the
+  // replica, equal on every rank with bit-identical parameters — the cheap
+  // per-step divergence check of trainer.cpp:442-453.
+  uint64_t replica_hash() {
+    uint64_t h = 0;
+    check(bo_replica_hash(ctx_, &h));
+    return h;
+  }
   bo_step_status status() {
     bo_step_status s;
     check(bo_get_status(ctx_, &s));

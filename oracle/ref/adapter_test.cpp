@@ -245,6 +245,15 @@ int main() {
         ctxs.push_back(pipes.back()->handle());
       }
       b200::check(bo_world_init_local(ctxs.data(), world));
+      // identical replicas: equal device hashes; the adapter's param_hash is
+      // the reference's own model_param_hash of the same parameters
+      {
+        Model ref_model = refshim::build_model_from_spec(spec, 1), scratch = refshim::build_model_from_spec(spec, 1);
+        for (int r = 0; r < world; ++r) {
+          EXPECT(pipes[static_cast<size_t>(r)]->replica_hash() == pipes[0]->replica_hash());
+          EXPECT(pipes[static_cast<size_t>(r)]->param_hash(scratch) == model_param_hash(ref_model));
+        }
+      }
       for (size_t n : {size_t{1}, size_t{5}, size_t{64}, size_t{1537}, size_t{100003}}) {
         for (int f16 = 0; f16 < 2; ++f16) {
           std::vector<std::vector<float>> ref(static_cast<size_t>(world)), dev;

@@ -75,6 +75,7 @@ SIGNATURES = {
     "bo_load_params": (_i32, [_vp, _vp, _i32]),
     "bo_read_params": (_i32, [_vp, _vp, _i32]),
     "bo_read_moments": (_i32, [_vp, _vp, _vp, _i32]),
+    "bo_replica_hash": (_i32, [_vp, _vp]),
     "bo_get_status": (_i32, [_vp, C.POINTER(StepStatusC)]),
     "bo_export_state": (_i32, [_vp, _vp, C.POINTER(_u64)]),
     "bo_import_state": (_i32, [_vp, _vp, _u64]),

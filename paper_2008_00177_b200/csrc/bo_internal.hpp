@@ -312,6 +312,7 @@ struct bo_ctx {
   int* d_push_group_tiles = nullptr;   // [G] tiles of group g on this rank
   unsigned* d_push_count = nullptr;    // [G] cumulative finished tiles
   cudaEvent_t params_done = nullptr;   // world 1: the step's update, for bo_params_wait
+  unsigned long long* hash_acc = nullptr;  // bo_replica_hash accumulator
   void* op_ws = nullptr;               // bo_ring_allreduce_* workspace (grow-only)
   size_t op_ws_bytes = 0;
   // Grouped LAMB (BO_LAMB_GROUP_ELEMS, world > 1): consecutive tensors (model

@@ -275,6 +275,28 @@ __global__ void k_synth(uint16_t* dst, int64_t begin, int64_t n, uint64_t base, 
   }
 }
 
+// Replica hash (the device counterpart of the reference's per-step
+// param_hash divergence check, trainer.cpp:136-142, 442-453): the sum mod 2^64
+// of mix64(mix64(t << 40 | i) ^ bits(w[t][i])) over every element i of every
+// tensor t of this rank's parameter replica. Integer addition is order-free,
+// so the value is deterministic and identical on ranks with identical
+// replicas, whatever the layout; one differing bit changes it.
+__global__ void __launch_bounds__(kThreads) k_replica_hash(const AccTile* __restrict__ tiles,
+                                                           const TensorDev* __restrict__ td,
+                                                           const float* __restrict__ w,
+                                                           unsigned long long* __restrict__ out) {
+  const AccTile tile = tiles[blockIdx.x];
+  const float* src = w + td[tile.t].flat_off + tile.e0;
+  unsigned long long h = 0;
+  for (int e = threadIdx.x; e < tile.len; e += kThreads) {
+    const uint64_t key = (static_cast<uint64_t>(tile.t) << 40) | static_cast<uint64_t>(tile.e0 + e);
+    h += mix64(mix64(key) ^ static_cast<uint64_t>(__float_as_uint(src[e])));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(out, h);
+}
+
 int grid_for(size_t n) {
   const size_t b = (n + kThreads - 1) / kThreads;
   return static_cast<int>(std::min<size_t>(std::max<size_t>(b, 1), 148 * 16));
@@ -512,6 +534,23 @@ bo_status bo_f16_round(float* x, size_t n, void* stream) {
     k_round_f16<<<grid_for(n), kThreads, 0, s>>>(x, n);
     check("k_round_f16");
   }
+  BO_OP_END
+}
+
+bo_status bo_replica_hash(bo_ctx* c, uint64_t* out) {
+  BO_OP_BEGIN
+  if (!c || !out) fail(BO_ERR_INVALID_CONFIG, "null argument");
+  if (c->sync_open) fail(BO_ERR_PROTOCOL, "bo_replica_hash while a sync micro (bo_sync_ready) is open");
+  if (!c->hash_acc) c->hash_acc = static_cast<unsigned long long*>(dev_alloc(c, sizeof(unsigned long long)));
+  BO_CUDA(cudaMemsetAsync(c->hash_acc, 0, sizeof(unsigned long long), c->stream));
+  if (c->n_acc_tiles > 0) {
+    k_replica_hash<<<c->n_acc_tiles, kThreads, 0, c->stream>>>(c->d_acc_tiles, c->d_tensors, c->w, c->hash_acc);
+    check_launch(c, "k_replica_hash");
+  }
+  unsigned long long h = 0;
+  BO_CUDA(cudaMemcpyAsync(&h, c->hash_acc, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+  BO_CUDA(cudaStreamSynchronize(c->stream));
+  *out = static_cast<uint64_t>(h);
   BO_OP_END
 }
 

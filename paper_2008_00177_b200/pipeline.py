@@ -325,6 +325,14 @@ class GradPipeline:
         _lib.check(self.lib.bo_read_params(self.ctx, out.ctypes.data, 1))
         return out
 
+    def replica_hash(self) -> int:
+        """bo_replica_hash: the device-side hash of this rank's parameter
+        replica (equal across ranks with identical replicas; the per-step
+        divergence check of trainer.cpp:442-453)."""
+        out = C.c_uint64()
+        _lib.check(self.lib.bo_replica_hash(self.ctx, C.byref(out)))
+        return int(out.value)
+
     def read_moments(self, m: np.ndarray | None = None, v: np.ndarray | None = None):
         m = np.zeros(self.P, np.float32) if m is None else m
         v = np.zeros(self.P, np.float32) if v is None else v
