@@ -556,8 +556,21 @@ def main_b200(args):
 
     # end to end through the public API with host buffers
     e2e = None
+    host = None
     if not args.no_e2e:
-        host = [torch.empty(total, dtype=torch.int16, pin_memory=True) for _ in range(K)]
+        # pinned host buffers + a second device slot set per rank: agree on
+        # them across ranks first, so a rank that cannot allocate them skips
+        # the e2e leg together with every other rank instead of hanging them
+        try:
+            host = [torch.empty(total, dtype=torch.int16, pin_memory=True) for _ in range(K)]
+        except Exception as e:  # noqa: BLE001
+            host, e2e = None, {"value": None, "error": f"pinned host buffers: {e}"[:200]}
+        ok = max_over_ranks(0.0 if host is not None else 1.0, world, local, emulated) == 0.0
+        if not ok:
+            host = None
+            if e2e is None:
+                e2e = {"value": None, "error": "a rank could not allocate its pinned host buffers"}
+    if host is not None:
         for k in range(K):
             host[k].copy_(bufs[k])
         stage_dev = bufs  # reuse the device slots as the H2D destination
