@@ -399,10 +399,17 @@ def main_b200(args):
     # NVLink bytes sent per rank: ring reduce-scatter; the parameter push
     # (k_shard_p2_push stores every updated element into the N-1 other replicas)
     nvl_bytes = {"reduce": (world - 1) / world * E * P, "lamb_update": (world - 1) * 4 * S_shard}
+    grouped = "lamb_grouped" in path
+    if grouped:
+        # grouped LAMB (default at world >= 4): one bracket holds phase 1, the
+        # per-group trust ratios and the posted parameter push that overlaps
+        # the next group's phase 1 — its bytes are both stages'
+        hbm_bytes["lamb_norms"] += hbm_bytes["lamb_update"]
+        nvl_bytes["lamb_norms"] = nvl_bytes["lamb_update"]
     if fused_last and "ring_push" not in path:
         # pull form: the fused last hop reads the left neighbour's partial over
         # NVLink (push form: it was pushed here by the previous hop; local read)
-        nvl_bytes["lamb_norms"] = E * S_shard
+        nvl_bytes["lamb_norms"] = nvl_bytes.get("lamb_norms", 0) + E * S_shard
     stages = {}
     for i, name in enumerate(STAGES):
         if stage_n[i] == 0:
@@ -479,7 +486,8 @@ def main_b200(args):
             gbs = entry["nvlink_bytes"] / (per * 1e-3) / 1e9
             entry.update({"nvlink_GB/s": round(gbs, 1), "nvlink_frac": round(gbs / NVLINK_GBS, 4)})
     kernel_names = {"accumulate": "k_accumulate", "finalize": "k_finalize",
-                    "lamb_norms": ("k_lamb_p1r" if resident else "k_lamb_p1") if world == 1 else "k_p1w",
+                    "lamb_norms": ("k_lamb_p1r" if resident else "k_lamb_p1") if world == 1 else
+                                  ("k_p1w + k_push_posted (grouped, overlapped)" if grouped else "k_p1w"),
                     "lamb_update": "k_lamb_p2" if world == 1 else "k_shard_p2_push",
                     "hop_kernels": "k_hopx"}
     if st_dom.get("nvlink_frac", 0.0) > st_dom["frac"]:

@@ -308,6 +308,7 @@ int64_t bo_launch_count(const bo_ctx* ctx);
 #define BO_PATH_OVERLAP 64           /* sync micro delivered through bo_sync_ready */
 #define BO_PATH_RESIDENT 128         /* bo_train_step: the K micros read in the sync pass */
 #define BO_PATH_RING_PUSH 256        /* ring hops push their output into the right neighbour's buffer over NVLink */
+#define BO_PATH_LAMB_GROUPED 512     /* LAMB in tensor groups, the push of group g overlapping phase 1 of g+1 */
 int32_t bo_path_flags(const bo_ctx* ctx);
 
 /* Event timeline in the reference's EventLog schema (trainer.cpp:43-71,

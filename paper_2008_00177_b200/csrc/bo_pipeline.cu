@@ -840,6 +840,90 @@ __global__ void k_step_final(const double* __restrict__ all_part, int N, int T, 
   }
 }
 
+// The parameter push as a FEW persistent CTAs with posted stores (grouped
+// LAMB, BO_PUSH_POSTED_CTAS): each thread takes one float4 of a tile (grid-
+// stride over the tiles, two in flight) and stores the new value into the master shard and — plain 16-byte stores, no completion
+// wait — into every rank's replica (rotated per tile). ~32-48 CTAs of 1024
+// threads keep the push at ~650 GB/s of NVLink while phase 1 of the next
+// group streams HBM on the other SMs at ~0.96 of its speed alone
+// (tools/nvl_partition.cu, profiles/r02_notes.md); the one-CTA-per-tile bulk
+// copy push needs every SM. Same arithmetic and destinations as
+// k_shard_p2_push; tiles whose shard and replica 16-byte phases differ go
+// scalar. Kernel completion performs the posted stores before the stream's
+// next work (the end-of-step barrier, k_rollback).
+constexpr int kPostThreads = 1024;
+static_assert(kPostThreads * 4 == kTileElems, "one float4 per thread per tile");
+__global__ void __launch_bounds__(kPostThreads, 1) k_push_posted(const LambTile* __restrict__ tiles,
+                                                                 int n_tiles, float* wsh_main,
+                                                                 const float* __restrict__ u,
+                                                                 const DevState* __restrict__ st,
+                                                                 LambConsts c,
+                                                                 const float* __restrict__ trust,
+                                                                 float* const* __restrict__ peer_w, int N,
+                                                                 float* wsh_alt) {
+  __shared__ float* dst[8];
+  if (static_cast<int>(threadIdx.x) < N) dst[threadIdx.x] = peer_w[threadIdx.x];
+  const bool speculative = wsh_alt != nullptr;
+  const bool update = speculative || st->do_update != 0;
+  const int par = speculative ? st->parity : 0;
+  const float* __restrict__ wsrc = par ? wsh_alt : wsh_main;
+  float* __restrict__ wdst = speculative ? (par ? wsh_main : wsh_alt) : wsh_main;
+  __syncthreads();
+  if (!update) return;
+  // two tiles per iteration (i and i + G), all their loads issued first
+  const int G = static_cast<int>(gridDim.x);
+  for (int i0 = static_cast<int>(blockIdx.x); i0 < n_tiles; i0 += 2 * G) {
+    float4 w4[2], u4[2];
+    bool body[2] = {false, false};
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int i = i0 + k * G;
+      if (i >= n_tiles) continue;
+      const LambTile t = tiles[i];
+      if (((t.s0 - t.w0) & 3) != 0) continue;
+      const Split sp = split_tile(t.s0, t.len);
+      body[k] = static_cast<int>(threadIdx.x) < sp.nv;
+      if (body[k]) {
+        const int64_t s = t.s0 + sp.head + 4 * static_cast<int64_t>(threadIdx.x);
+        w4[k] = *reinterpret_cast<const float4*>(wsrc + s);
+        u4[k] = __ldcs(reinterpret_cast<const float4*>(u + s));
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int i = i0 + k * G;
+      if (i >= n_tiles) continue;
+      const LambTile t = tiles[i];
+      const float sc = __fmul_rn(c.lr, trust[t.t]);
+      auto one = [&](int e) {
+        const int64_t s = t.s0 + e;
+        const float nw = __fsub_rn(wsrc[s], __fmul_rn(sc, u[s]));
+        wdst[s] = nw;
+        for (int q = 0; q < N; ++q) dst[(i + q) % N][t.w0 + e] = nw;
+      };
+      if (((t.s0 - t.w0) & 3) != 0) {  // shard and replica 16-byte phases differ
+        for (int e = threadIdx.x; e < t.len; e += kPostThreads) one(e);
+        continue;
+      }
+      const Split sp = split_tile(t.s0, t.len);
+      if (body[k]) {
+        const int e = sp.head + 4 * static_cast<int>(threadIdx.x);
+        const float4 n4 = make_float4(__fsub_rn(w4[k].x, __fmul_rn(sc, u4[k].x)),
+                                      __fsub_rn(w4[k].y, __fmul_rn(sc, u4[k].y)),
+                                      __fsub_rn(w4[k].z, __fmul_rn(sc, u4[k].z)),
+                                      __fsub_rn(w4[k].w, __fmul_rn(sc, u4[k].w)));
+        *reinterpret_cast<float4*>(wdst + t.s0 + e) = n4;
+        for (int q = 0; q < N; ++q) __stcs(reinterpret_cast<float4*>(dst[(i + q) % N] + t.w0 + e), n4);
+      }
+      if (static_cast<int>(threadIdx.x) < sp.head) one(threadIdx.x);
+      if (threadIdx.x >= 32 && static_cast<int>(threadIdx.x) - 32 < sp.tail) {
+        one(sp.head + 4 * sp.nv + static_cast<int>(threadIdx.x) - 32);
+      }
+    }
+  }
+}
+
+
 // A skipped (or abandoned) grouped step: the speculative pushes are undone by
 // pushing the unchanged current master shard into every replica again. Exits
 // at once on a normal step.
@@ -1003,6 +1087,7 @@ static void launch_p1w(bo_ctx* c, const PtrTable& tab, const W* in, const P1Args
 // independent tensor groups changes.
 template <typename W, bool kHop>
 static void lamb_grouped(bo_ctx* c, const PtrTable& tab, const W* in) {
+  c->path |= BO_PATH_LAMB_GROUPED;
   const int T = c->L.T;
   const float invn = 1.0f / static_cast<float>(c->world);  // trainer.cpp:212
   const P1Args A{c->d_tensors, c->acc, c->cfg.accumulation, invn, c->wsh, c->m, c->v,
@@ -1021,9 +1106,12 @@ static void lamb_grouped(bo_ctx* c, const PtrTable& tab, const W* in) {
   size_t half = 0;
   {
   StageTimer timer(c, BO_STAGE_LAMB_NORMS);
-  for (int g = 0; g < G; ++g) {
+  auto p1 = [&](int g) {
     const bo_ctx::LambGroup& lg = c->lamb_groups[static_cast<size_t>(g)];
     launch_p1w<W, kHop, true>(c, tab, in, A, lg.tile0, lg.tile1 - lg.tile0);
+  };
+  auto norms = [&](int g) {
+    const bo_ctx::LambGroup& lg = c->lamb_groups[static_cast<size_t>(g)];
     c->bar_epoch += 1;
     epoch = static_cast<unsigned>(c->bar_epoch);
     half = (c->bar_epoch & 1) * static_cast<size_t>(c->world) * slot;
@@ -1034,6 +1122,9 @@ static void lamb_grouped(bo_ctx* c, const PtrTable& tab, const W* in) {
                                                                c->rank_part, dst, lg.t0);
       check_launch(c, "k_norm_reduce");
     }
+  };
+  auto trust_push = [&](int g) {
+    const bo_ctx::LambGroup& lg = c->lamb_groups[static_cast<size_t>(g)];
     PeerFlags pf = c->peer_ctrl;
     if (c->lockstep) {
       lockstep_sync(c, "partials");
@@ -1046,12 +1137,25 @@ static void lamb_grouped(bo_ctx* c, const PtrTable& tab, const W* in) {
       BO_CUDA(cudaEventRecord(c->group_events[static_cast<size_t>(g)], c->stream));
       BO_CUDA(cudaStreamWaitEvent(ps, c->group_events[static_cast<size_t>(g)], 0));
     }
-    if (lg.tile1 > lg.tile0) {
+    if (lg.tile1 > lg.tile0 && c->push_posted_ctas > 0) {
+      k_push_posted<<<std::min(c->push_posted_ctas, lg.tile1 - lg.tile0), kPostThreads, 0, ps>>>(
+          c->d_lamb_tiles + lg.tile0, lg.tile1 - lg.tile0, c->wsh, c->u, c->state, c->lamb, c->trust,
+          c->d_peer_w, c->world, c->wsh_alt);
+      check_launch(c, "k_push_posted");
+    } else if (lg.tile1 > lg.tile0) {
       k_shard_p2_push<<<lg.tile1 - lg.tile0, kThreads, 0, ps>>>(
           c->d_lamb_tiles + lg.tile0, lg.tile1 - lg.tile0, c->wsh, c->u, c->state, c->lamb, c->trust,
           c->d_peer_w, c->world, none, c->wsh_alt);
       check_launch(c, "k_shard_p2_push");
     }
+  };
+  // compute stream: p1(g) norms(g) trust(g) [event -> push(g) on ps] p1(g+1)
+  // ... (issuing p1(g+1) ahead of trust(g) was measured slower: the push of
+  // g, the bottleneck, then starts a phase 1 later; profiles/r02_notes.md)
+  for (int g = 0; g < G; ++g) {
+    p1(g);
+    norms(g);
+    trust_push(g);
   }
   if (!c->lockstep) {
     BO_CUDA(cudaEventRecord(c->group_events[static_cast<size_t>(G)], ps));

@@ -191,8 +191,12 @@ void upload_tables(bo_ctx* c) {
     c->d_push_count = static_cast<unsigned*>(dev_alloc(c, static_cast<size_t>(c->n_push_groups) * sizeof(unsigned)));
 
     // Grouped LAMB: consecutive tensors in model order, >= BO_LAMB_GROUP_ELEMS
-    // elements each (unset / 0: one group, the serial path)
-    int64_t lg_elems = 0;
+    // elements each (0: one group, the serial path). Default: eight groups at
+    // world >= 4, where the parameter push (NVLink) is the largest stage and
+    // the few-CTA posted push of group g hides phase 1 of group g + 1 (BERT-
+    // large, 4 B200s: 2.64 vs 2.85 ms per step); serial below (2 B200s: the
+    // serial step is faster, profiles/r02_notes.md).
+    int64_t lg_elems = L.N >= 4 ? (L.P + 7) / 8 : 0;
     if (const char* e = std::getenv("BO_LAMB_GROUP_ELEMS")) lg_elems = std::max<int64_t>(0, std::atoll(e));
     c->lamb_groups.clear();
     if (lg_elems > 0) {

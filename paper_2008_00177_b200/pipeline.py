@@ -289,7 +289,7 @@ class GradPipeline:
     # -- introspection
     PATH_NAMES = {1: "one_rank_fused", 2: "one_rank_staged", 4: "ring_p2p", 8: "ring_sendrecv",
                   16: "last_hop_fused", 32: "nccl_reduce_scatter", 64: "overlap",
-                  128: "resident_micros", 256: "ring_push"}
+                  128: "resident_micros", 256: "ring_push", 512: "lamb_grouped"}
 
     def path(self) -> list[str]:
         """Implementation the last sync micro ran (BO_PATH_* names)."""

@@ -62,6 +62,8 @@ CASES = {
     # skipped steps included (the rollback path)
     "ring16_grouped": (True, 2, 8192, dict(init_scale=2.0 ** 13, growth_interval=3), 20, False, None),
     "ring16_grouped_resident": (True, 4, 8192, dict(init_scale=2.0 ** 13, growth_interval=3), 20, True, None),
+    # the serial LAMB (one group) at every world size (the default below 4)
+    "ring16_serial_resident": (True, 4, 8192, dict(init_scale=2.0 ** 13, growth_interval=3), 20, True, None),
 }
 
 
@@ -82,6 +84,8 @@ def test_world_lockstep_matches_oracle(torch_cuda, oracle, world, case, monkeypa
         monkeypatch.setenv("BO_COMM_GROUP_ELEMS", "20000")  # several communication groups
     if "grouped" in case:
         monkeypatch.setenv("BO_LAMB_GROUP_ELEMS", "30000")  # ~6 LAMB groups of BERT_TINY
+    if "serial" in case:
+        monkeypatch.setenv("BO_LAMB_GROUP_ELEMS", "0")
     spec = bert_spec(BERT_TINY)
     P = spec.param_count()
     p0 = oracle.build_params(spec, 21)
@@ -96,6 +100,8 @@ def test_world_lockstep_matches_oracle(torch_cuda, oracle, world, case, monkeypa
     _check(pipes, su, fi, ref)
     path = pipes[0].path()
     assert "ring_p2p" in path and "ring_push" in path
+    # grouped LAMB: requested by the case, or the default at world >= 4
+    assert ("lamb_grouped" in path) == ("grouped" in case or (world >= 4 and "serial" not in case))
     assert ("resident_micros" in path) == resident
     assert ("overlap" in path) == bool(overlap)
     if ppm:
