@@ -275,7 +275,10 @@ bo_status bo_sync_ready(bo_ctx* ctx, int32_t n, const int32_t* tensors, const ui
  * enqueued on `stream` afterwards read the new values; the rest of the push
  * continues on the context stream. The parameters read must not be those of
  * a later step still in flight. World 1: the stream waits for the whole
- * step. Bounded by the watchdog (bo_set_watchdog). */
+ * step. With the grouped LAMB (the default at world >= 4, where the push
+ * overlaps the next tensor group's phase 1 inside the step instead) the
+ * groups are published together at the end of the step. Bounded by the
+ * watchdog (bo_set_watchdog). */
 bo_status bo_params_wait(bo_ctx* ctx, int32_t tensor, void* stream);
 /* Parameter group of a tensor (world 1: 0; -1 for a bad index). */
 int32_t bo_param_group(const bo_ctx* ctx, int32_t tensor);
