@@ -486,7 +486,12 @@ __global__ void __launch_bounds__(kWarpTileCTA, kMinBlocks) k_p1w(const LambTile
   float* __restrict__ mn = par ? A.m0 : A.m1;
   float* __restrict__ vn = par ? A.v0 : A.v1;
   // kDbl (grouped LAMB): the master shard is double-buffered by parity
-  const float* __restrict__ wsh = (kDbl && par ? A.wsh_alt : A.wsh) + t.s0;
+  // (an arithmetic select: a branchy one made ptxas spill 64 more bytes)
+  const float* __restrict__ wsh =
+      (kDbl ? reinterpret_cast<const float*>(reinterpret_cast<uintptr_t>(A.wsh) +
+                                             (reinterpret_cast<uintptr_t>(A.wsh_alt) -
+                                              reinterpret_cast<uintptr_t>(A.wsh)) * static_cast<uintptr_t>(par != 0))
+           : A.wsh) + t.s0;
   float* __restrict__ u = A.u + t.s0;
   m += t.s0;
   v += t.s0;
