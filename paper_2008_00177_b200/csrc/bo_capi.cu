@@ -389,7 +389,7 @@ bo_status bo_create(const bo_trainer_config* cfg, int32_t n_tensors, const int64
   BO_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
   c->p1r_prefetch = 4 * c->num_sms / 3;
   if (const char* e = std::getenv("BO_P1R_PREFETCH")) c->p1r_prefetch = std::max(0, std::atoi(e));
-  c->push_posted_ctas = 64;  // measured best at 4 GPUs (profiles/r02_notes.md)
+  c->push_posted_ctas = 128;  // measured best at 4 GPUs (80-128 on a plateau; profiles/r02_notes.md)
   if (const char* e = std::getenv("BO_PUSH_POSTED_CTAS")) c->push_posted_ctas = std::max(0, std::atoi(e));
   BO_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   c->own_stream = true;

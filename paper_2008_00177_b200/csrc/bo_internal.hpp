@@ -256,7 +256,7 @@ struct bo_ctx {
   // best: profiles/r02_notes.md)
   int p1r_prefetch = 0;
   // grouped LAMB: the parameter push as this many persistent CTAs with
-  // posted stores (k_push_posted; BO_PUSH_POSTED_CTAS, default 64; 0 = one
+  // posted stores (k_push_posted; BO_PUSH_POSTED_CTAS, default 128; 0 = one
   // CTA per tile with bulk copies)
   int push_posted_ctas = 0;
   bool force_unfused = false;           // BO_UNFUSED=1: unfused kernels (one rank: multi-kernel LAMB; ring: staged last hop)

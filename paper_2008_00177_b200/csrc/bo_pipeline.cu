@@ -845,14 +845,15 @@ __global__ void k_step_final(const double* __restrict__ all_part, int N, int T, 
   }
 }
 
-// The parameter push as a FEW persistent CTAs with posted stores (grouped
-// LAMB, BO_PUSH_POSTED_CTAS): each thread takes one float4 of a tile (grid-
-// stride over the tiles, two in flight) and stores the new value into the master shard and — plain 16-byte stores, no completion
-// wait — into every rank's replica (rotated per tile). ~32-48 CTAs of 1024
-// threads keep the push at ~650 GB/s of NVLink while phase 1 of the next
-// group streams HBM on the other SMs at ~0.96 of its speed alone
-// (tools/nvl_partition.cu, profiles/r02_notes.md); the one-CTA-per-tile bulk
-// copy push needs every SM. Same arithmetic and destinations as
+// The parameter push as persistent CTAs with posted stores (grouped LAMB,
+// BO_PUSH_POSTED_CTAS, default 128): each thread takes one float4 of a tile
+// (grid-stride over the tiles, two in flight) and stores the new value into
+// the master shard and — plain 16-byte stores, no completion wait — into
+// every rank's replica (rotated per tile). Posted stores let even 24-64 CTAs
+// of 1024 threads drive ~650-700 GB/s of NVLink while phase 1 of the next
+// group streams HBM on the other SMs (tools/nvl_partition.cu,
+// profiles/r02_notes.md); the one-CTA-per-tile bulk-copy push, which waits
+// for its copies, needs every SM. Same arithmetic and destinations as
 // k_shard_p2_push; tiles whose shard and replica 16-byte phases differ go
 // scalar. Kernel completion performs the posted stores before the stream's
 // next work (the end-of-step barrier, k_rollback).
