@@ -69,9 +69,11 @@ def test_iteration_time_limit_cases():
 
 
 def test_b200_projection_tracks_single_node_measurements():
-    """Within 10% of the measured steps (2.33 / 2.50 / 2.84 ms)."""
+    """Within 10% of the measured steps of the stage-serial path the model
+    describes (2.28 / 2.51 / 2.85 ms at 1 / 2 / 4 GPUs; the
+    grouped LAMB default at 4 GPUs, 2.60 ms, overlaps stages the model adds)."""
     P = 336226108
-    for g, measured in [(1, 2.33), (2, 2.50), (4, 2.84)]:
+    for g, measured in [(1, 2.28), (2, 2.51), (4, 2.85)]:
         proj = project_step_ms(P, 4, 1, g)
         assert math.isclose(proj["step_ms"], measured, rel_tol=0.10), (g, proj)
     # more machines add the network stages; the step never gets shorter
