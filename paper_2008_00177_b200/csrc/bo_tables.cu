@@ -193,10 +193,24 @@ void upload_tables(bo_ctx* c) {
     // Grouped LAMB: consecutive tensors in model order, >= BO_LAMB_GROUP_ELEMS
     // elements each (0: one group, the serial path). Default: eight groups at
     // world >= 4, where the parameter push (NVLink) is the largest stage and
-    // the few-CTA posted push of group g hides phase 1 of group g + 1 (BERT-
-    // large, 4 B200s: 2.64 vs 2.85 ms per step); serial below (2 B200s: the
-    // serial step is faster, profiles/r02_notes.md).
+    // the posted push of group g hides phase 1 of group g + 1 (BERT-large,
+    // 4 B200s: 2.60 vs 2.85 ms per step); serial below (2 B200s: within
+    // box-to-box variance, profiles/r02_notes.md).
     int64_t lg_elems = L.N >= 4 ? (L.P + 7) / 8 : 0;
+    if (lg_elems > 0) {
+      // The posted push stores 16-byte vectors only where a rank's shard and
+      // the replica share their 16-byte phase, i.e. where owner * c_b is a
+      // multiple of 4; other chunks go element by element, which made the
+      // step 1.8x slower with 1 GiB buckets (two buckets, odd chunk sizes;
+      // profiles/r02_notes.md). Those layouts keep the serial path (its
+      // bulk-copy push stages every tile at the replica's phase). Decided
+      // from the layout alone, so every rank agrees.
+      int64_t odd = 0;
+      for (int b = 0; b < L.B; ++b) {
+        if (L.chunk[static_cast<size_t>(b)] % 4 != 0) odd += L.elems[static_cast<size_t>(b)];
+      }
+      if (odd * 10 > L.P) lg_elems = 0;  // > 10 % of the elements (64 MiB at 4 GPUs: 4 %, grouped still faster)
+    }
     if (const char* e = std::getenv("BO_LAMB_GROUP_ELEMS")) lg_elems = std::max<int64_t>(0, std::atoll(e));
     c->lamb_groups.clear();
     if (lg_elems > 0) {
